@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""BLF-LS benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = the full BLF-LS hot path (cfg.iters cascaded iterations of
+circular gradients -> brute-force (joint) BLF -> periodic FFT LS solve) over
+one batch of the config's synthetic images.  Default workload: BASELINE.json
+configs[1] ("c2": 1024x1024 RGB, r=7, sigma_s=7, sigma_r=0.1, lambda=1000,
+3 iterations).  For N > 1 (torchrun) every rank processes its own images of
+the same config (independent units, no data-path collective): weak scaling.
+
+metric: megapixels per second per iteration, MP/s = H*W*B*iters / t_step
+(SURVEY.md 8(d)), summed over ranks, t = max over ranks (CUDA events).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BLF-LS megapixels/sec (full solve, per iter)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/blfls_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self, under_load_mhz=900):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        self.path.unlink(missing_ok=True)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [s for s, _, _ in rows if s >= under_load_mhz] or [s for s, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- helpers --
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def config_json(cfg, n_gpus, extra=None):
+    d = {"workload": f"{cfg.name}: {cfg.height}x{cfg.width}x{cfg.channels} x{cfg.batch} images/rank, "
+                     f"r={cfg.radius}, sigma_s={cfg.sigma_s}, sigma_r={cfg.sigma_r}, "
+                     f"lambda={cfg.lam}, iters={cfg.iters}"
+                     + (", joint gray guide" if cfg.guide else ""),
+         "height": cfg.height, "width": cfg.width, "channels": cfg.channels,
+         "images_per_rank": cfg.batch, "radius": cfg.radius, "sigma_s": cfg.sigma_s,
+         "sigma_r": cfg.sigma_r, "lambda": cfg.lam, "iters": cfg.iters,
+         "boundary": "periodic (pad=0)", "guide": "grayscale joint" if cfg.guide else "self",
+         "parallelism": f"independent images x{n_gpus} ranks" if n_gpus > 1 else "single GPU"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def cpu_sample(cfg, threads=None):
+    """Reference CPU path on a bounded sample of the workload: the first image
+    of the config, ONE iteration (of cfg.iters), through oracle/_ref
+    (the reference's translation units + brute-force BLF with explicit r)."""
+    import numpy as np
+    from oracle import oracle as O
+    kind = "reference" if O.REF_SO.exists() else "port"
+    img = np.stack([O.gen_plane(s, cfg.height, cfg.width, n_sites=cfg.n_sites,
+                                p_sp=cfg.p_salt_pepper) for s in cfg.seeds(0)]).astype(np.float64)
+    guide = None
+    if cfg.guide:
+        guide = O.gen_plane(cfg.guide_seed(0), cfg.height, cfg.width, n_sites=cfg.n_sites)[None]
+        guide = guide.astype(np.float64)
+    fn = O.ref_blf_ls if kind == "reference" else O.blf_ls
+    t0 = time.perf_counter()
+    _, tb, ts = fn(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
+                   radius=cfg.radius, timed=True)
+    dt = time.perf_counter() - t0
+    mp = cfg.height * cfg.width / 1e6
+    return {"value": mp / dt, "unit": "MP/s", "cores": O.num_threads(), "kind": kind,
+            "sample": f"1 image x 1 iteration of {cfg.name} ({cfg.height}x{cfg.width}x{cfg.channels}), "
+                      f"double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
+            "seconds": dt, "blf_s": tb, "solve_s": ts}
+
+
+# ---------------------------------------------------------- reference arm --
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    res = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(cfg)
+        if i >= args.warmup:
+            res.append(r)
+    secs = [r["seconds"] for r in res]
+    t = statistics.mean(secs)
+    mp = cfg.height * cfg.width / 1e6
+    value = mp / t
+    line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Voronoi + ramp + noise, BASELINE generator)",
+            "impl": "reference",
+            "config": config_json(cfg, 1, {"step": "1 image x 1 iteration (bounded CPU sample)"}),
+            "cpu_baseline": {"value": value, "unit": "MP/s", "cores": res[0]["cores"],
+                             "kind": res[0]["kind"], "sample": res[0]["sample"]},
+            "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours --
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1812_07122_b200 as P
+    from paper_1812_07122_b200 import _capi
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    peaks, peak_src = load_peaks()
+
+    # inputs resident in HBM: this rank's images (image index offset by rank)
+    n = cfg.batch
+    seeds = [s for i in range(n) for s in cfg.seeds(rank * n + i)]
+    img = P.generate(cfg.height, cfg.width, seeds, n_sites=cfg.n_sites,
+                     p_salt_pepper=cfg.p_salt_pepper, device=dev).view(n, cfg.channels, cfg.height,
+                                                                        cfg.width)
+    guide = None
+    if cfg.guide:
+        guide = P.generate(cfg.height, cfg.width, [cfg.guide_seed(rank * n + i) for i in range(n)],
+                           n_sites=cfg.n_sites, device=dev).view(n, 1, cfg.height, cfg.width)
+    out = torch.empty_like(img)
+    kw = dict(lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=cfg.iters,
+              radius=cfg.radius, check_finite=False)
+    in_bytes = img.numel() * 4 + (guide.numel() * 4 if guide is not None else 0)
+    flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    l2_resident = in_bytes * 4 < 100e6
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.blf_ls(img, guide, out=out, **kw)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    plan = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, cfg.radius,
+                      cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev)
+
+    # ---- timed region: K steps, CUDA events per step, L2 flushed between steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clocks:
+        for k in range(args.steps):
+            if l2_resident:
+                flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    ms_step = statistics.mean(ms)
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    stats = plan.stats()
+    launches_per_step = int(stats.kernel_launches)
+
+    # ---- same K steps with per-stage CUDA events (direct launches) for the roofline
+    for k in range(args.steps):
+        if l2_resident:
+            flush.fill_(float(k))
+        P.blf_ls(img, guide, out=out, extra_flags=_capi.TIME_STAGES, **kw)
+    torch.cuda.synchronize()
+    stage_ms, stage_n = plan.stage_times()
+    blf_ms = stage_ms[1] / max(1, stage_n[1])
+    solve_ms = sum(stage_ms[2:5]) / max(1, stage_n[2])  # per iteration (r2c + col + c2r)
+    exps_per_launch = stats.exps / max(1, stats.blf_launches)
+
+    mufu_rate, mufu_clk = _capi.mufu_peak(dev)
+    # algorithmic exponentials per BLF launch / launch duration vs the SFU peak
+    sfu_peak_nominal = 148 * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+    achieved = exps_per_launch / (blf_ms * 1e-3)
+    # solve-stage algorithmic bytes per iteration (fold form, per plane):
+    # r2c reads f, Tx, Ty (12 HW) writes S; column reads+writes S; c2r reads S writes 4 HW
+    planes = n * cfg.channels
+    S = 8 * cfg.height * (cfg.width // 2 + 1)
+    solve_bytes = planes * (16 * cfg.height * cfg.width + 4 * S)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+
+    mp_step = cfg.height * cfg.width * n * cfg.iters / 1e6
+    value = mp_step * world / (ms_step * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        h_img = img.cpu().pin_memory()
+        h_guide = guide.cpu().pin_memory() if guide is not None else None
+        h_out = torch.empty(img.shape, dtype=torch.float32).pin_memory()
+        hkw = dict(kw)
+        hkw["check_finite"] = True  # the reference's require_finite, as a user call does
+        for _ in range(2):
+            P.blf_ls(h_img, h_guide, out=h_out, **hkw)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_ms = []
+        for k in range(args.steps):
+            if l2_resident:
+                flush.fill_(float(k))
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(torch.cuda.default_stream())
+            P.blf_ls(h_img, h_guide, out=h_out, **hkw)
+            b.record(torch.cuda.default_stream())
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        e_step = statistics.mean(e_ms)
+        if world > 1:
+            t = torch.tensor([e_step], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_step = float(t.item())
+        e2e = {"value": mp_step * world / (e_step * 1e-3), "unit": "MP/s",
+               "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out.numel() * 4,
+               "ms_per_step": e_step,
+               "path": "paper_1812_07122_b200.blf_ls(pinned host tensors) -> blfls_run(HOST_PTRS)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            c = cpu_sample(cfg)
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the baseline must not sink the bench line
+            cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": None,
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Voronoi + ramp + noise, BASELINE generator, generated on device)",
+            "config": config_json(cfg, world, {
+                "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2"}),
+            "roofline": {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
+                         "achieved": achieved / 1e9, "peak": mufu_rate / 1e9, "unit": "Gexp/s",
+                         "frac": achieved / mufu_rate,
+                         "peak_source": "measured MUFU.EX2 probe on this GPU "
+                                        f"(SM clock {mufu_clk / 1e6:.0f} MHz); nominal "
+                                        f"148x16x{peaks.get('sm_max_mhz', 1965.0):.0f} MHz = "
+                                        f"{sfu_peak_nominal / 1e9:.0f} Gexp/s",
+                         "frac_of_nominal": achieved / sfu_peak_nominal,
+                         "exps_per_launch": exps_per_launch, "launch_ms": blf_ms,
+                         "traffic": None},
+            "roofline_solve": {"bound": "hbm", "achieved": solve_bytes / (solve_ms * 1e-3) / 1e9,
+                               "peak": hbm_peak, "unit": "GB/s",
+                               "frac": solve_bytes / (solve_ms * 1e-3) / 1e9 / hbm_peak,
+                               "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                               "bytes_per_iter": solve_bytes, "ms_per_iter": solve_ms},
+            "stage_ms_per_step": {"minmax": stage_ms[0] / args.steps, "grad_blf": stage_ms[1] / args.steps,
+                                  "row_r2c": stage_ms[2] / args.steps, "col_solve": stage_ms[3] / args.steps,
+                                  "row_c2r": stage_ms[4] / args.steps},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_1812_07122_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * blfls.h -- C ABI of the B200-native BLF-LS hot path (sm_100a CUDA).
+ *
+ * This is the drop-in boundary.  The reference (/root/reference/proj) is a C++
+ * library with no FFI; its seams for this path are
+ *
+ *   PlanarImage epls::smooth(const PlanarImage&, const SmootherSpec&)
+ *       include/epls/pipelines.hpp:36, src/pipelines.cpp:57-94  (BLF_LS branch)
+ *   PlanarImage epls::flash_no_flash(noflash, flash, spec)   (joint variant)
+ *       include/epls/applications.hpp:29, src/applications.cpp:58-64
+ *   filter_gradients (pipelines.cpp:33-53) + blf_brute (bilateral.hpp:26)
+ *   PlanarImage epls::lsgrad_solve_fft(g, target, SolveParams)
+ *       include/epls/solver.hpp:43, src/solver.cpp:88-124
+ *   epls::detail::rfft2 / irfft2   src/fft2d.hpp:11,14
+ *
+ * and each entry point below names the one it replaces.  Conventions:
+ *  - images are planar fp32, [batch][channel][row][col] (the reference's
+ *    PlanarImage layout, image.hpp:9-41, one image after another);
+ *  - buffers are caller-owned; BLFLS_HOST_PTRS says they are host memory
+ *    (copied in/out on `stream` inside the call), otherwise device memory;
+ *  - no exception crosses the ABI: std::invalid_argument of the reference maps
+ *    to BLFLS_EINVAL, non-finite input (image.cpp:21-27) to BLFLS_ENONFINITE;
+ *    blfls_last_error() returns a thread-local message for the last failure;
+ *  - a plan is not thread-safe (one per host thread / stream); plans on
+ *    different devices run concurrently;
+ *  - there is no CPU fallback: without a usable sm_100 device every entry
+ *    point that computes returns BLFLS_ECUDA.
+ */
+#ifndef BLFLS_H
+#define BLFLS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLFLS_ABI_VERSION 1
+
+typedef enum blfls_status {
+    BLFLS_OK = 0,
+    BLFLS_EINVAL = 1,        /* std::invalid_argument in the reference */
+    BLFLS_ENONFINITE = 2,    /* require_finite, image.cpp:21-27 */
+    BLFLS_ECUDA = 3,         /* CUDA runtime error / no device */
+    BLFLS_ENOMEM = 4,        /* device allocation failed */
+    BLFLS_EUNSUPPORTED = 5   /* size/radius outside the supported envelope */
+} blfls_status;
+
+/* flags */
+#define BLFLS_DEVICE_PTRS 0u
+#define BLFLS_HOST_PTRS 1u     /* img/guide/out are host pointers (pinned is fastest) */
+#define BLFLS_CHECK_FINITE 2u  /* reject NaN/Inf input like require_finite (one sync) */
+#define BLFLS_SYNC 4u          /* synchronize `stream` before returning */
+#define BLFLS_NO_GRAPH 8u      /* launch kernels directly instead of a cached CUDA graph */
+#define BLFLS_TIME_STAGES 16u  /* bracket every stage with CUDA events (implies NO_GRAPH);
+                                  read the sums with blfls_stage_times */
+
+typedef struct blfls_plan_s* blfls_plan_t;
+
+/* Everything a plan is specialised on.  Mirrors SmootherSpec
+ * (pipelines.hpp:16-23) restricted to kind == BLF_LS, pad == 0. */
+typedef struct blfls_params {
+    int height, width;    /* image size, >= 2 each */
+    int channels;         /* 1 or 3 (image.cpp:16-17) */
+    int guide_channels;   /* 0 = self-guided; 1 = one grayscale guide shared by all
+                             channels; == channels = per-channel guide (smooth()
+                             with SmootherSpec::guidance, pipelines.cpp:81-84) */
+    int radius;           /* BLF window radius r; < 0 means ceil(3*sigma_s) as
+                             bilateral.cpp:37 */
+    double sigma_s;       /* RangeSpatialParams (bilateral.hpp:10-13) */
+    double sigma_r;
+    double lambda;        /* SolveParams::lambda (solver.hpp:12-15); pad is 0 */
+    int max_batch;        /* images per call the plan's workspace is sized for */
+    int device;           /* CUDA device ordinal */
+} blfls_params;
+
+/* Validates like validate_params / validate_solve_params (bilateral.cpp:12-24,
+ * solver.cpp:15-21) and caches twiddles, spectral denominators and workspaces. */
+blfls_status blfls_plan_create(const blfls_params* params, blfls_plan_t* plan);
+blfls_status blfls_plan_destroy(blfls_plan_t plan);
+
+/* Full BLF-LS: `iters` cascaded smooth() calls (each one normalise -> circular
+ * gradients -> brute-force (joint) BLF of each gradient field over the
+ * (2r+1)^2 clipped window -> periodic FFT least-squares solve -> denormalise),
+ * guide held fixed.  Replaces epls::smooth(g, spec) for kind == BLF_LS
+ * (pipelines.cpp:57-94) with blf_brute in place of blf_grid, and
+ * flash_no_flash (applications.cpp:58-64) when guide != NULL.
+ * img/out: batch x C x H x W; guide: batch x guide_channels x H x W or NULL. */
+blfls_status blfls_run(blfls_plan_t plan, const float* img, const float* guide, int batch,
+                       int iters, float* out, void* stream, unsigned flags);
+
+/* One iteration's gradient targets, as filter_gradients returns them
+ * (pipelines.cpp:33-53): gradients of the [0,1]-normalised image, filtered by
+ * the brute-force BLF.  tx/ty: batch x C x H x W. */
+blfls_status blfls_filter_gradients(blfls_plan_t plan, const float* img, const float* guide,
+                                    int batch, float* tx, float* ty, void* stream, unsigned flags);
+
+/* Row-band form of blfls_filter_gradients for the multi-GPU band driver:
+ * rows [y0, y1) of the targets of ONE image (batch index 0), written to
+ * tx/ty as (y1-y0) x W planes per channel, in RAW image units (not
+ * normalised; the solve consumes them directly).  The full image is read
+ * (the window clips at the global top/bottom, gy wraps at y = H-1). */
+blfls_status blfls_filter_gradients_rows(blfls_plan_t plan, const float* img, const float* guide,
+                                         int y0, int y1, float* tx, float* ty, void* stream,
+                                         unsigned flags);
+
+/* lsgrad_solve_fft(g, {tx, ty}, {lambda, 0}) (solver.cpp:88-124); all
+ * arguments batch x C x H x W.  tx/ty may both be NULL (ls_solve_fft,
+ * solver.cpp:67-86). */
+blfls_status blfls_solve(blfls_plan_t plan, const float* g, const float* tx, const float* ty,
+                         int batch, float* u, void* stream, unsigned flags);
+
+/* detail::rfft2 (fft2d.cpp:17-34): x is batch*C planes of H x W; spec is
+ * batch*C planes of H x (W/2+1) interleaved complex (re, im) fp32. */
+blfls_status blfls_rfft2(blfls_plan_t plan, const float* x, int batch, float* spec, void* stream,
+                         unsigned flags);
+/* detail::irfft2 (fft2d.cpp:36-52) including the 1/(H*W) scaling. */
+blfls_status blfls_irfft2(blfls_plan_t plan, const float* spec, int batch, float* out, void* stream,
+                          unsigned flags);
+
+/* Seeded synthetic planes of BASELINE.json (Voronoi levels + ramp + Gaussian
+ * noise + optional salt-and-pepper, clipped to [0,1]); one seed per plane.
+ * out: n_planes x H x W device memory. */
+blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t* seeds,
+                            int n_sites, double noise_sigma, double p_salt_pepper, float* out,
+                            void* stream, int device);
+
+/* Counters of the last blfls_run on this plan (for the bench's roofline). */
+typedef struct blfls_stats {
+    int radius;
+    long long blf_launches;      /* grad+BLF kernel launches */
+    long long kernel_launches;   /* all kernels issued by the last call */
+    double exps;                 /* range-kernel exponentials the algorithm needs */
+} blfls_stats;
+blfls_status blfls_last_stats(blfls_plan_t plan, blfls_stats* stats);
+
+/* Sums of the CUDA-event durations (ms) of every stage launched under
+ * BLFLS_TIME_STAGES since the last call, and launch counts, indexed
+ * 0 min/max, 1 grad+BLF, 2 row r2c, 3 column solve, 4 row c2r.  Synchronizes
+ * the recorded events. */
+blfls_status blfls_stage_times(blfls_plan_t plan, double* ms_sum5, long long* launches5);
+
+/* Measured MUFU.EX2 throughput of `device` (ex2 per second), from a
+ * dependency-free ex2 loop over all SMs: the SFU roofline denominator. */
+blfls_status blfls_mufu_peak(int device, double* ex2_per_second, double* sm_clock_hz);
+
+const char* blfls_last_error(void);
+const char* blfls_version(void);
+int blfls_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLFLS_H */

@@ -1,0 +1,361 @@
+"""Host-side mirror of the reference's BLF-LS entry points over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj, namespace ``epls``):
+
+=========================  ==================================================
+this module                reference
+=========================  ==================================================
+``SmootherSpec``           ``SmootherSpec`` (include/epls/pipelines.hpp:16-23)
+``RangeSpatialParams``     ``RangeSpatialParams`` (bilateral.hpp:10-13)
+``SolveParams``            ``SolveParams`` (solver.hpp:12-15)
+``smooth(g, spec)``        ``smooth`` (pipelines.cpp:57-94), BLF_LS and LS
+``flash_no_flash``         ``flash_no_flash`` (applications.cpp:58-64)
+``blf_ls``                 the north-star cascade: ``iters`` smooth() calls
+``filter_gradients``       ``filter_gradients`` (pipelines.cpp:33-53)
+``lsgrad_solve_fft``       ``lsgrad_solve_fft`` (solver.cpp:88-124)
+``ls_solve_fft``           ``ls_solve_fft`` (solver.cpp:67-86)
+``rfft2`` / ``irfft2``     ``detail::rfft2`` / ``irfft2`` (fft2d.hpp:11,14)
+=========================  ==================================================
+
+Differences, all deliberate and documented in DESIGN.md: the bilateral stage
+is the brute-force filter (the north star) where the reference's smooth()
+runs the bilateral grid; the window radius is explicit (``radius``; ``None``
+means the reference's ceil(3 sigma_s)); arithmetic is fp32 on the GPU; only
+``pad == 0`` (periodic boundary) is supported.
+
+Images are numpy arrays (host memory; copied through the C ABI with
+``BLFLS_HOST_PTRS``) or CUDA torch tensors (device memory, current stream).
+Shapes: (H, W), (C, H, W) or (B, C, H, W), C in {1, 3}.
+``std::invalid_argument`` of the reference surfaces as ``InvalidArgument``
+(a ``ValueError``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _capi
+from ._capi import (CHECK_FINITE, DEVICE_PTRS, HOST_PTRS, NO_GRAPH, SYNC, CudaError,
+                    InvalidArgument, Plan, Unsupported, check, lib)
+
+__all__ = [
+    "SmootherKind", "RangeSpatialParams", "SolveParams", "SmootherSpec", "smooth",
+    "flash_no_flash", "blf_ls", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
+    "rfft2", "irfft2", "generate", "get_plan", "InvalidArgument", "CudaError", "Unsupported",
+]
+
+
+class SmootherKind(enum.Enum):
+    LS = 0
+    WLS = 1
+    BLF_LS = 2
+    NC_LS = 3
+
+
+@dataclass
+class RangeSpatialParams:
+    sigma_s: float = 8.0
+    sigma_r: float = 0.1
+
+
+@dataclass
+class SolveParams:
+    lam: float = 1024.0
+    pad: int = 16
+
+
+@dataclass
+class SmootherSpec:
+    kind: SmootherKind = SmootherKind.BLF_LS
+    blf: RangeSpatialParams = field(default_factory=lambda: RangeSpatialParams(12.0, 0.04))
+    solve: SolveParams = field(default_factory=SolveParams)
+    guidance: Any = None          # non-owning guide image of the same shape (or 1 channel)
+    radius: int | None = None     # BLF window radius; None = ceil(3 sigma_s) (bilateral.cpp:37)
+
+
+# ----------------------------------------------------------------- plans --
+
+_tls = threading.local()
+
+
+def get_plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, batch, device) -> Plan:
+    """Per-thread plan cache (plans are not thread-safe, blfls.h)."""
+    cache = getattr(_tls, "plans", None)
+    if cache is None:
+        cache = _tls.plans = {}
+    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device)
+    p = cache.get(key)
+    if p is None or p.params.max_batch < batch:
+        p = Plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, max_batch=max(batch, 1), device=device)
+        cache[key] = p
+    return p
+
+
+def _radius(radius, sigma_s):
+    if radius is None:
+        return int(math.ceil(3.0 * sigma_s))
+    return int(radius)
+
+
+class _Img:
+    """Normalises an input image to a contiguous fp32 buffer + pointer."""
+
+    def __init__(self, x, name="image"):
+        self.torch = False
+        self.orig_dtype = None
+        try:
+            import torch  # noqa: F401
+            is_tensor = isinstance(x, torch.Tensor)
+        except ImportError:  # pragma: no cover
+            is_tensor = False
+        if is_tensor:
+            import torch
+            if not x.is_cuda:
+                x = x.detach().cpu().numpy()
+            else:
+                self.torch = True
+                self.orig_dtype = x.dtype
+                self.t = x.detach().to(torch.float32).contiguous()
+                self.shape = tuple(self.t.shape)
+                self.device = self.t.device.index
+                self.ptr = self.t.data_ptr()
+        if not self.torch:
+            a = np.asarray(x)
+            if a.dtype.kind not in "fiu":
+                raise InvalidArgument(_capi.BLFLS_EINVAL, f"{name}: numeric array required")
+            self.orig_dtype = a.dtype if a.dtype.kind == "f" else np.dtype(np.float64)
+            self.a = np.ascontiguousarray(a, dtype=np.float32)
+            self.shape = self.a.shape
+            self.device = None
+            self.ptr = self.a.ctypes.data
+        if len(self.shape) == 2:
+            self.b, self.c, (self.h, self.w) = 1, 1, self.shape
+        elif len(self.shape) == 3:
+            self.b, (self.c, self.h, self.w) = 1, self.shape
+        elif len(self.shape) == 4:
+            self.b, self.c, self.h, self.w = self.shape
+        else:
+            raise InvalidArgument(_capi.BLFLS_EINVAL, f"{name}: expected (H,W), (C,H,W) or (B,C,H,W)")
+        if self.c not in (1, 3):
+            raise InvalidArgument(_capi.BLFLS_EINVAL, "PlanarImage: channels must be 1 or 3")
+
+    def empty_like(self, shape=None):
+        shape = self.shape if shape is None else shape
+        if self.torch:
+            import torch
+            return torch.empty(shape, dtype=torch.float32, device=self.t.device)
+        return np.empty(shape, dtype=np.float32)
+
+    def finish(self, out):
+        if self.torch:
+            return out if self.orig_dtype == out.dtype else out.to(self.orig_dtype)
+        return out.astype(self.orig_dtype, copy=False)
+
+
+def _ptr(x):
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream_and_flags(img: _Img):
+    if img.torch:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(img.t.device).cuda_stream), DEVICE_PTRS
+    return C.c_void_p(0), HOST_PTRS
+
+
+def _device(img: _Img, guide: _Img | None) -> int:
+    if img.torch:
+        if guide is not None and (not guide.torch or guide.device != img.device):
+            raise InvalidArgument(_capi.BLFLS_EINVAL, "guide must live on the image's device")
+        return img.device
+    if guide is not None and guide.torch:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "guide must be host memory like the image")
+    return 0
+
+
+# ------------------------------------------------------------ entry points --
+
+def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, iters: int = 1,
+           radius: int | None = None, check_finite: bool = True, use_graph: bool = True,
+           out=None, extra_flags: int = 0):
+    """BLF-LS: ``iters`` cascaded smooth() passes with the brute-force (joint) BLF.
+
+    ``guide`` (optional) has 1 channel or the image's channel count and is held
+    fixed over the iterations.  Returns the smoothed image in the input's type
+    (written into ``out`` when given: an fp32 array/tensor of the image's shape
+    in the same memory space, e.g. pinned host memory).
+    """
+    img = _Img(image)
+    gd = None if guide is None else _Img(guide, "guide")
+    if gd is not None:
+        if (gd.h, gd.w) != (img.h, img.w) or gd.b != img.b or gd.c not in (1, img.c):
+            raise InvalidArgument(_capi.BLFLS_EINVAL,
+                                  "smooth: guidance image shape does not match input")
+    r = _radius(radius, sigma_s)
+    dev = _device(img, gd)
+    plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, lam,
+                    img.b, dev)
+    if out is None:
+        out = img.empty_like()
+        finish = True
+    else:
+        if isinstance(out, np.ndarray):
+            if img.torch or out.dtype != np.float32 or out.shape != tuple(img.shape) \
+                    or not out.flags.c_contiguous:
+                raise InvalidArgument(_capi.BLFLS_EINVAL, "out: fp32 host array of the image shape")
+        else:
+            import torch
+            if out.dtype != torch.float32 or tuple(out.shape) != tuple(img.shape) \
+                    or not out.is_contiguous() or out.is_cuda != img.torch:
+                raise InvalidArgument(_capi.BLFLS_EINVAL, "out: fp32 tensor of the image shape")
+            if not out.is_cuda:
+                out = out.numpy()
+        finish = False
+    stream, flags = _stream_and_flags(img)
+    if check_finite:
+        flags |= CHECK_FINITE
+    if not use_graph:
+        flags |= NO_GRAPH
+    flags |= int(extra_flags)
+    check(lib().blfls_run(plan.handle, img.ptr, None if gd is None else gd.ptr, img.b, int(iters),
+                          _ptr(out), stream, flags))
+    return img.finish(out) if finish else out
+
+
+def smooth(g, spec: SmootherSpec):
+    """``epls::smooth`` (pipelines.cpp:57-94) for kind BLF_LS (brute-force BLF) and LS."""
+    if spec.solve.pad != 0:
+        raise Unsupported(_capi.BLFLS_EUNSUPPORTED,
+                          "smooth: only pad == 0 (periodic boundary) is implemented")
+    if spec.kind == SmootherKind.BLF_LS:
+        return blf_ls(g, spec.guidance, lam=spec.solve.lam, sigma_s=spec.blf.sigma_s,
+                      sigma_r=spec.blf.sigma_r, iters=1, radius=spec.radius)
+    if spec.kind == SmootherKind.LS:
+        # affine-equivariant, so normalise/denormalise (pipelines.cpp:64,68) is the identity
+        return ls_solve_fft(g, SolveParams(spec.solve.lam, 0))
+    raise Unsupported(_capi.BLFLS_EUNSUPPORTED, f"smooth: {spec.kind} is out of scope")
+
+
+def flash_no_flash(noflash, flash, spec: SmootherSpec):
+    """``flash_no_flash`` (applications.cpp:58-64): joint smoothing guided by `flash`."""
+    a, b = _Img(noflash), _Img(flash, "guide")
+    if a.shape != b.shape:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "flash_no_flash: image shapes differ")
+    s = SmootherSpec(spec.kind, spec.blf, spec.solve, flash, spec.radius)
+    return smooth(noflash, s)
+
+
+def filter_gradients(image, guide=None, *, sigma_s: float, sigma_r: float,
+                     radius: int | None = None):
+    """Gradient targets of one smooth() call (pipelines.cpp:33-53, brute-force BLF),
+    in the reference's normalised units.  Returns (tx, ty)."""
+    img = _Img(image)
+    gd = None if guide is None else _Img(guide, "guide")
+    r = _radius(radius, sigma_s)
+    dev = _device(img, gd)
+    plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, 0.0,
+                    img.b, dev)
+    tx, ty = img.empty_like(), img.empty_like()
+    stream, flags = _stream_and_flags(img)
+    check(lib().blfls_filter_gradients(plan.handle, img.ptr, None if gd is None else gd.ptr, img.b,
+                                       _ptr(tx), _ptr(ty), stream, flags | CHECK_FINITE))
+    return img.finish(tx), img.finish(ty)
+
+
+def lsgrad_solve_fft(g, target, params: SolveParams):
+    """``lsgrad_solve_fft`` (solver.cpp:88-124); target = (tx, ty) or None."""
+    if params.pad != 0:
+        raise Unsupported(_capi.BLFLS_EUNSUPPORTED, "lsgrad_solve_fft: only pad == 0 is implemented")
+    if not (params.lam >= 0.0) or not math.isfinite(params.lam):
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "solver: lambda must be finite and >= 0")
+    img = _Img(g)
+    txp = typ = None
+    if target is not None:
+        tx, ty = _Img(target[0], "target"), _Img(target[1], "target")
+        if tx.shape != img.shape or ty.shape != img.shape:
+            raise InvalidArgument(_capi.BLFLS_EINVAL,
+                                  "lsgrad_solve_fft: target shape does not match image")
+        txp, typ = tx.ptr, ty.ptr
+    plan = get_plan(img.h, img.w, img.c, 0, 1, 1.0, 1.0, params.lam, img.b,
+                    _device(img, None))
+    out = img.empty_like()
+    stream, flags = _stream_and_flags(img)
+    check(lib().blfls_solve(plan.handle, img.ptr, txp, typ, img.b, _ptr(out), stream,
+                            flags | CHECK_FINITE))
+    return img.finish(out)
+
+
+def ls_solve_fft(g, params: SolveParams):
+    """``ls_solve_fft`` (solver.cpp:67-86)."""
+    return lsgrad_solve_fft(g, None, params)
+
+
+def rfft2(x):
+    """``detail::rfft2`` of each plane: complex64 (…, H, W//2+1)."""
+    img = _Img(x)
+    plan = get_plan(img.h, img.w, img.c, 0, 1, 1.0, 1.0, 0.0, img.b, _device(img, None))
+    shape = tuple(img.shape[:-1]) + (img.w // 2 + 1,)
+    if img.torch:
+        import torch
+        out = torch.empty(shape, dtype=torch.complex64, device=img.t.device)
+    else:
+        out = np.empty(shape, dtype=np.complex64)
+    stream, flags = _stream_and_flags(img)
+    check(lib().blfls_rfft2(plan.handle, img.ptr, img.b, _ptr(out), stream, flags))
+    return out
+
+
+def irfft2(spec, width: int):
+    """``detail::irfft2`` (with the 1/(H W) scaling) back to (…, H, width)."""
+    is_t = False
+    try:
+        import torch
+        is_t = isinstance(spec, torch.Tensor) and spec.is_cuda
+    except ImportError:  # pragma: no cover
+        pass
+    if is_t:
+        s = spec.to(torch.complex64).contiguous()
+    else:
+        s = np.ascontiguousarray(spec, dtype=np.complex64)
+    shape = tuple(s.shape[:-1]) + (int(width),)
+    if len(shape) == 2:
+        b, c, h = 1, 1, shape[0]
+    elif len(shape) == 3:
+        b, (c, h) = 1, shape[:2]
+    else:
+        b, c, h = shape[:3]
+    if s.shape[-1] != width // 2 + 1:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "irfft2: spectrum width does not match")
+    dev = s.device.index if is_t else 0
+    plan = get_plan(h, width, c, 0, 1, 1.0, 1.0, 0.0, b, dev)
+    if is_t:
+        out = torch.empty(shape, dtype=torch.float32, device=s.device)
+        stream, flags = C.c_void_p(torch.cuda.current_stream(s.device).cuda_stream), DEVICE_PTRS
+    else:
+        out = np.empty(shape, dtype=np.float32)
+        stream, flags = C.c_void_p(0), HOST_PTRS
+    check(lib().blfls_irfft2(plan.handle, _ptr(s), b, _ptr(out), stream, flags))
+    return out
+
+
+def generate(height: int, width: int, seeds, *, n_sites: int, noise_sigma: float = 0.03,
+             p_salt_pepper: float = 0.0, device: int = 0):
+    """BASELINE synthetic planes on the GPU: torch.float32 (len(seeds), H, W)."""
+    import torch
+    seeds = [int(s) for s in seeds]
+    out = torch.empty((len(seeds), height, width), dtype=torch.float32, device=f"cuda:{device}")
+    arr = (C.c_uint64 * len(seeds))(*seeds)
+    stream = C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    check(lib().blfls_generate(int(height), int(width), len(seeds), arr, int(n_sites),
+                               float(noise_sigma), float(p_salt_pepper), out.data_ptr(), stream,
+                               int(device)))
+    return out

@@ -1,0 +1,95 @@
+// blfls_internal.cuh -- shared definitions of the sm_100a BLF-LS library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "blfls/blfls.h"
+
+namespace blfls {
+
+constexpr int kMaxRadius = 48;     // smem tile envelope (radius <= 48)
+constexpr int kMaxFftRadices = 24;
+constexpr int kMaxGenericRadix = 31;
+
+// log2(e)
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------- min/max --
+// Order-preserving float <-> uint32 map so atomicMin/atomicMax on unsigned
+// implement float min/max (the per-image global range of image.cpp:46-60).
+__host__ __device__ inline uint32_t float_to_ordered(float f)
+{
+    uint32_t b;
+#ifdef __CUDA_ARCH__
+    b = __float_as_uint(f);
+#else
+    __builtin_memcpy(&b, &f, 4);
+#endif
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__host__ __device__ inline float ordered_to_float(uint32_t k)
+{
+    const uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(b);
+#else
+    float f;
+    __builtin_memcpy(&f, &b, 4);
+    return f;
+#endif
+}
+
+// --------------------------------------------------------------------- FFT --
+// Stockham autosort, decimation in frequency, radix stages in `radix[]`.
+// Stage with radix p, stride s (product of earlier radices), m = n/(s*p):
+//   butterfly b in [0, n/p): k = b % s, q = b / s
+//   a_r = x[b + r*n/p]                                  r in [0, p)
+//   y[k + s*(p*q + t)] = tw[q*t*s] * sum_r a_r * w_p^{r*t}   t in [0, p)
+// with tw[j] = exp(-2*pi*i*j/n).  The inverse conjugates every twiddle.
+struct FftDesc {
+    int n;
+    int nstages;
+    int radix[kMaxFftRadices];
+    const float2* tw;  // n entries, device
+};
+
+// ---------------------------------------------------------------- BLF args --
+struct BlfParams {
+    const float* f;        // current image, batch x C x H x W
+    const float* guide;    // batch x GC x H x W or nullptr (self-guided)
+    float* tx;             // targets, batch x C x rows x W
+    float* ty;
+    const uint32_t* lohi;  // per image ordered (lo, hi) of f
+    const uint32_t* glohi; // per image ordered (lo, hi) of the guide
+    int H, W, C, GC;
+    int y0, y1;            // output rows [y0, y1)
+    int out_rows;          // rows per plane of tx/ty (H, or y1 - y0 for bands)
+    int normalized_out;    // 1: write targets of the [0,1]-normalised image
+    int radius;
+    float range_coef;      // sqrt(log2(e) / (8 sigma_r^2)): exponent scale for raw
+                           // gradients of a unit-range image
+    float cs[kMaxRadius + 1];  // log2 spatial weight -d^2/(2 sigma_s^2) * log2(e)
+    float wrow[kMaxRadius + 1]; // exp2(cs[d]) : row factor
+};
+
+struct SolveParams {
+    const float* f;      // image (batch x C x H x W)
+    const float* tx;     // targets or nullptr
+    const float* ty;
+    float2* spec;        // planes x H x spitch
+    float* out;          // output image
+    uint32_t* lohi_out;  // per image ordered (lo, hi) of out, or nullptr
+    const float* gain_x; // 4 sin^2(pi v / W), v in [0, W/2]
+    const float* gain_y; // 4 sin^2(pi u / H)
+    const float2* post;  // exp(-2 pi i v / W), v in [0, W/2]  (real-FFT split)
+    int H, W, C;
+    int spitch;          // complex elements per spectrum row
+    int wc;              // W/2 + 1
+    float lambda;
+    float inv_hw;        // 1 / (H W)
+    int mode;            // column pass: 1 fwd, 2 inv, 3 fwd+scale+inv
+};
+
+}  // namespace blfls

@@ -1,0 +1,810 @@
+// capi.cu -- the extern "C" boundary (include/blfls/blfls.h): plans,
+// workspaces, validation with the reference's error semantics, and the
+// per-iteration kernel sequence
+//
+//   min/max(f) -> grad+BLF(f) -> row r2c (+ divergence fold) -> column solve
+//   -> row c2r (+ next min/max)
+//
+// replayed as a cached CUDA graph on the plan's own stream.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "blfls_internal.cuh"
+
+namespace blfls {
+
+cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st);
+cudaError_t launch_row_r2c(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
+                           bool odd, cudaStream_t st);
+cudaError_t launch_col(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
+                       cudaStream_t st);
+cudaError_t launch_row_c2r(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
+                           bool odd, cudaStream_t st);
+cudaError_t launch_minmax(const float* x, size_t per_image, int batch, uint32_t* lohi, int nsm,
+                          cudaStream_t st);
+cudaError_t launch_reset_lohi(uint32_t* lohi, int n, cudaStream_t st);
+cudaError_t launch_count_nonfinite(const float* x, size_t n, unsigned* count, int nsm, cudaStream_t st);
+cudaError_t launch_scale_by_range(float* x, size_t per_image, int batch, const uint32_t* lohi,
+                                  int to_raw, cudaStream_t st);
+cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int K, double sigma,
+                            double p_sp, float* out, cudaStream_t st);
+cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz);
+
+}  // namespace blfls
+
+using namespace blfls;
+
+namespace {
+
+thread_local std::string g_err;
+
+blfls_status fail(blfls_status st, const std::string& msg)
+{
+    g_err = msg;
+    return st;
+}
+
+blfls_status cuda_fail(cudaError_t e, const char* where)
+{
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? BLFLS_ENOMEM : BLFLS_ECUDA;
+}
+
+#define CK(expr)                                               \
+    do {                                                       \
+        cudaError_t e_ = (expr);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #expr);    \
+    } while (0)
+
+struct DevFft {
+    FftDesc desc{};
+    int V = 1;        // vectors per CTA
+    int threads = 32;
+    float2* tw = nullptr;
+};
+
+bool factorize(int n, std::vector<int>& radix)
+{
+    radix.clear();
+    int m = n;
+    while (m % 4 == 0) { radix.push_back(4); m /= 4; }
+    while (m % 2 == 0) { radix.push_back(2); m /= 2; }
+    for (int p : {3, 5}) while (m % p == 0) { radix.push_back(p); m /= p; }
+    for (int p = 7; p <= 13 && m > 1; p += 2)
+        while (m % p == 0) { radix.push_back(p); m /= p; }
+    return m == 1 && (int)radix.size() <= kMaxFftRadices;
+}
+
+// per-stage capacity of fft_stage<P> / fft_stage_generic for V vectors and T threads
+bool fits(const std::vector<int>& radix, int n, int V, int T, int regs_per_thread)
+{
+    for (int p : radix) {
+        const long nb = ((long)V * n / p + T - 1) / T;
+        if (p <= 5) {
+            if (nb > (regs_per_thread + p - 1) / p) return false;
+        } else if (nb * p > 32) {
+            return false;
+        }
+    }
+    return true;
+}
+
+// choose V vectors per CTA and T threads: V*n/T <= ratio, T <= 1024
+bool plan_fft(int n, int Vmax, int ratio, DevFft& out, std::vector<int>& radix)
+{
+    if (!factorize(n, radix)) return false;
+    for (int V = Vmax; V >= 1; V >>= 1) {
+        const long work = (long)V * n;
+        int T = (int)((work + ratio - 1) / ratio);
+        T = ((T + 31) / 32) * 32;
+        if (T < 32) T = 32;
+        if (T > 1024) continue;
+        if (work * 8 > 200 * 1024) continue;  // shared memory
+        if (!fits(radix, n, V, T, 16)) continue;
+        out.V = V;
+        out.threads = T;
+        return true;
+    }
+    return false;
+}
+
+std::vector<float2> twiddles(int n)
+{
+    std::vector<float2> t(n);
+    for (int j = 0; j < n; ++j) {
+        const double a = -2.0 * M_PI * (double)j / (double)n;
+        t[j] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    return t;
+}
+
+struct EventPair {
+    cudaEvent_t a, b;
+    int stage;
+};
+
+}  // namespace
+
+struct blfls_plan_s {
+    blfls_params prm{};
+    int radius = 0;
+    int mode = 0;  // BLF kernel mode: 0 self, 1 per-channel guide, 2 shared gray guide
+    int nsm = 148;
+    cudaStream_t ps = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    // FFT
+    bool odd = false;
+    int wc = 0, spitch = 0;
+    DevFft rowf, colf;
+    float* gain_x = nullptr;
+    float* gain_y = nullptr;
+    float2* post = nullptr;
+    // workspace (max_batch images)
+    size_t plane = 0, img_elems = 0;
+    float* buf[2] = {nullptr, nullptr};
+    float* tx = nullptr;
+    float* ty = nullptr;
+    float2* spec = nullptr;
+    float* in_dev = nullptr;     // host-pointer staging
+    float* guide_dev = nullptr;
+    float* out_dev = nullptr;
+    uint32_t* lohi = nullptr;    // [2][max_batch][2]
+    uint32_t* glohi = nullptr;   // [max_batch][2]
+    unsigned* nonfinite = nullptr;
+    BlfParams blf{};
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    const void* g_in = nullptr;
+    const void* g_guide = nullptr;
+    void* g_out = nullptr;
+    int g_batch = -1, g_iters = -1;
+    // stats
+    blfls_stats stats{};
+    long long launches = 0;
+    std::vector<EventPair> timing;
+    bool time_stages = false;
+};
+
+namespace {
+
+blfls_status set_device(blfls_plan_t p)
+{
+    CK(cudaSetDevice(p->prm.device));
+    return BLFLS_OK;
+}
+
+// --------------------------------------------------------------- stages --
+
+void stage_begin(blfls_plan_t p, int stage, cudaStream_t st)
+{
+    if (!p->time_stages) return;
+    EventPair e{};
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    e.stage = stage;
+    cudaEventRecord(e.a, st);
+    p->timing.push_back(e);
+}
+
+void stage_end(blfls_plan_t p, cudaStream_t st)
+{
+    if (!p->time_stages) return;
+    cudaEventRecord(p->timing.back().b, st);
+}
+
+SolveParams solve_params(blfls_plan_t p)
+{
+    SolveParams s{};
+    s.H = p->prm.height;
+    s.W = p->prm.width;
+    s.C = p->prm.channels;
+    s.spitch = p->spitch;
+    s.wc = p->wc;
+    s.lambda = (float)p->prm.lambda;
+    s.inv_hw = (float)(1.0 / ((double)s.H * (double)s.W));
+    s.gain_x = p->gain_x;
+    s.gain_y = p->gain_y;
+    s.post = p->post;
+    s.spec = p->spec;
+    return s;
+}
+
+blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const float* ty, float* out,
+                       uint32_t* lohi_out, int batch, cudaStream_t st)
+{
+    const int planes = batch * p->prm.channels;
+    SolveParams s = solve_params(p);
+    s.f = f;
+    s.tx = tx;
+    s.ty = ty;
+    s.out = out;
+    s.lohi_out = lohi_out;
+    s.mode = 3;
+    stage_begin(p, 2, st);
+    CK(launch_row_r2c(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+    stage_end(p, st);
+    stage_begin(p, 3, st);
+    CK(launch_col(s, p->colf.desc, p->colf.V, p->colf.threads, planes, st));
+    stage_end(p, st);
+    if (lohi_out) {
+        CK(launch_reset_lohi(lohi_out, batch, st));
+        p->launches++;
+    }
+    stage_begin(p, 4, st);
+    CK(launch_row_c2r(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+    stage_end(p, st);
+    p->launches += 3;
+    return BLFLS_OK;
+}
+
+blfls_status enq_blf(blfls_plan_t p, const float* f, const float* guide, const uint32_t* lohi,
+                     float* tx, float* ty, int batch, int y0, int y1, int out_rows, int normalized,
+                     cudaStream_t st)
+{
+    BlfParams b = p->blf;
+    b.f = f;
+    b.guide = guide;
+    b.tx = tx;
+    b.ty = ty;
+    b.lohi = lohi;
+    b.glohi = p->glohi;
+    b.y0 = y0;
+    b.y1 = y1;
+    b.out_rows = out_rows;
+    b.normalized_out = normalized;
+    stage_begin(p, 1, st);
+    CK(launch_grad_blf(b, p->mode, batch, st));
+    stage_end(p, st);
+    p->launches++;
+    p->stats.blf_launches++;
+    return BLFLS_OK;
+}
+
+blfls_status enq_minmax(blfls_plan_t p, const float* x, size_t per_image, int batch, uint32_t* lohi,
+                        cudaStream_t st)
+{
+    stage_begin(p, 0, st);
+    CK(launch_minmax(x, per_image, batch, lohi, p->nsm, st));
+    stage_end(p, st);
+    p->launches += 2;
+    return BLFLS_OK;
+}
+
+// the whole cascade on device pointers
+blfls_status enq_run(blfls_plan_t p, const float* in, const float* guide, float* out, int batch,
+                     int iters, cudaStream_t st)
+{
+    const size_t per_image = (size_t)p->prm.channels * p->plane;
+    const int mb = p->prm.max_batch;
+    blfls_status r;
+    if (guide) {
+        r = enq_minmax(p, guide, (size_t)p->prm.guide_channels * p->plane, batch, p->glohi, st);
+        if (r) return r;
+    }
+    r = enq_minmax(p, in, per_image, batch, p->lohi, st);
+    if (r) return r;
+    const float* cur = in;
+    for (int k = 0; k < iters; ++k) {
+        const bool last = k == iters - 1;
+        float* nxt = last ? out : p->buf[k & 1];
+        uint32_t* lo_cur = p->lohi + (size_t)(k & 1) * 2 * mb;
+        uint32_t* lo_nxt = last ? nullptr : p->lohi + (size_t)((k + 1) & 1) * 2 * mb;
+        r = enq_blf(p, cur, guide, lo_cur, p->tx, p->ty, batch, 0, p->prm.height, p->prm.height, 0, st);
+        if (r) return r;
+        r = enq_solve(p, cur, p->tx, p->ty, nxt, lo_nxt, batch, st);
+        if (r) return r;
+        cur = nxt;
+    }
+    return BLFLS_OK;
+}
+
+blfls_status validate_batch(blfls_plan_t p, int batch)
+{
+    if (!p) return fail(BLFLS_EINVAL, "null plan");
+    if (batch < 1 || batch > p->prm.max_batch)
+        return fail(BLFLS_EINVAL, "batch must be in [1, max_batch]");
+    return BLFLS_OK;
+}
+
+blfls_status check_finite(blfls_plan_t p, const float* x, size_t n, cudaStream_t st, const char* what)
+{
+    CK(cudaMemsetAsync(p->nonfinite, 0, sizeof(unsigned), st));
+    CK(launch_count_nonfinite(x, n, p->nonfinite, p->nsm, st));
+    unsigned h = 0;
+    CK(cudaMemcpyAsync(&h, p->nonfinite, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h) return fail(BLFLS_ENONFINITE, std::string(what) + ": non-finite sample in input image");
+    return BLFLS_OK;
+}
+
+// join the caller's stream into the plan stream and back
+blfls_status fork_in(blfls_plan_t p, cudaStream_t user)
+{
+    CK(cudaEventRecord(p->ev_in, user));
+    CK(cudaStreamWaitEvent(p->ps, p->ev_in, 0));
+    return BLFLS_OK;
+}
+
+blfls_status join_out(blfls_plan_t p, cudaStream_t user, unsigned flags)
+{
+    CK(cudaEventRecord(p->ev_out, p->ps));
+    CK(cudaStreamWaitEvent(user, p->ev_out, 0));
+    if (flags & BLFLS_SYNC) CK(cudaStreamSynchronize(user));
+    return BLFLS_OK;
+}
+
+void free_plan(blfls_plan_t p)
+{
+    if (!p) return;
+    cudaSetDevice(p->prm.device);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    for (auto& e : p->timing) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
+                    p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
+                    p->rowf.tw, p->colf.tw};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (p->ev_in) cudaEventDestroy(p->ev_in);
+    if (p->ev_out) cudaEventDestroy(p->ev_out);
+    if (p->ps) cudaStreamDestroy(p->ps);
+    delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* blfls_last_error(void) { return g_err.c_str(); }
+const char* blfls_version(void) { return "blfls-b200 0.1 (sm_100a)"; }
+int blfls_abi_version(void) { return BLFLS_ABI_VERSION; }
+
+blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
+{
+    if (!prm || !out) return fail(BLFLS_EINVAL, "null argument");
+    *out = nullptr;
+    const blfls_params& q = *prm;
+    // image.cpp:14-17, solver.cpp:35-36
+    if (q.height < 2 || q.width < 2)
+        return fail(BLFLS_EINVAL, "plan: height and width must be >= 2");
+    if (q.channels != 1 && q.channels != 3)
+        return fail(BLFLS_EINVAL, "plan: channels must be 1 or 3");
+    if (q.guide_channels != 0 && q.guide_channels != 1 && q.guide_channels != q.channels)
+        return fail(BLFLS_EINVAL, "plan: guide channels must be 0, 1 or match the image");
+    // bilateral.cpp:12-16
+    if (!(q.sigma_s > 0.0) || !std::isfinite(q.sigma_s) || !(q.sigma_r > 0.0) ||
+        !std::isfinite(q.sigma_r))
+        return fail(BLFLS_EINVAL, "bilateral: sigma_s and sigma_r must be positive and finite");
+    // solver.cpp:15-21
+    if (!(q.lambda >= 0.0) || !std::isfinite(q.lambda))
+        return fail(BLFLS_EINVAL, "solver: lambda must be finite and >= 0");
+    if (q.max_batch < 1) return fail(BLFLS_EINVAL, "plan: max_batch must be >= 1");
+    const int radius = q.radius < 0 ? (int)std::ceil(3.0 * q.sigma_s) : q.radius;
+    if (radius > kMaxRadius)
+        return fail(BLFLS_EUNSUPPORTED, "plan: radius above " + std::to_string(kMaxRadius));
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(BLFLS_ECUDA, "no CUDA device (this library has no CPU fallback)");
+    if (q.device < 0 || q.device >= ndev) return fail(BLFLS_EINVAL, "plan: bad device ordinal");
+
+    auto* p = new blfls_plan_s();
+    p->prm = q;
+    p->radius = radius;
+    p->mode = q.guide_channels == 0 ? 0 : (q.guide_channels == 1 && q.channels == 3 ? 2 : 1);
+    auto bail = [&](blfls_status st) {
+        free_plan(p);
+        return st;
+    };
+    if (cudaSetDevice(q.device) != cudaSuccess) return bail(fail(BLFLS_ECUDA, "cudaSetDevice failed"));
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, q.device);
+    if (prop.major < 10)
+        return bail(fail(BLFLS_ECUDA, std::string("device is not sm_100-class: ") + prop.name));
+    p->nsm = prop.multiProcessorCount;
+
+    const int H = q.height, W = q.width, C = q.channels;
+    p->odd = (W % 2) != 0;
+    p->wc = W / 2 + 1;
+    p->spitch = ((p->wc + 15) / 16) * 16;
+    const int nrow = p->odd ? W : W / 2;
+    std::vector<int> rrad, crad;
+    // rows: V*n <= 2048 elements per CTA, 8 values per thread
+    int vrow = 1;
+    while (vrow * 2 * nrow <= 2048 && vrow < 16) vrow *= 2;
+    if (!plan_fft(nrow, vrow, 8, p->rowf, rrad))
+        return bail(fail(BLFLS_EUNSUPPORTED, "FFT: width " + std::to_string(W) +
+                                                 " has a prime factor above 13 or too large"));
+    if (!plan_fft(H, 16, 16, p->colf, crad))
+        return bail(fail(BLFLS_EUNSUPPORTED, "FFT: height " + std::to_string(H) +
+                                                 " has a prime factor above 13 or too large"));
+
+    // tables (double -> float)
+    {
+        auto tr = twiddles(nrow);
+        auto tc = twiddles(H);
+        std::vector<float> gx(p->wc), gy(H);
+        std::vector<float2> post(p->wc);
+        for (int v = 0; v < p->wc; ++v) {
+            const double sx = std::sin(M_PI * v / W);
+            gx[v] = (float)(4.0 * sx * sx);
+            const double a = -2.0 * M_PI * v / W;
+            post[v] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        for (int u = 0; u < H; ++u) {
+            const double sy = std::sin(M_PI * u / H);
+            gy[u] = (float)(4.0 * sy * sy);
+        }
+        if (cudaMalloc(&p->rowf.tw, sizeof(float2) * nrow) != cudaSuccess ||
+            cudaMalloc(&p->colf.tw, sizeof(float2) * H) != cudaSuccess ||
+            cudaMalloc(&p->gain_x, sizeof(float) * p->wc) != cudaSuccess ||
+            cudaMalloc(&p->gain_y, sizeof(float) * H) != cudaSuccess ||
+            cudaMalloc(&p->post, sizeof(float2) * p->wc) != cudaSuccess)
+            return bail(fail(BLFLS_ENOMEM, "plan: table allocation failed"));
+        cudaMemcpy(p->rowf.tw, tr.data(), sizeof(float2) * nrow, cudaMemcpyHostToDevice);
+        cudaMemcpy(p->colf.tw, tc.data(), sizeof(float2) * H, cudaMemcpyHostToDevice);
+        cudaMemcpy(p->gain_x, gx.data(), sizeof(float) * p->wc, cudaMemcpyHostToDevice);
+        cudaMemcpy(p->gain_y, gy.data(), sizeof(float) * H, cudaMemcpyHostToDevice);
+        cudaMemcpy(p->post, post.data(), sizeof(float2) * p->wc, cudaMemcpyHostToDevice);
+        auto fill = [](DevFft& f, int n, const std::vector<int>& rad) {
+            f.desc.n = n;
+            f.desc.nstages = (int)rad.size();
+            for (size_t i = 0; i < rad.size(); ++i) f.desc.radix[i] = rad[i];
+            f.desc.tw = f.tw;
+        };
+        fill(p->rowf, nrow, rrad);
+        fill(p->colf, H, crad);
+    }
+
+    // BLF constants
+    {
+        BlfParams& b = p->blf;
+        b.H = H;
+        b.W = W;
+        b.C = C;
+        b.GC = q.guide_channels;
+        b.radius = radius;
+        b.range_coef = (float)std::sqrt(1.4426950408889634 / (8.0 * q.sigma_r * q.sigma_r));
+        for (int d = 0; d <= kMaxRadius; ++d) {
+            const double c = -(double)d * d / (2.0 * q.sigma_s * q.sigma_s) * 1.4426950408889634;
+            b.cs[d] = (float)c;
+            b.wrow[d] = (float)std::exp2(c);
+        }
+        // shared-memory envelope of the generic kernel
+        const int narr = p->mode == 0 ? 2 : (p->mode == 1 ? 4 : 8);
+        const size_t smem = (size_t)narr * (16 + 2 * radius) * (((64 + 2 * radius) + 3) & ~3) * 4;
+        if (smem > 227 * 1024)
+            return bail(fail(BLFLS_EUNSUPPORTED, "plan: radius too large for the shared-memory tile"));
+    }
+
+    // workspace
+    p->plane = (size_t)H * W;
+    p->img_elems = (size_t)q.max_batch * C * p->plane;
+    const size_t spec_elems = (size_t)q.max_batch * C * H * p->spitch;
+    if (cudaMalloc(&p->buf[0], sizeof(float) * p->img_elems) != cudaSuccess ||
+        cudaMalloc(&p->buf[1], sizeof(float) * p->img_elems) != cudaSuccess ||
+        cudaMalloc(&p->tx, sizeof(float) * p->img_elems) != cudaSuccess ||
+        cudaMalloc(&p->ty, sizeof(float) * p->img_elems) != cudaSuccess ||
+        cudaMalloc(&p->spec, sizeof(float2) * spec_elems) != cudaSuccess ||
+        cudaMalloc(&p->lohi, sizeof(uint32_t) * 4 * q.max_batch) != cudaSuccess ||
+        cudaMalloc(&p->glohi, sizeof(uint32_t) * 2 * q.max_batch) != cudaSuccess ||
+        cudaMalloc(&p->nonfinite, sizeof(unsigned)) != cudaSuccess)
+        return bail(fail(BLFLS_ENOMEM, "plan: workspace allocation failed"));
+    if (cudaStreamCreateWithFlags(&p->ps, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(BLFLS_ECUDA, "plan: stream creation failed"));
+    p->stats.radius = radius;
+    *out = p;
+    return BLFLS_OK;
+}
+
+blfls_status blfls_plan_destroy(blfls_plan_t p)
+{
+    free_plan(p);
+    return BLFLS_OK;
+}
+
+blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int batch, int iters,
+                       float* out, void* stream, unsigned flags)
+{
+    blfls_status r = validate_batch(p, batch);
+    if (r) return r;
+    if (iters < 1) return fail(BLFLS_EINVAL, "blf_ls: iters must be >= 1");
+    if (!img || !out) return fail(BLFLS_EINVAL, "blf_ls: null image/output");
+    if ((p->prm.guide_channels == 0) != (guide == nullptr))
+        return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
+    if ((r = set_device(p))) return r;
+    cudaStream_t us = (cudaStream_t)stream;
+    const size_t n = (size_t)batch * p->prm.channels * p->plane;
+    const size_t ng = guide ? (size_t)batch * p->prm.guide_channels * p->plane : 0;
+    const bool host = flags & BLFLS_HOST_PTRS;
+    if ((r = fork_in(p, us))) return r;
+    cudaStream_t st = p->ps;
+    const float* din = img;
+    const float* dguide = guide;
+    float* dout = out;
+    if (host) {
+        if (!p->in_dev) CK(cudaMalloc(&p->in_dev, sizeof(float) * p->img_elems));
+        if (!p->out_dev) CK(cudaMalloc(&p->out_dev, sizeof(float) * p->img_elems));
+        CK(cudaMemcpyAsync(p->in_dev, img, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        din = p->in_dev;
+        dout = p->out_dev;
+        if (guide) {
+            if (!p->guide_dev)
+                CK(cudaMalloc(&p->guide_dev,
+                              sizeof(float) * p->prm.max_batch * p->prm.guide_channels * p->plane));
+            CK(cudaMemcpyAsync(p->guide_dev, guide, sizeof(float) * ng, cudaMemcpyHostToDevice, st));
+            dguide = p->guide_dev;
+        }
+    }
+    if (flags & BLFLS_CHECK_FINITE) {
+        if ((r = check_finite(p, din, n, st, "smooth"))) return r;
+        if (dguide && (r = check_finite(p, dguide, ng, st, "normalize_to_unit"))) return r;
+    }
+    p->launches = 0;
+    p->stats.blf_launches = 0;
+    p->time_stages = (flags & BLFLS_TIME_STAGES) != 0;
+    const bool use_graph = !(flags & (BLFLS_NO_GRAPH | BLFLS_TIME_STAGES));
+    if (use_graph) {
+        if (!(p->gexec && p->g_in == din && p->g_guide == dguide && p->g_out == dout &&
+              p->g_batch == batch && p->g_iters == iters)) {
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            r = enq_run(p, din, dguide, dout, batch, iters, st);
+            cudaError_t ce = cudaStreamEndCapture(st, &g);
+            if (r) return r;
+            if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+            if (p->gexec) {
+                cudaGraphExecDestroy(p->gexec);
+                p->gexec = nullptr;
+            }
+            ce = cudaGraphInstantiate(&p->gexec, g, 0);
+            cudaGraphDestroy(g);
+            if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+            p->g_in = din;
+            p->g_guide = dguide;
+            p->g_out = dout;
+            p->g_batch = batch;
+            p->g_iters = iters;
+            p->stats.kernel_launches = p->launches;
+        }
+        CK(cudaGraphLaunch(p->gexec, st));
+    } else {
+        r = enq_run(p, din, dguide, dout, batch, iters, st);
+        p->time_stages = false;
+        if (r) return r;
+        p->stats.kernel_launches = p->launches;
+    }
+    if (host) CK(cudaMemcpyAsync(out, dout, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    const int G = p->mode == 2 ? 1 : p->prm.channels;
+    const double taps = (double)(2 * p->radius + 1) * (2 * p->radius + 1);
+    p->stats.exps = taps * (double)p->plane * 2.0 * batch * G * iters;
+    p->stats.blf_launches = iters;
+    return join_out(p, us, flags | (host ? BLFLS_SYNC : 0));
+}
+
+blfls_status blfls_filter_gradients(blfls_plan_t p, const float* img, const float* guide, int batch,
+                                    float* tx, float* ty, void* stream, unsigned flags)
+{
+    blfls_status r = validate_batch(p, batch);
+    if (r) return r;
+    if ((p->prm.guide_channels == 0) != (guide == nullptr))
+        return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
+    if ((r = set_device(p))) return r;
+    cudaStream_t us = (cudaStream_t)stream;
+    if ((r = fork_in(p, us))) return r;
+    cudaStream_t st = p->ps;
+    const size_t n = (size_t)batch * p->prm.channels * p->plane;
+    const size_t ng = guide ? (size_t)batch * p->prm.guide_channels * p->plane : 0;
+    const bool host = flags & BLFLS_HOST_PTRS;
+    const float* din = img;
+    const float* dguide = guide;
+    float* dtx = tx;
+    float* dty = ty;
+    if (host) {
+        CK(cudaMemcpyAsync(p->buf[0], img, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        din = p->buf[0];
+        if (guide) {
+            if (!p->guide_dev)
+                CK(cudaMalloc(&p->guide_dev,
+                              sizeof(float) * p->prm.max_batch * p->prm.guide_channels * p->plane));
+            CK(cudaMemcpyAsync(p->guide_dev, guide, sizeof(float) * ng, cudaMemcpyHostToDevice, st));
+            dguide = p->guide_dev;
+        }
+        dtx = p->tx;
+        dty = p->ty;
+    }
+    if (flags & BLFLS_CHECK_FINITE) {
+        if ((r = check_finite(p, din, n, st, "smooth"))) return r;
+        if (dguide && (r = check_finite(p, dguide, ng, st, "normalize_to_unit"))) return r;
+    }
+    if (dguide && (r = enq_minmax(p, dguide, (size_t)p->prm.guide_channels * p->plane, batch, p->glohi, st)))
+        return r;
+    if ((r = enq_minmax(p, din, (size_t)p->prm.channels * p->plane, batch, p->lohi, st))) return r;
+    if ((r = enq_blf(p, din, dguide, p->lohi, dtx, dty, batch, 0, p->prm.height, p->prm.height, 1, st)))
+        return r;
+    if (host) {
+        CK(cudaMemcpyAsync(tx, dtx, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ty, dty, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    }
+    return join_out(p, us, flags | (host ? BLFLS_SYNC : 0));
+}
+
+blfls_status blfls_filter_gradients_rows(blfls_plan_t p, const float* img, const float* guide, int y0,
+                                         int y1, float* tx, float* ty, void* stream, unsigned flags)
+{
+    blfls_status r = validate_batch(p, 1);
+    if (r) return r;
+    if (y0 < 0 || y1 > p->prm.height || y0 >= y1) return fail(BLFLS_EINVAL, "rows: bad row range");
+    if ((p->prm.guide_channels == 0) != (guide == nullptr))
+        return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
+    if (flags & BLFLS_HOST_PTRS) return fail(BLFLS_EINVAL, "rows: device pointers only");
+    if ((r = set_device(p))) return r;
+    cudaStream_t us = (cudaStream_t)stream;
+    if ((r = fork_in(p, us))) return r;
+    cudaStream_t st = p->ps;
+    if (guide && (r = enq_minmax(p, guide, (size_t)p->prm.guide_channels * p->plane, 1, p->glohi, st)))
+        return r;
+    if ((r = enq_minmax(p, img, (size_t)p->prm.channels * p->plane, 1, p->lohi, st))) return r;
+    if ((r = enq_blf(p, img, guide, p->lohi, tx, ty, 1, y0, y1, y1 - y0, 0, st))) return r;
+    return join_out(p, us, flags);
+}
+
+blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const float* ty, int batch,
+                         float* u, void* stream, unsigned flags)
+{
+    blfls_status r = validate_batch(p, batch);
+    if (r) return r;
+    if ((tx == nullptr) != (ty == nullptr))
+        return fail(BLFLS_EINVAL, "lsgrad_solve_fft: target shape does not match image");
+    if ((r = set_device(p))) return r;
+    cudaStream_t us = (cudaStream_t)stream;
+    if ((r = fork_in(p, us))) return r;
+    cudaStream_t st = p->ps;
+    const size_t n = (size_t)batch * p->prm.channels * p->plane;
+    const bool host = flags & BLFLS_HOST_PTRS;
+    const float* dg = g;
+    const float* dtx = tx;
+    const float* dty = ty;
+    float* du = u;
+    if (host) {
+        CK(cudaMemcpyAsync(p->buf[0], g, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        dg = p->buf[0];
+        if (tx) {
+            CK(cudaMemcpyAsync(p->tx, tx, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(p->ty, ty, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            dtx = p->tx;
+            dty = p->ty;
+        }
+        du = p->buf[1];
+    }
+    if (flags & BLFLS_CHECK_FINITE) {
+        if ((r = check_finite(p, dg, n, st, "lsgrad_solve_fft"))) return r;
+        if (dtx && (r = check_finite(p, dtx, n, st, "lsgrad_solve_fft"))) return r;
+        if (dty && (r = check_finite(p, dty, n, st, "lsgrad_solve_fft"))) return r;
+    }
+    if ((r = enq_solve(p, dg, dtx, dty, du, nullptr, batch, st))) return r;
+    if (host) CK(cudaMemcpyAsync(u, du, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    return join_out(p, us, flags | (host ? BLFLS_SYNC : 0));
+}
+
+static blfls_status fft_entry(blfls_plan_t p, const float* in, int batch, float* outp, void* stream,
+                              unsigned flags, bool forward)
+{
+    blfls_status r = validate_batch(p, batch);
+    if (r) return r;
+    if ((r = set_device(p))) return r;
+    cudaStream_t us = (cudaStream_t)stream;
+    if ((r = fork_in(p, us))) return r;
+    cudaStream_t st = p->ps;
+    const int planes = batch * p->prm.channels;
+    const size_t nreal = (size_t)planes * p->plane;
+    const size_t nspec = (size_t)planes * p->prm.height * p->wc;  // packed, caller layout
+    const bool host = flags & BLFLS_HOST_PTRS;
+    SolveParams s = solve_params(p);
+    // caller spectra are packed (pitch wc); the plan spectrum has pitch spitch
+    if (forward) {
+        const float* din = in;
+        if (host) {
+            CK(cudaMemcpyAsync(p->buf[0], in, sizeof(float) * nreal, cudaMemcpyHostToDevice, st));
+            din = p->buf[0];
+        }
+        s.f = din;
+        s.mode = 1;
+        CK(launch_row_r2c(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+        CK(launch_col(s, p->colf.desc, p->colf.V, p->colf.threads, planes, st));
+        CK(cudaMemcpy2DAsync(outp, sizeof(float2) * p->wc, p->spec, sizeof(float2) * p->spitch,
+                             sizeof(float2) * p->wc, (size_t)planes * p->prm.height,
+                             host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
+    } else {
+        CK(cudaMemcpy2DAsync(p->spec, sizeof(float2) * p->spitch, in, sizeof(float2) * p->wc,
+                             sizeof(float2) * p->wc, (size_t)planes * p->prm.height,
+                             host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+        float* dout = host ? p->buf[1] : outp;
+        s.out = dout;
+        s.mode = 2;
+        CK(launch_col(s, p->colf.desc, p->colf.V, p->colf.threads, planes, st));
+        CK(launch_row_c2r(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+        if (host) CK(cudaMemcpyAsync(outp, dout, sizeof(float) * nreal, cudaMemcpyDeviceToHost, st));
+    }
+    (void)nspec;
+    return join_out(p, us, flags | (host ? BLFLS_SYNC : 0));
+}
+
+blfls_status blfls_rfft2(blfls_plan_t p, const float* x, int batch, float* spec, void* stream,
+                         unsigned flags)
+{
+    return fft_entry(p, x, batch, spec, stream, flags, true);
+}
+
+blfls_status blfls_irfft2(blfls_plan_t p, const float* spec, int batch, float* out, void* stream,
+                          unsigned flags)
+{
+    return fft_entry(p, spec, batch, out, stream, flags, false);
+}
+
+blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t* seeds, int n_sites,
+                            double noise_sigma, double p_sp, float* out, void* stream, int device)
+{
+    if (height < 1 || width < 1 || n_planes < 1 || n_sites < 1 || n_sites > 1024 || !seeds || !out)
+        return fail(BLFLS_EINVAL, "generate: bad arguments");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t* dseeds = nullptr;
+    CK(cudaMallocAsync(&dseeds, sizeof(uint64_t) * n_planes, st));
+    CK(cudaMemcpyAsync(dseeds, seeds, sizeof(uint64_t) * n_planes, cudaMemcpyHostToDevice, st));
+    CK(launch_generate(height, width, n_planes, dseeds, n_sites, noise_sigma, p_sp, out, st));
+    CK(cudaFreeAsync(dseeds, st));
+    CK(cudaStreamSynchronize(st));
+    return BLFLS_OK;
+}
+
+blfls_status blfls_last_stats(blfls_plan_t p, blfls_stats* s)
+{
+    if (!p || !s) return fail(BLFLS_EINVAL, "null argument");
+    *s = p->stats;
+    return BLFLS_OK;
+}
+
+blfls_status blfls_stage_times(blfls_plan_t p, double* ms_sum5, long long* launches5)
+{
+    if (!p || !ms_sum5) return fail(BLFLS_EINVAL, "null argument");
+    blfls_status r;
+    if ((r = set_device(p))) return r;
+    for (int i = 0; i < 5; ++i) {
+        ms_sum5[i] = 0.0;
+        if (launches5) launches5[i] = 0;
+    }
+    for (auto& e : p->timing) {
+        CK(cudaEventSynchronize(e.b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e.a, e.b));
+        ms_sum5[e.stage] += ms;
+        if (launches5) launches5[e.stage]++;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    p->timing.clear();
+    return BLFLS_OK;
+}
+
+blfls_status blfls_mufu_peak(int device, double* ex2_per_second, double* sm_clock_hz)
+{
+    if (!ex2_per_second) return fail(BLFLS_EINVAL, "null argument");
+    CK(cudaSetDevice(device));
+    double rate = 0.0, clk = 0.0;
+    cudaError_t e = measure_mufu(device, &rate, &clk);
+    if (e != cudaSuccess) return cuda_fail(e, "measure_mufu");
+    *ex2_per_second = rate;
+    if (sm_clock_hz) *sm_clock_hz = clk;
+    return BLFLS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,386 @@
+// k_blf.cu -- fused circular-gradient + brute-force (joint) bilateral filter.
+//
+// Replaces, per smooth() iteration, forward_gradients (image.cpp:72-95),
+// to_unit_range / from_unit_range_into (pipelines.cpp:17-31), the per-axis,
+// per-channel loop of filter_gradients (pipelines.cpp:33-53) and the
+// brute-force filter itself (bilateral.cpp:28-77, with an explicit radius in
+// place of ceil(3 sigma_s) at bilateral.cpp:37).
+//
+// Algebra ("Fold"): the [0,1] remap halves gradient
+// differences, and the image normalisation divides them by (hi - lo), so the
+// reference's range weight exp(-d^2 / (2 sr^2)) on remapped normalised
+// gradients equals exp2(-(s * dg)^2) on RAW gradient differences dg with
+// s = sqrt(log2(e) / (8 sr^2)) / (hi - lo).  The spatial weight is
+// exp2(cs[|dx|] + cs[|dy|]).  The window is clipped at the image border
+// (bilateral.cpp:56-57) while the gradients wrap (image.cpp:82,88): halo
+// cells outside the image carry a huge guide value so their weight is
+// exactly 0, never a zero-filled sample.
+//
+// Tiling: a 256-thread CTA owns a TH x TW = 16 x (16*P) output tile; each
+// thread owns P horizontally adjacent outputs of one row and slides a
+// register window along the (2R+1)-tap row, so one shared-memory vector load
+// feeds P outputs.  Per tap: FADD, FFMA (exponent with the spatial term as a
+// constant-bank operand), MUFU.EX2, FADD, FFMA -- the SFU pipe (16 ex2 per
+// clock per SM) is the roofline.
+#include "blfls_internal.cuh"
+
+namespace blfls {
+
+constexpr float kSentinel = 1.0e15f;
+
+__device__ __forceinline__ float fast_ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void decode_range(const uint32_t* lohi, int b, float coef, float& s,
+                                             float& range)
+{
+    const float lo = ordered_to_float(lohi[2 * b]);
+    const float hi = ordered_to_float(lohi[2 * b + 1]);
+    range = hi - lo;
+    // constant image: every gradient is exactly 0 and any finite scale works
+    s = range > 0.f ? coef / range : coef;
+}
+
+// MODE 0: self-guided (guide = the filtered gradient itself), one channel per CTA
+// MODE 1: joint, guide channel == image channel (or C == GC == 1)
+// MODE 2: joint, one grayscale guide shared by NC = 3 image channels: one
+//         exponential per tap serves all three channels.
+template <int R, int P, int MODE>
+__global__ void __launch_bounds__(256) k_grad_blf(const BlfParams p)
+{
+    constexpr int TW = 16 * P;
+    constexpr int TH = 16;
+    constexpr int NC = MODE == 2 ? 3 : 1;
+    constexpr int ROWS = TH + 2 * R;
+    constexpr int COLS = TW + 2 * R;
+    constexpr int PITCH = (COLS + 3) & ~3;
+    constexpr int VN = 2 * R + P;                 // register window per row
+    constexpr int VEC = P % 4 == 0 ? 4 : 2;       // shared-memory vector width
+    constexpr int NV = (VN + VEC - 1) / VEC;
+    constexpr int NS = MODE == 0 ? 0 : NC;        // separate source arrays per axis
+
+    extern __shared__ __align__(16) float sm[];
+    float* G = sm;                                 // [2][ROWS][PITCH] guide (scaled)
+    float* S = sm + 2 * ROWS * PITCH;              // [2][NS][ROWS][PITCH] raw gradients
+
+    const int H = p.H, W = p.W, C = p.C;
+    const int b = MODE == 2 ? blockIdx.z : blockIdx.z / C;
+    const int c0 = MODE == 2 ? 0 : blockIdx.z % C;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+
+    float s, range;
+    decode_range(p.lohi, b, p.range_coef, s, range);
+    float sg = s, grange = range;
+    if (MODE != 0) decode_range(p.glohi, b, p.range_coef, sg, grange);
+
+    // ---- prologue: circular gradients of the tile + R halo into shared memory
+    const float* fimg = p.f + ((size_t)b * C + c0) * plane;
+    const float* gimg = nullptr;
+    if (MODE == 1) gimg = p.guide + ((size_t)b * p.GC + (p.GC == 1 ? 0 : c0)) * plane;
+    if (MODE == 2) gimg = p.guide + (size_t)b * p.GC * plane;
+    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += 256) {
+        const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
+        const int y = ty0 - R + i, x = tx0 - R + j;
+        const bool in = y >= 0 && y < H && x >= 0 && x < W;
+        const int o = i * PITCH + j;
+        if (in) {
+            const int xn = x + 1 == W ? 0 : x + 1;
+            const int yn = y + 1 == H ? 0 : y + 1;
+            const size_t r0 = (size_t)y * W, r1 = (size_t)yn * W;
+            if (MODE == 0) {
+                const float v = __ldg(fimg + r0 + x);
+                G[o] = (__ldg(fimg + r0 + xn) - v) * s;
+                G[ROWS * PITCH + o] = (__ldg(fimg + r1 + x) - v) * s;
+            } else {
+                const float gv = __ldg(gimg + r0 + x);
+                G[o] = (__ldg(gimg + r0 + xn) - gv) * sg;
+                G[ROWS * PITCH + o] = (__ldg(gimg + r1 + x) - gv) * sg;
+#pragma unroll
+                for (int c = 0; c < NS; ++c) {
+                    const float* fc = fimg + (size_t)c * plane;
+                    const float v = __ldg(fc + r0 + x);
+                    S[(0 * NS + c) * ROWS * PITCH + o] = __ldg(fc + r0 + xn) - v;
+                    S[(1 * NS + c) * ROWS * PITCH + o] = __ldg(fc + r1 + x) - v;
+                }
+            }
+        } else {
+            G[o] = kSentinel;
+            G[ROWS * PITCH + o] = kSentinel;
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+                S[(0 * NS + c) * ROWS * PITCH + o] = 0.f;
+                S[(1 * NS + c) * ROWS * PITCH + o] = 0.f;
+            }
+        }
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int oy = ty0 + ty;
+    const int ox = tx0 + tx * P;
+
+    // output scale: MODE 0 accumulates scaled gradients (s * g)
+    float oscale;
+    if (MODE == 0)
+        oscale = p.normalized_out ? 1.f / p.range_coef : 1.f / s;
+    else
+        oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
+
+#pragma unroll 1
+    for (int axis = 0; axis < 2; ++axis) {
+        const float* Ga = G + axis * ROWS * PITCH;
+        const float* Sa = S + axis * NS * ROWS * PITCH;
+        float gs[P], z[P], num[NC][P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            gs[q] = Ga[(ty + R) * PITCH + tx * P + q + R];
+            z[q] = 0.f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) num[c][q] = 0.f;
+        }
+#pragma unroll 1
+        for (int dy = -R; dy <= R; ++dy) {
+            const int row = (ty + R + dy) * PITCH + tx * P;
+            float gv[NV * VEC];
+            float sv[NS == 0 ? 1 : NS][NV * VEC];
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                if (VEC == 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(Ga + row + 4 * k);
+                    gv[4 * k] = t.x; gv[4 * k + 1] = t.y; gv[4 * k + 2] = t.z; gv[4 * k + 3] = t.w;
+                } else {
+                    const float2 t = *reinterpret_cast<const float2*>(Ga + row + 2 * k);
+                    gv[2 * k] = t.x; gv[2 * k + 1] = t.y;
+                }
+#pragma unroll
+                for (int c = 0; c < NS; ++c) {
+                    const float* Sc = Sa + c * ROWS * PITCH;
+                    if (VEC == 4) {
+                        const float4 t = *reinterpret_cast<const float4*>(Sc + row + 4 * k);
+                        sv[c][4 * k] = t.x; sv[c][4 * k + 1] = t.y; sv[c][4 * k + 2] = t.z; sv[c][4 * k + 3] = t.w;
+                    } else {
+                        const float2 t = *reinterpret_cast<const float2*>(Sc + row + 2 * k);
+                        sv[c][2 * k] = t.x; sv[c][2 * k + 1] = t.y;
+                    }
+                }
+            }
+            float zr[P], nr[NC][P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                zr[q] = 0.f;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) nr[c][q] = 0.f;
+            }
+#pragma unroll
+            for (int dx = -R; dx <= R; ++dx) {
+                const float cx = p.cs[dx < 0 ? -dx : dx];
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const float v = gv[q + dx + R];
+                    const float d = gs[q] - v;
+                    const float w = fast_ex2(fmaf(-d, d, cx));
+                    zr[q] += w;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        nr[c][q] = fmaf(w, MODE == 0 ? v : sv[c][q + dx + R], nr[c][q]);
+                }
+            }
+            const float wy = p.wrow[dy < 0 ? -dy : dy];
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                z[q] = fmaf(zr[q], wy, z[q]);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) num[c][q] = fmaf(nr[c][q], wy, num[c][q]);
+            }
+        }
+        // ---- epilogue
+        if (oy < p.y1) {
+            float* dst = axis == 0 ? p.tx : p.ty;
+            const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float* o = dst + ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow;
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (ox + q < W) o[ox + q] = num[c][q] / z[q] * oscale;
+            }
+        }
+    }
+}
+
+// Generic-radius variant (any R up to kMaxRadius): same tiling, window loops
+// not unrolled, taps read straight from shared memory.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_grad_blf_any(const BlfParams p)
+{
+    constexpr int P = 4, TW = 64, TH = 16;
+    constexpr int NC = MODE == 2 ? 3 : 1;
+    constexpr int NS = MODE == 0 ? 0 : NC;
+    const int R = p.radius;
+    const int ROWS = TH + 2 * R, COLS = TW + 2 * R, PITCH = (COLS + 3) & ~3;
+    extern __shared__ __align__(16) float sm[];
+    float* G = sm;
+    float* S = sm + 2 * ROWS * PITCH;
+    const int H = p.H, W = p.W, C = p.C;
+    const int b = MODE == 2 ? blockIdx.z : blockIdx.z / C;
+    const int c0 = MODE == 2 ? 0 : blockIdx.z % C;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range;
+    decode_range(p.lohi, b, p.range_coef, s, range);
+    float sg = s, grange = range;
+    if (MODE != 0) decode_range(p.glohi, b, p.range_coef, sg, grange);
+    const float* fimg = p.f + ((size_t)b * C + c0) * plane;
+    const float* gimg = nullptr;
+    if (MODE == 1) gimg = p.guide + ((size_t)b * p.GC + (p.GC == 1 ? 0 : c0)) * plane;
+    if (MODE == 2) gimg = p.guide + (size_t)b * p.GC * plane;
+    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += 256) {
+        const int i = idx / COLS, j = idx % COLS;
+        const int y = ty0 - R + i, x = tx0 - R + j;
+        const bool in = y >= 0 && y < H && x >= 0 && x < W;
+        const int o = i * PITCH + j;
+        if (in) {
+            const int xn = x + 1 == W ? 0 : x + 1;
+            const int yn = y + 1 == H ? 0 : y + 1;
+            const size_t r0 = (size_t)y * W, r1 = (size_t)yn * W;
+            if (MODE == 0) {
+                const float v = fimg[r0 + x];
+                G[o] = (fimg[r0 + xn] - v) * s;
+                G[ROWS * PITCH + o] = (fimg[r1 + x] - v) * s;
+            } else {
+                const float gv = gimg[r0 + x];
+                G[o] = (gimg[r0 + xn] - gv) * sg;
+                G[ROWS * PITCH + o] = (gimg[r1 + x] - gv) * sg;
+                for (int c = 0; c < NS; ++c) {
+                    const float* fc = fimg + (size_t)c * plane;
+                    const float v = fc[r0 + x];
+                    S[(0 * NS + c) * ROWS * PITCH + o] = fc[r0 + xn] - v;
+                    S[(1 * NS + c) * ROWS * PITCH + o] = fc[r1 + x] - v;
+                }
+            }
+        } else {
+            G[o] = kSentinel;
+            G[ROWS * PITCH + o] = kSentinel;
+            for (int c = 0; c < NS; ++c) {
+                S[(0 * NS + c) * ROWS * PITCH + o] = 0.f;
+                S[(1 * NS + c) * ROWS * PITCH + o] = 0.f;
+            }
+        }
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int oy = ty0 + ty, ox = tx0 + tx * P;
+    float oscale;
+    if (MODE == 0)
+        oscale = p.normalized_out ? 1.f / p.range_coef : 1.f / s;
+    else
+        oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
+    for (int axis = 0; axis < 2; ++axis) {
+        const float* Ga = G + axis * ROWS * PITCH;
+        const float* Sa = S + axis * NS * ROWS * PITCH;
+        float z[P], num[NC][P], gs[P];
+        for (int q = 0; q < P; ++q) {
+            gs[q] = Ga[(ty + R) * PITCH + tx * P + q + R];
+            z[q] = 0.f;
+            for (int c = 0; c < NC; ++c) num[c][q] = 0.f;
+        }
+        for (int dy = -R; dy <= R; ++dy) {
+            const int row = (ty + R + dy) * PITCH + tx * P;
+            const float wy = p.wrow[dy < 0 ? -dy : dy];
+            for (int dx = -R; dx <= R; ++dx) {
+                const float cx = p.cs[dx < 0 ? -dx : dx];
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const float v = Ga[row + q + dx + R];
+                    const float d = gs[q] - v;
+                    const float w = fast_ex2(fmaf(-d, d, cx)) * wy;
+                    z[q] += w;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        num[c][q] = fmaf(w, MODE == 0 ? v : Sa[c * ROWS * PITCH + row + q + dx + R], num[c][q]);
+                }
+            }
+        }
+        if (oy < p.y1) {
+            float* dst = axis == 0 ? p.tx : p.ty;
+            const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
+            for (int c = 0; c < NC; ++c) {
+                float* o = dst + ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow;
+                for (int q = 0; q < P; ++q)
+                    if (ox + q < W) o[ox + q] = num[c][q] / z[q] * oscale;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- dispatch --
+
+template <int R, int P, int MODE>
+static cudaError_t launch_fixed(const BlfParams& p, int nz, cudaStream_t st)
+{
+    constexpr int TW = 16 * P, TH = 16;
+    constexpr int ROWS = TH + 2 * R, COLS = TW + 2 * R, PITCH = (COLS + 3) & ~3;
+    constexpr int NARR = MODE == 0 ? 2 : (MODE == 1 ? 4 : 8);
+    const size_t smem = (size_t)NARR * ROWS * PITCH * sizeof(float);
+    // not a stream operation: legal while the stream is being captured
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + TW - 1) / TW, (p.y1 - p.y0 + TH - 1) / TH, nz);
+    k_grad_blf<R, P, MODE><<<grid, 256, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_any(const BlfParams& p, int nz, cudaStream_t st)
+{
+    const int R = p.radius;
+    const int ROWS = 16 + 2 * R, COLS = 64 + 2 * R, PITCH = (COLS + 3) & ~3;
+    const int NARR = MODE == 0 ? 2 : (MODE == 1 ? 4 : 8);
+    const size_t smem = (size_t)NARR * ROWS * PITCH * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf_any<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + 63) / 64, (p.y1 - p.y0 + 15) / 16, nz);
+    k_grad_blf_any<MODE><<<grid, 256, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
+{
+    constexpr int P = MODE == 2 ? 2 : 4;
+    switch (p.radius) {
+        case 1: return launch_fixed<1, P, MODE>(p, nz, st);
+        case 2: return launch_fixed<2, P, MODE>(p, nz, st);
+        case 3: return launch_fixed<3, P, MODE>(p, nz, st);
+        case 4: return launch_fixed<4, P, MODE>(p, nz, st);
+        case 5: return launch_fixed<5, P, MODE>(p, nz, st);
+        case 6: return launch_fixed<6, P, MODE>(p, nz, st);
+        case 7: return launch_fixed<7, P, MODE>(p, nz, st);
+        case 8: return launch_fixed<8, P, MODE>(p, nz, st);
+        case 10: return launch_fixed<10, P, MODE>(p, nz, st);
+        case 12: return launch_fixed<12, P, MODE>(p, nz, st);
+        case 15: return launch_fixed<15, P, MODE>(p, nz, st);
+        default: return launch_any<MODE>(p, nz, st);
+    }
+}
+
+// mode: 0 self, 1 joint per-channel / single-channel, 2 joint shared gray guide (C == 3)
+cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st)
+{
+    switch (mode) {
+        case 0: return dispatch_mode<0>(p, batch * p.C, st);
+        case 1: return dispatch_mode<1>(p, batch * p.C, st);
+        default: return dispatch_mode<2>(p, batch, st);
+    }
+}
+
+}  // namespace blfls

@@ -1,0 +1,471 @@
+// k_solve.cu -- periodic least-squares solve (solver.cpp:88-124) as three
+// kernels over one half spectrum per plane:
+//
+//   row r2c  : r = f + lambda (Dx^T Tx + Dy^T Ty)   (divergence fold, exact:
+//              conj(otf) F(T) = F(D^T T); Dx^T t[x] = t[x-1] - t[x], circular)
+//              then the W-point real FFT of each row as a W/2-point complex
+//              Stockham FFT plus the even/odd split (post-twiddle exp(-2 pi i v/W))
+//   column   : H-point FFT of V adjacent spectrum columns, divide by
+//              H W (1 + lambda (4 sin^2(pi u/H) + 4 sin^2(pi v/W))), inverse FFT
+//              (solver.cpp:117-118 with the 1/(hw) of fft2d.cpp:49-51 folded in)
+//   row c2r  : inverse real FFT of each row, written as the next image; the
+//              epilogue reduces min/max for the next iteration's normalisation
+//              (image.cpp:46-60) with ordered-integer atomics.
+//
+// Spectrum layout: plane-major, H rows of `spitch` complex64 (W/2+1 used).
+#include "blfls_internal.cuh"
+#include "fft.cuh"
+
+namespace blfls {
+
+__device__ __forceinline__ float fold_value(const SolveParams& p, const float* f, const float* tx,
+                                            const float* ty, int y, int x)
+{
+    float v = f[(size_t)y * p.W + x];
+    if (tx != nullptr) {
+        const int xm = x == 0 ? p.W - 1 : x - 1;
+        const int ym = y == 0 ? p.H - 1 : y - 1;
+        const float dx = tx[(size_t)y * p.W + xm] - tx[(size_t)y * p.W + x];
+        const float dy = ty[(size_t)ym * p.W + x] - ty[(size_t)y * p.W + x];
+        v = fmaf(p.lambda, dx + dy, v);
+    }
+    return v;
+}
+
+// grid: (ceil(H / V), planes); V rows per CTA; n = W/2 (even W) or W (odd W)
+template <bool ODD>
+__global__ void k_row_r2c(const SolveParams p, const FftDesc d, int V)
+{
+    extern __shared__ __align__(16) float2 buf[];
+    const int n = d.n;
+    const int plane = blockIdx.y;
+    const int row0 = blockIdx.x * V;
+    const size_t poff = (size_t)plane * p.H * p.W;
+    const float* f = p.f + poff;
+    const float* tx = p.tx ? p.tx + poff : nullptr;
+    const float* ty = p.ty ? p.ty + poff : nullptr;
+    for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
+        const int v = idx / n, j = idx - (idx / n) * n;
+        const int y = row0 + v;
+        float2 z = make_float2(0.f, 0.f);
+        if (y < p.H) {
+            if (!ODD) {
+                z.x = fold_value(p, f, tx, ty, y, 2 * j);
+                z.y = fold_value(p, f, tx, ty, y, 2 * j + 1);
+            } else {
+                z.x = fold_value(p, f, tx, ty, y, j);
+            }
+        }
+        buf[idx] = z;
+    }
+    __syncthreads();
+    fft_run<false>(buf, d, V, false);
+    const int wc = p.wc;
+    for (int idx = threadIdx.x; idx < V * wc; idx += blockDim.x) {
+        const int v = idx / wc, k = idx - (idx / wc) * wc;
+        const int y = row0 + v;
+        if (y >= p.H) continue;
+        float2 X;
+        if (!ODD) {
+            const float2 zk = buf[v * n + (k == n ? 0 : k)];
+            const float2 zn = cconj(buf[v * n + (k == 0 ? 0 : n - k)]);
+            const float2 e = cscale(cadd(zk, zn), 0.5f);
+            const float2 o = cscale(cmuli(csub(zk, zn), -1.0f), 0.5f);  // (zk - zn) / (2i)
+            X = cadd(e, cmul(__ldg(&p.post[k]), o));
+        } else {
+            X = buf[v * n + k];
+        }
+        p.spec[((size_t)plane * p.H + y) * p.spitch + k] = X;
+    }
+}
+
+// grid: (ceil(wc / V), planes); V adjacent columns per CTA, layout buf[u*V + c]
+__global__ void k_col(const SolveParams p, const FftDesc d, int V)
+{
+    extern __shared__ __align__(16) float2 buf[];
+    const int H = p.H;
+    const int plane = blockIdx.y;
+    const int v0 = blockIdx.x * V;
+    float2* spec = p.spec + (size_t)plane * H * p.spitch;
+    for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
+        const int u = idx / V, c = idx - (idx / V) * V;
+        const int v = v0 + c;
+        buf[idx] = v < p.wc ? spec[(size_t)u * p.spitch + v] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    if (p.mode & 1) fft_run<true>(buf, d, V, false);
+    if (p.mode & 2) {
+        for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
+            const int u = idx / V, c = idx - (idx / V) * V;
+            const int v = v0 + c;
+            float sc = p.inv_hw;
+            if (p.mode == 3 && v < p.wc)
+                sc = p.inv_hw / fmaf(p.lambda, __ldg(&p.gain_y[u]) + __ldg(&p.gain_x[v]), 1.0f);
+            buf[idx] = cscale(buf[idx], sc);
+        }
+        __syncthreads();
+        fft_run<true>(buf, d, V, true);
+    }
+    for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
+        const int u = idx / V, c = idx - (idx / V) * V;
+        const int v = v0 + c;
+        if (v < p.wc) spec[(size_t)u * p.spitch + v] = buf[idx];
+    }
+}
+
+__device__ __forceinline__ void block_minmax_atomic(float lo, float hi, uint32_t* slot)
+{
+    __shared__ float slo[32], shi[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        slo[warp] = lo;
+        shi[warp] = hi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        lo = lane < nw ? slo[lane] : INFINITY;
+        hi = lane < nw ? shi[lane] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            atomicMin(slot, float_to_ordered(lo));
+            atomicMax(slot + 1, float_to_ordered(hi));
+        }
+    }
+}
+
+// grid: (ceil(H / V), planes)
+template <bool ODD>
+__global__ void k_row_c2r(const SolveParams p, const FftDesc d, int V)
+{
+    extern __shared__ __align__(16) float2 buf[];
+    const int n = d.n;
+    const int plane = blockIdx.y;
+    const int row0 = blockIdx.x * V;
+    const int W = p.W;
+    for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
+        const int v = idx / n, k = idx - (idx / n) * n;
+        const int y = row0 + v;
+        float2 Z = make_float2(0.f, 0.f);
+        if (y < p.H) {
+            const float2* srow = p.spec + ((size_t)plane * p.H + y) * p.spitch;
+            if (!ODD) {
+                float2 xk = srow[k];
+                float2 xn = srow[n - k];
+                if (k == 0) {  // c2r ignores Im of DC and Nyquist
+                    xk.y = 0.f;
+                    xn.y = 0.f;
+                }
+                const float2 xnc = cconj(xn);
+                const float2 a = cadd(xk, xnc);
+                const float2 bb = cmul(csub(xk, xnc), cconj(__ldg(&p.post[k])));
+                Z = cadd(a, cmuli(bb, 1.0f));
+            } else {
+                if (k <= (W - 1) / 2) {
+                    Z = srow[k];
+                    if (k == 0) Z.y = 0.f;
+                } else {
+                    Z = cconj(srow[W - k]);
+                }
+            }
+        }
+        buf[idx] = Z;
+    }
+    __syncthreads();
+    fft_run<false>(buf, d, V, true);
+    float lo = INFINITY, hi = -INFINITY;
+    float* out = p.out + (size_t)plane * p.H * W;
+    for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
+        const int v = idx / n, j = idx - (idx / n) * n;
+        const int y = row0 + v;
+        if (y >= p.H) continue;
+        const float2 z = buf[idx];
+        if (!ODD) {
+            *reinterpret_cast<float2*>(out + (size_t)y * W + 2 * j) = z;
+            lo = fminf(lo, fminf(z.x, z.y));
+            hi = fmaxf(hi, fmaxf(z.x, z.y));
+        } else {
+            out[(size_t)y * W + j] = z.x;
+            lo = fminf(lo, z.x);
+            hi = fmaxf(hi, z.x);
+        }
+    }
+    if (p.lohi_out != nullptr) block_minmax_atomic(lo, hi, p.lohi_out + 2 * (plane / p.C));
+}
+
+// ---------------------------------------------------------------- misc --
+
+// per-image min/max over all channels; grid (blocks, batch)
+__global__ void k_minmax(const float* __restrict__ x, size_t per_image, uint32_t* lohi)
+{
+    const float* xi = x + (size_t)blockIdx.y * per_image;
+    float lo = INFINITY, hi = -INFINITY;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((per_image & 3) == 0 && (reinterpret_cast<uintptr_t>(xi) & 15) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(xi);
+        for (size_t k = i; k < per_image / 4; k += stride) {
+            const float4 t = __ldg(x4 + k);
+            lo = fminf(lo, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
+            hi = fmaxf(hi, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
+        }
+    } else {
+        for (size_t k = i; k < per_image; k += stride) {
+            const float t = __ldg(xi + k);
+            lo = fminf(lo, t);
+            hi = fmaxf(hi, t);
+        }
+    }
+    block_minmax_atomic(lo, hi, lohi + 2 * blockIdx.y);
+}
+
+__global__ void k_reset_lohi(uint32_t* lohi, int n)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        lohi[2 * i] = 0xffffffffu;
+        lohi[2 * i + 1] = 0u;
+    }
+}
+
+// counts non-finite samples (require_finite, image.cpp:21-27)
+__global__ void k_count_nonfinite(const float* __restrict__ x, size_t n, unsigned* count)
+{
+    unsigned local = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        local += !isfinite(__ldg(x + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+// targets in normalised units -> raw: t * (hi - lo) (stage entry helper)
+__global__ void k_scale_by_range(float* x, size_t per_image, const uint32_t* lohi, int to_raw)
+{
+    const float lo = ordered_to_float(lohi[2 * blockIdx.y]);
+    const float hi = ordered_to_float(lohi[2 * blockIdx.y + 1]);
+    const float r = hi - lo;
+    const float sc = r > 0.f ? (to_raw ? r : 1.f / r) : (to_raw ? 0.f : 1.f);
+    float* xi = x + (size_t)blockIdx.y * per_image;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_image;
+         i += (size_t)gridDim.x * blockDim.x)
+        xi[i] *= sc;
+}
+
+// SplitMix64 draw j of the stream `seed` (testimage.cpp:11-21: state += gamma, mix)
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t j)
+{
+    uint64_t z = seed + (j + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform_at(uint64_t seed, uint64_t j)
+{
+    return (double)(splitmix_at(seed, j) >> 11) * 0x1.0p-53;
+}
+
+// BASELINE synthetic generator; grid (ceil(H*W/256), planes).  Draw
+// layout (the test checker restates it): sites at draws 3s..3s+2,
+// pixel i at 3K + 3i + {0, 1, 2}.
+__global__ void k_generate(int H, int W, const uint64_t* seeds, int K, double noise_sigma, double p_sp,
+                           float* out)
+{
+    extern __shared__ double site[];  // 3K doubles
+    const uint64_t seed = seeds[blockIdx.y];
+    for (int s = threadIdx.x; s < K; s += blockDim.x) {
+        site[3 * s] = uniform_at(seed, 3 * (uint64_t)s) * W;
+        site[3 * s + 1] = uniform_at(seed, 3 * (uint64_t)s + 1) * H;
+        site[3 * s + 2] = uniform_at(seed, 3 * (uint64_t)s + 2);
+    }
+    __syncthreads();
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)H * W) return;
+    const int y = (int)(i / W), x = (int)(i % W);
+    int best = 0;
+    double bd = 1e300;
+    for (int s = 0; s < K; ++s) {
+        const double dx = x - site[3 * s], dy = y - site[3 * s + 1];
+        const double dd = dx * dx + dy * dy;
+        if (dd < bd) {
+            bd = dd;
+            best = s;
+        }
+    }
+    const double rx = W > 1 ? 1.0 / (W - 1) : 0.0;
+    const double ry = H > 1 ? 1.0 / (H - 1) : 0.0;
+    double v = site[3 * best + 2] + 0.2 * ((x * rx + y * ry) * 0.5 - 0.5);
+    const uint64_t base = 3 * (uint64_t)K;
+    const double u1 = uniform_at(seed, base + 3 * i);
+    const double u2 = uniform_at(seed, base + 3 * i + 1);
+    v += noise_sigma * sqrt(-2.0 * log(1.0 - u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+    if (p_sp > 0.0) {
+        const double u3 = uniform_at(seed, base + 3 * i + 2);
+        if (u3 < 0.5 * p_sp)
+            v = 0.0;
+        else if (u3 < p_sp)
+            v = 1.0;
+    }
+    v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    out[(size_t)blockIdx.y * H * W + i] = (float)v;
+}
+
+// -------------------------------------------------------------- launchers --
+
+cudaError_t launch_row_r2c(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
+                           bool odd, cudaStream_t st)
+{
+    const size_t smem = (size_t)V * d.n * sizeof(float2);
+    dim3 grid((p.H + V - 1) / V, planes);
+    if (odd) {
+        cudaFuncSetAttribute(k_row_r2c<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_row_r2c<true><<<grid, threads, smem, st>>>(p, d, V);
+    } else {
+        cudaFuncSetAttribute(k_row_r2c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_row_r2c<false><<<grid, threads, smem, st>>>(p, d, V);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_col(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
+                       cudaStream_t st)
+{
+    const size_t smem = (size_t)V * d.n * sizeof(float2);
+    cudaFuncSetAttribute(k_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((p.wc + V - 1) / V, planes);
+    k_col<<<grid, threads, smem, st>>>(p, d, V);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_c2r(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
+                           bool odd, cudaStream_t st)
+{
+    const size_t smem = (size_t)V * d.n * sizeof(float2);
+    dim3 grid((p.H + V - 1) / V, planes);
+    if (odd) {
+        cudaFuncSetAttribute(k_row_c2r<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_row_c2r<true><<<grid, threads, smem, st>>>(p, d, V);
+    } else {
+        cudaFuncSetAttribute(k_row_c2r<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_row_c2r<false><<<grid, threads, smem, st>>>(p, d, V);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_minmax(const float* x, size_t per_image, int batch, uint32_t* lohi, int nsm,
+                          cudaStream_t st)
+{
+    k_reset_lohi<<<(batch + 127) / 128, 128, 0, st>>>(lohi, batch);
+    size_t blocks = (per_image / 4 + 255) / 256;
+    const size_t cap = (size_t)nsm * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    dim3 grid((unsigned)blocks, batch);
+    k_minmax<<<grid, 256, 0, st>>>(x, per_image, lohi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reset_lohi(uint32_t* lohi, int n, cudaStream_t st)
+{
+    k_reset_lohi<<<(n + 127) / 128, 128, 0, st>>>(lohi, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_nonfinite(const float* x, size_t n, unsigned* count, int nsm, cudaStream_t st)
+{
+    size_t blocks = (n + 255) / 256;
+    if (blocks > (size_t)nsm * 8) blocks = (size_t)nsm * 8;
+    if (blocks < 1) blocks = 1;
+    k_count_nonfinite<<<(unsigned)blocks, 256, 0, st>>>(x, n, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale_by_range(float* x, size_t per_image, int batch, const uint32_t* lohi,
+                                  int to_raw, cudaStream_t st)
+{
+    dim3 grid(256, batch);
+    k_scale_by_range<<<grid, 256, 0, st>>>(x, per_image, lohi, to_raw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int K, double sigma,
+                            double p_sp, float* out, cudaStream_t st)
+{
+    dim3 grid((unsigned)(((size_t)H * W + 255) / 256), planes);
+    k_generate<<<grid, 256, sizeof(double) * 3 * K, st>>>(H, W, seeds, K, sigma, p_sp, out);
+    return cudaGetLastError();
+}
+
+
+
+// ------------------------------------------------------ SFU peak probe --
+// 8 independent ex2 chains per thread: throughput-bound MUFU.EX2 loop.  Block
+// 0 thread 0 samples clock64/globaltimer to report the SM clock under load.
+__global__ void k_mufu_probe(int iters, float* sink, unsigned long long* clk)
+{
+    float y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) y[k] = 0.1f * (k + 1) + 1e-7f * threadIdx.x;
+    unsigned long long c0 = 0, t0 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c0 = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y[k]) : "f"(-y[k]));
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += y[k];
+    if (s == 12345.f) sink[threadIdx.x] = s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long c1 = clock64(), t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        clk[0] = c1 - c0;
+        clk[1] = t1 - t0;
+    }
+}
+
+cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz)
+{
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, device);
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+    float* sink = nullptr;
+    unsigned long long* clk = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&sink, 1024 * sizeof(float))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&clk, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_mufu_probe<<<blocks, threads>>>(iters, sink, clk);  // warm-up
+    cudaEventRecord(a);
+    for (int r = 0; r < 5; ++r) k_mufu_probe<<<blocks, threads>>>(iters, sink, clk);
+    cudaEventRecord(b);
+    e = cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    unsigned long long hc[2] = {0, 0};
+    cudaMemcpy(hc, clk, sizeof(hc), cudaMemcpyDeviceToHost);
+    *ex2_per_s = 5.0 * (double)blocks * threads * iters * 8 / (ms * 1e-3);
+    *clock_hz = hc[1] ? (double)hc[0] / ((double)hc[1] * 1e-9) : 0.0;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    cudaFree(clk);
+    return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+}  // namespace blfls

@@ -1,0 +1,27 @@
+"""Golden-vector cases (shared by make_golden.py and the tests).
+
+Inputs come from the reference's own seeded test-image generators
+(testimage.cpp: natural_scene, random_image) rounded to fp32, because the GPU
+path consumes fp32.  Outputs are the reference pipeline pieces run in double
+(oracle/_ref): smooth() with the unmodified brute-force blf_brute whenever
+radius == ceil(3 sigma_s), iterated `iters` times with the guide fixed.
+"""
+CASES = [
+    # name, (w, h, c), scene, seed, guide, (sigma_s, sigma_r, lambda, iters, radius)
+    dict(name="gray_40x32_self", w=40, h=32, c=1, scene="natural", seed=3, guide=None,
+         sigma_s=2.0, sigma_r=0.05, lam=200.0, iters=1, radius=6),
+    dict(name="gray_40x32_r3_it2", w=40, h=32, c=1, scene="natural", seed=9, guide=None,
+         sigma_s=2.0, sigma_r=0.1, lam=1000.0, iters=2, radius=3),
+    dict(name="rgb_24x20_self_it3", w=24, h=20, c=3, scene="natural", seed=8, guide=None,
+         sigma_s=1.5, sigma_r=0.1, lam=500.0, iters=3, radius=5),
+    dict(name="rgb_30x18_joint_rgb", w=30, h=18, c=3, scene="natural", seed=4, guide=("natural", 5, 3),
+         sigma_s=1.0, sigma_r=0.08, lam=300.0, iters=2, radius=3),
+    dict(name="rgb_32x24_joint_gray", w=32, h=24, c=3, scene="natural", seed=6, guide=("natural", 11, 1),
+         sigma_s=1.0, sigma_r=0.1, lam=1000.0, iters=3, radius=3),
+    dict(name="gray_15x13_odd", w=15, h=13, c=1, scene="random", seed=21, guide=None,
+         sigma_s=1.0, sigma_r=0.15, lam=7.0, iters=1, radius=3),
+    dict(name="gray_36x20_constant", w=36, h=20, c=1, scene="constant", seed=0, guide=None,
+         sigma_s=2.0, sigma_r=0.05, lam=1000.0, iters=2, radius=6),
+    dict(name="gray_48x40_wide_range", w=48, h=40, c=1, scene="natural", seed=3, guide=None,
+         sigma_s=2.0, sigma_r=1e6, lam=1e-9, iters=1, radius=6),
+]

@@ -1,0 +1,294 @@
+"""GPU parity: the sm_100a path, called through the C ABI (via the host
+mirror), against the CPU oracle on identical fp32 inputs.
+
+Tolerances (BASELINE north star): max-abs <= 1e-4 on [0,1] images for the
+full BLF-LS output; stage gates: filter_gradients targets <= 2e-5, the FFT
+solve <= 5e-6 (fp32 FFT round-off with double-derived twiddles).
+"""
+from __future__ import annotations
+
+import math
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE / "golden"))
+from cases import CASES  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL_OUT = 1e-4
+TOL_TARGET = 2e-5
+TOL_SOLVE = 5e-6
+
+
+def maxabs(a, b):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64))))
+
+
+# ------------------------------------------------------------ golden --
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_golden_vectors(gpu, case):
+    d = np.load(HERE / "golden" / f"{case['name']}.npz")
+    guide = d["guide"] if "guide" in d else None
+    out = gpu.blf_ls(d["img"], guide, lam=case["lam"], sigma_s=case["sigma_s"],
+                     sigma_r=case["sigma_r"], iters=case["iters"], radius=case["radius"])
+    assert out.shape == d["out"].shape
+    assert maxabs(out, d["out"]) <= TOL_OUT
+
+
+# ------------------------------------------------------ vs the oracle --
+
+def _img(oracle, c, h, w, seed, sites=12, sp=0.0):
+    return np.stack([oracle.gen_plane(seed * 10 + k, h, w, n_sites=sites, p_sp=sp)
+                     for k in range(c)])
+
+
+@pytest.mark.parametrize("c,h,w,r,ss,sr,lam,iters", [
+    (1, 64, 64, 5, 5.0, 0.05, 1000.0, 1),
+    (3, 48, 80, 7, 7.0, 0.1, 1000.0, 3),
+    (3, 54, 96, 5, 5.0, 0.05, 500.0, 3),        # 2*3^3 x 2^5*3 mixed radix
+    (1, 60, 50, 15, 12.0, 0.08, 2000.0, 2),     # large window, 5 | W
+    (1, 45, 75, 9, 3.0, 0.1, 100.0, 1),         # generic-radius kernel, odd H
+    (1, 33, 35, 4, 2.0, 0.07, 50.0, 2),         # odd W (complex row FFT)
+])
+def test_self_guided_vs_oracle(gpu, oracle, c, h, w, r, ss, sr, lam, iters):
+    img = _img(oracle, c, h, w, 7 + c + h)
+    ref = oracle.blf_ls(img.astype(np.float64), lam=lam, sigma_s=ss, sigma_r=sr, iters=iters,
+                        radius=r)
+    out = gpu.blf_ls(img, lam=lam, sigma_s=ss, sigma_r=sr, iters=iters, radius=r)
+    assert maxabs(out, ref) <= TOL_OUT
+
+
+@pytest.mark.parametrize("c,gc,r", [(3, 1, 7), (3, 3, 5), (1, 1, 6), (3, 1, 11)])
+def test_joint_vs_oracle(gpu, oracle, c, gc, r):
+    h, w = 40, 64
+    img = _img(oracle, c, h, w, 31)
+    guide = _img(oracle, gc, h, w, 77)
+    ref = oracle.blf_ls(img.astype(np.float64), guide.astype(np.float64), lam=1000.0, sigma_s=7.0,
+                        sigma_r=0.1, iters=3, radius=r)
+    out = gpu.blf_ls(img, guide, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=3, radius=r)
+    assert maxabs(out, ref) <= TOL_OUT
+
+
+def test_batch_matches_single(gpu, oracle):
+    imgs = np.stack([_img(oracle, 3, 32, 48, 100 + i) for i in range(4)])
+    guides = np.stack([_img(oracle, 1, 32, 48, 200 + i) for i in range(4)])
+    batched = gpu.blf_ls(imgs, guides, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+    for i in range(4):
+        single = gpu.blf_ls(imgs[i], guides[i], lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2,
+                            radius=7)
+        assert maxabs(batched[i], single) == 0.0
+        ref = oracle.blf_ls(imgs[i].astype(np.float64), guides[i].astype(np.float64), lam=1000.0,
+                            sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+        assert maxabs(batched[i], ref) <= TOL_OUT
+
+
+def test_filter_gradients_stage(gpu, oracle):
+    """Targets of one smooth() call vs the oracle's filter_gradients."""
+    img = _img(oracle, 3, 40, 56, 5)
+    tx, ty = gpu.filter_gradients(img, sigma_s=5.0, sigma_r=0.05, radius=5)
+    g = img.astype(np.float64)
+    gn, lo, hi = oracle.normalize_to_unit(g)
+    gx, gy = oracle.forward_gradients(gn)
+    for t, gr in ((tx, gx), (ty, gy)):
+        ref = np.stack([2.0 * oracle.blf_brute_r((gr[c:c + 1] + 1) / 2, (gr[c:c + 1] + 1) / 2,
+                                                 sigma_s=5.0, sigma_r=0.05, radius=5)[0] - 1.0
+                        for c in range(3)])
+        assert maxabs(t, ref) <= TOL_TARGET
+
+
+def test_solve_stage_vs_oracle_and_dense(gpu, oracle):
+    rng = np.random.default_rng(13)
+    for (h, w, lam) in [(16, 16, 7.0), (30, 18, 1000.0), (64, 80, 2000.0), (15, 10, 3.0)]:
+        g = rng.random((1, h, w)).astype(np.float32)
+        tx, ty = rng.uniform(-1, 1, (2, 1, h, w)).astype(np.float32)
+        u = gpu.lsgrad_solve_fft(g, (tx, ty), gpu.SolveParams(lam, 0))
+        ref = oracle.lsgrad_solve_fft(g, tx, ty, lam=lam)
+        assert maxabs(u, ref) <= TOL_SOLVE * max(1.0, lam / 100.0)
+        if h * w <= 1024:
+            assert maxabs(u, oracle.dense_solve(g, tx, ty, lam=lam)) <= TOL_SOLVE * max(1.0, lam / 100.0)
+
+
+def test_solve_fixed_point_and_identity(gpu, oracle):
+    """lsgrad(g, grad g) = g (test_solver.cpp:120-127); lambda 0 = identity (101-106)."""
+    rng = np.random.default_rng(55)
+    for lam in (32.0, 1024.0):
+        g = rng.random((1, 32, 32)).astype(np.float32)
+        gx, gy = oracle.forward_gradients(g.astype(np.float64))
+        u = gpu.lsgrad_solve_fft(g, (gx.astype(np.float32), gy.astype(np.float32)),
+                                 gpu.SolveParams(lam, 0))
+        assert maxabs(u, g) <= 1e-5
+    g = rng.random((3, 9, 13)).astype(np.float32)
+    assert maxabs(gpu.ls_solve_fft(g, gpu.SolveParams(0.0, 0)), g) <= 1e-6
+
+
+@pytest.mark.parametrize("h,w", [(32, 32), (54, 96), (13, 9), (30, 18), (120, 1920 // 8)])
+def test_rfft2_roundtrip_vs_numpy(gpu, h, w):
+    rng = np.random.default_rng(h * w)
+    x = rng.random((1, h, w)).astype(np.float32)
+    spec = gpu.rfft2(x)
+    ref = np.fft.rfft2(x[0].astype(np.float64))
+    scale = np.abs(ref).max()
+    assert np.abs(spec[0] - ref).max() <= 2e-6 * scale
+    back = gpu.irfft2(spec, w)
+    assert maxabs(back, x) <= 2e-6
+
+
+def test_generator_matches_oracle(gpu, oracle):
+    import torch
+    seeds = [2000, 2001, 3002]
+    t = gpu.generate(96, 128, seeds, n_sites=12, p_salt_pepper=0.05)
+    torch.cuda.synchronize()
+    for i, s in enumerate(seeds):
+        ref = oracle.gen_plane(s, 96, 128, n_sites=12, p_sp=0.05)
+        assert maxabs(t[i].cpu().numpy(), ref) <= 1e-6
+
+
+# ----------------------------------------------------------- edge cases --
+
+def test_constant_image_fixed_point(gpu):
+    # test_pipelines.cpp:33-38 and acceptance c8
+    g = np.full((3, 30, 40), 0.55, np.float32)
+    out = gpu.blf_ls(g, lam=1024.0, sigma_s=2.0, sigma_r=0.05, iters=3, radius=4)
+    assert maxabs(out, g) <= 1e-6
+
+
+def test_guidance_equal_input_matches_self(gpu, oracle):
+    # test_pipelines.cpp:49-56 (one smooth() call)
+    g = _img(oracle, 3, 32, 40, 4)
+    a = gpu.blf_ls(g, lam=1024.0, sigma_s=2.0, sigma_r=0.05, iters=1, radius=4)
+    b = gpu.blf_ls(g, g, lam=1024.0, sigma_s=2.0, sigma_r=0.05, iters=1, radius=4)
+    assert maxabs(a, b) <= 1e-6
+
+
+def test_fidelity_monotone_in_lambda(gpu, oracle):
+    # test_pipelines.cpp:58-69
+    g = _img(oracle, 1, 56, 56, 9)
+    prev = -1.0
+    for lam in (32.0, 128.0, 512.0, 1024.0):
+        d = float(np.mean((gpu.blf_ls(g, lam=lam, sigma_s=6.0, sigma_r=0.05, radius=6)
+                           .astype(np.float64) - g) ** 2))
+        assert d >= prev - 1e-9
+        prev = d
+
+
+def test_nonfinite_and_shape_errors(gpu):
+    g = np.full((1, 16, 16), 0.5, np.float32)
+    bad = g.copy()
+    bad[0, 2, 3] = np.nan
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_ls(bad, lam=1.0, sigma_s=1.0, sigma_r=0.1, radius=2)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_ls(g, np.full((1, 16, 17), 0.5, np.float32), lam=1.0, sigma_s=1.0, sigma_r=0.1)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_ls(g, lam=-1.0, sigma_s=1.0, sigma_r=0.1)
+    with pytest.raises(gpu.Unsupported):
+        gpu.blf_ls(np.zeros((1, 17, 16), np.float32), lam=1.0, sigma_s=1.0, sigma_r=0.1, radius=2)
+
+
+def test_minimum_size_and_ragged(gpu, oracle):
+    for (h, w) in [(2, 2), (3, 5), (7, 2)]:
+        g = np.random.default_rng(h + w).random((1, h, w)).astype(np.float32)
+        ref = oracle.blf_ls(g.astype(np.float64), lam=10.0, sigma_s=1.0, sigma_r=0.1, iters=1,
+                            radius=2)
+        out = gpu.blf_ls(g, lam=10.0, sigma_s=1.0, sigma_r=0.1, radius=2)
+        assert maxabs(out, ref) <= TOL_OUT
+
+
+def test_device_tensors_and_stream(gpu, oracle):
+    import torch
+    img = _img(oracle, 3, 64, 64, 12)
+    t = torch.from_numpy(img).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        out = gpu.blf_ls(t, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+    s.synchronize()
+    host = gpu.blf_ls(img, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+    assert maxabs(out.cpu().numpy(), host) == 0.0
+    # graph replay gives identical results to direct launches
+    again = gpu.blf_ls(t, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7, use_graph=False)
+    torch.cuda.synchronize()
+    assert maxabs(again.cpu().numpy(), host) == 0.0
+
+
+# ------------------------------------------------- BASELINE configurations --
+
+def _config_inputs(gpu, cfg, images=None):
+    import torch
+    n = cfg.batch if images is None else images
+    planes = [s for i in range(n) for s in cfg.seeds(i)]
+    img = gpu.generate(cfg.height, cfg.width, planes, n_sites=cfg.n_sites,
+                       p_salt_pepper=cfg.p_salt_pepper).view(n, cfg.channels, cfg.height, cfg.width)
+    guide = None
+    if cfg.guide:
+        guide = gpu.generate(cfg.height, cfg.width, [cfg.guide_seed(i) for i in range(n)],
+                             n_sites=cfg.n_sites).view(n, 1, cfg.height, cfg.width)
+    torch.cuda.synchronize()
+    return img, guide
+
+
+def _oracle_cfg(oracle, cfg, img, guide, i=0):
+    return oracle.blf_ls(img[i].cpu().numpy().astype(np.float64),
+                         None if guide is None else guide[i].cpu().numpy().astype(np.float64),
+                         lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=cfg.iters,
+                         radius=cfg.radius)
+
+
+def _run_cfg(gpu, cfg, img, guide):
+    import torch
+    out = gpu.blf_ls(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r,
+                     iters=cfg.iters, radius=cfg.radius)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_baseline_config_full_parity(gpu, oracle, name):
+    cfg = gpu.CONFIGS[name]
+    img, guide = _config_inputs(gpu, cfg)
+    out = _run_cfg(gpu, cfg, img, guide)
+    ref = _oracle_cfg(oracle, cfg, img, guide)
+    assert maxabs(out[0].cpu().numpy(), ref) <= TOL_OUT
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_baseline_config_properties(gpu, oracle, name):
+    """Full-size c4 / c5: size-independent properties (the oracle takes
+    minutes there; BLFLS_FULL_PARITY=1 adds the full comparison)."""
+    import torch
+    cfg = gpu.CONFIGS[name]
+    images = cfg.batch if name != "c5" else 8
+    img, guide = _config_inputs(gpu, cfg, images)
+    out = _run_cfg(gpu, cfg, img, guide)
+    assert torch.isfinite(out).all()
+    # the solve is a weighted mean: range never grows (convex-hull property of
+    # the BLF plus the maximum principle of the LS operator, up to round-off)
+    lo, hi = img.amin().item(), img.amax().item()
+    assert out.amin().item() >= lo - 1e-3 and out.amax().item() <= hi + 1e-3
+    # fixed point of the solve at full size: lsgrad(u, grad u) == u
+    u0 = out[:1, :1].contiguous()
+    gx = torch.roll(u0, -1, dims=3) - u0
+    gy = torch.roll(u0, -1, dims=2) - u0
+    u1 = gpu.lsgrad_solve_fft(u0, (gx, gy), gpu.SolveParams(cfg.lam, 0))
+    torch.cuda.synchronize()
+    assert (u1 - u0).abs().max().item() <= 2e-5
+    # a constant image of this size is a fixed point of the whole pipeline
+    const = torch.full_like(img[:1], 0.4)
+    cg = None if guide is None else guide[:1]
+    cu = gpu.blf_ls(const, cg, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r,
+                    iters=cfg.iters, radius=cfg.radius)
+    torch.cuda.synchronize()
+    assert (cu - 0.4).abs().max().item() <= 1e-5
+    # batch-sharding invariance: image i alone equals image i of the batch
+    if img.shape[0] > 1:
+        one = _run_cfg(gpu, cfg, img[1:2].contiguous(), None if guide is None else guide[1:2].contiguous())
+        assert (one[0] - out[1]).abs().max().item() == 0.0
+    if os.environ.get("BLFLS_FULL_PARITY") == "1":
+        ref = _oracle_cfg(oracle, cfg, img, guide)
+        assert maxabs(out[0].cpu().numpy(), ref) <= TOL_OUT
