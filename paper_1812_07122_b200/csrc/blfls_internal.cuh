@@ -55,6 +55,15 @@ struct FftDesc {
     const float2* tw;  // n entries, device
 };
 
+// launch geometry of one FFT pass: V vectors per CTA, threads = V * TV
+struct FftGeom {
+    FftDesc desc;
+    int V, log2V, threads;
+    int E;         // complex values per thread across a stage barrier (8 or 16)
+    bool generic;  // a radix other than 2/3/4/5 occurs
+    bool ct;       // a compile-time specialised engine exists for (n, V, threads)
+};
+
 // ---------------------------------------------------------------- BLF args --
 struct BlfParams {
     const float* f;        // current image, batch x C x H x W

@@ -6,6 +6,7 @@
 //   -> row c2r (+ next min/max)
 //
 // replayed as a cached CUDA graph on the plan's own stream.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,12 +19,11 @@
 namespace blfls {
 
 cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st);
-cudaError_t launch_row_r2c(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
-                           bool odd, cudaStream_t st);
-cudaError_t launch_col(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
-                       cudaStream_t st);
-cudaError_t launch_row_c2r(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
-                           bool odd, cudaStream_t st);
+cudaError_t launch_row_r2c(const SolveParams& p, const FftGeom& g, int planes, bool odd,
+                           cudaStream_t st);
+cudaError_t launch_col(const SolveParams& p, const FftGeom& g, int planes, cudaStream_t st);
+cudaError_t launch_row_c2r(const SolveParams& p, const FftGeom& g, int planes, bool odd,
+                           cudaStream_t st);
 cudaError_t launch_minmax(const float* x, size_t per_image, int batch, uint32_t* lohi, int nsm,
                           cudaStream_t st);
 cudaError_t launch_reset_lohi(uint32_t* lohi, int n, cudaStream_t st);
@@ -33,6 +33,7 @@ cudaError_t launch_scale_by_range(float* x, size_t per_image, int batch, const u
 cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int K, double sigma,
                             double p_sp, float* out, cudaStream_t st);
 cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz);
+bool ct_geometry(bool cols, int n, int* V, int* threads);
 
 }  // namespace blfls
 
@@ -61,9 +62,7 @@ blfls_status cuda_fail(cudaError_t e, const char* where)
     } while (0)
 
 struct DevFft {
-    FftDesc desc{};
-    int V = 1;        // vectors per CTA
-    int threads = 32;
+    FftGeom g{};
     float2* tw = nullptr;
 };
 
@@ -79,35 +78,54 @@ bool factorize(int n, std::vector<int>& radix)
     return m == 1 && (int)radix.size() <= kMaxFftRadices;
 }
 
-// per-stage capacity of fft_stage<P> / fft_stage_generic for V vectors and T threads
-bool fits(const std::vector<int>& radix, int n, int V, int T, int regs_per_thread)
+// threads per vector so that every stage fits the E-register budget of fft_stage
+int threads_per_vector(const std::vector<int>& radix, int n, int E)
 {
+    int tv = 1;
     for (int p : radix) {
-        const long nb = ((long)V * n / p + T - 1) / T;
-        if (p <= 5) {
-            if (nb > (regs_per_thread + p - 1) / p) return false;
-        } else if (nb * p > 32) {
-            return false;
-        }
+        const int nbp = n / p;
+        const int nb = p <= 5 ? (E + p - 1) / p : (2 * E) / p;
+        if (nb < 1) return 1 << 30;
+        tv = std::max(tv, (nbp + nb - 1) / nb);
     }
-    return true;
+    return tv;
 }
 
-// choose V vectors per CTA and T threads: V*n/T <= ratio, T <= 1024
-bool plan_fft(int n, int Vmax, int ratio, DevFft& out, std::vector<int>& radix)
+// V (power of two, <= Vmax) vectors of length n per CTA, <= 1024 threads,
+// <= smem_cap bytes of shared memory; largest V first, then the smaller E.
+bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, DevFft& out,
+              std::vector<int>& radix)
 {
     if (!factorize(n, radix)) return false;
-    for (int V = Vmax; V >= 1; V >>= 1) {
-        const long work = (long)V * n;
-        int T = (int)((work + ratio - 1) / ratio);
-        T = ((T + 31) / 32) * 32;
-        if (T < 32) T = 32;
-        if (T > 1024) continue;
-        if (work * 8 > 200 * 1024) continue;  // shared memory
-        if (!fits(radix, n, V, T, 16)) continue;
-        out.V = V;
-        out.threads = T;
+    bool generic = false;
+    for (int p : radix) generic |= p > 5;
+    int cv = 0, ct = 0;
+    if (!odd && ct_geometry(cols, n, &cv, &ct)) {
+        FftGeom& g = out.g;
+        g.V = cv;
+        g.log2V = 0;
+        while ((1 << g.log2V) < cv) ++g.log2V;
+        g.threads = ct;
+        g.E = 16;
+        g.generic = false;
+        g.ct = true;
         return true;
+    }
+    for (int V = Vmax; V >= 1; V >>= 1) {
+        if ((size_t)V * n * 8 > smem_cap) continue;
+        for (int E : {8, 16}) {
+            const int tv = threads_per_vector(radix, n, E);
+            if ((long)tv * V > 1024) continue;
+            FftGeom& g = out.g;
+            g.V = V;
+            g.log2V = 0;
+            while ((1 << g.log2V) < V) ++g.log2V;
+            g.threads = tv * V;
+            g.E = E;
+            g.generic = generic;
+            g.ct = false;
+            return true;
+        }
     }
     return false;
 }
@@ -225,17 +243,17 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
     s.lohi_out = lohi_out;
     s.mode = 3;
     stage_begin(p, 2, st);
-    CK(launch_row_r2c(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+    CK(launch_row_r2c(s, p->rowf.g, planes, p->odd, st));
     stage_end(p, st);
     stage_begin(p, 3, st);
-    CK(launch_col(s, p->colf.desc, p->colf.V, p->colf.threads, planes, st));
+    CK(launch_col(s, p->colf.g, planes, st));
     stage_end(p, st);
     if (lohi_out) {
         CK(launch_reset_lohi(lohi_out, batch, st));
         p->launches++;
     }
     stage_begin(p, 4, st);
-    CK(launch_row_c2r(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+    CK(launch_row_c2r(s, p->rowf.g, planes, p->odd, st));
     stage_end(p, st);
     p->launches += 3;
     return BLFLS_OK;
@@ -415,13 +433,13 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     p->spitch = ((p->wc + 15) / 16) * 16;
     const int nrow = p->odd ? W : W / 2;
     std::vector<int> rrad, crad;
-    // rows: V*n <= 2048 elements per CTA, 8 values per thread
+    // rows: about 2048 complex values per CTA
     int vrow = 1;
     while (vrow * 2 * nrow <= 2048 && vrow < 16) vrow *= 2;
-    if (!plan_fft(nrow, vrow, 8, p->rowf, rrad))
+    if (!plan_fft(nrow, vrow, 64 * 1024, false, p->odd, p->rowf, rrad))
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: width " + std::to_string(W) +
                                                  " has a prime factor above 13 or too large"));
-    if (!plan_fft(H, 16, 16, p->colf, crad))
+    if (!plan_fft(H, 16, 128 * 1024, true, false, p->colf, crad))
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: height " + std::to_string(H) +
                                                  " has a prime factor above 13 or too large"));
 
@@ -453,10 +471,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         cudaMemcpy(p->gain_y, gy.data(), sizeof(float) * H, cudaMemcpyHostToDevice);
         cudaMemcpy(p->post, post.data(), sizeof(float2) * p->wc, cudaMemcpyHostToDevice);
         auto fill = [](DevFft& f, int n, const std::vector<int>& rad) {
-            f.desc.n = n;
-            f.desc.nstages = (int)rad.size();
-            for (size_t i = 0; i < rad.size(); ++i) f.desc.radix[i] = rad[i];
-            f.desc.tw = f.tw;
+            f.g.desc.n = n;
+            f.g.desc.nstages = (int)rad.size();
+            for (size_t i = 0; i < rad.size(); ++i) f.g.desc.radix[i] = rad[i];
+            f.g.desc.tw = f.tw;
         };
         fill(p->rowf, nrow, rrad);
         fill(p->colf, H, crad);
@@ -718,8 +736,8 @@ static blfls_status fft_entry(blfls_plan_t p, const float* in, int batch, float*
         }
         s.f = din;
         s.mode = 1;
-        CK(launch_row_r2c(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
-        CK(launch_col(s, p->colf.desc, p->colf.V, p->colf.threads, planes, st));
+        CK(launch_row_r2c(s, p->rowf.g, planes, p->odd, st));
+        CK(launch_col(s, p->colf.g, planes, st));
         CK(cudaMemcpy2DAsync(outp, sizeof(float2) * p->wc, p->spec, sizeof(float2) * p->spitch,
                              sizeof(float2) * p->wc, (size_t)planes * p->prm.height,
                              host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
@@ -730,8 +748,8 @@ static blfls_status fft_entry(blfls_plan_t p, const float* in, int batch, float*
         float* dout = host ? p->buf[1] : outp;
         s.out = dout;
         s.mode = 2;
-        CK(launch_col(s, p->colf.desc, p->colf.V, p->colf.threads, planes, st));
-        CK(launch_row_c2r(s, p->rowf.desc, p->rowf.V, p->rowf.threads, planes, p->odd, st));
+        CK(launch_col(s, p->colf.g, planes, st));
+        CK(launch_row_c2r(s, p->rowf.g, planes, p->odd, st));
         if (host) CK(cudaMemcpyAsync(outp, dout, sizeof(float) * nreal, cudaMemcpyDeviceToHost, st));
     }
     (void)nspec;

@@ -3,13 +3,20 @@
 // Replaces the reference's FFTW calls (src/fft2d.cpp:17-52).  A CTA holds V
 // complex vectors of length n in ONE shared buffer; every stage reads each
 // thread's butterfly inputs into registers, barriers, then writes the outputs
-// back to the same buffer (no ping-pong, so a column strip of V vectors uses
-// V*n*8 bytes).  Layouts:
-//   ROWS: element j of vector v at buf[v*n + j]   (vectors along a row)
-//   COLS: element j of vector v at buf[j*V + v]   (V adjacent spectrum columns,
-//         so consecutive threads touch consecutive banks)
-// Radices 2, 3, 4, 5 are specialised; any other prime up to 31 goes through a
-// generic radix stage (used only by odd test sizes).
+// back to the same buffer (no ping-pong, so a strip of V vectors costs V*n*8
+// bytes).  Threads are split into V groups of TV = blockDim/V threads, one
+// group per vector, so butterfly indices need no division by n.  Layouts:
+//   ROWS: element j of vector v at buf[v*n + j]    thread -> v = tid / TV
+//   COLS: element j of vector v at buf[j*V + v]    thread -> v = tid % V
+//         (V adjacent spectrum columns: consecutive threads hit consecutive
+//         banks and global loads are V*8-byte row segments)
+// Stockham stage, radix p, stride s (product of earlier radices):
+//   butterfly bb in [0, n/p): k = bb % s, q = bb / s, a_r = x[bb + r n/p]
+//   y[k + s (p q + t)] = tw[q t s] * sum_r a_r w_p^{r t}
+// tw[j] = exp(-2 pi i j / n) from double-precision host tables; the inverse
+// conjugates every twiddle.  Radices 2, 3, 4, 5 are specialised; other primes
+// up to 13 use the generic stage, compiled only into the GENERIC kernels that
+// the plan selects for such (test-only) sizes.
 #pragma once
 
 #include "blfls_internal.cuh"
@@ -26,9 +33,6 @@ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2
 // multiply by +i (sg = +1) or -i (sg = -1)
 __device__ __forceinline__ float2 cmuli(float2 a, float sg) { return make_float2(-sg * a.y, sg * a.x); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-
-// values per thread held across a stage barrier
-constexpr int kFftRegs = 16;
 
 template <int P>
 __device__ __forceinline__ void dft_small(float2 (&a)[P], float sg /* -1 fwd, +1 inv */)
@@ -71,113 +75,243 @@ __device__ __forceinline__ void dft_small(float2 (&a)[P], float sg /* -1 fwd, +1
     }
 }
 
+// per-thread view of a CTA holding V vectors
+struct FftLane {
+    int v;    // vector owned by this thread
+    int t;    // index within the vector's thread group
+    int TV;   // threads per vector
+};
+
 template <bool COLS>
-__device__ __forceinline__ int fft_addr(int v, int j, int n, int V)
+__device__ __forceinline__ FftLane fft_lane(int V, int log2V)
 {
-    return COLS ? j * V + v : v * n + j;
+    FftLane l;
+    l.TV = blockDim.x >> log2V;
+    if (COLS) {
+        l.v = threadIdx.x & (V - 1);
+        l.t = threadIdx.x >> log2V;
+    } else {
+        l.v = threadIdx.x / l.TV;
+        l.t = threadIdx.x - l.v * l.TV;
+    }
+    return l;
 }
 
-template <int P, bool COLS>
-__device__ __forceinline__ void fft_stage(float2* buf, int n, int V, int s,
+template <bool COLS>
+__device__ __forceinline__ int fft_addr(const FftLane& l, int j, int n, int V)
+{
+    return COLS ? j * V + l.v : l.v * n + j;
+}
+
+// E = complex values a thread holds across the stage barrier
+template <int P, int E, bool COLS>
+__device__ __forceinline__ void fft_stage(float2* buf, const FftLane& l, int n, int V, int s,
                                           const float2* __restrict__ tw, bool inv)
 {
-    constexpr int NB = (kFftRegs + P - 1) / P;
+    constexpr int NB = (E + P - 1) / P;
     const int nbp = n / P;
-    const int total = V * nbp;
-    const int T = blockDim.x;
     const float sg = inv ? 1.0f : -1.0f;
     float2 a[NB][P];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const int b = threadIdx.x + i * T;
-        if (b < total) {
-            const int v = COLS ? b % V : b / nbp;
-            const int bb = COLS ? b / V : b % nbp;
+        const int bb = l.t + i * l.TV;
+        if (bb < nbp) {
 #pragma unroll
-            for (int r = 0; r < P; ++r) a[i][r] = buf[fft_addr<COLS>(v, bb + r * nbp, n, V)];
+            for (int r = 0; r < P; ++r) a[i][r] = buf[fft_addr<COLS>(l, bb + r * nbp, n, V)];
         }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const int b = threadIdx.x + i * T;
-        if (b < total) {
-            const int v = COLS ? b % V : b / nbp;
-            const int bb = COLS ? b / V : b % nbp;
-            const int k = bb % s, q = bb / s;
+        const int bb = l.t + i * l.TV;
+        if (bb < nbp) {
+            const int q = bb / s, k = bb - q * s;
             dft_small<P>(a[i], sg);
             const int obase = k + s * P * q;
-            buf[fft_addr<COLS>(v, obase, n, V)] = a[i][0];
+            buf[fft_addr<COLS>(l, obase, n, V)] = a[i][0];
 #pragma unroll
             for (int t = 1; t < P; ++t) {
                 float2 w = __ldg(&tw[q * t * s]);
                 if (inv) w.y = -w.y;
-                buf[fft_addr<COLS>(v, obase + s * t, n, V)] = cmul(a[i][t], w);
+                buf[fft_addr<COLS>(l, obase + s * t, n, V)] = cmul(a[i][t], w);
             }
         }
     }
     __syncthreads();
 }
 
-// Generic odd prime radix (7..31), O(p^2) per butterfly, local-memory staging.
-template <bool COLS>
-__device__ void fft_stage_generic(float2* buf, int n, int V, int s, int P,
+// Generic odd prime radix (7, 11, 13), O(p^2) per butterfly; test sizes only.
+template <int E, bool COLS>
+__device__ void fft_stage_generic(float2* buf, const FftLane& l, int n, int V, int s, int P,
                                   const float2* __restrict__ tw, bool inv)
 {
     const int nbp = n / P;
-    const int total = V * nbp;
-    const int T = blockDim.x;
-    const int NB = (total + T - 1) / T;  // plan guarantees NB * P <= 32
-    float2 a[32];
+    const int NB = (nbp + l.TV - 1) / l.TV;  // plan guarantees NB * P <= 2E
+    float2 a[2 * E];
     for (int i = 0; i < NB; ++i) {
-        const int b = threadIdx.x + i * T;
-        if (b < total) {
-            const int v = COLS ? b % V : b / nbp;
-            const int bb = COLS ? b / V : b % nbp;
-            for (int r = 0; r < P; ++r) a[i * P + r] = buf[fft_addr<COLS>(v, bb + r * nbp, n, V)];
-        }
+        const int bb = l.t + i * l.TV;
+        if (bb < nbp)
+            for (int r = 0; r < P; ++r) a[i * P + r] = buf[fft_addr<COLS>(l, bb + r * nbp, n, V)];
     }
     __syncthreads();
-    const int wstep = n / P;
     for (int i = 0; i < NB; ++i) {
-        const int b = threadIdx.x + i * T;
-        if (b < total) {
-            const int v = COLS ? b % V : b / nbp;
-            const int bb = COLS ? b / V : b % nbp;
-            const int k = bb % s, q = bb / s;
+        const int bb = l.t + i * l.TV;
+        if (bb < nbp) {
+            const int q = bb / s, k = bb - q * s;
             for (int t = 0; t < P; ++t) {
                 float2 acc = make_float2(0.f, 0.f);
                 for (int r = 0; r < P; ++r) {
-                    float2 w = __ldg(&tw[((r * t) % P) * wstep]);
+                    float2 w = __ldg(&tw[((r * t) % P) * nbp]);
                     if (inv) w.y = -w.y;
-                    const float2 pr = cmul(a[i * P + r], w);
-                    acc = cadd(acc, pr);
+                    acc = cadd(acc, cmul(a[i * P + r], w));
                 }
                 float2 w2 = __ldg(&tw[q * t * s]);
                 if (inv) w2.y = -w2.y;
-                buf[fft_addr<COLS>(v, k + s * (P * q + t), n, V)] = cmul(acc, w2);
+                buf[fft_addr<COLS>(l, k + s * (P * q + t), n, V)] = cmul(acc, w2);
             }
         }
     }
     __syncthreads();
 }
 
-// Full transform of V vectors in `buf` (unnormalised; inverse = conjugate twiddles).
-template <bool COLS>
-__device__ void fft_run(float2* buf, const FftDesc& d, int V, bool inv)
+// Full transform of the CTA's V vectors (unnormalised; inverse = conjugate twiddles).
+template <int E, bool COLS, bool GENERIC>
+__device__ void fft_run(float2* buf, const FftDesc& d, int V, int log2V, bool inv)
 {
+    const FftLane l = fft_lane<COLS>(V, log2V);
     int s = 1;
     for (int st = 0; st < d.nstages; ++st) {
         const int p = d.radix[st];
-        switch (p) {
-            case 2: fft_stage<2, COLS>(buf, d.n, V, s, d.tw, inv); break;
-            case 3: fft_stage<3, COLS>(buf, d.n, V, s, d.tw, inv); break;
-            case 4: fft_stage<4, COLS>(buf, d.n, V, s, d.tw, inv); break;
-            case 5: fft_stage<5, COLS>(buf, d.n, V, s, d.tw, inv); break;
-            default: fft_stage_generic<COLS>(buf, d.n, V, s, p, d.tw, inv); break;
-        }
+        if (p == 4)
+            fft_stage<4, E, COLS>(buf, l, d.n, V, s, d.tw, inv);
+        else if (p == 2)
+            fft_stage<2, E, COLS>(buf, l, d.n, V, s, d.tw, inv);
+        else if (p == 3)
+            fft_stage<3, E, COLS>(buf, l, d.n, V, s, d.tw, inv);
+        else if (p == 5)
+            fft_stage<5, E, COLS>(buf, l, d.n, V, s, d.tw, inv);
+        else if constexpr (GENERIC)
+            fft_stage_generic<E, COLS>(buf, l, d.n, V, s, p, d.tw, inv);
         s *= p;
     }
 }
+
+}  // namespace blfls
+
+// ===================================================================
+// Compile-time engine: length N, V vectors per CTA, TV threads per vector.
+// Every index (stage stride, butterfly count, predicate) folds to a
+// constant.  Instantiated for the BASELINE sizes (capi.cu / k_solve.cu).
+namespace blfls {
+
+constexpr int ct_count(int n, int p) { return n % p == 0 ? 1 + ct_count(n / p, p) : 0; }
+constexpr int ct_n4(int n) { return ct_count(n, 4); }
+constexpr int ct_rest2(int n)
+{
+    int m = n;
+    for (int i = 0; i < ct_n4(n); ++i) m /= 4;
+    return m % 2 == 0 ? 1 : 0;
+}
+constexpr int ct_nstages(int n) { return ct_n4(n) + ct_rest2(n) + ct_count(n, 3) + ct_count(n, 5); }
+constexpr int ct_radix(int n, int i)
+{
+    if (i < ct_n4(n)) return 4;
+    i -= ct_n4(n);
+    if (i < ct_rest2(n)) return 2;
+    i -= ct_rest2(n);
+    if (i < ct_count(n, 3)) return 3;
+    return 5;
+}
+constexpr int ct_stride(int n, int i)
+{
+    int s = 1;
+    for (int k = 0; k < i; ++k) s *= ct_radix(n, k);
+    return s;
+}
+constexpr bool ct_supported(int n)
+{
+    int m = n;
+    for (int p : {2, 3, 5})
+        while (m % p == 0) m /= p;
+    return m == 1;
+}
+
+template <int N, int V, int TV, bool COLS, bool INV, int P, int S>
+__device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2* __restrict__ tw)
+{
+    constexpr int NBP = N / P;
+    constexpr int NB = (NBP + TV - 1) / TV;
+    constexpr bool PRED = NB * TV != NBP;
+    constexpr float sg = INV ? 1.0f : -1.0f;
+    auto addr = [&](int j) { return COLS ? j * V + v : v * N + j; };
+    float2 a[NB][P];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int bb = t + i * TV;
+        if (!PRED || bb < NBP) {
+#pragma unroll
+            for (int r = 0; r < P; ++r) a[i][r] = buf[addr(bb + r * NBP)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int bb = t + i * TV;
+        if (!PRED || bb < NBP) {
+            const int q = bb / S, k = bb - q * S;
+            dft_small<P>(a[i], sg);
+            const int obase = k + S * P * q;
+            buf[addr(obase)] = a[i][0];
+#pragma unroll
+            for (int tt = 1; tt < P; ++tt) {
+                float2 w = __ldg(&tw[q * tt * S]);
+                if (INV) w.y = -w.y;
+                buf[addr(obase + S * tt)] = cmul(a[i][tt], w);
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <int N, int V, int TV, bool COLS, bool INV, int I>
+__device__ __forceinline__ void ct_stages(float2* buf, int v, int t, const float2* __restrict__ tw)
+{
+    if constexpr (I < ct_nstages(N)) {
+        ct_stage<N, V, TV, COLS, INV, ct_radix(N, I), ct_stride(N, I)>(buf, v, t, tw);
+        ct_stages<N, V, TV, COLS, INV, I + 1>(buf, v, t, tw);
+    }
+}
+
+// engine policies used by the solve kernels
+template <int N_, int V_, int TV_>
+struct CtFft {
+    static constexpr int N = N_, V = V_, TV = TV_, THREADS = V_ * TV_;
+    const float2* tw;
+    __device__ __forceinline__ int n() const { return N; }
+    __device__ __forceinline__ int vecs() const { return V; }
+    template <bool COLS>
+    __device__ __forceinline__ void run(float2* buf, bool inv) const
+    {
+        const int v = COLS ? (int)threadIdx.x % V : (int)threadIdx.x / TV;
+        const int t = COLS ? (int)threadIdx.x / V : (int)threadIdx.x % TV;
+        if (inv)
+            ct_stages<N, V, TV, COLS, true, 0>(buf, v, t, tw);
+        else
+            ct_stages<N, V, TV, COLS, false, 0>(buf, v, t, tw);
+    }
+};
+
+template <int E, bool GENERIC>
+struct RtFft {
+    FftDesc d;
+    int V, log2V;
+    __device__ __forceinline__ int n() const { return d.n; }
+    __device__ __forceinline__ int vecs() const { return V; }
+    template <bool COLS>
+    __device__ __forceinline__ void run(float2* buf, bool inv) const
+    {
+        fft_run<E, COLS, GENERIC>(buf, d, V, log2V, inv);
+    }
+};
 
 }  // namespace blfls

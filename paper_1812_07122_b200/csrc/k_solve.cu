@@ -33,11 +33,11 @@ __device__ __forceinline__ float fold_value(const SolveParams& p, const float* f
 }
 
 // grid: (ceil(H / V), planes); V rows per CTA; n = W/2 (even W) or W (odd W)
-template <bool ODD>
-__global__ void k_row_r2c(const SolveParams p, const FftDesc d, int V)
+template <bool ODD, class F>
+__global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F fft)
 {
     extern __shared__ __align__(16) float2 buf[];
-    const int n = d.n;
+    const int n = fft.n(), V = fft.vecs();
     const int plane = blockIdx.y;
     const int row0 = blockIdx.x * V;
     const size_t poff = (size_t)plane * p.H * p.W;
@@ -59,7 +59,7 @@ __global__ void k_row_r2c(const SolveParams p, const FftDesc d, int V)
         buf[idx] = z;
     }
     __syncthreads();
-    fft_run<false>(buf, d, V, false);
+    fft.template run<false>(buf, false);
     const int wc = p.wc;
     for (int idx = threadIdx.x; idx < V * wc; idx += blockDim.x) {
         const int v = idx / wc, k = idx - (idx / wc) * wc;
@@ -80,10 +80,11 @@ __global__ void k_row_r2c(const SolveParams p, const FftDesc d, int V)
 }
 
 // grid: (ceil(wc / V), planes); V adjacent columns per CTA, layout buf[u*V + c]
-__global__ void k_col(const SolveParams p, const FftDesc d, int V)
+template <class F>
+__global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
 {
     extern __shared__ __align__(16) float2 buf[];
-    const int H = p.H;
+    const int H = p.H, V = fft.vecs();
     const int plane = blockIdx.y;
     const int v0 = blockIdx.x * V;
     float2* spec = p.spec + (size_t)plane * H * p.spitch;
@@ -93,7 +94,7 @@ __global__ void k_col(const SolveParams p, const FftDesc d, int V)
         buf[idx] = v < p.wc ? spec[(size_t)u * p.spitch + v] : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    if (p.mode & 1) fft_run<true>(buf, d, V, false);
+    if (p.mode & 1) fft.template run<true>(buf, false);
     if (p.mode & 2) {
         for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
             const int u = idx / V, c = idx - (idx / V) * V;
@@ -104,7 +105,7 @@ __global__ void k_col(const SolveParams p, const FftDesc d, int V)
             buf[idx] = cscale(buf[idx], sc);
         }
         __syncthreads();
-        fft_run<true>(buf, d, V, true);
+        fft.template run<true>(buf, true);
     }
     for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
         const int u = idx / V, c = idx - (idx / V) * V;
@@ -144,11 +145,11 @@ __device__ __forceinline__ void block_minmax_atomic(float lo, float hi, uint32_t
 }
 
 // grid: (ceil(H / V), planes)
-template <bool ODD>
-__global__ void k_row_c2r(const SolveParams p, const FftDesc d, int V)
+template <bool ODD, class F>
+__global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F fft)
 {
     extern __shared__ __align__(16) float2 buf[];
-    const int n = d.n;
+    const int n = fft.n(), V = fft.vecs();
     const int plane = blockIdx.y;
     const int row0 = blockIdx.x * V;
     const int W = p.W;
@@ -181,7 +182,7 @@ __global__ void k_row_c2r(const SolveParams p, const FftDesc d, int V)
         buf[idx] = Z;
     }
     __syncthreads();
-    fft_run<false>(buf, d, V, true);
+    fft.template run<false>(buf, true);
     float lo = INFINITY, hi = -INFINITY;
     float* out = p.out + (size_t)plane * p.H * W;
     for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
@@ -322,44 +323,100 @@ __global__ void k_generate(int H, int W, const uint64_t* seeds, int K, double no
 
 // -------------------------------------------------------------- launchers --
 
-cudaError_t launch_row_r2c(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
-                           bool odd, cudaStream_t st)
+template <class K>
+static void set_smem(K kernel, size_t smem)
 {
-    const size_t smem = (size_t)V * d.n * sizeof(float2);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// which = 0 row r2c, 1 column, 2 row c2r
+template <class F>
+static void launch_pass(int which, const SolveParams& p, const F& f, int V, int n, int threads,
+                        int planes, bool odd, cudaStream_t st)
+{
+    const size_t smem = (size_t)V * n * sizeof(float2);
+    if (which == 1) {
+        dim3 grid((p.wc + V - 1) / V, planes);
+        set_smem(k_col<F>, smem);
+        k_col<F><<<grid, threads, smem, st>>>(p, f);
+        return;
+    }
     dim3 grid((p.H + V - 1) / V, planes);
-    if (odd) {
-        cudaFuncSetAttribute(k_row_r2c<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_row_r2c<true><<<grid, threads, smem, st>>>(p, d, V);
+    if (which == 0) {
+        if (odd) { set_smem(k_row_r2c<true, F>, smem); k_row_r2c<true, F><<<grid, threads, smem, st>>>(p, f); }
+        else { set_smem(k_row_r2c<false, F>, smem); k_row_r2c<false, F><<<grid, threads, smem, st>>>(p, f); }
     } else {
-        cudaFuncSetAttribute(k_row_r2c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_row_r2c<false><<<grid, threads, smem, st>>>(p, d, V);
+        if (odd) { set_smem(k_row_c2r<true, F>, smem); k_row_c2r<true, F><<<grid, threads, smem, st>>>(p, f); }
+        else { set_smem(k_row_c2r<false, F>, smem); k_row_c2r<false, F><<<grid, threads, smem, st>>>(p, f); }
+    }
+}
+
+// Compile-time geometries of the BASELINE sizes.  Rows (V*TV = 256 threads,
+// ~8 values per thread): n = W/2 for W in {512, 1024, 1920, 2048, 4096}.
+// Columns (V*TV <= 1024 threads, ~16 values per thread, V*8 >= 32-byte row
+// segments): H in {512, 1024, 1080, 2048, 4096}.
+#define BLFLS_CT_ROWS(X) X(256, 8, 32) X(512, 4, 64) X(960, 2, 128) X(1024, 2, 128) X(2048, 1, 256)
+#define BLFLS_CT_COLS(X) X(512, 16, 32) X(1024, 16, 64) X(1080, 8, 128) X(2048, 8, 128) X(4096, 4, 256)
+
+bool ct_geometry(bool cols, int n, int* V, int* threads)
+{
+#define BLFLS_GEOM(N, VV, TV) \
+    if (n == N) { *V = VV; *threads = VV * TV; return true; }
+    if (cols) {
+        BLFLS_CT_COLS(BLFLS_GEOM)
+    } else {
+        BLFLS_CT_ROWS(BLFLS_GEOM)
+    }
+#undef BLFLS_GEOM
+    return false;
+}
+
+static cudaError_t launch_fft_pass(int which, const SolveParams& p, const FftGeom& g, int planes,
+                                   bool odd, cudaStream_t st)
+{
+    const int n = g.desc.n;
+    if (g.ct && !odd) {
+#define BLFLS_CT_LAUNCH(N, VV, TV)                                                          \
+    if (n == N) {                                                                          \
+        launch_pass(which, p, CtFft<N, VV, TV>{g.desc.tw}, VV, N, VV * TV, planes, odd, st); \
+        return cudaGetLastError();                                                         \
+    }
+        if (which == 1) {
+            BLFLS_CT_COLS(BLFLS_CT_LAUNCH)
+        } else {
+            BLFLS_CT_ROWS(BLFLS_CT_LAUNCH)
+        }
+#undef BLFLS_CT_LAUNCH
+    }
+    if (g.E == 16) {
+        if (g.generic)
+            launch_pass(which, p, RtFft<16, true>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+        else
+            launch_pass(which, p, RtFft<16, false>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+    } else {
+        if (g.generic)
+            launch_pass(which, p, RtFft<8, true>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+        else
+            launch_pass(which, p, RtFft<8, false>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_col(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
-                       cudaStream_t st)
+cudaError_t launch_row_r2c(const SolveParams& p, const FftGeom& g, int planes, bool odd,
+                           cudaStream_t st)
 {
-    const size_t smem = (size_t)V * d.n * sizeof(float2);
-    cudaFuncSetAttribute(k_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((p.wc + V - 1) / V, planes);
-    k_col<<<grid, threads, smem, st>>>(p, d, V);
-    return cudaGetLastError();
+    return launch_fft_pass(0, p, g, planes, odd, st);
 }
 
-cudaError_t launch_row_c2r(const SolveParams& p, const FftDesc& d, int V, int threads, int planes,
-                           bool odd, cudaStream_t st)
+cudaError_t launch_col(const SolveParams& p, const FftGeom& g, int planes, cudaStream_t st)
 {
-    const size_t smem = (size_t)V * d.n * sizeof(float2);
-    dim3 grid((p.H + V - 1) / V, planes);
-    if (odd) {
-        cudaFuncSetAttribute(k_row_c2r<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_row_c2r<true><<<grid, threads, smem, st>>>(p, d, V);
-    } else {
-        cudaFuncSetAttribute(k_row_c2r<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_row_c2r<false><<<grid, threads, smem, st>>>(p, d, V);
-    }
-    return cudaGetLastError();
+    return launch_fft_pass(1, p, g, planes, false, st);
+}
+
+cudaError_t launch_row_c2r(const SolveParams& p, const FftGeom& g, int planes, bool odd,
+                           cudaStream_t st)
+{
+    return launch_fft_pass(2, p, g, planes, odd, st);
 }
 
 cudaError_t launch_minmax(const float* x, size_t per_image, int batch, uint32_t* lohi, int nsm,
