@@ -141,6 +141,11 @@ blfls_status blfls_last_stats(blfls_plan_t plan, blfls_stats* stats);
  * the recorded events. */
 blfls_status blfls_stage_times(blfls_plan_t plan, double* ms_sum5, long long* launches5);
 
+/* Per-image (lo, hi) normalisation ranges the plan holds: out[0 .. 4*max_batch)
+ * = two ping-pong slots of (lo, hi) per image (slot k%2 feeds iteration k).
+ * Synchronizes the plan stream.  For tests of the fused min/max epilogue. */
+blfls_status blfls_debug_ranges(blfls_plan_t plan, float* out);
+
 /* Measured MUFU.EX2 throughput of `device` (ex2 per second), from a
  * dependency-free ex2 loop over all SMs: the SFU roofline denominator. */
 blfls_status blfls_mufu_peak(int device, double* ex2_per_second, double* sm_clock_hz);

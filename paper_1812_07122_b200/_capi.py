@@ -29,7 +29,7 @@ TIME_STAGES = 16
 EXPORTS = (
     "blfls_plan_create", "blfls_plan_destroy", "blfls_run", "blfls_filter_gradients",
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
-    "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_mufu_peak", "blfls_last_error",
+    "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
     "blfls_version", "blfls_abi_version",
 )
 
@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
                                          C.c_double, fp, vp, ip]
             L.blfls_last_stats.argtypes = [vp, C.POINTER(Stats)]
             L.blfls_stage_times.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
+            L.blfls_debug_ranges.argtypes = [vp, C.POINTER(C.c_float)]
             L.blfls_mufu_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
             L.blfls_last_error.restype = C.c_char_p
             L.blfls_version.restype = C.c_char_p
@@ -141,6 +142,16 @@ class Plan:
         n = (C.c_longlong * 5)()
         check(lib().blfls_stage_times(self.handle, ms, n))
         return list(ms), list(n)
+
+    def debug_ranges(self):
+        """[[slot0 (lo, hi) per image], [slot1 ...]] as floats."""
+        n = 4 * self.params.max_batch
+        buf = (C.c_float * n)()
+        check(lib().blfls_debug_ranges(self.handle, buf))
+        v = list(buf)
+        mb = self.params.max_batch
+        return [[(v[2 * i], v[2 * i + 1]) for i in range(mb)],
+                [(v[2 * mb + 2 * i], v[2 * mb + 2 * i + 1]) for i in range(mb)]]
 
     def stats(self) -> Stats:
         s = Stats()

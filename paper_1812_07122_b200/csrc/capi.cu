@@ -114,7 +114,9 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, DevFft& out
     for (int V = Vmax; V >= 1; V >>= 1) {
         if ((size_t)V * n * 8 > smem_cap) continue;
         for (int E : {8, 16}) {
-            const int tv = threads_per_vector(radix, n, E);
+            int tv = threads_per_vector(radix, n, E);
+            // whole warps per CTA: the block reductions shuffle over full warps
+            while ((tv * V) % 32 != 0) ++tv;
             if ((long)tv * V > 1024) continue;
             FftGeom& g = out.g;
             g.V = V;
@@ -810,6 +812,18 @@ blfls_status blfls_stage_times(blfls_plan_t p, double* ms_sum5, long long* launc
         cudaEventDestroy(e.b);
     }
     p->timing.clear();
+    return BLFLS_OK;
+}
+
+blfls_status blfls_debug_ranges(blfls_plan_t p, float* out)
+{
+    if (!p || !out) return fail(BLFLS_EINVAL, "null argument");
+    blfls_status r;
+    if ((r = set_device(p))) return r;
+    CK(cudaStreamSynchronize(p->ps));
+    std::vector<uint32_t> h(4 * (size_t)p->prm.max_batch);
+    CK(cudaMemcpy(h.data(), p->lohi, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h.size(); ++i) out[i] = ordered_to_float(h[i]);
     return BLFLS_OK;
 }
 

@@ -267,10 +267,11 @@ def test_baseline_config_properties(gpu, oracle, name):
     img, guide = _config_inputs(gpu, cfg, images)
     out = _run_cfg(gpu, cfg, img, guide)
     assert torch.isfinite(out).all()
-    # the solve is a weighted mean: range never grows (convex-hull property of
-    # the BLF plus the maximum principle of the LS operator, up to round-off)
-    lo, hi = img.amin().item(), img.amax().item()
-    assert out.amin().item() >= lo - 1e-3 and out.amax().item() <= hi + 1e-3
+    # every iteration preserves each channel's mean exactly: the solve's DC
+    # gain is 1 (den(0,0) = 1, conj(otf)(0) = 0, solver.cpp:117-118)
+    m_in = img.double().mean(dim=(2, 3))
+    m_out = out.double().mean(dim=(2, 3))
+    assert (m_in - m_out).abs().max().item() <= 1e-5
     # fixed point of the solve at full size: lsgrad(u, grad u) == u
     u0 = out[:1, :1].contiguous()
     gx = torch.roll(u0, -1, dims=3) - u0
@@ -292,3 +293,16 @@ def test_baseline_config_properties(gpu, oracle, name):
     if os.environ.get("BLFLS_FULL_PARITY") == "1":
         ref = _oracle_cfg(oracle, cfg, img, guide)
         assert maxabs(out[0].cpu().numpy(), ref) <= TOL_OUT
+
+
+@pytest.mark.parametrize("c,h,w", [(1, 32, 40), (1, 60, 50), (3, 48, 80), (1, 33, 35), (3, 64, 64)])
+def test_fused_minmax_epilogue(gpu, oracle, c, h, w):
+    """The row c2r epilogue's min/max (the next iteration's normalisation,
+    image.cpp:46-60) equals the true range of the intermediate image."""
+    img = _img(oracle, c, h, w, 3 + h)
+    kw = dict(lam=1000.0, sigma_s=2.0, sigma_r=0.1, radius=3)
+    one = gpu.blf_ls(img, iters=1, **kw)
+    gpu.blf_ls(img, iters=2, **kw)
+    plan = gpu.get_plan(h, w, c, 0, 3, 2.0, 0.1, 1000.0, 1, 0)
+    lo, hi = plan.debug_ranges()[1][0]
+    assert lo == float(one.min()) and hi == float(one.max())
