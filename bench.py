@@ -54,6 +54,17 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def load_traffic(name):
+    """DRAM bytes per launch of the BLF kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        t = json.loads(p.read_text()).get(name)
+        return None if t is None else {"bytes": t["bytes"], "unit": "B", "kernel": t["kernel"],
+                                       "source": t["source"]}
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -338,7 +349,7 @@ def run_ours(args, cfg):
                                         f"{sfu_peak_nominal / 1e9:.0f} Gexp/s",
                          "frac_of_nominal": achieved / sfu_peak_nominal,
                          "exps_per_launch": exps_per_launch, "launch_ms": blf_ms,
-                         "traffic": None},
+                         "traffic": load_traffic(cfg.name)},
             "roofline_solve": {"bound": "hbm", "achieved": solve_bytes / (solve_ms * 1e-3) / 1e9,
                                "peak": hbm_peak, "unit": "GB/s",
                                "frac": solve_bytes / (solve_ms * 1e-3) / 1e9 / hbm_peak,
