@@ -116,7 +116,8 @@ class ClockSampler:
         reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
         loaded = [s for s, _, _ in rows if s >= under_load_mhz] or [s for s, _, _ in rows]
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "window": "1 s loaded soak of the same steps + the timed region"}
 
 
 # --------------------------------------------------------------- helpers --
@@ -146,7 +147,9 @@ def config_json(cfg, n_gpus, extra=None):
 def cpu_sample(cfg, threads=None):
     """Reference CPU path on a bounded sample of the workload: the first image
     of the config, ONE iteration (of cfg.iters), through oracle/_ref
-    (the reference's translation units + brute-force BLF with explicit r)."""
+    (the reference's translation units + brute-force BLF with explicit r).
+    Configs whose single iteration exceeds ~4e9 taps (c4) run on a centred
+    crop of the same image so the sample stays ~10 s; MP/s is per pixel."""
     import numpy as np
     from oracle import oracle as O
     kind = "reference" if O.REF_SO.exists() else "port"
@@ -156,16 +159,25 @@ def cpu_sample(cfg, threads=None):
     if cfg.guide:
         guide = O.gen_plane(cfg.guide_seed(0), cfg.height, cfg.width, n_sites=cfg.n_sites)[None]
         guide = guide.astype(np.float64)
+    taps = img.size * 2 * (2 * cfg.radius + 1) ** 2
+    crop = ""
+    if taps > 4e9:
+        side = int(cfg.height * (4e9 / taps) ** 0.5) // 16 * 16
+        y0, x0 = (cfg.height - side) // 2, (cfg.width - side) // 2
+        img = np.ascontiguousarray(img[:, y0:y0 + side, x0:x0 + side])
+        if guide is not None:
+            guide = np.ascontiguousarray(guide[:, y0:y0 + side, x0:x0 + side])
+        crop = f", centred {side}x{side} crop"
     fn = O.ref_blf_ls if kind == "reference" else O.blf_ls
     t0 = time.perf_counter()
     _, tb, ts = fn(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
                    radius=cfg.radius, timed=True)
     dt = time.perf_counter() - t0
-    mp = cfg.height * cfg.width / 1e6
+    mp = img.shape[1] * img.shape[2] / 1e6
     return {"value": mp / dt, "unit": "MP/s", "cores": O.num_threads(), "kind": kind,
-            "sample": f"1 image x 1 iteration of {cfg.name} ({cfg.height}x{cfg.width}x{cfg.channels}), "
-                      f"double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
-            "seconds": dt, "blf_s": tb, "solve_s": ts}
+            "sample": f"1 image x 1 iteration of {cfg.name} ({cfg.height}x{cfg.width}x{cfg.channels}"
+                      f"{crop}), double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
+            "seconds": dt, "mp": mp, "blf_s": tb, "solve_s": ts}
 
 
 # ---------------------------------------------------------- reference arm --
@@ -181,8 +193,7 @@ def run_reference(args, cfg):
             res.append(r)
     secs = [r["seconds"] for r in res]
     t = statistics.mean(secs)
-    mp = cfg.height * cfg.width / 1e6
-    value = mp / t
+    value = res[0]["mp"] / t
     line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -246,6 +257,11 @@ def run_ours(args, cfg):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clocks:
+        # ~1 s of untimed steps so the 100 ms sampler sees the loaded clocks
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 1.0:
+            step()
+            torch.cuda.synchronize()
         for k in range(args.steps):
             if l2_resident:
                 flush.fill_(float(k))

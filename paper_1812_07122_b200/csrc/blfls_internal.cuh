@@ -77,6 +77,7 @@ struct BlfParams {
     int out_rows;          // rows per plane of tx/ty (H, or y1 - y0 for bands)
     int normalized_out;    // 1: write targets of the [0,1]-normalised image
     int radius;
+    int poly_period;       // SFU offload period of k_grad_blf (< 0: per-mode default)
     float range_coef;      // sqrt(log2(e) / (8 sigma_r^2)): exponent scale for raw
                            // gradients of a unit-range image
     float cs[kMaxRadius + 1];  // log2 spatial weight -d^2/(2 sigma_s^2) * log2(e)

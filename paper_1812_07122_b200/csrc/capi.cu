@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -490,6 +491,8 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         b.C = C;
         b.GC = q.guide_channels;
         b.radius = radius;
+        b.poly_period = -1;
+        if (const char* ev = std::getenv("BLFLS_POLY_PERIOD")) b.poly_period = std::atoi(ev);
         b.range_coef = (float)std::sqrt(1.4426950408889634 / (8.0 * q.sigma_r * q.sigma_r));
         for (int d = 0; d <= kMaxRadius; ++d) {
             const double c = -(double)d * d / (2.0 * q.sigma_s * q.sigma_s) * 1.4426950408889634;

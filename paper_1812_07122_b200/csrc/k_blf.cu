@@ -35,6 +35,26 @@ __device__ __forceinline__ float fast_ex2(float x)
     return y;
 }
 
+// exp2 on the FMA/ALU pipes (FlashAttention-4-style SFU offload): round to
+// nearest with the 1.5*2^23 magic constant, degree-5 near-minimax polynomial
+// for 2^f on [-0.5, 0.5] (max relative error 2.3e-7 in fp32 Horner, on par
+// with ex2.approx), exponent added in the integer domain.  Inputs below -125
+// are clamped (weights < 2^-125 are zero for every practical purpose; the
+// MUFU path flushes them to exactly 0).
+__device__ __forceinline__ float poly_ex2(float x)
+{
+    x = fmaxf(x, -125.0f);
+    const float t = x + 12582912.0f;
+    const float j = t - 12582912.0f;
+    const float f = x - j;
+    float p = fmaf(0.001327647129073739f, f, 0.009675541892647743f);
+    p = fmaf(p, f, 0.05550713092088699f);
+    p = fmaf(p, f, 0.24022120237350464f);
+    p = fmaf(p, f, 0.6931469440460205f);
+    p = fmaf(p, f, 1.0000001192092896f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ void decode_range(const uint32_t* lohi, int b, float coef, float& s,
                                              float& range)
 {
@@ -49,7 +69,9 @@ __device__ __forceinline__ void decode_range(const uint32_t* lohi, int b, float 
 // MODE 1: joint, guide channel == image channel (or C == GC == 1)
 // MODE 2: joint, one grayscale guide shared by NC = 3 image channels: one
 //         exponential per tap serves all three channels.
-template <int R, int P, int MODE>
+// POLY: every POLY-th tap of a row evaluates its exponential with poly_ex2
+// on the FMA pipe instead of MUFU.EX2 (0 = never), balancing the two pipes.
+template <int R, int P, int MODE, int POLY>
 __global__ void __launch_bounds__(256) k_grad_blf(const BlfParams p)
 {
     constexpr int TW = 16 * P;
@@ -184,7 +206,9 @@ __global__ void __launch_bounds__(256) k_grad_blf(const BlfParams p)
                 for (int q = 0; q < P; ++q) {
                     const float v = gv[q + dx + R];
                     const float d = gs[q] - v;
-                    const float w = fast_ex2(fmaf(-d, d, cx));
+                    const float e = fmaf(-d, d, cx);
+                    const int tap = (dx + R) * P + q;
+                    const float w = (POLY > 0 && tap % POLY == POLY - 1) ? poly_ex2(e) : fast_ex2(e);
                     zr[q] += w;
 #pragma unroll
                     for (int c = 0; c < NC; ++c)
@@ -322,7 +346,7 @@ __global__ void __launch_bounds__(256) k_grad_blf_any(const BlfParams p)
 
 // ------------------------------------------------------------- dispatch --
 
-template <int R, int P, int MODE>
+template <int R, int P, int MODE, int POLY>
 static cudaError_t launch_fixed(const BlfParams& p, int nz, cudaStream_t st)
 {
     constexpr int TW = 16 * P, TH = 16;
@@ -330,11 +354,11 @@ static cudaError_t launch_fixed(const BlfParams& p, int nz, cudaStream_t st)
     constexpr int NARR = MODE == 0 ? 2 : (MODE == 1 ? 4 : 8);
     const size_t smem = (size_t)NARR * ROWS * PITCH * sizeof(float);
     // not a stream operation: legal while the stream is being captured
-    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE, POLY>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + TW - 1) / TW, (p.y1 - p.y0 + TH - 1) / TH, nz);
-    k_grad_blf<R, P, MODE><<<grid, 256, smem, st>>>(p);
+    k_grad_blf<R, P, MODE, POLY><<<grid, 256, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -353,22 +377,42 @@ static cudaError_t launch_any(const BlfParams& p, int nz, cudaStream_t st)
     return cudaGetLastError();
 }
 
+// default SFU-offload period per mode: self / per-channel joint spend 4 FP32
+// ops per tap next to the MUFU op, the shared-guide mode 6 (3 channels)
+template <int MODE>
+constexpr int kPolyDefault = MODE == 2 ? 0 : 6;
+
+template <int R, int P, int MODE>
+static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
+{
+    // p.poly_period < 0: the per-mode default; otherwise an experiment override
+    switch (p.poly_period < 0 ? kPolyDefault<MODE> : p.poly_period) {
+        case 0: return launch_fixed<R, P, MODE, 0>(p, nz, st);
+        case 4: return launch_fixed<R, P, MODE, 4>(p, nz, st);
+        case 5: return launch_fixed<R, P, MODE, 5>(p, nz, st);
+        case 8: return launch_fixed<R, P, MODE, 8>(p, nz, st);
+        case 12: return launch_fixed<R, P, MODE, 12>(p, nz, st);
+        default: return launch_fixed<R, P, MODE, 6>(p, nz, st);
+    }
+}
+
 template <int MODE>
 static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 {
     constexpr int P = MODE == 2 ? 2 : 4;
+    constexpr int D = kPolyDefault<MODE>;
     switch (p.radius) {
-        case 1: return launch_fixed<1, P, MODE>(p, nz, st);
-        case 2: return launch_fixed<2, P, MODE>(p, nz, st);
-        case 3: return launch_fixed<3, P, MODE>(p, nz, st);
-        case 4: return launch_fixed<4, P, MODE>(p, nz, st);
-        case 5: return launch_fixed<5, P, MODE>(p, nz, st);
-        case 6: return launch_fixed<6, P, MODE>(p, nz, st);
-        case 7: return launch_fixed<7, P, MODE>(p, nz, st);
-        case 8: return launch_fixed<8, P, MODE>(p, nz, st);
-        case 10: return launch_fixed<10, P, MODE>(p, nz, st);
-        case 12: return launch_fixed<12, P, MODE>(p, nz, st);
-        case 15: return launch_fixed<15, P, MODE>(p, nz, st);
+        case 1: return launch_fixed<1, P, MODE, D>(p, nz, st);
+        case 2: return launch_fixed<2, P, MODE, D>(p, nz, st);
+        case 3: return launch_fixed<3, P, MODE, D>(p, nz, st);
+        case 4: return launch_fixed<4, P, MODE, D>(p, nz, st);
+        case 5: return launch_poly<5, P, MODE>(p, nz, st);
+        case 6: return launch_fixed<6, P, MODE, D>(p, nz, st);
+        case 7: return launch_poly<7, P, MODE>(p, nz, st);
+        case 8: return launch_fixed<8, P, MODE, D>(p, nz, st);
+        case 10: return launch_fixed<10, P, MODE, D>(p, nz, st);
+        case 12: return launch_fixed<12, P, MODE, D>(p, nz, st);
+        case 15: return launch_poly<15, P, MODE>(p, nz, st);
         default: return launch_any<MODE>(p, nz, st);
     }
 }
