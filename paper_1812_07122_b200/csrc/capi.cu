@@ -493,6 +493,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         b.radius = radius;
         b.poly_period = -1;
         if (const char* ev = std::getenv("BLFLS_POLY_PERIOD")) b.poly_period = std::atoi(ev);
+        b.legacy_joint3 = 0;
+        if (const char* ev = std::getenv("BLFLS_PACKED_JOINT3")) b.legacy_joint3 = -std::atoi(ev);
+        b.joint3_rows = 2;
+        if (const char* ev = std::getenv("BLFLS_J3_ROWS")) b.joint3_rows = std::atoi(ev);
         b.range_coef = (float)std::sqrt(1.4426950408889634 / (8.0 * q.sigma_r * q.sigma_r));
         for (int d = 0; d <= kMaxRadius; ++d) {
             const double c = -(double)d * d / (2.0 * q.sigma_s * q.sigma_s) * 1.4426950408889634;

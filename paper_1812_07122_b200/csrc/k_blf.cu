@@ -238,6 +238,175 @@ __global__ void __launch_bounds__(256) k_grad_blf(const BlfParams p)
     }
 }
 
+// MODE 2 with packed accumulation: one grayscale guide shared by three image
+// channels.  Channels are interleaved in shared memory as {g0, g1} and
+// {g2, 1}, so each tap's weight updates all four sums (three numerators and
+// the normaliser) with two FFMA2 (sm_100 packed f32x2) instead of four FP32
+// instructions: per tap FADD, FFMA, MUFU.EX2, 2x FFMA2.
+__device__ __forceinline__ unsigned long long pk2(float a, float b)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r)
+{
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c)
+{
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+template <int R, int QR, int P, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_grad_blf_joint3(const BlfParams p)
+{
+    // 256 threads = 16 x 16; a thread owns QR rows x P = 2 columns of outputs,
+    // so every shared-memory window row it loads feeds QR output rows (fewer
+    // MIO ops per MUFU.EX2).  One gradient axis is staged at a time.
+    constexpr int TW = 16 * P, TH = 16 * QR;
+    constexpr int ROWS = TH + 2 * R;
+    constexpr int COLS = TW + 2 * R;
+    constexpr int PITCH = (COLS + 3) & ~1;        // float2 elements (+ room for vector tails)
+    constexpr int VN = 2 * R + P;
+    constexpr int GP = (COLS + 3) & ~3;           // guide pitch (floats)
+    extern __shared__ __align__(16) float sm[];
+    float* G = sm;                                          // [ROWS][GP]
+    float2* S01 = reinterpret_cast<float2*>(sm + ROWS * GP); // [ROWS][PITCH] {g0, g1}
+    float2* S2 = S01 + ROWS * PITCH;                        // [ROWS][PITCH] {g2, 1}
+
+    const int H = p.H, W = p.W;
+    const int b = blockIdx.z;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range, sg, grange;
+    decode_range(p.lohi, b, p.range_coef, s, range);
+    decode_range(p.glohi, b, p.range_coef, sg, grange);
+    const float* fimg = p.f + (size_t)b * 3 * plane;
+    const float* gimg = p.guide + (size_t)b * p.GC * plane;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int ox = tx0 + tx * P;
+    const float oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
+
+#pragma unroll 1
+    for (int axis = 0; axis < 2; ++axis) {
+        if (axis) __syncthreads();
+        for (int idx = threadIdx.x; idx < ROWS * COLS; idx += 256) {
+            const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
+            const int y = ty0 - R + i, x = tx0 - R + j;
+            const bool in = y >= 0 && y < H && x >= 0 && x < W;
+            const int og = i * GP + j, o = i * PITCH + j;
+            if (in) {
+                const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                const int y1 = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+                const size_t r0 = (size_t)y * W + x, r1 = (size_t)y1 * W + x1;
+                G[og] = (__ldg(gimg + r1) - __ldg(gimg + r0)) * sg;
+                float g[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float* fc = fimg + (size_t)c * plane;
+                    g[c] = __ldg(fc + r1) - __ldg(fc + r0);
+                }
+                S01[o] = make_float2(g[0], g[1]);
+                S2[o] = make_float2(g[2], 1.0f);
+            } else {
+                G[og] = kSentinel;
+                S01[o] = make_float2(0.f, 0.f);
+                S2[o] = make_float2(0.f, 0.f);
+            }
+        }
+        __syncthreads();
+
+        const unsigned long long* A01 = reinterpret_cast<const unsigned long long*>(S01);
+        const unsigned long long* A2 = reinterpret_cast<const unsigned long long*>(S2);
+        float gs[QR][P];
+        unsigned long long acc01[QR][P], acc2z[QR][P];
+#pragma unroll
+        for (int i = 0; i < QR; ++i)
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                gs[i][q] = G[(ty * QR + i + R) * GP + tx * P + q + R];
+                acc01[i][q] = 0ull;
+                acc2z[i][q] = 0ull;
+            }
+        // source rows ty*QR + sr, sr in [0, QR + 2R): output row i sees dy = sr - i - R
+#pragma unroll 1
+        for (int sr = 0; sr < QR + 2 * R; ++sr) {
+            const int rowg = (ty * QR + sr) * GP + tx * P;
+            const int rows = (ty * QR + sr) * PITCH + tx * P;
+            float gv[VN];
+#pragma unroll
+            for (int k = 0; k < VN / 2; ++k) {
+                const float2 t = *reinterpret_cast<const float2*>(G + rowg + 2 * k);
+                gv[2 * k] = t.x;
+                gv[2 * k + 1] = t.y;
+            }
+            unsigned long long a01[VN], a2[VN];
+#pragma unroll
+            for (int k = 0; k < VN; ++k) {
+                a01[k] = A01[rows + k];
+                a2[k] = A2[rows + k];
+            }
+#pragma unroll
+            for (int i = 0; i < QR; ++i) {
+                const int dy = sr - i - R;
+                if (dy < -R || dy > R) continue;  // warp-uniform
+                unsigned long long r01[P], r2z[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    r01[q] = 0ull;
+                    r2z[q] = 0ull;
+                }
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) {
+                    const float cx = p.cs[dx < 0 ? -dx : dx];
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int k = q + dx + R;
+                        const float d = gs[i][q] - gv[k];
+                        const float w = fast_ex2(fmaf(-d, d, cx));
+                        const unsigned long long ww = pk2(w, w);
+                        r01[q] = ffma2(ww, a01[k], r01[q]);
+                        r2z[q] = ffma2(ww, a2[k], r2z[q]);
+                    }
+                }
+                const float wy = p.wrow[dy < 0 ? -dy : dy];
+                const unsigned long long wyy = pk2(wy, wy);
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    acc01[i][q] = ffma2(r01[q], wyy, acc01[i][q]);
+                    acc2z[i][q] = ffma2(r2z[q], wyy, acc2z[i][q]);
+                }
+            }
+        }
+        float* dst = axis == 0 ? p.tx : p.ty;
+        const size_t pl = (size_t)p.out_rows * W;
+#pragma unroll
+        for (int i = 0; i < QR; ++i) {
+            const int oy = ty0 + ty * QR + i;
+            if (oy >= p.y1) continue;
+            const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                if (ox + q >= W) continue;
+                const float2 n01 = upk2(acc01[i][q]);
+                const float2 n2z = upk2(acc2z[i][q]);
+                const float inv = oscale / n2z.y;
+                const size_t o = orow + ox + q;
+                dst[((size_t)b * 3 + 0) * pl + o] = n01.x * inv;
+                dst[((size_t)b * 3 + 1) * pl + o] = n01.y * inv;
+                dst[((size_t)b * 3 + 2) * pl + o] = n2z.x * inv;
+            }
+        }
+    }
+}
+
 // Generic-radius variant (any R up to kMaxRadius): same tiling, window loops
 // not unrolled, taps read straight from shared memory.
 template <int MODE>
@@ -380,7 +549,34 @@ static cudaError_t launch_any(const BlfParams& p, int nz, cudaStream_t st)
 // default SFU-offload period per mode: self / per-channel joint spend 4 FP32
 // ops per tap next to the MUFU op, the shared-guide mode 6 (3 channels)
 template <int MODE>
-constexpr int kPolyDefault = MODE == 2 ? 0 : 6;
+constexpr int kPolyDefault = 0;  // r01 sweep (tools/poly_sweep.py): offload does not pay yet
+
+template <int R, int QR, int P, int MINB>
+static cudaError_t launch_joint3_q(const BlfParams& p, int nz, cudaStream_t st)
+{
+    constexpr int TW = 16 * P, TH = 16 * QR, ROWS = TH + 2 * R, COLS = TW + 2 * R;
+    constexpr int PITCH = (COLS + 3) & ~1, GP = (COLS + 3) & ~3;
+    const size_t smem = (size_t)ROWS * GP * sizeof(float) + (size_t)2 * ROWS * PITCH * sizeof(float2);
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf_joint3<R, QR, P, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + TW - 1) / TW, (p.y1 - p.y0 + TH - 1) / TH, nz);
+    k_grad_blf_joint3<R, QR, P, MINB><<<grid, 256, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_joint3(const BlfParams& p, int nz, cudaStream_t st)
+{
+    // rows per thread: experiment override via BLFLS_J3_ROWS, default 2
+    switch (p.joint3_rows) {
+        case 2: return launch_joint3_q<R, 2, 2, 1>(p, nz, st);
+        case 4: return launch_joint3_q<R, 1, 4, 1>(p, nz, st);   // 4 columns per thread
+        case 5: return launch_joint3_q<R, 1, 4, 2>(p, nz, st);   // 4 columns, <= 128 regs
+        case 6: return launch_joint3_q<R, 1, 2, 3>(p, nz, st);   // 2 columns, <= 80 regs
+        default: return launch_joint3_q<R, 1, 2, 1>(p, nz, st);
+    }
+}
 
 template <int R, int P, int MODE>
 static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
@@ -399,8 +595,23 @@ static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
 template <int MODE>
 static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 {
-    constexpr int P = MODE == 2 ? 2 : 4;
+    constexpr int P = 4;
     constexpr int D = kPolyDefault<MODE>;
+    if constexpr (MODE == 2) {
+        // experiment only (BLFLS_PACKED_JOINT3=1): FFMA2-packed accumulation.
+        // r01 sweep (tools/variant_sweep.py, c5): the unpacked 4-column kernel
+        // is faster (0.70 vs 0.64-0.66 of MUFU peak), so it is the default.
+        if (p.legacy_joint3 < 0) {
+            switch (p.radius) {
+                case 3: return launch_joint3<3>(p, nz, st);
+                case 5: return launch_joint3<5>(p, nz, st);
+                case 7: return launch_joint3<7>(p, nz, st);
+                case 11: return launch_joint3<11>(p, nz, st);
+                case 15: return launch_joint3<15>(p, nz, st);
+                default: break;
+            }
+        }
+    }
     switch (p.radius) {
         case 1: return launch_fixed<1, P, MODE, D>(p, nz, st);
         case 2: return launch_fixed<2, P, MODE, D>(p, nz, st);
