@@ -306,3 +306,38 @@ def test_fused_minmax_epilogue(gpu, oracle, c, h, w):
     plan = gpu.get_plan(h, w, c, 0, 3, 2.0, 0.1, 1000.0, 1, 0)
     lo, hi = plan.debug_ranges()[1][0]
     assert lo == float(one.min()) and hi == float(one.max())
+
+
+@pytest.mark.parametrize("nbands", [1, 2, 3, 4])
+def test_band_mode_matches_single_gpu(gpu, oracle, nbands):
+    """Row-band decomposition (multi-GPU band driver), bands run one after the
+    other on this GPU: identical to the single-GPU path."""
+    import torch
+    from paper_1812_07122_b200.multigpu import band_rows, gpu_band_ops
+    c, h, w = 1, 96, 128
+    img = torch.from_numpy(_img(oracle, c, h, w, 21)).cuda()
+    kw = dict(lam=2000.0, sigma_s=12.0, sigma_r=0.08, radius=15)
+    ref = gpu.blf_ls(img, iters=2, **kw)
+    fr, so = gpu_band_ops(h, w, c, 0, device=0, **kw)
+    f = img
+    for _ in range(2):
+        parts = [fr(f, None, y0, y1) for y0, y1 in band_rows(h, nbands)]
+        tx = torch.cat([p[0] for p in parts], dim=1).contiguous()
+        ty = torch.cat([p[1] for p in parts], dim=1).contiguous()
+        f = so(f, tx, ty)
+    torch.cuda.synchronize()
+    assert (f - ref).abs().max().item() == 0.0
+
+
+def test_band_driver_single_rank(gpu, oracle):
+    import torch
+    from paper_1812_07122_b200.multigpu import band_blf_ls, gpu_band_ops
+    c, h, w = 3, 64, 80
+    img = torch.from_numpy(_img(oracle, c, h, w, 5)).cuda()
+    guide = torch.from_numpy(_img(oracle, 1, h, w, 6)).cuda()
+    kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, radius=7)
+    fr, so = gpu_band_ops(h, w, c, 1, device=0, **kw)
+    out = band_blf_ls(img, guide, 3, filter_rows=fr, solve=so)
+    ref = oracle.blf_ls(img.cpu().numpy().astype(np.float64), guide.cpu().numpy().astype(np.float64),
+                        iters=3, **kw)
+    assert maxabs(out.cpu().numpy(), ref) <= TOL_OUT

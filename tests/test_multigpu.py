@@ -1,0 +1,151 @@
+"""Multi-GPU host logic on CPU: world_size 2 over gloo (127.0.0.1).
+
+The band driver (paper_1812_07122_b200.multigpu.band_blf_ls) is run with
+the CPU oracle standing in for the two device stages; its result must equal
+the single-process oracle cascade.  The batch sharding is checked the same way.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1812_07122_b200.multigpu import band_blf_ls, band_rows, batch_shard  # noqa: E402
+
+PRM = dict(lam=800.0, sigma_s=3.0, sigma_r=0.1, radius=4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_ops():
+    from oracle import oracle as O
+
+    def filter_rows(f, guide, y0, y1):
+        g = f.double().numpy()
+        gn, lo, hi = O.normalize_to_unit(g)
+        rng = hi - lo
+        if guide is not None:
+            gd = guide.double().numpy()
+            gdn, _, _ = O.normalize_to_unit(gd)
+            gx_g, gy_g = O.forward_gradients(np.repeat(gdn, g.shape[0], axis=0) if gdn.shape[0] == 1 else gdn)
+        gx, gy = O.forward_gradients(gn)
+        if guide is None:
+            gx_g, gy_g = gx, gy
+        out = []
+        for src, gd in ((gx, gx_g), (gy, gy_g)):
+            t = np.stack([2.0 * O.blf_brute_r((src[c:c + 1] + 1) / 2, (gd[c:c + 1] + 1) / 2,
+                                              sigma_s=PRM["sigma_s"], sigma_r=PRM["sigma_r"],
+                                              radius=PRM["radius"])[0] - 1.0
+                          for c in range(g.shape[0])])
+            out.append(torch.from_numpy(t[:, y0:y1] * rng))
+        return out[0], out[1]
+
+    def solve(f, tx, ty):
+        u = O.lsgrad_solve_fft(f.double().numpy(), tx.double().numpy(), ty.double().numpy(),
+                               lam=PRM["lam"])
+        return torch.from_numpy(u)
+
+    return filter_rows, solve
+
+
+def _band_worker(rank, world, port, img, guide, iters, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fr, so = oracle_ops()
+        out = band_blf_ls(torch.from_numpy(img), None if guide is None else torch.from_numpy(guide),
+                          iters, filter_rows=fr, solve=so)
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, fn, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, *args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_band_rows_partition():
+    for h in (5, 16, 17, 1080, 4096):
+        for w in (1, 2, 3, 4, 8):
+            if h < w:
+                continue
+            b = band_rows(h, w)
+            assert b[0][0] == 0 and b[-1][1] == h
+            assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+            assert all(y1 > y0 for y0, y1 in b)
+    with pytest.raises(ValueError):
+        band_rows(3, 4)
+
+
+def test_batch_shard_partition():
+    for n in (1, 7, 64):
+        for w in (1, 2, 3, 8):
+            sh = [batch_shard(n, w, r) for r in range(w)]
+            assert sh[0][0] == 0 and sh[-1][1] == n
+            assert all(sh[i][1] == sh[i + 1][0] for i in range(w - 1))
+
+
+@pytest.mark.parametrize("h,w,c,guided", [(24, 20, 1, False), (23, 16, 3, True)])
+def test_band_driver_world2_matches_cascade(oracle, h, w, c, guided):
+    rng = np.random.default_rng(h * w)
+    img = rng.random((c, h, w))
+    guide = rng.random((1, h, w)) if guided else None
+    res = _run(2, _band_worker, img, guide, 2)
+    ref = oracle.blf_ls(img, guide, iters=2, **PRM)
+    for r in (0, 1):
+        assert np.abs(res[r] - ref).max() < 1e-10
+    assert np.array_equal(res[0], res[1])
+
+
+def _batch_worker(rank, world, port, imgs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        i0, i1 = batch_shard(imgs.shape[0], world, rank)
+        mine = np.stack([O.blf_ls(imgs[i], iters=1, **PRM) for i in range(i0, i1)])
+        per = -(-imgs.shape[0] // world)
+        buf = torch.zeros((per,) + mine.shape[1:], dtype=torch.float64)
+        buf[: mine.shape[0]] = torch.from_numpy(mine)
+        allb = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(allb, buf)
+        parts = [allb[r][: batch_shard(imgs.shape[0], world, r)[1] - batch_shard(imgs.shape[0], world, r)[0]]
+                 for r in range(world)]
+        q.put((rank, torch.cat(parts).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_sharding_world2(oracle):
+    rng = np.random.default_rng(5)
+    imgs = rng.random((3, 1, 16, 20))
+    res = _run(2, _batch_worker, imgs)
+    for i in range(3):
+        ref = oracle.blf_ls(imgs[i], iters=1, **PRM)
+        assert np.abs(res[0][i] - ref).max() == 0.0
