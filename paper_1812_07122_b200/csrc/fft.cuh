@@ -58,6 +58,25 @@ __device__ __forceinline__ void dft_small(float2 (&a)[P], float sg /* -1 fwd, +1
         a[2] = csub(s02, s13);
         a[1] = cadd(d02, jd);
         a[3] = csub(d02, jd);
+    } else if constexpr (P == 8) {
+        // radix-2 DIF step (twiddles w8^k) then two radix-4 DFTs
+        constexpr float r = 0.70710678118654752440f;
+        float2 b[4], c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            b[k] = cadd(a[k], a[k + 4]);
+            c[k] = csub(a[k], a[k + 4]);
+        }
+        c[1] = make_float2(r * (c[1].x - sg * c[1].y), r * (c[1].y + sg * c[1].x));    // * (r, sg r)
+        c[2] = cmuli(c[2], sg);                                                         // * (0, sg)
+        c[3] = make_float2(r * (-c[3].x - sg * c[3].y), r * (-c[3].y + sg * c[3].x));  // * (-r, sg r)
+        dft_small<4>(b, sg);
+        dft_small<4>(c, sg);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            a[2 * m] = b[m];
+            a[2 * m + 1] = c[m];
+        }
     } else if constexpr (P == 5) {
         const float c1 = 0.30901699437494742410f, c2 = -0.80901699437494742410f;
         const float s1 = 0.95105651629515357212f * sg, s2 = 0.58778525229247312917f * sg;
@@ -205,20 +224,21 @@ __device__ void fft_run(float2* buf, const FftDesc& d, int V, int log2V, bool in
 namespace blfls {
 
 constexpr int ct_count(int n, int p) { return n % p == 0 ? 1 + ct_count(n / p, p) : 0; }
-constexpr int ct_n4(int n) { return ct_count(n, 4); }
-constexpr int ct_rest2(int n)
+// power-of-two part as radix 8s, then one 4 or 2; then 3s, then 5s
+constexpr int ct_n8(int n) { return ct_count(n, 2) / 3; }
+constexpr int ct_rest(int n) { return ct_count(n, 2) % 3; }  // 0, 1 (radix 2) or 2 (radix 4)
+constexpr int ct_nstages(int n)
 {
-    int m = n;
-    for (int i = 0; i < ct_n4(n); ++i) m /= 4;
-    return m % 2 == 0 ? 1 : 0;
+    return ct_n8(n) + (ct_rest(n) ? 1 : 0) + ct_count(n, 3) + ct_count(n, 5);
 }
-constexpr int ct_nstages(int n) { return ct_n4(n) + ct_rest2(n) + ct_count(n, 3) + ct_count(n, 5); }
 constexpr int ct_radix(int n, int i)
 {
-    if (i < ct_n4(n)) return 4;
-    i -= ct_n4(n);
-    if (i < ct_rest2(n)) return 2;
-    i -= ct_rest2(n);
+    if (i < ct_n8(n)) return 8;
+    i -= ct_n8(n);
+    if (ct_rest(n)) {
+        if (i == 0) return ct_rest(n) == 2 ? 4 : 2;
+        i -= 1;
+    }
     if (i < ct_count(n, 3)) return 3;
     return 5;
 }
@@ -236,6 +256,22 @@ constexpr bool ct_supported(int n)
     return m == 1;
 }
 
+// Shared-memory padding of the compile-time engine: the first Stockham
+// stages write with a stride of 8 complex (rows) or 8 rows of V complex
+// (columns), which would map 16 lanes onto 1-2 bank pairs.  One pad element
+// per 8 (rows) / V pad elements per 8*V (columns) spreads them over all banks.
+template <int V>
+constexpr int ct_log2(int v) { return v <= 1 ? 0 : 1 + ct_log2<V>(v / 2); }
+template <int V, bool COLS>
+__device__ __forceinline__ int ct_pad(int flat)
+{
+    if (COLS) {
+        constexpr int L = ct_log2<V>(V);
+        return flat + ((flat >> (3 + L)) << L);
+    }
+    return flat + (flat >> 3);
+}
+
 template <int N, int V, int TV, bool COLS, bool INV, int P, int S>
 __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2* __restrict__ tw)
 {
@@ -243,7 +279,7 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
     constexpr int NB = (NBP + TV - 1) / TV;
     constexpr bool PRED = NB * TV != NBP;
     constexpr float sg = INV ? 1.0f : -1.0f;
-    auto addr = [&](int j) { return COLS ? j * V + v : v * N + j; };
+    auto addr = [&](int j) { return ct_pad<V, COLS>(COLS ? j * V + v : v * N + j); };
     float2 a[NB][P];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -290,6 +326,16 @@ struct CtFft {
     __device__ __forceinline__ int n() const { return N; }
     __device__ __forceinline__ int vecs() const { return V; }
     template <bool COLS>
+    __device__ __forceinline__ int pad(int flat) const { return ct_pad<V, COLS>(flat); }
+    __device__ __forceinline__ int threads() const { return THREADS; }  // compile-time
+    static size_t smem_bytes(bool cols)
+    {
+        const int last = V * N - 1;
+        const int L = ct_log2<V>(V);
+        const int padded = cols ? last + ((last >> (3 + L)) << L) : last + (last >> 3);
+        return (size_t)(padded + 1) * sizeof(float2);
+    }
+    template <bool COLS>
     __device__ __forceinline__ void run(float2* buf, bool inv) const
     {
         const int v = COLS ? (int)threadIdx.x % V : (int)threadIdx.x / TV;
@@ -307,6 +353,10 @@ struct RtFft {
     int V, log2V;
     __device__ __forceinline__ int n() const { return d.n; }
     __device__ __forceinline__ int vecs() const { return V; }
+    template <bool COLS>
+    __device__ __forceinline__ int pad(int flat) const { return flat; }
+    __device__ __forceinline__ int threads() const { return blockDim.x; }
+    size_t smem_bytes(bool) const { return (size_t)V * d.n * sizeof(float2); }
     template <bool COLS>
     __device__ __forceinline__ void run(float2* buf, bool inv) const
     {

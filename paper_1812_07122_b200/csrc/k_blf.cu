@@ -407,6 +407,183 @@ __global__ void __launch_bounds__(256, MINB) k_grad_blf_joint3(const BlfParams p
     }
 }
 
+// ---------------------------------------------------------------------------
+// Packed self-guided kernel (MODE 0): pairs of adjacent outputs (q, q+1)
+// share every instruction through sm_100 f32x2 math:
+//   d = {gs_q, gs_q+1} - {v_k, v_k+1}        FADD2
+//   e = -d*d + {c_dx, c_dx}                  FFMA2
+//   w = {ex2(e.x), ex2(e.y)}                 2x MUFU.EX2 (or the FMA-pipe poly)
+//   {z_q, z_q+1} += w ; {n_q, n_q+1} += w*v  FADD2 + FFMA2
+// so a tap costs 2 issue slots + 1 MUFU instead of 4 + 1.  {v_k, v_k+1} must be
+// an aligned register pair; the window is kept twice (from the gradient array
+// and from a copy shifted by one column) so both parities of k are aligned.
+// POLY: every POLY-th pair-tap evaluates both exponentials with poly_ex2 on
+// the FMA pipe, balancing the FMA and SFU pipes.
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x f2(float a, float b)
+{
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2u(f2x r)
+{
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b)
+{
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x sub2(f2x a, f2x b)
+{
+    f2x d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c)
+{
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2x neg2(f2x a) { return a ^ 0x8000000080000000ull; }
+
+__device__ __forceinline__ f2x poly_ex2x2(f2x e)
+{
+    float2 x = f2u(e);
+    x.x = fmaxf(x.x, -125.0f);
+    x.y = fmaxf(x.y, -125.0f);
+    const f2x xx = f2(x.x, x.y);
+    const f2x magic = f2(12582912.0f, 12582912.0f);
+    const f2x t = add2(xx, magic);
+    const f2x f = sub2(xx, sub2(t, magic));
+    f2x p = fma2(f2(0.001327647129073739f, 0.001327647129073739f), f,
+                 f2(0.009675541892647743f, 0.009675541892647743f));
+    p = fma2(p, f, f2(0.05550713092088699f, 0.05550713092088699f));
+    p = fma2(p, f, f2(0.24022120237350464f, 0.24022120237350464f));
+    p = fma2(p, f, f2(0.6931469440460205f, 0.6931469440460205f));
+    p = fma2(p, f, f2(1.0000001192092896f, 1.0000001192092896f));
+    const float2 pp = f2u(p), tt = f2u(t);
+    return f2(__int_as_float(__float_as_int(pp.x) + (__float_as_int(tt.x) << 23)),
+              __int_as_float(__float_as_int(pp.y) + (__float_as_int(tt.y) << 23)));
+}
+
+template <int R, int POLY>
+__global__ void __launch_bounds__(256) k_grad_blf_x2(const BlfParams p)
+{
+    constexpr int P = 4, TW = 64, TH = 16;
+    constexpr int ROWS = TH + 2 * R;
+    constexpr int COLS = TW + 2 * R;
+    constexpr int PITCH = ((COLS + 3) & ~3) + 4;  // room for the +1-shifted copy's tail
+    constexpr int VN = ((2 * R + P + 1) + 3) & ~3; // window floats (multiple of 4)
+    constexpr int NV = VN / 4;
+    extern __shared__ __align__(16) float sm[];
+    float* G0 = sm;                 // [ROWS][PITCH] scaled gradients of this axis
+    float* G1 = sm + ROWS * PITCH;  // G1[i][j] = G0[i][j + 1]
+
+    const int H = p.H, W = p.W, C = p.C;
+    const int b = blockIdx.z / C;
+    const int c0 = blockIdx.z % C;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range;
+    decode_range(p.lohi, b, p.range_coef, s, range);
+    const float* fimg = p.f + ((size_t)b * C + c0) * plane;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int oy = ty0 + ty;
+    const int ox = tx0 + tx * P;
+    const float oscale = p.normalized_out ? 1.f / p.range_coef : 1.f / s;
+
+#pragma unroll 1
+    for (int axis = 0; axis < 2; ++axis) {
+        if (axis) __syncthreads();
+        for (int idx = threadIdx.x; idx < ROWS * (COLS + 1); idx += 256) {
+            const int i = idx / (COLS + 1), j = idx - (idx / (COLS + 1)) * (COLS + 1);
+            const int y = ty0 - R + i, x = tx0 - R + j;
+            float g = kSentinel;
+            if (y >= 0 && y < H && x >= 0 && x < W) {
+                const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                const int y1 = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+                g = (__ldg(fimg + (size_t)y1 * W + x1) - __ldg(fimg + (size_t)y * W + x)) * s;
+            }
+            if (j < COLS) G0[i * PITCH + j] = g;
+            if (j > 0) G1[i * PITCH + j - 1] = g;
+        }
+        __syncthreads();
+
+        f2x gs01, gs23, z01 = 0ull, z23 = 0ull, n01 = 0ull, n23 = 0ull;
+        {
+            const float* c = G0 + (ty + R) * PITCH + tx * P + R;
+            gs01 = f2(c[0], c[1]);
+            gs23 = f2(c[2], c[3]);
+        }
+#pragma unroll 1
+        for (int dy = -R; dy <= R; ++dy) {
+            const int row = (ty + R + dy) * PITCH + tx * P;
+            // wa[m] = {v_2m, v_2m+1}, wb[m] = {v_2m+1, v_2m+2}
+            f2x wa[VN / 2], wb[VN / 2];
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const float4 a = *reinterpret_cast<const float4*>(G0 + row + 4 * k);
+                const float4 c = *reinterpret_cast<const float4*>(G1 + row + 4 * k);
+                wa[2 * k] = f2(a.x, a.y);
+                wa[2 * k + 1] = f2(a.z, a.w);
+                wb[2 * k] = f2(c.x, c.y);
+                wb[2 * k + 1] = f2(c.z, c.w);
+            }
+            f2x zr01 = 0ull, zr23 = 0ull, nr01 = 0ull, nr23 = 0ull;
+#pragma unroll
+            for (int dx = -R; dx <= R; ++dx) {
+                const float cxs = p.cs[dx < 0 ? -dx : dx];
+                const f2x cx = f2(cxs, cxs);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {       // output pair (0,1) or (2,3)
+                    const int k = 2 * h + dx + R;   // window index of output 2h's tap
+                    const f2x v = (k & 1) ? wb[k >> 1] : wa[k >> 1];
+                    const f2x d = sub2(h ? gs23 : gs01, v);
+                    const f2x e = fma2(neg2(d), d, cx);
+                    f2x w;
+                    if (POLY > 0 && ((dx + R) * 2 + h) % POLY == POLY - 1) {
+                        w = poly_ex2x2(e);
+                    } else {
+                        const float2 ee = f2u(e);
+                        w = f2(fast_ex2(ee.x), fast_ex2(ee.y));
+                    }
+                    if (h) {
+                        zr23 = add2(zr23, w);
+                        nr23 = fma2(w, v, nr23);
+                    } else {
+                        zr01 = add2(zr01, w);
+                        nr01 = fma2(w, v, nr01);
+                    }
+                }
+            }
+            const float wys = p.wrow[dy < 0 ? -dy : dy];
+            const f2x wy = f2(wys, wys);
+            z01 = fma2(zr01, wy, z01);
+            z23 = fma2(zr23, wy, z23);
+            n01 = fma2(nr01, wy, n01);
+            n23 = fma2(nr23, wy, n23);
+        }
+        if (oy < p.y1) {
+            float* dst = axis == 0 ? p.tx : p.ty;
+            float* o = dst + ((size_t)b * C + c0) * ((size_t)p.out_rows * W) +
+                       (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
+            const float2 za = f2u(z01), zb = f2u(z23), na = f2u(n01), nb = f2u(n23);
+            const float r[4] = {na.x / za.x * oscale, na.y / za.y * oscale, nb.x / zb.x * oscale,
+                                nb.y / zb.y * oscale};
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+                if (ox + q < W) o[ox + q] = r[q];
+        }
+    }
+}
+
 // Generic-radius variant (any R up to kMaxRadius): same tiling, window loops
 // not unrolled, taps read straight from shared memory.
 template <int MODE>
@@ -578,6 +755,33 @@ static cudaError_t launch_joint3(const BlfParams& p, int nz, cudaStream_t st)
     }
 }
 
+template <int R, int POLY>
+static cudaError_t launch_x2(const BlfParams& p, int nz, cudaStream_t st)
+{
+    constexpr int TW = 64, TH = 16, ROWS = TH + 2 * R, COLS = TW + 2 * R;
+    constexpr int PITCH = ((COLS + 3) & ~3) + 4;
+    const size_t smem = (size_t)2 * ROWS * PITCH * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf_x2<R, POLY>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + TW - 1) / TW, (p.y1 - p.y0 + TH - 1) / TH, nz);
+    k_grad_blf_x2<R, POLY><<<grid, 256, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_x2_poly(const BlfParams& p, int nz, cudaStream_t st)
+{
+    switch (p.x2_poly) {
+        case 0: return launch_x2<R, 0>(p, nz, st);
+        case 3: return launch_x2<R, 3>(p, nz, st);
+        case 5: return launch_x2<R, 5>(p, nz, st);
+        case 6: return launch_x2<R, 6>(p, nz, st);
+        case 8: return launch_x2<R, 8>(p, nz, st);
+        default: return launch_x2<R, 4>(p, nz, st);
+    }
+}
+
 template <int R, int P, int MODE>
 static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
 {
@@ -597,6 +801,19 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 {
     constexpr int P = 4;
     constexpr int D = kPolyDefault<MODE>;
+    if constexpr (MODE == 0) {
+        if (p.x2_poly >= 0) {
+            switch (p.radius) {
+                case 3: return launch_x2_poly<3>(p, nz, st);
+                case 4: return launch_x2_poly<4>(p, nz, st);
+                case 5: return launch_x2_poly<5>(p, nz, st);
+                case 6: return launch_x2_poly<6>(p, nz, st);
+                case 7: return launch_x2_poly<7>(p, nz, st);
+                case 15: return launch_x2_poly<15>(p, nz, st);
+                default: break;
+            }
+        }
+    }
     if constexpr (MODE == 2) {
         // experiment only (BLFLS_PACKED_JOINT3=1): FFMA2-packed accumulation.
         // r01 sweep (tools/variant_sweep.py, c5): the unpacked 4-column kernel

@@ -44,36 +44,67 @@ __global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F f
     const float* f = p.f + poff;
     const float* tx = p.tx ? p.tx + poff : nullptr;
     const float* ty = p.ty ? p.ty + poff : nullptr;
-    for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
-        const int v = idx / n, j = idx - (idx / n) * n;
-        const int y = row0 + v;
-        float2 z = make_float2(0.f, 0.f);
-        if (y < p.H) {
-            if (!ODD) {
-                z.x = fold_value(p, f, tx, ty, y, 2 * j);
-                z.y = fold_value(p, f, tx, ty, y, 2 * j + 1);
-            } else {
-                z.x = fold_value(p, f, tx, ty, y, j);
+    if (!ODD && (p.W & 3) == 0) {
+        // 4 pixels (2 complex) per thread: float4 loads of f, Tx, Ty and the
+        // previous Ty row; Tx[x-1] is one scalar load (fold r = f + lambda D^T T)
+        const int w4 = p.W >> 2;
+#pragma unroll 4
+        for (int e = threadIdx.x; e < V * w4; e += fft.threads()) {
+            const int v = e / w4, x4 = e - v * w4;
+            const int y = row0 + v;
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (y < p.H) {
+                const size_t o = (size_t)y * p.W + 4 * x4;
+                r = __ldg(reinterpret_cast<const float4*>(f + o));
+                if (tx != nullptr) {
+                    const int ym = y == 0 ? p.H - 1 : y - 1;
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(tx + o));
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(ty + o));
+                    const float4 c = __ldg(reinterpret_cast<const float4*>(ty + (size_t)ym * p.W + 4 * x4));
+                    const float am = __ldg(tx + (size_t)y * p.W + (x4 == 0 ? p.W - 1 : 4 * x4 - 1));
+                    const float L = p.lambda;
+                    r.x = fmaf(L, (am - a.x) + (c.x - b.x), r.x);
+                    r.y = fmaf(L, (a.x - a.y) + (c.y - b.y), r.y);
+                    r.z = fmaf(L, (a.y - a.z) + (c.z - b.z), r.z);
+                    r.w = fmaf(L, (a.z - a.w) + (c.w - b.w), r.w);
+                }
             }
+            const int j = v * n + 2 * x4;
+            buf[fft.template pad<false>(j)] = make_float2(r.x, r.y);
+            buf[fft.template pad<false>(j + 1)] = make_float2(r.z, r.w);
         }
-        buf[idx] = z;
+    } else {
+        for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
+            const int v = idx / n, j = idx - (idx / n) * n;
+            const int y = row0 + v;
+            float2 z = make_float2(0.f, 0.f);
+            if (y < p.H) {
+                if (!ODD) {
+                    z.x = fold_value(p, f, tx, ty, y, 2 * j);
+                    z.y = fold_value(p, f, tx, ty, y, 2 * j + 1);
+                } else {
+                    z.x = fold_value(p, f, tx, ty, y, j);
+                }
+            }
+            buf[fft.template pad<false>(idx)] = z;
+        }
     }
     __syncthreads();
     fft.template run<false>(buf, false);
     const int wc = p.wc;
-    for (int idx = threadIdx.x; idx < V * wc; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < V * wc; idx += fft.threads()) {
         const int v = idx / wc, k = idx - (idx / wc) * wc;
         const int y = row0 + v;
         if (y >= p.H) continue;
         float2 X;
         if (!ODD) {
-            const float2 zk = buf[v * n + (k == n ? 0 : k)];
-            const float2 zn = cconj(buf[v * n + (k == 0 ? 0 : n - k)]);
+            const float2 zk = buf[fft.template pad<false>(v * n + (k == n ? 0 : k))];
+            const float2 zn = cconj(buf[fft.template pad<false>(v * n + (k == 0 ? 0 : n - k))]);
             const float2 e = cscale(cadd(zk, zn), 0.5f);
             const float2 o = cscale(cmuli(csub(zk, zn), -1.0f), 0.5f);  // (zk - zn) / (2i)
             X = cadd(e, cmul(__ldg(&p.post[k]), o));
         } else {
-            X = buf[v * n + k];
+            X = buf[fft.template pad<false>(v * n + k)];
         }
         p.spec[((size_t)plane * p.H + y) * p.spitch + k] = X;
     }
@@ -88,29 +119,40 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
     const int plane = blockIdx.y;
     const int v0 = blockIdx.x * V;
     float2* spec = p.spec + (size_t)plane * H * p.spitch;
-    for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
+    // cp.async (LDGSTS) straight into the padded strip: every copy of the
+    // thread is in flight at once instead of one load per loop trip
+    for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
         const int u = idx / V, c = idx - (idx / V) * V;
         const int v = v0 + c;
-        buf[idx] = v < p.wc ? spec[(size_t)u * p.spitch + v] : make_float2(0.f, 0.f);
+        float2* dst = buf + fft.template pad<true>(idx);
+        if (v < p.wc) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
+                         "l"(spec + (size_t)u * p.spitch + v));
+        } else {
+            *dst = make_float2(0.f, 0.f);
+        }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (p.mode & 1) fft.template run<true>(buf, false);
     if (p.mode & 2) {
-        for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
+        for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
             const int u = idx / V, c = idx - (idx / V) * V;
             const int v = v0 + c;
             float sc = p.inv_hw;
             if (p.mode == 3 && v < p.wc)
                 sc = p.inv_hw / fmaf(p.lambda, __ldg(&p.gain_y[u]) + __ldg(&p.gain_x[v]), 1.0f);
-            buf[idx] = cscale(buf[idx], sc);
+            const int pi = fft.template pad<true>(idx);
+            buf[pi] = cscale(buf[pi], sc);
         }
         __syncthreads();
         fft.template run<true>(buf, true);
     }
-    for (int idx = threadIdx.x; idx < V * H; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
         const int u = idx / V, c = idx - (idx / V) * V;
         const int v = v0 + c;
-        if (v < p.wc) spec[(size_t)u * p.spitch + v] = buf[idx];
+        if (v < p.wc) spec[(size_t)u * p.spitch + v] = buf[fft.template pad<true>(idx)];
     }
 }
 
@@ -153,7 +195,8 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
     const int plane = blockIdx.y;
     const int row0 = blockIdx.x * V;
     const int W = p.W;
-    for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < V * n; idx += fft.threads()) {
         const int v = idx / n, k = idx - (idx / n) * n;
         const int y = row0 + v;
         float2 Z = make_float2(0.f, 0.f);
@@ -179,17 +222,17 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
                 }
             }
         }
-        buf[idx] = Z;
+        buf[fft.template pad<false>(idx)] = Z;
     }
     __syncthreads();
     fft.template run<false>(buf, true);
     float lo = INFINITY, hi = -INFINITY;
     float* out = p.out + (size_t)plane * p.H * W;
-    for (int idx = threadIdx.x; idx < V * n; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < V * n; idx += fft.threads()) {
         const int v = idx / n, j = idx - (idx / n) * n;
         const int y = row0 + v;
         if (y >= p.H) continue;
-        const float2 z = buf[idx];
+        const float2 z = buf[fft.template pad<false>(idx)];
         if (!ODD) {
             *reinterpret_cast<float2*>(out + (size_t)y * W + 2 * j) = z;
             lo = fminf(lo, fminf(z.x, z.y));
@@ -334,7 +377,7 @@ template <class F>
 static void launch_pass(int which, const SolveParams& p, const F& f, int V, int n, int threads,
                         int planes, bool odd, cudaStream_t st)
 {
-    const size_t smem = (size_t)V * n * sizeof(float2);
+    const size_t smem = f.smem_bytes(which == 1);
     if (which == 1) {
         dim3 grid((p.wc + V - 1) / V, planes);
         set_smem(k_col<F>, smem);
@@ -352,11 +395,12 @@ static void launch_pass(int which, const SolveParams& p, const F& f, int V, int 
 }
 
 // Compile-time geometries of the BASELINE sizes.  Rows (V*TV = 256 threads,
-// ~8 values per thread): n = W/2 for W in {512, 1024, 1920, 2048, 4096}.
-// Columns (V*TV <= 1024 threads, ~16 values per thread, V*8 >= 32-byte row
-// segments): H in {512, 1024, 1080, 2048, 4096}.
+// one radix-8 butterfly per thread per stage): n = W/2 for W in {512, 1024,
+// 1920, 2048, 4096}.  Columns (512 threads and <= 64 KB so two CTAs share an
+// SM and overlap load / compute / store; V*8 >= 32-byte row segments; 4096
+// needs 1024 threads): H in {512, 1024, 1080, 2048, 4096}.
 #define BLFLS_CT_ROWS(X) X(256, 8, 32) X(512, 4, 64) X(960, 2, 128) X(1024, 2, 128) X(2048, 1, 256)
-#define BLFLS_CT_COLS(X) X(512, 16, 32) X(1024, 16, 64) X(1080, 8, 128) X(2048, 8, 128) X(4096, 4, 256)
+#define BLFLS_CT_COLS(X) X(512, 16, 32) X(1024, 8, 64) X(1080, 4, 128) X(2048, 4, 128) X(4096, 4, 256)
 
 bool ct_geometry(bool cols, int n, int* V, int* threads)
 {
