@@ -39,6 +39,25 @@ def _needs(obj: Path, src: Path) -> bool:
     return any(p.stat().st_mtime > t for p in [src, *_headers(), Path(__file__)])
 
 
+CLI_SRC = ROOT / "tools" / "blfls_cli.cpp"
+CLI = OUT_DIR / "blfls"
+
+
+def build_cli(verbose: bool = False) -> Path:
+    """The epls-style command-line front end (tools/blfls_cli.cpp) over libblfls.so."""
+    if CLI.exists() and CLI.stat().st_mtime > max(CLI_SRC.stat().st_mtime, LIB.stat().st_mtime,
+                                                   (INCLUDE / "blfls" / "blfls.hpp").stat().st_mtime):
+        return CLI
+    cmd = ["g++", "-std=c++17", "-O2", f"-I{INCLUDE}", str(CLI_SRC), "-o", str(CLI), f"-L{OUT_DIR}",
+           "-lblfls", f"-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
+
+
 def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
     OUT_DIR.mkdir(exist_ok=True)
     objs = []
@@ -67,6 +86,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
     if jobs or not LIB.exists():
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static"]
         run(cmd)
+    build_cli(verbose)
     return LIB
 
 

@@ -1,0 +1,110 @@
+"""The epls-style CLI (tools/blfls_cli.cpp): exit codes like the reference
+(tests/test_cli.cpp:74-85 of the reference), PFM/PNM I/O conventions, and on a
+GPU the pixel-exact lambda-0 round trip (test_cli.cpp:45-59) and run-to-run
+byte-identical output (test_cli.cpp:87-99)."""
+from __future__ import annotations
+
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def cli():
+    from paper_1812_07122_b200 import build
+    build.build()
+    return str(build.CLI)
+
+
+def run(cli, *args):
+    return subprocess.run([cli, *map(str, args)], capture_output=True, text=True, timeout=300)
+
+
+def write_pfm(path, img):
+    """img: (C, H, W) float; PFM little endian, rows bottom-up."""
+    c, h, w = img.shape
+    with open(path, "wb") as f:
+        f.write(f"P{'F' if c == 3 else 'f'}\n{w} {h}\n-1.0\n".encode())
+        f.write(np.ascontiguousarray(img.transpose(1, 2, 0)[::-1]).astype("<f4").tobytes())
+
+
+def read_pfm(path):
+    data = Path(path).read_bytes()
+    parts = data.split(b"\n", 3)
+    c = 3 if parts[0] == b"PF" else 1
+    w, h = map(int, parts[1].split())
+    scale = float(parts[2])
+    arr = np.frombuffer(parts[3], dtype="<f4" if scale < 0 else ">f4").reshape(h, w, c)
+    return arr[::-1].transpose(2, 0, 1).astype(np.float64)
+
+
+def write_pgm(path, img8):
+    h, w = img8.shape
+    with open(path, "wb") as f:
+        f.write(f"P5\n{w} {h}\n255\n".encode())
+        f.write(img8.astype(np.uint8).tobytes())
+
+
+def test_usage_errors_exit_2(cli, tmp_path):
+    assert run(cli).returncode == 2
+    assert run(cli, "frobnicate", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "smooth").returncode == 2
+    assert run(cli, "smooth", "--method", "bogus", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "smooth", "--sigma-s", "-1", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "smooth", "--pad", "16", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "joint", "in.pfm", "out.pfm").returncode == 2  # --guide required
+
+
+def test_unreadable_input_exits_1(cli, tmp_path):
+    assert run(cli, "smooth", "/nonexistent/input.pfm", tmp_path / "o.pfm").returncode == 1
+    bad = tmp_path / "bad.pfm"
+    bad.write_bytes(b"P7\n1 1\n")
+    assert run(cli, "smooth", bad, tmp_path / "o.pfm").returncode == 1
+    assert run(cli, "smooth", tmp_path / "x.png", tmp_path / "o.pfm").returncode == 1
+
+
+@pytest.mark.gpu
+def test_ls_lambda0_pgm_round_trip_pixel_exact(gpu, cli, tmp_path):
+    rng = np.random.default_rng(81)
+    img8 = rng.integers(0, 256, (32, 40))
+    write_pgm(tmp_path / "in.pgm", img8)
+    r = run(cli, "smooth", "--method", "ls", "--lambda", "0", tmp_path / "in.pgm", tmp_path / "out.pgm")
+    assert r.returncode == 0, r.stderr
+    data = (tmp_path / "out.pgm").read_bytes()
+    out = np.frombuffer(data[-32 * 40:], dtype=np.uint8).reshape(32, 40)
+    assert np.array_equal(out, img8)
+
+
+@pytest.mark.gpu
+def test_blf_ls_pfm_matches_api_and_is_deterministic(gpu, cli, oracle, tmp_path):
+    img = np.stack([oracle.gen_plane(900 + c, 48, 64, n_sites=12) for c in range(3)])
+    write_pfm(tmp_path / "in.pfm", img)
+    args = ["--sigma-s", "3", "--sigma-r", "0.1", "--lambda", "500", "--radius", "5", "--iters", "2"]
+    for k in (1, 2):
+        r = run(cli, "smooth", *args, tmp_path / "in.pfm", tmp_path / f"o{k}.pfm")
+        assert r.returncode == 0, r.stderr
+    assert (tmp_path / "o1.pfm").read_bytes() == (tmp_path / "o2.pfm").read_bytes()
+    out = read_pfm(tmp_path / "o1.pfm")
+    api = gpu.blf_ls(img, lam=500.0, sigma_s=3.0, sigma_r=0.1, iters=2, radius=5)
+    assert np.abs(out - api).max() == 0.0
+    ref = oracle.blf_ls(img.astype(np.float64), lam=500.0, sigma_s=3.0, sigma_r=0.1, iters=2, radius=5)
+    assert np.abs(out - ref).max() <= 1e-4
+
+
+@pytest.mark.gpu
+def test_joint_subcommand(gpu, cli, oracle, tmp_path):
+    img = np.stack([oracle.gen_plane(910 + c, 40, 48, n_sites=12) for c in range(3)])
+    guide = oracle.gen_plane(999, 40, 48, n_sites=12)[None]
+    write_pfm(tmp_path / "in.pfm", img)
+    write_pfm(tmp_path / "g.pfm", np.repeat(guide, 3, axis=0))
+    r = run(cli, "joint", "--guide", tmp_path / "g.pfm", "--sigma-r", "0.1", "--sigma-s", "3",
+            "--radius", "4", "--lambda", "800", tmp_path / "in.pfm", tmp_path / "o.pfm")
+    assert r.returncode == 0, r.stderr
+    out = read_pfm(tmp_path / "o.pfm")
+    ref = oracle.blf_ls(img.astype(np.float64), guide.astype(np.float64), lam=800.0, sigma_s=3.0,
+                        sigma_r=0.1, iters=1, radius=4)
+    assert np.abs(out - ref).max() <= 1e-4

@@ -1,0 +1,305 @@
+// blfls_cli.cpp -- command-line front end over the C ABI, mirroring the
+// reference CLI's hot-path subcommands (/root/reference/proj/tools/epls_main.cpp):
+//
+//   blfls smooth [--method blf-ls|ls] [--sigma-s S] [--sigma-r R] [--lambda L]
+//                [--pad 0] [--radius r] [--iters k] [--device d] input output
+//   blfls joint  --guide G [same flags] input output
+//
+// Defaults follow epls_main.cpp: sigma_s 12, sigma_r 0.04 (joint: 12 / 0.003,
+// its preparse defaults), lambda 1024.  Differences: the bilateral stage is
+// the brute-force filter (north star) with an explicit --radius (default
+// ceil(3 sigma_s) like bilateral.cpp:37); --iters cascades smooth() calls; the
+// GPU solve is periodic, so --pad defaults to 0 and pad > 0 is rejected.
+// Image formats: PFM (float, 'Pf' gray / 'PF' RGB, bottom-up, either endian)
+// and binary PGM/PPM (P5/P6, 8 or 16 bit) with the reference's conventions
+// (image_io.cpp: PNM values / maxval, PNM output clamped and rounded to 8 bit).
+// PNG / HDR need libpng / the Radiance codec and are not built.
+// Exit codes as the reference: 0 ok, 2 usage or invalid argument, 1 other.
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "blfls/blfls.hpp"
+
+namespace {
+
+struct UsageError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+using FilePtr = std::unique_ptr<std::FILE, int (*)(std::FILE*)>;
+
+FilePtr open_file(const std::string& path, const char* mode)
+{
+    std::FILE* f = std::fopen(path.c_str(), mode);
+    if (!f) throw std::runtime_error("cannot open '" + path + "'");
+    return FilePtr(f, &std::fclose);
+}
+
+std::string ext_of(const std::string& path)
+{
+    const auto dot = path.find_last_of('.');
+    std::string e = dot == std::string::npos ? "" : path.substr(dot + 1);
+    for (char& c : e) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    return e;
+}
+
+int header_int(std::FILE* f)
+{
+    int c = std::fgetc(f);
+    while (c != EOF && (std::isspace(c) || c == '#')) {
+        if (c == '#')
+            while (c != EOF && c != '\n') c = std::fgetc(f);
+        c = std::fgetc(f);
+    }
+    int v = 0;
+    bool any = false;
+    while (c != EOF && std::isdigit(c)) {
+        v = v * 10 + (c - '0');
+        any = true;
+        c = std::fgetc(f);
+    }
+    return any ? v : -1;
+}
+
+blfls::Image load_pfm(const std::string& path)
+{
+    FilePtr f = open_file(path, "rb");
+    char m[2];
+    if (std::fread(m, 1, 2, f.get()) != 2 || m[0] != 'P' || (m[1] != 'F' && m[1] != 'f'))
+        throw std::runtime_error("'" + path + "': expected PFM header");
+    const int ch = m[1] == 'F' ? 3 : 1;
+    const int w = header_int(f.get()), h = header_int(f.get());
+    double scale = 0.0;
+    if (std::fscanf(f.get(), "%lf", &scale) != 1 || scale == 0.0 || w <= 0 || h <= 0)
+        throw std::runtime_error("'" + path + "': bad PFM header");
+    std::fgetc(f.get());
+    const std::size_t n = static_cast<std::size_t>(w) * h * ch;
+    std::vector<float> buf(n);
+    if (std::fread(buf.data(), sizeof(float), n, f.get()) != n)
+        throw std::runtime_error("'" + path + "': truncated PFM data");
+    if (scale > 0.0)  // big endian
+        for (float& v : buf) {
+            unsigned char* b = reinterpret_cast<unsigned char*>(&v);
+            std::swap(b[0], b[3]);
+            std::swap(b[1], b[2]);
+        }
+    blfls::Image img(w, h, ch);
+    std::size_t i = 0;
+    for (int y = h - 1; y >= 0; --y)  // scanlines bottom to top
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < ch; ++c) img.at(c, y, x) = buf[i++];
+    return img;
+}
+
+void save_pfm(const std::string& path, const blfls::Image& img)
+{
+    FilePtr f = open_file(path, "wb");
+    const int ch = img.channels();
+    std::fprintf(f.get(), "P%c\n%d %d\n-1.0\n", ch == 3 ? 'F' : 'f', img.width(), img.height());
+    std::vector<float> buf(img.size());
+    std::size_t i = 0;
+    for (int y = img.height() - 1; y >= 0; --y)
+        for (int x = 0; x < img.width(); ++x)
+            for (int c = 0; c < ch; ++c) buf[i++] = static_cast<float>(img.at(c, y, x));
+    if (std::fwrite(buf.data(), sizeof(float), buf.size(), f.get()) != buf.size())
+        throw std::runtime_error("'" + path + "': short write");
+}
+
+blfls::Image load_pnm(const std::string& path)
+{
+    FilePtr f = open_file(path, "rb");
+    char m[2];
+    if (std::fread(m, 1, 2, f.get()) != 2 || m[0] != 'P' || (m[1] != '5' && m[1] != '6'))
+        throw std::runtime_error("'" + path + "': expected binary PGM (P5) or PPM (P6)");
+    const int ch = m[1] == '6' ? 3 : 1;
+    const int w = header_int(f.get()), h = header_int(f.get()), maxval = header_int(f.get());
+    if (w <= 0 || h <= 0 || maxval <= 0 || maxval > 65535)
+        throw std::runtime_error("'" + path + "': bad PNM header");
+    const std::size_t n = static_cast<std::size_t>(w) * h * ch;
+    const int bytes = maxval < 256 ? 1 : 2;
+    std::vector<unsigned char> buf(n * bytes);
+    if (std::fread(buf.data(), 1, buf.size(), f.get()) != buf.size())
+        throw std::runtime_error("'" + path + "': truncated PNM data");
+    blfls::Image img(w, h, ch);
+    std::size_t i = 0;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < ch; ++c) {
+                const int v = bytes == 1 ? buf[i] : (buf[i] << 8 | buf[i + 1]);
+                i += bytes;
+                img.at(c, y, x) = v / static_cast<double>(maxval);
+            }
+    return img;
+}
+
+void save_pnm(const std::string& path, const blfls::Image& img)
+{
+    FilePtr f = open_file(path, "wb");
+    const int ch = img.channels();
+    std::fprintf(f.get(), "P%c\n%d %d\n255\n", ch == 3 ? '6' : '5', img.width(), img.height());
+    std::vector<unsigned char> buf(img.size());
+    std::size_t i = 0;
+    for (int y = 0; y < img.height(); ++y)
+        for (int x = 0; x < img.width(); ++x)
+            for (int c = 0; c < ch; ++c) {
+                const double v = std::clamp(img.at(c, y, x), 0.0, 1.0);
+                buf[i++] = static_cast<unsigned char>(std::lround(v * 255.0));
+            }
+    if (std::fwrite(buf.data(), 1, buf.size(), f.get()) != buf.size())
+        throw std::runtime_error("'" + path + "': short write");
+}
+
+blfls::Image load_image(const std::string& path)
+{
+    const std::string e = ext_of(path);
+    if (e == "pfm") return load_pfm(path);
+    if (e == "pgm" || e == "ppm") return load_pnm(path);
+    throw std::runtime_error("'" + path + "': unsupported image extension ." + e +
+                             " (this build reads .pfm/.pgm/.ppm)");
+}
+
+void save_image(const std::string& path, const blfls::Image& img)
+{
+    const std::string e = ext_of(path);
+    if (e == "pfm") return save_pfm(path, img);
+    if (e == "pgm" || e == "ppm") return save_pnm(path, img);
+    throw std::runtime_error("'" + path + "': unsupported image extension ." + e +
+                             " (this build writes .pfm/.pgm/.ppm)");
+}
+
+struct Options {
+    std::string cmd, input, output, guide, method = "blf-ls";
+    double sigma_s = 12.0, sigma_r = 0.04, lambda = -1.0;
+    int pad = 0, radius = -1, iters = 1, device = 0;
+};
+
+double parse_double(const std::string& flag, const char* v)
+{
+    char* end = nullptr;
+    const double d = std::strtod(v, &end);
+    if (!end || *end || !std::isfinite(d)) throw UsageError(flag + ": not a number: " + v);
+    return d;
+}
+
+int parse_int(const std::string& flag, const char* v)
+{
+    char* end = nullptr;
+    const long d = std::strtol(v, &end, 10);
+    if (!end || *end) throw UsageError(flag + ": not an integer: " + v);
+    return static_cast<int>(d);
+}
+
+Options parse(int argc, char** argv)
+{
+    if (argc < 2) throw UsageError("a subcommand is required: smooth | joint");
+    Options o;
+    o.cmd = argv[1];
+    if (o.cmd != "smooth" && o.cmd != "joint") throw UsageError("unknown subcommand '" + o.cmd + "'");
+    if (o.cmd == "joint") {  // epls_main.cpp preparse defaults of `joint`
+        o.sigma_s = 12.0;
+        o.sigma_r = 0.003;
+    }
+    std::vector<std::string> pos;
+    for (int i = 2; i < argc; ++i) {
+        const std::string a = argv[i];
+        auto next = [&]() -> const char* {
+            if (i + 1 >= argc) throw UsageError(a + " needs a value");
+            return argv[++i];
+        };
+        if (a == "--method") {
+            o.method = next();
+            if (o.method != "blf-ls" && o.method != "ls")
+                throw UsageError("--method: GPU build supports blf-ls and ls, got '" + o.method + "'");
+        } else if (a == "--sigma-s") {
+            o.sigma_s = parse_double(a, next());
+            if (!(o.sigma_s > 0)) throw UsageError("--sigma-s must be positive");
+        } else if (a == "--sigma-r") {
+            o.sigma_r = parse_double(a, next());
+            if (!(o.sigma_r > 0)) throw UsageError("--sigma-r must be positive");
+        } else if (a == "--lambda") {
+            o.lambda = parse_double(a, next());
+        } else if (a == "--pad") {
+            o.pad = parse_int(a, next());
+            if (o.pad < 0) throw UsageError("--pad must be non-negative");
+        } else if (a == "--radius") {
+            o.radius = parse_int(a, next());
+        } else if (a == "--iters") {
+            o.iters = parse_int(a, next());
+            if (o.iters < 1) throw UsageError("--iters must be >= 1");
+        } else if (a == "--iterations") {
+            next();  // domain-transform pass count of the reference; no effect on blf-ls
+        } else if (a == "--device") {
+            o.device = parse_int(a, next());
+        } else if (a == "--guide" && o.cmd == "joint") {
+            o.guide = next();
+        } else if (a == "--threads") {
+            next();  // host thread count of the reference; the GPU path ignores it
+        } else if (!a.empty() && a[0] == '-' && a.size() > 1) {
+            throw UsageError("unknown option " + a);
+        } else {
+            pos.push_back(a);
+        }
+    }
+    if (pos.size() != 2) throw UsageError("expected: input output");
+    if (o.cmd == "joint" && o.guide.empty()) throw UsageError("joint: --guide is required");
+    o.input = pos[0];
+    o.output = pos[1];
+    if (o.pad != 0) throw UsageError("--pad > 0: the GPU solve is periodic (pad 0 only)");
+    return o;
+}
+
+int run(const Options& o)
+{
+    const blfls::Image in = load_image(o.input);
+    const double lam = o.lambda >= 0.0 ? o.lambda : 1024.0;
+    blfls::Image out;
+    if (o.method == "ls") {
+        blfls::Image zero(in.width(), in.height(), in.channels(), 0.0);
+        // plain LS == lsgrad with a zero target (test_solver.cpp:129-134); the
+        // reference normalises first (pipelines.cpp:64-68), a no-op for this
+        // affine-equivariant solve
+        out = blfls::lsgrad_solve_fft(in, zero, zero, lam, o.device);
+    } else if (o.cmd == "joint") {
+        const blfls::Image guide = load_image(o.guide);
+        if (guide.width() != in.width() || guide.height() != in.height())
+            throw std::invalid_argument("flash_no_flash: image shapes differ");
+        out = blfls::blf_ls(in, &guide, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device);
+    } else {
+        out = blfls::blf_ls(in, nullptr, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device);
+    }
+    save_image(o.output, out);
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv)
+{
+    Options o;
+    try {
+        o = parse(argc, argv);
+    } catch (const UsageError& e) {
+        std::fprintf(stderr, "usage error: %s\n", e.what());
+        return 2;
+    }
+    try {
+        return run(o);
+    } catch (const std::invalid_argument& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 2;
+    } catch (const std::domain_error& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+}
