@@ -81,6 +81,8 @@ struct BlfParams {
     int legacy_joint3;     // 1: shared-guide mode uses the unpacked kernel (experiments)
     int joint3_rows;       // output rows per thread of the packed shared-guide kernel
     int x2_poly;           // packed self-guided kernel: FMA-pipe exp2 period (< 0: off)
+    int tile_rows;         // k_grad_blf tile height override (0: auto, 8 or 16)
+    int cols_per_thread;   // experiment: outputs per thread of k_grad_blf (4 default, 8)
     float range_coef;      // sqrt(log2(e) / (8 sigma_r^2)): exponent scale for raw
                            // gradients of a unit-range image
     float cs[kMaxRadius + 1];  // log2 spatial weight -d^2/(2 sigma_s^2) * log2(e)

@@ -497,6 +497,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         if (const char* ev = std::getenv("BLFLS_PACKED_JOINT3")) b.legacy_joint3 = -std::atoi(ev);
         b.x2_poly = -1;  // r01 sweep: packed kernel slower (FP32 pipe co-saturated); experiment only
         if (const char* ev = std::getenv("BLFLS_X2")) b.x2_poly = std::atoi(ev);
+        b.cols_per_thread = 4;
+        if (const char* ev = std::getenv("BLFLS_COLS")) b.cols_per_thread = std::atoi(ev);
+        b.tile_rows = 0;
+        if (const char* ev = std::getenv("BLFLS_TILE_ROWS")) b.tile_rows = std::atoi(ev);
         b.joint3_rows = 2;
         if (const char* ev = std::getenv("BLFLS_J3_ROWS")) b.joint3_rows = std::atoi(ev);
         b.range_coef = (float)std::sqrt(1.4426950408889634 / (8.0 * q.sigma_r * q.sigma_r));

@@ -71,11 +71,11 @@ __device__ __forceinline__ void decode_range(const uint32_t* lohi, int b, float 
 //         exponential per tap serves all three channels.
 // POLY: every POLY-th tap of a row evaluates its exponential with poly_ex2
 // on the FMA pipe instead of MUFU.EX2 (0 = never), balancing the two pipes.
-template <int R, int P, int MODE, int POLY>
-__global__ void __launch_bounds__(256) k_grad_blf(const BlfParams p)
+template <int R, int P, int MODE, int POLY, int TH = 16>
+__global__ void __launch_bounds__(16 * TH) k_grad_blf(const BlfParams p)
 {
     constexpr int TW = 16 * P;
-    constexpr int TH = 16;
+    constexpr int NT = 16 * TH;  // threads: 16 per output row
     constexpr int NC = MODE == 2 ? 3 : 1;
     constexpr int ROWS = TH + 2 * R;
     constexpr int COLS = TW + 2 * R;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) k_grad_blf(const BlfParams p)
     const float* gimg = nullptr;
     if (MODE == 1) gimg = p.guide + ((size_t)b * p.GC + (p.GC == 1 ? 0 : c0)) * plane;
     if (MODE == 2) gimg = p.guide + (size_t)b * p.GC * plane;
-    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += 256) {
+    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += NT) {
         const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
         const int y = ty0 - R + i, x = tx0 - R + j;
         const bool in = y >= 0 && y < H && x >= 0 && x < W;
@@ -692,20 +692,32 @@ __global__ void __launch_bounds__(256) k_grad_blf_any(const BlfParams p)
 
 // ------------------------------------------------------------- dispatch --
 
-template <int R, int P, int MODE, int POLY>
-static cudaError_t launch_fixed(const BlfParams& p, int nz, cudaStream_t st)
+template <int R, int P, int MODE, int POLY, int TH>
+static cudaError_t launch_fixed_th(const BlfParams& p, int nz, cudaStream_t st)
 {
-    constexpr int TW = 16 * P, TH = 16;
+    constexpr int TW = 16 * P;
     constexpr int ROWS = TH + 2 * R, COLS = TW + 2 * R, PITCH = (COLS + 3) & ~3;
     constexpr int NARR = MODE == 0 ? 2 : (MODE == 1 ? 4 : 8);
     const size_t smem = (size_t)NARR * ROWS * PITCH * sizeof(float);
     // not a stream operation: legal while the stream is being captured
-    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE, POLY>,
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE, POLY, TH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + TW - 1) / TW, (p.y1 - p.y0 + TH - 1) / TH, nz);
-    k_grad_blf<R, P, MODE, POLY><<<grid, 256, smem, st>>>(p);
+    k_grad_blf<R, P, MODE, POLY, TH><<<grid, 16 * TH, smem, st>>>(p);
     return cudaGetLastError();
+}
+
+// Tile height: 16 rows (256 threads) normally; 8 rows (128 threads) when the
+// 16-row grid would fill fewer than ~8 waves of resident CTAs, so the last
+// partial wave idles a smaller fraction of the SMs (r01: c2 = 3.5 waves).
+template <int R, int P, int MODE, int POLY>
+static cudaError_t launch_fixed(const BlfParams& p, int nz, cudaStream_t st)
+{
+    const long tiles16 = (long)((p.W + 16 * P - 1) / (16 * P)) * ((p.y1 - p.y0 + 15) / 16) * nz;
+    const int th = p.tile_rows > 0 ? p.tile_rows : (tiles16 < 8L * 148 * 6 ? 8 : 16);
+    if (th == 8) return launch_fixed_th<R, P, MODE, POLY, 8>(p, nz, st);
+    return launch_fixed_th<R, P, MODE, POLY, 16>(p, nz, st);
 }
 
 template <int MODE>
@@ -785,6 +797,7 @@ static cudaError_t launch_x2_poly(const BlfParams& p, int nz, cudaStream_t st)
 template <int R, int P, int MODE>
 static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
 {
+    if (p.cols_per_thread == 8) return launch_fixed<R, 8, MODE, 0>(p, nz, st);  // experiment
     // p.poly_period < 0: the per-mode default; otherwise an experiment override
     switch (p.poly_period < 0 ? kPolyDefault<MODE> : p.poly_period) {
         case 0: return launch_fixed<R, P, MODE, 0>(p, nz, st);
