@@ -55,6 +55,12 @@ typedef enum blfls_status {
 #define BLFLS_NO_GRAPH 8u      /* launch kernels directly instead of a cached CUDA graph */
 #define BLFLS_TIME_STAGES 16u  /* bracket every stage with CUDA events (implies NO_GRAPH);
                                   read the sums with blfls_stage_times */
+#define BLFLS_ASYNC 32u        /* with HOST_PTRS: return without waiting; the copies run on
+                                  their own streams through two staging slots, so
+                                  consecutive calls overlap H2D / compute / D2H.  Inputs
+                                  must stay valid and outputs are readable only after
+                                  blfls_sync (which also reports deferred non-finite
+                                  input when CHECK_FINITE is set). */
 
 typedef struct blfls_plan_s* blfls_plan_t;
 
@@ -89,6 +95,10 @@ blfls_status blfls_plan_destroy(blfls_plan_t plan);
  * img/out: batch x C x H x W; guide: batch x guide_channels x H x W or NULL. */
 blfls_status blfls_run(blfls_plan_t plan, const float* img, const float* guide, int batch,
                        int iters, float* out, void* stream, unsigned flags);
+
+/* Wait for every call issued on the plan; returns BLFLS_ENONFINITE if an
+ * ASYNC | CHECK_FINITE call since the previous sync saw NaN/Inf input. */
+blfls_status blfls_sync(blfls_plan_t plan);
 
 /* One iteration's gradient targets, as filter_gradients returns them
  * (pipelines.cpp:33-53): gradients of the [0,1]-normalised image, filtered by

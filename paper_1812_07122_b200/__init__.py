@@ -8,12 +8,12 @@ is the Python mirror of the reference's ``epls`` entry points
 """
 from .blfls import (CudaError, InvalidArgument, RangeSpatialParams, SmootherKind, SmootherSpec,
                     SolveParams, Unsupported, blf_ls, filter_gradients, flash_no_flash, generate,
-                    get_plan, irfft2, ls_solve_fft, lsgrad_solve_fft, rfft2, smooth)
+                    get_plan, irfft2, ls_solve_fft, lsgrad_solve_fft, rfft2, smooth, sync_plans)
 from .configs import CONFIGS, Config
 
 __all__ = [
     "CudaError", "InvalidArgument", "RangeSpatialParams", "SmootherKind", "SmootherSpec",
     "SolveParams", "Unsupported", "blf_ls", "filter_gradients", "flash_no_flash", "generate",
-    "get_plan", "irfft2", "ls_solve_fft", "lsgrad_solve_fft", "rfft2", "smooth", "CONFIGS",
+    "get_plan", "irfft2", "ls_solve_fft", "lsgrad_solve_fft", "rfft2", "smooth", "sync_plans", "CONFIGS",
     "Config",
 ]

@@ -24,10 +24,11 @@ CHECK_FINITE = 2
 SYNC = 4
 NO_GRAPH = 8
 TIME_STAGES = 16
+ASYNC = 32
 
 # every symbol include/blfls/blfls.h declares
 EXPORTS = (
-    "blfls_plan_create", "blfls_plan_destroy", "blfls_run", "blfls_filter_gradients",
+    "blfls_plan_create", "blfls_plan_destroy", "blfls_run", "blfls_sync", "blfls_filter_gradients",
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
     "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
     "blfls_version", "blfls_abi_version",
@@ -87,6 +88,7 @@ def lib() -> C.CDLL:
             L.blfls_plan_create.argtypes = [C.POINTER(Params), C.POINTER(vp)]
             L.blfls_plan_destroy.argtypes = [vp]
             L.blfls_run.argtypes = [vp, fp, fp, ip, ip, fp, vp, C.c_uint]
+            L.blfls_sync.argtypes = [vp]
             L.blfls_filter_gradients.argtypes = [vp, fp, fp, ip, fp, fp, vp, C.c_uint]
             L.blfls_filter_gradients_rows.argtypes = [vp, fp, fp, ip, ip, fp, fp, vp, C.c_uint]
             L.blfls_solve.argtypes = [vp, fp, fp, fp, ip, fp, vp, C.c_uint]
@@ -135,6 +137,10 @@ class Plan:
         if h is not None and h.value and _lib is not None:
             _lib.blfls_plan_destroy(h)
             self.handle = None
+
+    def sync(self) -> None:
+        """Wait for all calls on this plan (reports deferred non-finite input)."""
+        check(lib().blfls_sync(self.handle))
 
     def stage_times(self):
         """(ms sums, launch counts) per stage: minmax, blf, r2c, col, c2r."""

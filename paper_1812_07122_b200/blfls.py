@@ -42,13 +42,14 @@ from typing import Any
 import numpy as np
 
 from . import _capi
-from ._capi import (CHECK_FINITE, DEVICE_PTRS, HOST_PTRS, NO_GRAPH, SYNC, CudaError,
+from ._capi import (ASYNC, CHECK_FINITE, DEVICE_PTRS, HOST_PTRS, NO_GRAPH, SYNC, CudaError,
                     InvalidArgument, Plan, Unsupported, check, lib)
 
 __all__ = [
     "SmootherKind", "RangeSpatialParams", "SolveParams", "SmootherSpec", "smooth",
     "flash_no_flash", "blf_ls", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
-    "rfft2", "irfft2", "generate", "get_plan", "InvalidArgument", "CudaError", "Unsupported",
+    "rfft2", "irfft2", "generate", "get_plan", "sync_plans", "InvalidArgument", "CudaError",
+    "Unsupported",
 ]
 
 
@@ -186,13 +187,18 @@ def _device(img: _Img, guide: _Img | None) -> int:
 
 def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, iters: int = 1,
            radius: int | None = None, check_finite: bool = True, use_graph: bool = True,
-           out=None, extra_flags: int = 0):
+           out=None, extra_flags: int = 0, wait: bool = True):
     """BLF-LS: ``iters`` cascaded smooth() passes with the brute-force (joint) BLF.
 
     ``guide`` (optional) has 1 channel or the image's channel count and is held
     fixed over the iterations.  Returns the smoothed image in the input's type
     (written into ``out`` when given: an fp32 array/tensor of the image's shape
     in the same memory space, e.g. pinned host memory).
+
+    ``wait=False`` (host memory only, ``out`` required, input already fp32
+    contiguous) returns immediately: H2D, compute and D2H are queued on the
+    plan's copy/compute streams so consecutive calls overlap; call
+    ``get_plan(...).sync()`` (or ``sync_plans()``) before reading ``out``.
     """
     img = _Img(image)
     gd = None if guide is None else _Img(guide, "guide")
@@ -226,9 +232,23 @@ def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, ite
     if not use_graph:
         flags |= NO_GRAPH
     flags |= int(extra_flags)
+    if not wait:
+        if img.torch or finish:
+            raise InvalidArgument(_capi.BLFLS_EINVAL, "wait=False needs host memory and `out`")
+        src = image.numpy() if hasattr(image, "numpy") and not isinstance(image, np.ndarray) else image
+        if not (isinstance(src, np.ndarray) and src.dtype == np.float32 and src.flags.c_contiguous):
+            raise InvalidArgument(_capi.BLFLS_EINVAL,
+                                  "wait=False needs a contiguous fp32 input that outlives the call")
+        flags |= ASYNC
     check(lib().blfls_run(plan.handle, img.ptr, None if gd is None else gd.ptr, img.b, int(iters),
                           _ptr(out), stream, flags))
     return img.finish(out) if finish else out
+
+
+def sync_plans() -> None:
+    """Wait for every plan of this thread (after ``blf_ls(..., wait=False)``)."""
+    for p in getattr(_tls, "plans", {}).values():
+        p.sync()
 
 
 def smooth(g, spec: SmootherSpec):

@@ -170,19 +170,36 @@ struct blfls_plan_s {
     float* tx = nullptr;
     float* ty = nullptr;
     float2* spec = nullptr;
-    float* in_dev = nullptr;     // host-pointer staging
+    float* in_dev = nullptr;     // host-pointer staging (stage entry points)
     float* guide_dev = nullptr;
     float* out_dev = nullptr;
+    // blfls_run with host pointers: two staging slots, H2D / D2H on their own
+    // streams, so consecutive BLFLS_ASYNC calls overlap copies with compute
+    struct HostSlot {
+        float* in = nullptr;
+        float* guide = nullptr;
+        float* out = nullptr;
+        cudaEvent_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+        bool used = false;
+    } slot[2];
+    int next_slot = 0;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    unsigned* nonfinite_acc = nullptr;  // deferred non-finite count of ASYNC calls
     uint32_t* lohi = nullptr;    // [2][max_batch][2]
     uint32_t* glohi = nullptr;   // [max_batch][2]
     unsigned* nonfinite = nullptr;
     BlfParams blf{};
-    // graph cache
-    cudaGraphExec_t gexec = nullptr;
-    const void* g_in = nullptr;
-    const void* g_guide = nullptr;
-    void* g_out = nullptr;
-    int g_batch = -1, g_iters = -1;
+    // graph cache: instantiated iteration sequences keyed on their pointers
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        const void* in = nullptr;
+        const void* guide = nullptr;
+        void* out = nullptr;
+        int batch = -1, iters = -1;
+        long long last = 0;
+        long long launches = 0;
+    } graphs[4];
+    long long graph_clock = 0;
     // stats
     blfls_stats stats{};
     long long launches = 0;
@@ -362,7 +379,19 @@ void free_plan(blfls_plan_t p)
 {
     if (!p) return;
     cudaSetDevice(p->prm.device);
-    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    for (auto& g : p->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto& sl : p->slot) {
+        if (sl.in) cudaFree(sl.in);
+        if (sl.guide) cudaFree(sl.guide);
+        if (sl.out) cudaFree(sl.out);
+        if (sl.h2d) cudaEventDestroy(sl.h2d);
+        if (sl.comp) cudaEventDestroy(sl.comp);
+        if (sl.d2h) cudaEventDestroy(sl.d2h);
+    }
+    if (p->nonfinite_acc) cudaFree(p->nonfinite_acc);
+    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
     for (auto& e : p->timing) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -544,6 +573,70 @@ blfls_status blfls_plan_destroy(blfls_plan_t p)
     return BLFLS_OK;
 }
 
+namespace {
+
+// Launch the cached graph of the iteration sequence for these pointers
+// (capturing and instantiating it on first use).
+blfls_status launch_graph(blfls_plan_t p, const float* din, const float* dguide, float* dout, int batch,
+                          int iters, cudaStream_t st)
+{
+    blfls_plan_s::GraphEntry* hit = nullptr;
+    for (auto& g : p->graphs)
+        if (g.exec && g.in == din && g.guide == dguide && g.out == dout && g.batch == batch &&
+            g.iters == iters)
+            hit = &g;
+    if (!hit) {
+        hit = &p->graphs[0];
+        for (auto& g : p->graphs)
+            if (!g.exec || g.last < hit->last) hit = &g;
+        if (hit->exec) {
+            cudaGraphExecDestroy(hit->exec);
+            hit->exec = nullptr;
+        }
+        p->launches = 0;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        blfls_status r = enq_run(p, din, dguide, dout, batch, iters, st);
+        cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (r) return r;
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+        ce = cudaGraphInstantiate(&hit->exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+        hit->in = din;
+        hit->guide = dguide;
+        hit->out = dout;
+        hit->batch = batch;
+        hit->iters = iters;
+        hit->launches = p->launches;
+    }
+    hit->last = ++p->graph_clock;
+    p->stats.kernel_launches = hit->launches;
+    CK(cudaGraphLaunch(hit->exec, st));
+    return BLFLS_OK;
+}
+
+blfls_status ensure_host_slots(blfls_plan_t p)
+{
+    if (p->s_h2d) return BLFLS_OK;
+    CK(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+    CK(cudaMalloc(&p->nonfinite_acc, sizeof(unsigned)));
+    CK(cudaMemset(p->nonfinite_acc, 0, sizeof(unsigned)));
+    for (auto& sl : p->slot) {
+        CK(cudaMalloc(&sl.in, sizeof(float) * p->img_elems));
+        CK(cudaMalloc(&sl.out, sizeof(float) * p->img_elems));
+        if (p->prm.guide_channels)
+            CK(cudaMalloc(&sl.guide, sizeof(float) * p->prm.max_batch * p->prm.guide_channels * p->plane));
+        CK(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sl.comp, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming));
+    }
+    return BLFLS_OK;
+}
+
+}  // namespace
+
 blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int batch, int iters,
                        float* out, void* stream, unsigned flags)
 {
@@ -558,69 +651,85 @@ blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int
     const size_t n = (size_t)batch * p->prm.channels * p->plane;
     const size_t ng = guide ? (size_t)batch * p->prm.guide_channels * p->plane : 0;
     const bool host = flags & BLFLS_HOST_PTRS;
-    if ((r = fork_in(p, us))) return r;
+    const bool async = (flags & BLFLS_ASYNC) && host;
+    // ASYNC host calls are ordered by blfls_sync, not by the caller's stream:
+    // joining it would chain call k+1's H2D behind call k's D2H
+    if (!async && (r = fork_in(p, us))) return r;
     cudaStream_t st = p->ps;
     const float* din = img;
     const float* dguide = guide;
     float* dout = out;
+    blfls_plan_s::HostSlot* sl = nullptr;
     if (host) {
-        if (!p->in_dev) CK(cudaMalloc(&p->in_dev, sizeof(float) * p->img_elems));
-        if (!p->out_dev) CK(cudaMalloc(&p->out_dev, sizeof(float) * p->img_elems));
-        CK(cudaMemcpyAsync(p->in_dev, img, sizeof(float) * n, cudaMemcpyHostToDevice, st));
-        din = p->in_dev;
-        dout = p->out_dev;
-        if (guide) {
-            if (!p->guide_dev)
-                CK(cudaMalloc(&p->guide_dev,
-                              sizeof(float) * p->prm.max_batch * p->prm.guide_channels * p->plane));
-            CK(cudaMemcpyAsync(p->guide_dev, guide, sizeof(float) * ng, cudaMemcpyHostToDevice, st));
-            dguide = p->guide_dev;
-        }
+        if ((r = ensure_host_slots(p))) return r;
+        sl = &p->slot[p->next_slot];
+        p->next_slot ^= 1;
+        // H2D on its own stream once the slot's previous input was consumed
+        if (!async) CK(cudaStreamWaitEvent(p->s_h2d, p->ev_in, 0));
+        if (sl->used) CK(cudaStreamWaitEvent(p->s_h2d, sl->comp, 0));
+        CK(cudaMemcpyAsync(sl->in, img, sizeof(float) * n, cudaMemcpyHostToDevice, p->s_h2d));
+        if (guide)
+            CK(cudaMemcpyAsync(sl->guide, guide, sizeof(float) * ng, cudaMemcpyHostToDevice, p->s_h2d));
+        CK(cudaEventRecord(sl->h2d, p->s_h2d));
+        CK(cudaStreamWaitEvent(st, sl->h2d, 0));
+        if (sl->used) CK(cudaStreamWaitEvent(st, sl->d2h, 0));  // slot output drained
+        din = sl->in;
+        dguide = guide ? sl->guide : nullptr;
+        dout = sl->out;
     }
     if (flags & BLFLS_CHECK_FINITE) {
-        if ((r = check_finite(p, din, n, st, "smooth"))) return r;
-        if (dguide && (r = check_finite(p, dguide, ng, st, "normalize_to_unit"))) return r;
+        if (async) {
+            // deferred: counted on the device, reported by blfls_sync
+            CK(launch_count_nonfinite(din, n, p->nonfinite_acc, p->nsm, st));
+            if (dguide) CK(launch_count_nonfinite(dguide, ng, p->nonfinite_acc, p->nsm, st));
+        } else {
+            if ((r = check_finite(p, din, n, st, "smooth"))) return r;
+            if (dguide && (r = check_finite(p, dguide, ng, st, "normalize_to_unit"))) return r;
+        }
     }
-    p->launches = 0;
     p->stats.blf_launches = 0;
     p->time_stages = (flags & BLFLS_TIME_STAGES) != 0;
     const bool use_graph = !(flags & (BLFLS_NO_GRAPH | BLFLS_TIME_STAGES));
     if (use_graph) {
-        if (!(p->gexec && p->g_in == din && p->g_guide == dguide && p->g_out == dout &&
-              p->g_batch == batch && p->g_iters == iters)) {
-            cudaGraph_t g;
-            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            r = enq_run(p, din, dguide, dout, batch, iters, st);
-            cudaError_t ce = cudaStreamEndCapture(st, &g);
-            if (r) return r;
-            if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-            if (p->gexec) {
-                cudaGraphExecDestroy(p->gexec);
-                p->gexec = nullptr;
-            }
-            ce = cudaGraphInstantiate(&p->gexec, g, 0);
-            cudaGraphDestroy(g);
-            if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
-            p->g_in = din;
-            p->g_guide = dguide;
-            p->g_out = dout;
-            p->g_batch = batch;
-            p->g_iters = iters;
-            p->stats.kernel_launches = p->launches;
-        }
-        CK(cudaGraphLaunch(p->gexec, st));
+        if ((r = launch_graph(p, din, dguide, dout, batch, iters, st))) return r;
     } else {
+        p->launches = 0;
         r = enq_run(p, din, dguide, dout, batch, iters, st);
         p->time_stages = false;
         if (r) return r;
         p->stats.kernel_launches = p->launches;
     }
-    if (host) CK(cudaMemcpyAsync(out, dout, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
     const int G = p->mode == 2 ? 1 : p->prm.channels;
     const double taps = (double)(2 * p->radius + 1) * (2 * p->radius + 1);
     p->stats.exps = taps * (double)p->plane * 2.0 * batch * G * iters;
     p->stats.blf_launches = iters;
-    return join_out(p, us, flags | (host ? BLFLS_SYNC : 0));
+    if (!host) return join_out(p, us, flags);
+    CK(cudaEventRecord(sl->comp, st));
+    CK(cudaStreamWaitEvent(p->s_d2h, sl->comp, 0));
+    CK(cudaMemcpyAsync(out, sl->out, sizeof(float) * n, cudaMemcpyDeviceToHost, p->s_d2h));
+    CK(cudaEventRecord(sl->d2h, p->s_d2h));
+    sl->used = true;
+    if (async) return BLFLS_OK;
+    CK(cudaStreamWaitEvent(us, sl->d2h, 0));
+    CK(cudaEventSynchronize(sl->d2h));
+    return BLFLS_OK;
+}
+
+blfls_status blfls_sync(blfls_plan_t p)
+{
+    if (!p) return fail(BLFLS_EINVAL, "null plan");
+    blfls_status r;
+    if ((r = set_device(p))) return r;
+    CK(cudaStreamSynchronize(p->ps));
+    if (p->s_h2d) {
+        CK(cudaStreamSynchronize(p->s_h2d));
+        CK(cudaStreamSynchronize(p->s_d2h));
+        unsigned h = 0;
+        CK(cudaMemcpy(&h, p->nonfinite_acc, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        CK(cudaMemset(p->nonfinite_acc, 0, sizeof(unsigned)));
+        if (h) return fail(BLFLS_ENONFINITE, "smooth: non-finite sample in input image");
+    }
+    return BLFLS_OK;
 }
 
 blfls_status blfls_filter_gradients(blfls_plan_t p, const float* img, const float* guide, int batch,

@@ -341,3 +341,26 @@ def test_band_driver_single_rank(gpu, oracle):
     ref = oracle.blf_ls(img.cpu().numpy().astype(np.float64), guide.cpu().numpy().astype(np.float64),
                         iters=3, **kw)
     assert maxabs(out.cpu().numpy(), ref) <= TOL_OUT
+
+
+def test_async_host_pipeline(gpu, oracle):
+    """blf_ls(wait=False) overlaps consecutive host-memory calls (two staging
+    slots); every output equals the synchronous result, and deferred
+    non-finite input is reported by sync."""
+    imgs = [_img(oracle, 3, 48, 64, 300 + i).astype(np.float32) for i in range(5)]
+    kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+    ref = [gpu.blf_ls(x, **kw) for x in imgs]
+    outs = [np.empty_like(x) for x in imgs]
+    for x, o in zip(imgs, outs):
+        gpu.blf_ls(x, out=o, wait=False, **kw)
+    plan = gpu.get_plan(48, 64, 3, 0, 7, 7.0, 0.1, 1000.0, 1, 0)
+    plan.sync()
+    for o, r in zip(outs, ref):
+        assert maxabs(o, r) == 0.0
+    bad = imgs[0].copy()
+    bad[1, 2, 3] = np.inf
+    o = np.empty_like(bad)
+    gpu.blf_ls(bad, out=o, wait=False, **kw)
+    with pytest.raises(gpu.InvalidArgument):
+        plan.sync()
+    plan.sync()  # the deferred error is reported once
