@@ -100,6 +100,7 @@ struct SolveParams {
     const float* gain_y; // 4 sin^2(pi u / H)
     const float2* post;  // exp(-2 pi i v / W), v in [0, W/2]  (real-FFT split)
     int H, W, C;
+    int plane0;          // global index of the first plane (per-image min/max slot)
     int spitch;          // complex elements per spectrum row
     int wc;              // W/2 + 1
     float lambda;

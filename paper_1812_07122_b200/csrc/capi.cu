@@ -157,6 +157,11 @@ struct blfls_plan_s {
     int nsm = 148;
     cudaStream_t ps = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    // plane-grouped solve: each group's half spectrum stays L2-resident across
+    // its r2c -> column -> c2r kernels; two groups in flight on ps / ps2
+    int solve_group = 0;           // planes per group (0: one launch over all planes)
+    cudaStream_t ps2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // FFT
     bool odd = false;
     int wc = 0, spitch = 0;
@@ -262,20 +267,54 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
     s.out = out;
     s.lohi_out = lohi_out;
     s.mode = 3;
-    stage_begin(p, 2, st);
-    CK(launch_row_r2c(s, p->rowf.g, planes, p->odd, st));
-    stage_end(p, st);
-    stage_begin(p, 3, st);
-    CK(launch_col(s, p->colf.g, planes, st));
-    stage_end(p, st);
+    s.plane0 = 0;
+    const int grp = p->solve_group;
+    if (grp <= 0 || grp >= planes) {
+        stage_begin(p, 2, st);
+        CK(launch_row_r2c(s, p->rowf.g, planes, p->odd, st));
+        stage_end(p, st);
+        stage_begin(p, 3, st);
+        CK(launch_col(s, p->colf.g, planes, st));
+        stage_end(p, st);
+        if (lohi_out) {
+            CK(launch_reset_lohi(lohi_out, batch, st));
+            p->launches++;
+        }
+        stage_begin(p, 4, st);
+        CK(launch_row_c2r(s, p->rowf.g, planes, p->odd, st));
+        stage_end(p, st);
+        p->launches += 3;
+        return BLFLS_OK;
+    }
+    // grouped: spectrum regions 0 / 1 alternate between the two streams
+    const size_t pimg = (size_t)p->prm.height * p->prm.width;
+    const size_t pspec = (size_t)p->prm.height * p->spitch;
     if (lohi_out) {
         CK(launch_reset_lohi(lohi_out, batch, st));
         p->launches++;
     }
-    stage_begin(p, 4, st);
-    CK(launch_row_c2r(s, p->rowf.g, planes, p->odd, st));
+    stage_begin(p, 2, st);  // the whole grouped solve is timed as stage 2
+    CK(cudaEventRecord(p->ev_fork, st));
+    CK(cudaStreamWaitEvent(p->ps2, p->ev_fork, 0));
+    int k = 0;
+    for (int p0 = 0; p0 < planes; p0 += grp, ++k) {
+        const int np = std::min(grp, planes - p0);
+        cudaStream_t cs = (k & 1) ? p->ps2 : st;
+        SolveParams g = s;
+        g.plane0 = p0;
+        g.f = f + p0 * pimg;
+        g.tx = tx ? tx + p0 * pimg : nullptr;
+        g.ty = ty ? ty + p0 * pimg : nullptr;
+        g.out = out + p0 * pimg;
+        g.spec = p->spec + (size_t)(k & 1) * grp * pspec;
+        CK(launch_row_r2c(g, p->rowf.g, np, p->odd, cs));
+        CK(launch_col(g, p->colf.g, np, cs));
+        CK(launch_row_c2r(g, p->rowf.g, np, p->odd, cs));
+        p->launches += 3;
+    }
+    CK(cudaEventRecord(p->ev_join, p->ps2));
+    CK(cudaStreamWaitEvent(st, p->ev_join, 0));
     stage_end(p, st);
-    p->launches += 3;
     return BLFLS_OK;
 }
 
@@ -402,6 +441,9 @@ void free_plan(blfls_plan_t p)
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->ps2) cudaStreamDestroy(p->ps2);
     if (p->ev_out) cudaEventDestroy(p->ev_out);
     if (p->ps) cudaStreamDestroy(p->ps);
     delete p;
@@ -558,6 +600,19 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         cudaMalloc(&p->glohi, sizeof(uint32_t) * 2 * q.max_batch) != cudaSuccess ||
         cudaMalloc(&p->nonfinite, sizeof(unsigned)) != cudaSuccess)
         return bail(fail(BLFLS_ENOMEM, "plan: workspace allocation failed"));
+    {
+        // group planes when all spectra together would not stay in L2
+        const double spec_plane = (double)H * p->spitch * sizeof(float2);
+        const double total = spec_plane * q.max_batch * C;
+        int grp = 0;
+        if (total > 64e6) grp = std::max(1, (int)(24e6 / spec_plane));
+        if (const char* ev = std::getenv("BLFLS_SOLVE_GROUP")) grp = std::atoi(ev);
+        p->solve_group = grp;
+    }
+    if (cudaStreamCreateWithFlags(&p->ps2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(BLFLS_ECUDA, "plan: stream creation failed"));
     if (cudaStreamCreateWithFlags(&p->ps, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) != cudaSuccess)

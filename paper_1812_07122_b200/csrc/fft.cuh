@@ -298,11 +298,15 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
             dft_small<P>(a[i], sg);
             const int obase = k + S * P * q;
             buf[addr(obase)] = a[i][0];
+            // twiddles w^t, w = tw[q S]: one coalesced load, powers by complex
+            // multiplication (relative error <= (P-1) ulp-level products)
+            float2 w1 = __ldg(&tw[q * S]);
+            if (INV) w1.y = -w1.y;
+            float2 wt = w1;
 #pragma unroll
             for (int tt = 1; tt < P; ++tt) {
-                float2 w = __ldg(&tw[q * tt * S]);
-                if (INV) w.y = -w.y;
-                buf[addr(obase + S * tt)] = cmul(a[i][tt], w);
+                buf[addr(obase + S * tt)] = cmul(a[i][tt], wt);
+                if (tt + 1 < P) wt = (tt + 1 == 2 || tt + 1 == 4) ? cmul(wt, wt) : cmul(wt, w1);
             }
         }
     }

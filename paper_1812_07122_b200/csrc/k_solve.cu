@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
             hi = fmaxf(hi, z.x);
         }
     }
-    if (p.lohi_out != nullptr) block_minmax_atomic(lo, hi, p.lohi_out + 2 * (plane / p.C));
+    if (p.lohi_out != nullptr) block_minmax_atomic(lo, hi, p.lohi_out + 2 * ((p.plane0 + plane) / p.C));
 }
 
 // ---------------------------------------------------------------- misc --
