@@ -306,7 +306,7 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
 #pragma unroll
             for (int tt = 1; tt < P; ++tt) {
                 buf[addr(obase + S * tt)] = cmul(a[i][tt], wt);
-                if (tt + 1 < P) wt = (tt + 1 == 2 || tt + 1 == 4) ? cmul(wt, wt) : cmul(wt, w1);
+                if (tt + 1 < P) wt = cmul(wt, w1);  // w^(t+1)
             }
         }
     }
