@@ -47,8 +47,8 @@ __global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F f
     if (!ODD && (p.W & 3) == 0) {
         // 4 pixels (2 complex) per thread: float4 loads of f, Tx, Ty and the
         // previous Ty row; Tx[x-1] is one scalar load (fold r = f + lambda D^T T)
-        const int w4 = p.W >> 2;
-#pragma unroll 4
+        const int w4 = fft.n() >> 1;  // = W / 4, compile-time for the CT engine
+#pragma unroll
         for (int e = threadIdx.x; e < V * w4; e += fft.threads()) {
             const int v = e / w4, x4 = e - v * w4;
             const int y = row0 + v;
@@ -115,7 +115,7 @@ template <class F>
 __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
 {
     extern __shared__ __align__(16) float2 buf[];
-    const int H = p.H, V = fft.vecs();
+    const int H = fft.n(), V = fft.vecs();  // compile-time for the CT engine
     const int plane = blockIdx.y;
     const int v0 = blockIdx.x * V;
     float2* spec = p.spec + (size_t)plane * H * p.spitch;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
             const int v = v0 + c;
             float sc = p.inv_hw;
             if (p.mode == 3 && v < p.wc)
-                sc = p.inv_hw / fmaf(p.lambda, __ldg(&p.gain_y[u]) + __ldg(&p.gain_x[v]), 1.0f);
+                sc = p.inv_hw * __frcp_rn(fmaf(p.lambda, __ldg(&p.gain_y[u]) + __ldg(&p.gain_x[v]), 1.0f));
             const int pi = fft.template pad<true>(idx);
             buf[pi] = cscale(buf[pi], sc);
         }
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
     const int plane = blockIdx.y;
     const int row0 = blockIdx.x * V;
     const int W = p.W;
-#pragma unroll 4
+#pragma unroll 8
     for (int idx = threadIdx.x; idx < V * n; idx += fft.threads()) {
         const int v = idx / n, k = idx - (idx / n) * n;
         const int y = row0 + v;
