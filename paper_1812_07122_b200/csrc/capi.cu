@@ -34,7 +34,7 @@ cudaError_t launch_scale_by_range(float* x, size_t per_image, int batch, const u
 cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int K, double sigma,
                             double p_sp, float* out, cudaStream_t st);
 cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz);
-bool ct_geometry(bool cols, int n, int* V, int* threads);
+bool ct_geometry(bool cols, int n, int nvec, int planes, int nsm, int* V, int* threads);
 
 }  // namespace blfls
 
@@ -94,14 +94,14 @@ int threads_per_vector(const std::vector<int>& radix, int n, int E)
 
 // V (power of two, <= Vmax) vectors of length n per CTA, <= 1024 threads,
 // <= smem_cap bytes of shared memory; largest V first, then the smaller E.
-bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, DevFft& out,
-              std::vector<int>& radix)
+bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, int planes, int nsm,
+              DevFft& out, std::vector<int>& radix)
 {
     if (!factorize(n, radix)) return false;
     bool generic = false;
     for (int p : radix) generic |= p > 5;
     int cv = 0, ct = 0;
-    if (!odd && ct_geometry(cols, n, &cv, &ct)) {
+    if (!odd && ct_geometry(cols, n, nvec, planes, nsm, &cv, &ct)) {
         FftGeom& g = out.g;
         g.V = cv;
         g.log2V = 0;
@@ -510,10 +510,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     // rows: about 2048 complex values per CTA
     int vrow = 1;
     while (vrow * 2 * nrow <= 2048 && vrow < 16) vrow *= 2;
-    if (!plan_fft(nrow, vrow, 64 * 1024, false, p->odd, p->rowf, rrad))
+    if (!plan_fft(nrow, vrow, 64 * 1024, false, p->odd, H, q.max_batch * C, p->nsm, p->rowf, rrad))
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: width " + std::to_string(W) +
                                                  " has a prime factor above 13 or too large"));
-    if (!plan_fft(H, 16, 128 * 1024, true, false, p->colf, crad))
+    if (!plan_fft(H, 16, 128 * 1024, true, false, p->wc, q.max_batch * C, p->nsm, p->colf, crad))
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: height " + std::to_string(H) +
                                                  " has a prime factor above 13 or too large"));
 

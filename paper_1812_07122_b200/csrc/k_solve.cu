@@ -394,24 +394,52 @@ static void launch_pass(int which, const SolveParams& p, const F& f, int V, int 
     }
 }
 
-// Compile-time geometries of the BASELINE sizes.  Rows (V*TV = 256 threads,
-// one radix-8 butterfly per thread per stage): n = W/2 for W in {512, 1024,
-// 1920, 2048, 4096}.  Columns (512 threads and <= 64 KB so two CTAs share an
-// SM and overlap load / compute / store; V*8 >= 32-byte row segments; 4096
-// needs 1024 threads): H in {512, 1024, 1080, 2048, 4096}.
-#define BLFLS_CT_ROWS(X) X(256, 8, 32) X(512, 4, 64) X(960, 2, 128) X(1024, 2, 128) X(2048, 1, 256)
-#define BLFLS_CT_COLS(X) X(512, 16, 32) X(1024, 8, 64) X(1080, 4, 128) X(2048, 4, 128) X(4096, 4, 256)
+// Compile-time geometries of the BASELINE sizes (N, V vectors per CTA, TV
+// threads per vector).  Rows: ~256 threads, one radix-8 butterfly per thread
+// per stage, n = W/2 for W in {512, 1024, 1920, 2048, 4096}.  Columns: 512
+// threads and <= 64 KB so two CTAs share an SM (4096 needs 1024 threads),
+// V*8 >= 32-byte row segments, H in {512, 1024, 1080, 2048, 4096}.  Narrow
+// variants (small V) keep small images from running a handful of CTAs.
+#define BLFLS_CT_ROWS(X) X(256, 8, 32) X(256, 2, 32) X(512, 4, 64) X(512, 1, 64) X(960, 2, 128) \
+    X(1024, 2, 128) X(2048, 1, 256)
+#define BLFLS_CT_COLS(X) X(512, 16, 32) X(512, 2, 64) X(1024, 8, 64) X(1024, 2, 128) \
+    X(1080, 4, 128) X(2048, 4, 128) X(4096, 4, 256)
 
-bool ct_geometry(bool cols, int n, int* V, int* threads)
+// Largest-V geometry that still launches >= 2 CTAs per SM for `planes`
+// planes; otherwise the narrowest one.
+// nvec: vectors per plane (spectrum columns W/2+1, or image rows H)
+bool ct_geometry(bool cols, int n, int nvec, int planes, int nsm, int* V, int* threads)
 {
-#define BLFLS_GEOM(N, VV, TV) \
-    if (n == N) { *V = VV; *threads = VV * TV; return true; }
+    int bestV = 0, bestT = 0, narrowV = 1 << 30, narrowT = 0;
+    auto consider = [&](int N, int VV, int TV) {
+        if (n != N) return;
+        const long ctas = (long)planes * ((nvec + VV - 1) / VV);
+        if (ctas >= 2L * nsm && VV > bestV) {
+            bestV = VV;
+            bestT = VV * TV;
+        }
+        if (VV < narrowV) {
+            narrowV = VV;
+            narrowT = VV * TV;
+        }
+    };
+#define BLFLS_GEOM(N, VV, TV) consider(N, VV, TV);
     if (cols) {
         BLFLS_CT_COLS(BLFLS_GEOM)
     } else {
         BLFLS_CT_ROWS(BLFLS_GEOM)
     }
 #undef BLFLS_GEOM
+    if (bestV) {
+        *V = bestV;
+        *threads = bestT;
+        return true;
+    }
+    if (narrowT) {
+        *V = narrowV;
+        *threads = narrowT;
+        return true;
+    }
     return false;
 }
 
@@ -421,7 +449,7 @@ static cudaError_t launch_fft_pass(int which, const SolveParams& p, const FftGeo
     const int n = g.desc.n;
     if (g.ct && !odd) {
 #define BLFLS_CT_LAUNCH(N, VV, TV)                                                          \
-    if (n == N) {                                                                          \
+    if (n == N && g.V == VV) {                                                             \
         launch_pass(which, p, CtFft<N, VV, TV>{g.desc.tw}, VV, N, VV * TV, planes, odd, st); \
         return cudaGetLastError();                                                         \
     }
