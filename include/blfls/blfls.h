@@ -65,7 +65,7 @@ typedef enum blfls_status {
 typedef struct blfls_plan_s* blfls_plan_t;
 
 /* Everything a plan is specialised on.  Mirrors SmootherSpec
- * (pipelines.hpp:16-23) restricted to kind == BLF_LS, pad == 0. */
+ * (pipelines.hpp:16-23) restricted to kind == BLF_LS. */
 typedef struct blfls_params {
     int height, width;    /* image size, >= 2 each */
     int channels;         /* 1 or 3 (image.cpp:16-17) */
@@ -79,6 +79,11 @@ typedef struct blfls_params {
     double lambda;        /* SolveParams::lambda (solver.hpp:12-15); pad is 0 */
     int max_batch;        /* images per call the plan's workspace is sized for */
     int device;           /* CUDA device ordinal */
+    int pad;              /* SolveParams::pad: reflect padding before the gradients and
+                             the FFT solve, cropped at the end (pipelines.cpp:76-92,
+                             image.cpp:185-230); 0 = periodic boundary.  Besides
+                             blfls_run, blfls_solve honours it; the other stage
+                             entry points require pad == 0. */
 } blfls_params;
 
 /* Validates like validate_params / validate_solve_params (bilateral.cpp:12-24,
@@ -115,9 +120,10 @@ blfls_status blfls_filter_gradients_rows(blfls_plan_t plan, const float* img, co
                                          int y0, int y1, float* tx, float* ty, void* stream,
                                          unsigned flags);
 
-/* lsgrad_solve_fft(g, {tx, ty}, {lambda, 0}) (solver.cpp:88-124); all
- * arguments batch x C x H x W.  tx/ty may both be NULL (ls_solve_fft,
- * solver.cpp:67-86). */
+/* lsgrad_solve_fft(g, {tx, ty}, {lambda, pad}) (solver.cpp:88-124) with the
+ * plan's pad (image and targets reflect-padded as plain rasters, result
+ * cropped); all arguments batch x C x H x W.  tx/ty may both be NULL
+ * (ls_solve_fft, solver.cpp:67-86). */
 blfls_status blfls_solve(blfls_plan_t plan, const float* g, const float* tx, const float* ty,
                          int batch, float* u, void* stream, unsigned flags);
 

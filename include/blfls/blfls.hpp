@@ -65,7 +65,7 @@ struct RangeSpatialParams {
 
 struct SolveParams {
     double lambda = 1024.0;
-    int pad = 16;  // only 0 (periodic) is implemented on the GPU
+    int pad = 16;  // reflect padding (solver.hpp:12-15); 0 = periodic
 };
 
 struct SmootherSpec {
@@ -96,9 +96,9 @@ struct PlanDeleter {
 using PlanPtr = std::unique_ptr<blfls_plan_s, PlanDeleter>;
 
 inline PlanPtr make_plan(int h, int w, int c, int gc, int radius, double ss, double sr, double lam,
-                         int batch, int device)
+                         int batch, int device, int pad = 0)
 {
-    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device};
+    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device, pad};
     blfls_plan_t raw = nullptr;
     check(blfls_plan_create(&p, &raw));
     return PlanPtr(raw);
@@ -116,14 +116,14 @@ inline std::vector<float> to_f32(const Image& img)
 /// `iters` cascaded smooth() calls with the brute-force (joint) BLF, guide
 /// held fixed.  guide: nullptr, 1 channel, or img.channels() channels.
 inline Image blf_ls(const Image& img, const Image* guide, double lambda, double sigma_s,
-                    double sigma_r, int iters = 1, int radius = -1, int device = 0)
+                    double sigma_r, int iters = 1, int radius = -1, int device = 0, int pad = 0)
 {
     if (guide && (guide->width() != img.width() || guide->height() != img.height() ||
                   (guide->channels() != 1 && guide->channels() != img.channels())))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
     auto plan = detail::make_plan(img.height(), img.width(), img.channels(),
                                   guide ? guide->channels() : 0, radius, sigma_s, sigma_r, lambda,
-                                  1, device);
+                                  1, device, pad);
     std::vector<float> in = detail::to_f32(img), out(img.size()), gd;
     if (guide) gd = detail::to_f32(*guide);
     detail::check(blfls_run(plan.get(), in.data(), guide ? gd.data() : nullptr, 1, iters,
@@ -133,15 +133,13 @@ inline Image blf_ls(const Image& img, const Image* guide, double lambda, double 
     return res;
 }
 
-/// epls::smooth for kind BLF_LS (brute-force BLF), pad must be 0.
+/// epls::smooth for kind BLF_LS (brute-force BLF), including reflect padding.
 inline Image smooth(const Image& g, const SmootherSpec& spec)
 {
-    if (spec.solve.pad != 0)
-        throw std::domain_error("smooth: only pad == 0 (periodic boundary) is implemented");
     if (spec.guidance && !spec.guidance->same_shape(g))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
     return blf_ls(g, spec.guidance, spec.solve.lambda, spec.blf.sigma_s, spec.blf.sigma_r, 1,
-                  spec.radius, spec.device);
+                  spec.radius, spec.device, spec.solve.pad);
 }
 
 /// epls::flash_no_flash: joint smoothing of `noflash` guided by `flash`.
@@ -153,14 +151,15 @@ inline Image flash_no_flash(const Image& noflash, const Image& flash, SmootherSp
     return smooth(noflash, spec);
 }
 
-/// epls::lsgrad_solve_fft with pad 0.
+/// epls::lsgrad_solve_fft (targets and image reflect-padded by `pad`).
 inline Image lsgrad_solve_fft(const Image& g, const Image& tx, const Image& ty, double lambda,
-                              int device = 0)
+                              int device = 0, int pad = 0)
 {
     if (!g.same_shape(tx) || !g.same_shape(ty))
         throw std::invalid_argument("lsgrad_solve_fft: target shape does not match image");
+    if (pad < 0) throw std::invalid_argument("solver: pad must be >= 0");
     auto plan = detail::make_plan(g.height(), g.width(), g.channels(), 0, 1, 1.0, 1.0, lambda, 1,
-                                  device);
+                                  device, pad);
     std::vector<float> a = detail::to_f32(g), b = detail::to_f32(tx), c = detail::to_f32(ty),
                        out(g.size());
     detail::check(blfls_solve(plan.get(), a.data(), b.data(), c.data(), 1, out.data(), nullptr,

@@ -635,9 +635,9 @@ int orc_smooth_brute(const double* g, int c, int h, int w, const double* guide, 
     return smooth_core(g, c, h, w, guide, radius, sigma_s, sigma_r, lambda, pad, out, NULL, NULL);
 }
 
-int orc_blf_ls_timed(const double* g, int c, int h, int w, const double* guide, int guide_c,
-                     int radius, double sigma_s, double sigma_r, double lambda, int iters,
-                     double* out, double* t_blf, double* t_solve)
+static int blf_ls_core(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                       int radius, double sigma_s, double sigma_r, double lambda, int iters, int pad,
+                       double* out, double* t_blf, double* t_solve)
 {
     if (c != 1 && c != 3) return ORC_EINVAL;
     if (h < 1 || w < 1 || iters < 1) return ORC_EINVAL;
@@ -656,7 +656,7 @@ int orc_blf_ls_timed(const double* g, int c, int h, int w, const double* guide, 
     if (t_solve) *t_solve = 0.0;
     int st = ORC_OK;
     for (int k = 0; k < iters && st == ORC_OK; ++k) {
-        st = smooth_core(f, c, h, w, guide_rep, radius, sigma_s, sigma_r, lambda, 0, out, t_blf,
+        st = smooth_core(f, c, h, w, guide_rep, radius, sigma_s, sigma_r, lambda, pad, out, t_blf,
                          t_solve);
         memcpy(f, out, sizeof(double) * n);
     }
@@ -665,11 +665,28 @@ int orc_blf_ls_timed(const double* g, int c, int h, int w, const double* guide, 
     return st;
 }
 
+int orc_blf_ls_timed(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                     int radius, double sigma_s, double sigma_r, double lambda, int iters,
+                     double* out, double* t_blf, double* t_solve)
+{
+    return blf_ls_core(g, c, h, w, guide, guide_c, radius, sigma_s, sigma_r, lambda, iters, 0, out,
+                       t_blf, t_solve);
+}
+
 int orc_blf_ls(const double* g, int c, int h, int w, const double* guide, int guide_c, int radius,
                double sigma_s, double sigma_r, double lambda, int iters, double* out)
 {
-    return orc_blf_ls_timed(g, c, h, w, guide, guide_c, radius, sigma_s, sigma_r, lambda, iters, out,
-                            NULL, NULL);
+    return blf_ls_core(g, c, h, w, guide, guide_c, radius, sigma_s, sigma_r, lambda, iters, 0, out,
+                       NULL, NULL);
+}
+
+int orc_blf_ls_pad(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                   int radius, double sigma_s, double sigma_r, double lambda, int iters, int pad,
+                   double* out)
+{
+    if (pad < 0) return ORC_EINVAL;
+    return blf_ls_core(g, c, h, w, guide, guide_c, radius, sigma_s, sigma_r, lambda, iters, pad, out,
+                       NULL, NULL);
 }
 
 /* ------------------------------------------------------------ generator -- */

@@ -88,6 +88,11 @@ int orc_smooth_brute(const double* g, int c, int h, int w, const double* guide, 
  * replicated into c channels (the reference rejects the mismatch). */
 int orc_blf_ls(const double* g, int c, int h, int w, const double* guide, int guide_c, int radius,
                double sigma_s, double sigma_r, double lambda, int iters, double* out);
+/* Same cascade with the reference's reflect padding (SolveParams::pad,
+ * pipelines.cpp:76-92) in every smooth() call. */
+int orc_blf_ls_pad(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                   int radius, double sigma_s, double sigma_r, double lambda, int iters, int pad,
+                   double* out);
 
 /* Per-stage split of one smooth_brute call (for the CPU baseline report):
  * returns seconds spent in the BLF stage and in the solve stage. */

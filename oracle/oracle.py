@@ -69,7 +69,7 @@ def lib() -> C.CDLL:
         _lib.orc_splitmix64_at.argtypes = [C.c_uint64, C.c_uint64]
         _lib.orc_diff_gain_sq.restype = C.c_double
         _lib.orc_gen_plane.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _fp]
-        for name in ("orc_blf_ls", "orc_blf_ls_timed", "orc_smooth_brute", "orc_blf_brute_r",
+        for name in ("orc_blf_ls", "orc_blf_ls_timed", "orc_blf_ls_pad", "orc_smooth_brute", "orc_blf_brute_r",
                      "orc_lsgrad_solve_fft", "orc_dense_solve"):
             getattr(_lib, name).restype = C.c_int
     return _lib
@@ -114,13 +114,20 @@ def _check(fn: str, st: int):
 
 # ---------------------------------------------------------------- oracle --
 
-def blf_ls(img, guide=None, *, lam, sigma_s, sigma_r, iters, radius, timed=False):
-    """North-star cascade (orc_blf_ls): f <- smooth_brute(f) `iters` times."""
+def blf_ls(img, guide=None, *, lam, sigma_s, sigma_r, iters, radius, timed=False, pad=0):
+    """North-star cascade (orc_blf_ls): f <- smooth_brute(f) `iters` times
+    (with the reference's reflect padding when pad > 0)."""
     g = _f64(img)
     c, h, w = _shape3(g)
     out = np.empty((c, h, w))
     gd = None if guide is None else _f64(guide)
     gc = 0 if gd is None else _shape3(gd)[0]
+    if pad:
+        assert not timed
+        st = lib().orc_blf_ls_pad(_d(g), c, h, w, _d(gd), gc, int(radius), C.c_double(sigma_s),
+                                  C.c_double(sigma_r), C.c_double(lam), int(iters), int(pad), _d(out))
+        _check("orc_blf_ls_pad", st)
+        return out
     if timed:
         tb, ts = C.c_double(), C.c_double()
         st = lib().orc_blf_ls_timed(_d(g), c, h, w, _d(gd), gc, int(radius), C.c_double(sigma_s),
@@ -325,7 +332,7 @@ def ref_smooth_grid(img, guide=None, *, lam, sigma_s, sigma_r, pad=0):
     return out
 
 
-def ref_blf_ls(img, guide=None, *, lam, sigma_s, sigma_r, iters, radius, timed=False):
+def ref_blf_ls(img, guide=None, *, lam, sigma_s, sigma_r, iters, radius, timed=False, pad=0):
     g = _f64(img)
     c, h, w = _shape3(g)
     out = np.empty((c, h, w))
@@ -333,9 +340,9 @@ def ref_blf_ls(img, guide=None, *, lam, sigma_s, sigma_r, iters, radius, timed=F
     gc = 0 if gd is None else _shape3(gd)[0]
     tb, ts = C.c_double(), C.c_double()
     _check("ref_blf_ls",
-           ref().ref_blf_ls(_d(g), c, h, w, _d(gd), gc, int(radius), C.c_double(sigma_s),
-                            C.c_double(sigma_r), C.c_double(lam), int(iters), _d(out), C.byref(tb),
-                            C.byref(ts)))
+           ref().ref_blf_ls_pad(_d(g), c, h, w, _d(gd), gc, int(radius), C.c_double(sigma_s),
+                                C.c_double(sigma_r), C.c_double(lam), int(iters), int(pad), _d(out),
+                                C.byref(tb), C.byref(ts)))
     if timed:
         return out, tb.value, ts.value
     return out

@@ -258,16 +258,16 @@ int ref_smooth_brute(const double* g, int c, int h, int w, const double* guide, 
 // The north-star cascade over the reference pieces: f <- smooth_brute(f)
 // `iters` times with the guide fixed; a 1-channel guide for a c-channel image
 // is replicated (smooth() rejects the mismatch, pipelines.cpp:60-62).
-int ref_blf_ls(const double* g, int c, int h, int w, const double* guide, int guide_c, int radius,
-               double sigma_s, double sigma_r, double lambda, int iters, double* out,
-               double* t_blf, double* t_solve)
+int ref_blf_ls_pad(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                   int radius, double sigma_s, double sigma_r, double lambda, int iters, int pad,
+                   double* out, double* t_blf, double* t_solve)
 {
     return guarded([&] {
         if (iters < 1) throw std::invalid_argument("blf_ls: iters must be >= 1");
         SmootherSpec s;
         s.kind = SmootherKind::BLF_LS;
         s.blf = {sigma_s, sigma_r};
-        s.solve = {lambda, 0};
+        s.solve = {lambda, pad};
         PlanarImage gd;
         if (guide) {
             if (guide_c != 1 && guide_c != c)
@@ -284,6 +284,14 @@ int ref_blf_ls(const double* g, int c, int h, int w, const double* guide, int gu
         for (int k = 0; k < iters; ++k) f = smooth_brute(f, s, radius, t_blf, t_solve);
         unwrap(f, out);
     });
+}
+
+int ref_blf_ls(const double* g, int c, int h, int w, const double* guide, int guide_c, int radius,
+               double sigma_s, double sigma_r, double lambda, int iters, double* out,
+               double* t_blf, double* t_solve)
+{
+    return ref_blf_ls_pad(g, c, h, w, guide, guide_c, radius, sigma_s, sigma_r, lambda, iters, 0, out,
+                          t_blf, t_solve);
 }
 
 int ref_random_image(int w, int h, int c, unsigned long long seed, double lo, double hi, double* out)

@@ -86,15 +86,16 @@ class SmootherSpec:
 _tls = threading.local()
 
 
-def get_plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, batch, device) -> Plan:
+def get_plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, batch, device, pad=0) -> Plan:
     """Per-thread plan cache (plans are not thread-safe, blfls.h)."""
     cache = getattr(_tls, "plans", None)
     if cache is None:
         cache = _tls.plans = {}
-    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device)
+    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device, int(pad))
     p = cache.get(key)
     if p is None or p.params.max_batch < batch:
-        p = Plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, max_batch=max(batch, 1), device=device)
+        p = Plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, max_batch=max(batch, 1), device=device,
+                 pad=pad)
         cache[key] = p
     return p
 
@@ -187,11 +188,14 @@ def _device(img: _Img, guide: _Img | None) -> int:
 
 def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, iters: int = 1,
            radius: int | None = None, check_finite: bool = True, use_graph: bool = True,
-           out=None, extra_flags: int = 0, wait: bool = True):
+           out=None, extra_flags: int = 0, wait: bool = True, pad: int = 0):
     """BLF-LS: ``iters`` cascaded smooth() passes with the brute-force (joint) BLF.
 
     ``guide`` (optional) has 1 channel or the image's channel count and is held
-    fixed over the iterations.  Returns the smoothed image in the input's type
+    fixed over the iterations.  ``pad`` reflect-pads every smooth() input before
+    the gradients and the solve and crops the result (SolveParams::pad,
+    pipelines.cpp:76-92; the reference default is 16, the BASELINE configs
+    use 0 = periodic).  Returns the smoothed image in the input's type
     (written into ``out`` when given: an fp32 array/tensor of the image's shape
     in the same memory space, e.g. pinned host memory).
 
@@ -208,8 +212,10 @@ def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, ite
                                   "smooth: guidance image shape does not match input")
     r = _radius(radius, sigma_s)
     dev = _device(img, gd)
+    if int(pad) < 0:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "solver: pad must be >= 0")
     plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, lam,
-                    img.b, dev)
+                    img.b, dev, pad=int(pad))
     if out is None:
         out = img.empty_like()
         finish = True
@@ -252,16 +258,14 @@ def sync_plans() -> None:
 
 
 def smooth(g, spec: SmootherSpec):
-    """``epls::smooth`` (pipelines.cpp:57-94) for kind BLF_LS (brute-force BLF) and LS."""
-    if spec.solve.pad != 0:
-        raise Unsupported(_capi.BLFLS_EUNSUPPORTED,
-                          "smooth: only pad == 0 (periodic boundary) is implemented")
+    """``epls::smooth`` (pipelines.cpp:57-94) for kind BLF_LS (brute-force BLF) and LS,
+    including the reference's reflect padding ``spec.solve.pad`` (default 16)."""
     if spec.kind == SmootherKind.BLF_LS:
         return blf_ls(g, spec.guidance, lam=spec.solve.lam, sigma_s=spec.blf.sigma_s,
-                      sigma_r=spec.blf.sigma_r, iters=1, radius=spec.radius)
+                      sigma_r=spec.blf.sigma_r, iters=1, radius=spec.radius, pad=spec.solve.pad)
     if spec.kind == SmootherKind.LS:
         # affine-equivariant, so normalise/denormalise (pipelines.cpp:64,68) is the identity
-        return ls_solve_fft(g, SolveParams(spec.solve.lam, 0))
+        return ls_solve_fft(g, spec.solve)
     raise Unsupported(_capi.BLFLS_EUNSUPPORTED, f"smooth: {spec.kind} is out of scope")
 
 
@@ -292,9 +296,10 @@ def filter_gradients(image, guide=None, *, sigma_s: float, sigma_r: float,
 
 
 def lsgrad_solve_fft(g, target, params: SolveParams):
-    """``lsgrad_solve_fft`` (solver.cpp:88-124); target = (tx, ty) or None."""
-    if params.pad != 0:
-        raise Unsupported(_capi.BLFLS_EUNSUPPORTED, "lsgrad_solve_fft: only pad == 0 is implemented")
+    """``lsgrad_solve_fft`` (solver.cpp:88-124); target = (tx, ty) or None; the image
+    and targets are reflect-padded by ``params.pad`` and the result cropped."""
+    if params.pad < 0:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "solver: pad must be >= 0")
     if not (params.lam >= 0.0) or not math.isfinite(params.lam):
         raise InvalidArgument(_capi.BLFLS_EINVAL, "solver: lambda must be finite and >= 0")
     img = _Img(g)
@@ -306,7 +311,7 @@ def lsgrad_solve_fft(g, target, params: SolveParams):
                                   "lsgrad_solve_fft: target shape does not match image")
         txp, typ = tx.ptr, ty.ptr
     plan = get_plan(img.h, img.w, img.c, 0, 1, 1.0, 1.0, params.lam, img.b,
-                    _device(img, None))
+                    _device(img, None), pad=int(params.pad))
     out = img.empty_like()
     stream, flags = _stream_and_flags(img)
     check(lib().blfls_solve(plan.handle, img.ptr, txp, typ, img.b, _ptr(out), stream,

@@ -9,7 +9,7 @@
 namespace blfls {
 
 constexpr int kMaxRadius = 48;     // smem tile envelope (radius <= 48)
-constexpr int kMaxFftRadices = 24;
+constexpr int kMaxFftRadices = 32;
 constexpr int kMaxGenericRadix = 31;
 
 // log2(e)
@@ -61,6 +61,7 @@ struct FftGeom {
     int V, log2V, threads;
     int E;         // complex values per thread across a stage barrier (8 or 16)
     bool generic;  // a radix other than 2/3/4/5 occurs
+    bool direct;   // a prime factor above 13 (direct DFT stage, 2x shared memory)
     bool ct;       // a compile-time specialised engine exists for (n, V, threads)
 };
 
@@ -94,7 +95,8 @@ struct SolveParams {
     const float* tx;     // targets or nullptr
     const float* ty;
     float2* spec;        // planes x H x spitch
-    float* out;          // output image
+    float* out;          // output image (oH x oW per plane: the padded grid cropped by opad)
+    int oH, oW, opad;
     uint32_t* lohi_out;  // per image ordered (lo, hi) of out, or nullptr
     const float* gain_x; // 4 sin^2(pi v / W), v in [0, W/2]
     const float* gain_y; // 4 sin^2(pi u / H)

@@ -34,6 +34,8 @@ cudaError_t launch_scale_by_range(float* x, size_t per_image, int batch, const u
 cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int K, double sigma,
                             double p_sp, float* out, cudaStream_t st);
 cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz);
+cudaError_t launch_reflect_pad(const float* src, float* dst, int H, int W, int pad, size_t planes,
+                               int nsm, cudaStream_t st);
 bool ct_geometry(bool cols, int n, int nvec, int planes, int nsm, int* V, int* threads);
 
 }  // namespace blfls
@@ -74,9 +76,12 @@ bool factorize(int n, std::vector<int>& radix)
     while (m % 4 == 0) { radix.push_back(4); m /= 4; }
     while (m % 2 == 0) { radix.push_back(2); m /= 2; }
     for (int p : {3, 5}) while (m % p == 0) { radix.push_back(p); m /= p; }
-    for (int p = 7; p <= 13 && m > 1; p += 2)
+    // any other prime: 7..13 register-staged generic stage, larger ones the
+    // direct DFT stage (sizes produced by reflect padding)
+    for (int p = 7; (long)p * p <= m; p += 2)
         while (m % p == 0) { radix.push_back(p); m /= p; }
-    return m == 1 && (int)radix.size() <= kMaxFftRadices;
+    if (m > 1) radix.push_back(m);
+    return (int)radix.size() <= kMaxFftRadices;
 }
 
 // threads per vector so that every stage fits the E-register budget of fft_stage
@@ -84,6 +89,7 @@ int threads_per_vector(const std::vector<int>& radix, int n, int E)
 {
     int tv = 1;
     for (int p : radix) {
+        if (p > 13) continue;  // direct stage: any thread count
         const int nbp = n / p;
         const int nb = p <= 5 ? (E + p - 1) / p : (2 * E) / p;
         if (nb < 1) return 1 << 30;
@@ -98,8 +104,11 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
               DevFft& out, std::vector<int>& radix)
 {
     if (!factorize(n, radix)) return false;
-    bool generic = false;
-    for (int p : radix) generic |= p > 5;
+    bool generic = false, direct = false;
+    for (int p : radix) {
+        generic |= p > 5;
+        direct |= p > 13;
+    }
     int cv = 0, ct = 0;
     if (!odd && ct_geometry(cols, n, nvec, planes, nsm, &cv, &ct)) {
         FftGeom& g = out.g;
@@ -109,11 +118,12 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
         g.threads = ct;
         g.E = 16;
         g.generic = false;
+        g.direct = false;
         g.ct = true;
         return true;
     }
     for (int V = Vmax; V >= 1; V >>= 1) {
-        if ((size_t)V * n * 8 > smem_cap) continue;
+        if ((size_t)V * n * 8 * (direct ? 2 : 1) > smem_cap) continue;
         for (int E : {8, 16}) {
             int tv = threads_per_vector(radix, n, E);
             // whole warps per CTA: the block reductions shuffle over full warps
@@ -126,6 +136,7 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
             g.threads = tv * V;
             g.E = E;
             g.generic = generic;
+            g.direct = direct;
             g.ct = false;
             return true;
         }
@@ -170,7 +181,12 @@ struct blfls_plan_s {
     float* gain_y = nullptr;
     float2* post = nullptr;
     // workspace (max_batch images)
-    size_t plane = 0, img_elems = 0;
+    size_t plane = 0, img_elems = 0;  // user (unpadded) plane H*W
+    // reflect padding: the BLF and the solve run on the padded grid Hp x Wp
+    int pad = 0, Hp = 0, Wp = 0;
+    size_t pplane = 0;
+    float* fpad = nullptr;   // padded current image
+    float* gpad = nullptr;   // padded guide
     float* buf[2] = {nullptr, nullptr};
     float* tx = nullptr;
     float* ty = nullptr;
@@ -242,9 +258,12 @@ void stage_end(blfls_plan_t p, cudaStream_t st)
 SolveParams solve_params(blfls_plan_t p)
 {
     SolveParams s{};
-    s.H = p->prm.height;
-    s.W = p->prm.width;
+    s.H = p->Hp;
+    s.W = p->Wp;
     s.C = p->prm.channels;
+    s.oH = p->prm.height;
+    s.oW = p->prm.width;
+    s.opad = p->pad;
     s.spitch = p->spitch;
     s.wc = p->wc;
     s.lambda = (float)p->prm.lambda;
@@ -287,8 +306,9 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
         return BLFLS_OK;
     }
     // grouped: spectrum regions 0 / 1 alternate between the two streams
-    const size_t pimg = (size_t)p->prm.height * p->prm.width;
-    const size_t pspec = (size_t)p->prm.height * p->spitch;
+    const size_t pimg = p->pplane;                      // padded inputs
+    const size_t pout = p->plane;                       // cropped outputs
+    const size_t pspec = (size_t)p->Hp * p->spitch;
     if (lohi_out) {
         CK(launch_reset_lohi(lohi_out, batch, st));
         p->launches++;
@@ -305,7 +325,7 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
         g.f = f + p0 * pimg;
         g.tx = tx ? tx + p0 * pimg : nullptr;
         g.ty = ty ? ty + p0 * pimg : nullptr;
-        g.out = out + p0 * pimg;
+        g.out = out + p0 * pout;
         g.spec = p->spec + (size_t)(k & 1) * grp * pspec;
         CK(launch_row_r2c(g, p->rowf.g, np, p->odd, cs));
         CK(launch_col(g, p->colf.g, np, cs));
@@ -364,15 +384,29 @@ blfls_status enq_run(blfls_plan_t p, const float* in, const float* guide, float*
     }
     r = enq_minmax(p, in, per_image, batch, p->lohi, st);
     if (r) return r;
+    const float* g_use = guide;
+    if (guide && p->pad > 0) {  // pipelines.cpp:82-83: the guide is padded once
+        CK(launch_reflect_pad(guide, p->gpad, p->prm.height, p->prm.width, p->pad,
+                              (size_t)batch * p->prm.guide_channels, p->nsm, st));
+        p->launches++;
+        g_use = p->gpad;
+    }
     const float* cur = in;
     for (int k = 0; k < iters; ++k) {
         const bool last = k == iters - 1;
         float* nxt = last ? out : p->buf[k & 1];
         uint32_t* lo_cur = p->lohi + (size_t)(k & 1) * 2 * mb;
         uint32_t* lo_nxt = last ? nullptr : p->lohi + (size_t)((k + 1) & 1) * 2 * mb;
-        r = enq_blf(p, cur, guide, lo_cur, p->tx, p->ty, batch, 0, p->prm.height, p->prm.height, 0, st);
+        const float* f = cur;
+        if (p->pad > 0) {  // pipelines.cpp:76-78: reflect-pad every smooth() input
+            CK(launch_reflect_pad(cur, p->fpad, p->prm.height, p->prm.width, p->pad,
+                                  (size_t)batch * p->prm.channels, p->nsm, st));
+            p->launches++;
+            f = p->fpad;
+        }
+        r = enq_blf(p, f, g_use, lo_cur, p->tx, p->ty, batch, 0, p->Hp, p->Hp, 0, st);
         if (r) return r;
-        r = enq_solve(p, cur, p->tx, p->ty, nxt, lo_nxt, batch, st);
+        r = enq_solve(p, f, p->tx, p->ty, nxt, lo_nxt, batch, st);  // c2r crops (pipelines.cpp:92)
         if (r) return r;
         cur = nxt;
     }
@@ -437,7 +471,7 @@ void free_plan(blfls_plan_t p)
     }
     void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
-                    p->rowf.tw, p->colf.tw};
+                    p->rowf.tw, p->colf.tw, p->fpad, p->gpad};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
@@ -477,6 +511,8 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     if (!(q.lambda >= 0.0) || !std::isfinite(q.lambda))
         return fail(BLFLS_EINVAL, "solver: lambda must be finite and >= 0");
     if (q.max_batch < 1) return fail(BLFLS_EINVAL, "plan: max_batch must be >= 1");
+    if (q.pad < 0) return fail(BLFLS_EINVAL, "solver: pad must be >= 0");  // solver.cpp:19-20
+    if (q.pad > 4096) return fail(BLFLS_EUNSUPPORTED, "plan: pad above 4096");
     const int radius = q.radius < 0 ? (int)std::ceil(3.0 * q.sigma_s) : q.radius;
     if (radius > kMaxRadius)
         return fail(BLFLS_EUNSUPPORTED, "plan: radius above " + std::to_string(kMaxRadius));
@@ -501,7 +537,12 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         return bail(fail(BLFLS_ECUDA, std::string("device is not sm_100-class: ") + prop.name));
     p->nsm = prop.multiProcessorCount;
 
-    const int H = q.height, W = q.width, C = q.channels;
+    const int C = q.channels;
+    p->pad = q.pad;
+    p->Hp = q.height + 2 * q.pad;
+    p->Wp = q.width + 2 * q.pad;
+    // everything spectral and the BLF run on the padded grid
+    const int H = p->Hp, W = p->Wp;
     p->odd = (W % 2) != 0;
     p->wc = W / 2 + 1;
     p->spitch = ((p->wc + 15) / 16) * 16;
@@ -512,10 +553,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     while (vrow * 2 * nrow <= 2048 && vrow < 16) vrow *= 2;
     if (!plan_fft(nrow, vrow, 64 * 1024, false, p->odd, H, q.max_batch * C, p->nsm, p->rowf, rrad))
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: width " + std::to_string(W) +
-                                                 " has a prime factor above 13 or too large"));
+                                                 " too large for the shared-memory row FFT"));
     if (!plan_fft(H, 16, 128 * 1024, true, false, p->wc, q.max_batch * C, p->nsm, p->colf, crad))
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: height " + std::to_string(H) +
-                                                 " has a prime factor above 13 or too large"));
+                                                 " too large for the shared-memory column FFT"));
 
     // tables (double -> float)
     {
@@ -588,13 +629,20 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     }
 
     // workspace
-    p->plane = (size_t)H * W;
+    p->plane = (size_t)q.height * q.width;
+    p->pplane = (size_t)H * W;
     p->img_elems = (size_t)q.max_batch * C * p->plane;
+    const size_t pad_elems = (size_t)q.max_batch * C * p->pplane;
     const size_t spec_elems = (size_t)q.max_batch * C * H * p->spitch;
+    if (p->pad > 0 &&
+        (cudaMalloc(&p->fpad, sizeof(float) * pad_elems) != cudaSuccess ||
+         (q.guide_channels &&
+          cudaMalloc(&p->gpad, sizeof(float) * q.max_batch * q.guide_channels * p->pplane) != cudaSuccess)))
+        return bail(fail(BLFLS_ENOMEM, "plan: padded workspace allocation failed"));
     if (cudaMalloc(&p->buf[0], sizeof(float) * p->img_elems) != cudaSuccess ||
         cudaMalloc(&p->buf[1], sizeof(float) * p->img_elems) != cudaSuccess ||
-        cudaMalloc(&p->tx, sizeof(float) * p->img_elems) != cudaSuccess ||
-        cudaMalloc(&p->ty, sizeof(float) * p->img_elems) != cudaSuccess ||
+        cudaMalloc(&p->tx, sizeof(float) * pad_elems) != cudaSuccess ||
+        cudaMalloc(&p->ty, sizeof(float) * pad_elems) != cudaSuccess ||
         cudaMalloc(&p->spec, sizeof(float2) * spec_elems) != cudaSuccess ||
         cudaMalloc(&p->lohi, sizeof(uint32_t) * 4 * q.max_batch) != cudaSuccess ||
         cudaMalloc(&p->glohi, sizeof(uint32_t) * 2 * q.max_batch) != cudaSuccess ||
@@ -756,7 +804,7 @@ blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int
     }
     const int G = p->mode == 2 ? 1 : p->prm.channels;
     const double taps = (double)(2 * p->radius + 1) * (2 * p->radius + 1);
-    p->stats.exps = taps * (double)p->plane * 2.0 * batch * G * iters;
+    p->stats.exps = taps * (double)p->pplane * 2.0 * batch * G * iters;
     p->stats.blf_launches = iters;
     if (!host) return join_out(p, us, flags);
     CK(cudaEventRecord(sl->comp, st));
@@ -791,6 +839,8 @@ blfls_status blfls_filter_gradients(blfls_plan_t p, const float* img, const floa
                                     float* tx, float* ty, void* stream, unsigned flags)
 {
     blfls_status r = validate_batch(p, batch);
+    if (r) return r;
+    if (p->pad) return fail(BLFLS_EUNSUPPORTED, "stage entry points require pad == 0");
     if (r) return r;
     if ((p->prm.guide_channels == 0) != (guide == nullptr))
         return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
@@ -839,6 +889,8 @@ blfls_status blfls_filter_gradients_rows(blfls_plan_t p, const float* img, const
 {
     blfls_status r = validate_batch(p, 1);
     if (r) return r;
+    if (p->pad) return fail(BLFLS_EUNSUPPORTED, "stage entry points require pad == 0");
+    if (r) return r;
     if (y0 < 0 || y1 > p->prm.height || y0 >= y1) return fail(BLFLS_EINVAL, "rows: bad row range");
     if ((p->prm.guide_channels == 0) != (guide == nullptr))
         return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
@@ -862,6 +914,7 @@ blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const 
     if ((tx == nullptr) != (ty == nullptr))
         return fail(BLFLS_EINVAL, "lsgrad_solve_fft: target shape does not match image");
     if ((r = set_device(p))) return r;
+    if (p->pad && (r = ensure_host_slots(p))) return r;  // unpadded staging for the padded path
     cudaStream_t us = (cudaStream_t)stream;
     if ((r = fork_in(p, us))) return r;
     cudaStream_t st = p->ps;
@@ -872,13 +925,17 @@ blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const 
     const float* dty = ty;
     float* du = u;
     if (host) {
-        CK(cudaMemcpyAsync(p->buf[0], g, sizeof(float) * n, cudaMemcpyHostToDevice, st));
-        dg = p->buf[0];
+        // with padding the targets are staged unpadded and padded into p->tx/ty below
+        float* sg = p->pad ? p->slot[0].in : p->buf[0];
+        float* stx = p->pad ? p->slot[1].in : p->tx;
+        float* sty = p->pad ? p->slot[1].out : p->ty;
+        CK(cudaMemcpyAsync(sg, g, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        dg = sg;
         if (tx) {
-            CK(cudaMemcpyAsync(p->tx, tx, sizeof(float) * n, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(p->ty, ty, sizeof(float) * n, cudaMemcpyHostToDevice, st));
-            dtx = p->tx;
-            dty = p->ty;
+            CK(cudaMemcpyAsync(stx, tx, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(sty, ty, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            dtx = stx;
+            dty = sty;
         }
         du = p->buf[1];
     }
@@ -886,6 +943,19 @@ blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const 
         if ((r = check_finite(p, dg, n, st, "lsgrad_solve_fft"))) return r;
         if (dtx && (r = check_finite(p, dtx, n, st, "lsgrad_solve_fft"))) return r;
         if (dty && (r = check_finite(p, dty, n, st, "lsgrad_solve_fft"))) return r;
+    }
+    if (p->pad) {
+        // solver.cpp:97-99: the image and the targets are reflect-padded as
+        // plain rasters; the solve crops (solver.cpp:123)
+        const size_t planes = (size_t)batch * p->prm.channels;
+        CK(launch_reflect_pad(dg, p->fpad, p->prm.height, p->prm.width, p->pad, planes, p->nsm, st));
+        dg = p->fpad;
+        if (dtx) {
+            CK(launch_reflect_pad(dtx, p->tx, p->prm.height, p->prm.width, p->pad, planes, p->nsm, st));
+            CK(launch_reflect_pad(dty, p->ty, p->prm.height, p->prm.width, p->pad, planes, p->nsm, st));
+            dtx = p->tx;
+            dty = p->ty;
+        }
     }
     if ((r = enq_solve(p, dg, dtx, dty, du, nullptr, batch, st))) return r;
     if (host) CK(cudaMemcpyAsync(u, du, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
@@ -896,6 +966,8 @@ static blfls_status fft_entry(blfls_plan_t p, const float* in, int batch, float*
                               unsigned flags, bool forward)
 {
     blfls_status r = validate_batch(p, batch);
+    if (r) return r;
+    if (p->pad) return fail(BLFLS_EUNSUPPORTED, "stage entry points require pad == 0");
     if (r) return r;
     if ((r = set_device(p))) return r;
     cudaStream_t us = (cudaStream_t)stream;

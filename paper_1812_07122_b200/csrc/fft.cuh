@@ -193,6 +193,37 @@ __device__ void fft_stage_generic(float2* buf, const FftLane& l, int n, int V, i
     __syncthreads();
 }
 
+// Direct DFT stage for primes above 13 (reflect-padded sizes such as
+// 1952 = 2^5 * 61 or 1112 = 2^3 * 139): every output sums its p inputs from
+// shared memory (p complex MACs per element) into `scratch`, then the stage
+// result is copied back.  Only sizes with such a factor take this path.
+template <bool COLS>
+__device__ void fft_stage_direct(float2* buf, float2* scratch, const FftLane& l, int n, int V, int s,
+                                 int P, const float2* __restrict__ tw, bool inv)
+{
+    const int nbp = n / P;
+    for (int o = l.t; o < n; o += l.TV) {
+        const int k = o % s, rest = o / s;
+        const int t = rest % P, q = rest / P;
+        const int bb = q * s + k;
+        float2 acc = make_float2(0.f, 0.f);
+        int e = 0;  // (r * t) mod P
+        for (int r = 0; r < P; ++r) {
+            float2 w = __ldg(&tw[e * nbp]);
+            if (inv) w.y = -w.y;
+            acc = cadd(acc, cmul(buf[fft_addr<COLS>(l, bb + r * nbp, n, V)], w));
+            e += t;
+            if (e >= P) e -= P;
+        }
+        float2 w2 = __ldg(&tw[q * t * s]);
+        if (inv) w2.y = -w2.y;
+        scratch[fft_addr<COLS>(l, o, n, V)] = cmul(acc, w2);
+    }
+    __syncthreads();
+    for (int o = l.t; o < n; o += l.TV) buf[fft_addr<COLS>(l, o, n, V)] = scratch[fft_addr<COLS>(l, o, n, V)];
+    __syncthreads();
+}
+
 // Full transform of the CTA's V vectors (unnormalised; inverse = conjugate twiddles).
 template <int E, bool COLS, bool GENERIC>
 __device__ void fft_run(float2* buf, const FftDesc& d, int V, int log2V, bool inv)
@@ -201,7 +232,9 @@ __device__ void fft_run(float2* buf, const FftDesc& d, int V, int log2V, bool in
     int s = 1;
     for (int st = 0; st < d.nstages; ++st) {
         const int p = d.radix[st];
-        if (p == 4)
+        if (GENERIC && p > 13)
+            fft_stage_direct<COLS>(buf, buf + (size_t)V * d.n, l, d.n, V, s, p, d.tw, inv);
+        else if (p == 4)
             fft_stage<4, E, COLS>(buf, l, d.n, V, s, d.tw, inv);
         else if (p == 2)
             fft_stage<2, E, COLS>(buf, l, d.n, V, s, d.tw, inv);
@@ -357,10 +390,11 @@ struct RtFft {
     int V, log2V;
     __device__ __forceinline__ int n() const { return d.n; }
     __device__ __forceinline__ int vecs() const { return V; }
+    bool direct;  // a prime factor above 13: the direct stage needs a scratch buffer
     template <bool COLS>
     __device__ __forceinline__ int pad(int flat) const { return flat; }
     __device__ __forceinline__ int threads() const { return blockDim.x; }
-    size_t smem_bytes(bool) const { return (size_t)V * d.n * sizeof(float2); }
+    size_t smem_bytes(bool) const { return (size_t)V * d.n * sizeof(float2) * (direct ? 2 : 1); }
     template <bool COLS>
     __device__ __forceinline__ void run(float2* buf, bool inv) const
     {

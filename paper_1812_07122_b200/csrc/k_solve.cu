@@ -227,20 +227,38 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
     __syncthreads();
     fft.template run<false>(buf, true);
     float lo = INFINITY, hi = -INFINITY;
-    float* out = p.out + (size_t)plane * p.H * W;
+    // crop (reflect-padded grids): only rows/cols [opad, opad + oH/oW) are written
+    float* out = p.out + (size_t)plane * p.oH * p.oW;
     for (int idx = threadIdx.x; idx < V * n; idx += fft.threads()) {
         const int v = idx / n, j = idx - (idx / n) * n;
         const int y = row0 + v;
-        if (y >= p.H) continue;
+        const int yo = y - p.opad;
+        if (y >= p.H || yo < 0 || yo >= p.oH) continue;
         const float2 z = buf[fft.template pad<false>(idx)];
-        if (!ODD) {
-            *reinterpret_cast<float2*>(out + (size_t)y * W + 2 * j) = z;
+        float* orow = out + (size_t)yo * p.oW;
+        if (!ODD && p.opad == 0) {
+            *reinterpret_cast<float2*>(orow + 2 * j) = z;
             lo = fminf(lo, fminf(z.x, z.y));
             hi = fmaxf(hi, fmaxf(z.x, z.y));
+        } else if (!ODD) {
+            const int x0 = 2 * j - p.opad;
+            if (x0 >= 0 && x0 < p.oW) {
+                orow[x0] = z.x;
+                lo = fminf(lo, z.x);
+                hi = fmaxf(hi, z.x);
+            }
+            if (x0 + 1 >= 0 && x0 + 1 < p.oW) {
+                orow[x0 + 1] = z.y;
+                lo = fminf(lo, z.y);
+                hi = fmaxf(hi, z.y);
+            }
         } else {
-            out[(size_t)y * W + j] = z.x;
-            lo = fminf(lo, z.x);
-            hi = fmaxf(hi, z.x);
+            const int xo = j - p.opad;
+            if (xo >= 0 && xo < p.oW) {
+                orow[xo] = z.x;
+                lo = fminf(lo, z.x);
+                hi = fmaxf(hi, z.x);
+            }
         }
     }
     if (p.lohi_out != nullptr) block_minmax_atomic(lo, hi, p.lohi_out + 2 * ((p.plane0 + plane) / p.C));
@@ -291,6 +309,40 @@ __global__ void k_count_nonfinite(const float* __restrict__ x, size_t n, unsigne
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+// reflect padding without edge repeat (image.cpp:185-212): dst (H+2pad) x
+// (W+2pad) per plane from src H x W; grid-stride over all planes
+__device__ __forceinline__ int reflect_index(int q, int n)
+{
+    if (n == 1) return 0;
+    const int period = 2 * (n - 1);
+    q = abs(q) % period;
+    return q < n ? q : period - q;
+}
+
+__global__ void k_reflect_pad(const float* __restrict__ src, float* __restrict__ dst, int H, int W,
+                              int pad, size_t planes)
+{
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const size_t per = (size_t)Hp * Wp, total = per * planes;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const size_t pl = i / per, r = i - pl * per;
+        const int y = (int)(r / Wp), x = (int)(r - (size_t)y * Wp);
+        const int sy = reflect_index(y - pad, H), sx = reflect_index(x - pad, W);
+        dst[i] = __ldg(src + pl * H * W + (size_t)sy * W + sx);
+    }
+}
+
+cudaError_t launch_reflect_pad(const float* src, float* dst, int H, int W, int pad, size_t planes,
+                               int nsm, cudaStream_t st)
+{
+    size_t total = (size_t)(H + 2 * pad) * (W + 2 * pad) * planes;
+    size_t blocks = (total + 255) / 256;
+    if (blocks > (size_t)nsm * 16) blocks = (size_t)nsm * 16;
+    k_reflect_pad<<<(unsigned)blocks, 256, 0, st>>>(src, dst, H, W, pad, planes);
+    return cudaGetLastError();
 }
 
 // targets in normalised units -> raw: t * (hi - lo) (stage entry helper)
@@ -462,14 +514,14 @@ static cudaError_t launch_fft_pass(int which, const SolveParams& p, const FftGeo
     }
     if (g.E == 16) {
         if (g.generic)
-            launch_pass(which, p, RtFft<16, true>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<16, true>{g.desc, g.V, g.log2V, g.direct}, g.V, n, g.threads, planes, odd, st);
         else
-            launch_pass(which, p, RtFft<16, false>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<16, false>{g.desc, g.V, g.log2V, false}, g.V, n, g.threads, planes, odd, st);
     } else {
         if (g.generic)
-            launch_pass(which, p, RtFft<8, true>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<8, true>{g.desc, g.V, g.log2V, g.direct}, g.V, n, g.threads, planes, odd, st);
         else
-            launch_pass(which, p, RtFft<8, false>{g.desc, g.V, g.log2V}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<8, false>{g.desc, g.V, g.log2V, false}, g.V, n, g.threads, planes, odd, st);
     }
     return cudaGetLastError();
 }

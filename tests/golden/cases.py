@@ -24,4 +24,12 @@ CASES = [
          sigma_s=2.0, sigma_r=0.05, lam=1000.0, iters=2, radius=6),
     dict(name="gray_48x40_wide_range", w=48, h=40, c=1, scene="natural", seed=3, guide=None,
          sigma_s=2.0, sigma_r=1e6, lam=1e-9, iters=1, radius=6),
+    # reflect padding (SolveParams::pad, the reference default is 16); the
+    # padded grids carry prime factors 43 and 17 (direct-DFT FFT stages)
+    dict(name="gray_37x45_pad3", w=37, h=45, c=1, scene="natural", seed=12, guide=None,
+         sigma_s=1.0, sigma_r=0.1, lam=300.0, iters=2, radius=3, pad=3),
+    dict(name="rgb_34x30_pad16_default", w=34, h=30, c=3, scene="natural", seed=13, guide=None,
+         sigma_s=1.0, sigma_r=0.04, lam=1024.0, iters=1, radius=3, pad=16),
+    dict(name="rgb_32x24_joint_gray_pad4", w=32, h=24, c=3, scene="natural", seed=6,
+         guide=("natural", 11, 1), sigma_s=1.0, sigma_r=0.1, lam=1000.0, iters=2, radius=3, pad=4),
 ]

@@ -39,7 +39,7 @@ def main():
             guide = scene(kind, cs["w"], cs["h"], gc, seed).astype(np.float32)
         out = O.ref_blf_ls(img.astype(np.float64), None if guide is None else guide.astype(np.float64),
                            lam=cs["lam"], sigma_s=cs["sigma_s"], sigma_r=cs["sigma_r"],
-                           iters=cs["iters"], radius=cs["radius"])
+                           iters=cs["iters"], radius=cs["radius"], pad=cs.get("pad", 0))
         arrays = dict(img=img, out=out)
         if guide is not None:
             arrays["guide"] = guide

@@ -63,6 +63,7 @@ def test_plan_create_validation_without_gpu(lib):
         _capi.Params(16, 16, 1, 0, 3, 1.0, -0.1, 1.0, 1, 0),   # sigma_r
         _capi.Params(16, 16, 1, 0, 3, 1.0, 0.1, -1.0, 1, 0),   # lambda
         _capi.Params(16, 16, 1, 0, 3, 1.0, 0.1, float("nan"), 1, 0),
+        _capi.Params(16, 16, 1, 0, 3, 1.0, 0.1, 1.0, 1, 0, -1),    # pad < 0
     ]
     for p in bad:
         assert L.blfls_plan_create(ctypes.byref(p), ctypes.byref(h)) == _capi.BLFLS_EINVAL
@@ -82,8 +83,8 @@ def test_host_mirror_rejects_bad_shapes():
     with pytest.raises(P.InvalidArgument):
         P.blf_ls(np.zeros((8, 8), np.float32), np.zeros((9, 8), np.float32), lam=1.0,
                  sigma_s=1.0, sigma_r=0.1)
-    with pytest.raises(P.Unsupported):
-        P.smooth(np.zeros((8, 8), np.float32), P.SmootherSpec())  # reference default pad = 16
+    with pytest.raises(P.InvalidArgument):
+        P.blf_ls(np.zeros((8, 8), np.float32), lam=1.0, sigma_s=1.0, sigma_r=0.1, pad=-1)
 
 
 def test_no_cpu_fallback_in_product():

@@ -55,7 +55,7 @@ def test_usage_errors_exit_2(cli, tmp_path):
     assert run(cli, "smooth").returncode == 2
     assert run(cli, "smooth", "--method", "bogus", "in.pfm", "out.pfm").returncode == 2
     assert run(cli, "smooth", "--sigma-s", "-1", "in.pfm", "out.pfm").returncode == 2
-    assert run(cli, "smooth", "--pad", "16", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "smooth", "--pad", "-1", "in.pfm", "out.pfm").returncode == 2
     assert run(cli, "joint", "in.pfm", "out.pfm").returncode == 2  # --guide required
 
 
@@ -83,7 +83,8 @@ def test_ls_lambda0_pgm_round_trip_pixel_exact(gpu, cli, tmp_path):
 def test_blf_ls_pfm_matches_api_and_is_deterministic(gpu, cli, oracle, tmp_path):
     img = np.stack([oracle.gen_plane(900 + c, 48, 64, n_sites=12) for c in range(3)])
     write_pfm(tmp_path / "in.pfm", img)
-    args = ["--sigma-s", "3", "--sigma-r", "0.1", "--lambda", "500", "--radius", "5", "--iters", "2"]
+    args = ["--sigma-s", "3", "--sigma-r", "0.1", "--lambda", "500", "--radius", "5", "--iters", "2",
+            "--pad", "0"]
     for k in (1, 2):
         r = run(cli, "smooth", *args, tmp_path / "in.pfm", tmp_path / f"o{k}.pfm")
         assert r.returncode == 0, r.stderr
@@ -102,9 +103,22 @@ def test_joint_subcommand(gpu, cli, oracle, tmp_path):
     write_pfm(tmp_path / "in.pfm", img)
     write_pfm(tmp_path / "g.pfm", np.repeat(guide, 3, axis=0))
     r = run(cli, "joint", "--guide", tmp_path / "g.pfm", "--sigma-r", "0.1", "--sigma-s", "3",
-            "--radius", "4", "--lambda", "800", tmp_path / "in.pfm", tmp_path / "o.pfm")
+            "--radius", "4", "--lambda", "800", "--pad", "0", tmp_path / "in.pfm", tmp_path / "o.pfm")
     assert r.returncode == 0, r.stderr
     out = read_pfm(tmp_path / "o.pfm")
     ref = oracle.blf_ls(img.astype(np.float64), guide.astype(np.float64), lam=800.0, sigma_s=3.0,
                         sigma_r=0.1, iters=1, radius=4)
     assert np.abs(out - ref).max() <= 1e-4
+
+
+@pytest.mark.gpu
+def test_reference_default_padding(gpu, cli, oracle, tmp_path):
+    """`smooth` with no --pad uses the reference default 16 (epls_main.cpp:34)."""
+    img = np.stack([oracle.gen_plane(950 + c, 30, 34, n_sites=12) for c in range(3)])
+    write_pfm(tmp_path / "in.pfm", img)
+    r = run(cli, "smooth", "--sigma-s", "1", "--sigma-r", "0.1", "--radius", "3", "--lambda", "600",
+            tmp_path / "in.pfm", tmp_path / "o.pfm")
+    assert r.returncode == 0, r.stderr
+    ref = oracle.blf_ls(img.astype(np.float64), lam=600.0, sigma_s=1.0, sigma_r=0.1, iters=1,
+                        radius=3, pad=16)
+    assert np.abs(read_pfm(tmp_path / "o.pfm") - ref).max() <= 1e-4

@@ -37,7 +37,8 @@ def test_golden_vectors(gpu, case):
     d = np.load(HERE / "golden" / f"{case['name']}.npz")
     guide = d["guide"] if "guide" in d else None
     out = gpu.blf_ls(d["img"], guide, lam=case["lam"], sigma_s=case["sigma_s"],
-                     sigma_r=case["sigma_r"], iters=case["iters"], radius=case["radius"])
+                     sigma_r=case["sigma_r"], iters=case["iters"], radius=case["radius"],
+                     pad=case.get("pad", 0))
     assert out.shape == d["out"].shape
     assert maxabs(out, d["out"]) <= TOL_OUT
 
@@ -189,7 +190,9 @@ def test_nonfinite_and_shape_errors(gpu):
     with pytest.raises(gpu.InvalidArgument):
         gpu.blf_ls(g, lam=-1.0, sigma_s=1.0, sigma_r=0.1)
     with pytest.raises(gpu.Unsupported):
-        gpu.blf_ls(np.zeros((1, 17, 16), np.float32), lam=1.0, sigma_s=1.0, sigma_r=0.1, radius=2)
+        gpu.blf_ls(g, lam=1.0, sigma_s=1.0, sigma_r=0.1, radius=60)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_ls(g, lam=1.0, sigma_s=1.0, sigma_r=0.1, radius=2, pad=-1)
 
 
 def test_minimum_size_and_ragged(gpu, oracle):
@@ -364,3 +367,43 @@ def test_async_host_pipeline(gpu, oracle):
     with pytest.raises(gpu.InvalidArgument):
         plan.sync()
     plan.sync()  # the deferred error is reported once
+
+
+@pytest.mark.parametrize("c,h,w,r,pad,guided", [
+    (1, 45, 37, 3, 3, False),    # 51 x 43: prime 43 (direct DFT stage), odd padded width
+    (3, 30, 34, 3, 16, False),   # the reference default pad: 62 x 66 (31, 11)
+    (1, 17, 16, 2, 0, False),    # unpadded prime height 17
+    (3, 40, 56, 7, 16, True),    # joint gray guide, padded 72 x 88
+    (1, 96, 128, 15, 16, False), # large window on a padded 128 x 160 grid
+])
+def test_reflect_padding_vs_oracle(gpu, oracle, c, h, w, r, pad, guided):
+    img = _img(oracle, c, h, w, 40 + h + pad)
+    guide = _img(oracle, 1, h, w, 90 + h) if guided else None
+    kw = dict(lam=800.0, sigma_s=r / 2.0, sigma_r=0.1, iters=2, radius=r)
+    ref = oracle.blf_ls(img.astype(np.float64), None if guide is None else guide.astype(np.float64),
+                        pad=pad, **kw)
+    out = gpu.blf_ls(img, guide, pad=pad, **kw)
+    assert out.shape == img.shape
+    assert maxabs(out, ref) <= TOL_OUT
+
+
+def test_smooth_reference_defaults(gpu, oracle):
+    """smooth(g, SmootherSpec()) with the reference's defaults (sigma 12 / 0.04,
+    lambda 1024, pad 16; radius ceil(3*12) = 36)."""
+    img = _img(oracle, 3, 48, 40, 7)
+    out = gpu.smooth(img, gpu.SmootherSpec())
+    ref = oracle.blf_ls(img.astype(np.float64), lam=1024.0, sigma_s=12.0, sigma_r=0.04, iters=1,
+                        radius=36, pad=16)
+    assert maxabs(out, ref) <= TOL_OUT
+
+
+@pytest.mark.parametrize("pad", [0, 4, 16])
+def test_solve_with_padding_vs_oracle(gpu, oracle, pad):
+    rng = np.random.default_rng(pad + 3)
+    g = rng.random((3, 26, 34)).astype(np.float32)
+    tx, ty = rng.uniform(-0.2, 0.2, (2, 3, 26, 34)).astype(np.float32)
+    u = gpu.lsgrad_solve_fft(g, (tx, ty), gpu.SolveParams(500.0, pad))
+    ref = oracle.lsgrad_solve_fft(g, tx, ty, lam=500.0, pad=pad)
+    assert maxabs(u, ref) <= 5e-5
+    ls = gpu.ls_solve_fft(g, gpu.SolveParams(500.0, pad))
+    assert maxabs(ls, oracle.lsgrad_solve_fft(g, None, None, lam=500.0, pad=pad)) <= 5e-5

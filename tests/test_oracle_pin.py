@@ -226,8 +226,20 @@ def test_oracle_matches_golden(oracle, case):
     img = d["img"].astype(np.float64)
     guide = d["guide"].astype(np.float64) if "guide" in d else None
     out = oracle.blf_ls(img, guide, lam=case["lam"], sigma_s=case["sigma_s"],
-                        sigma_r=case["sigma_r"], iters=case["iters"], radius=case["radius"])
+                        sigma_r=case["sigma_r"], iters=case["iters"], radius=case["radius"],
+                        pad=case.get("pad", 0))
     assert maxabs(out, d["out"]) < 1e-12
+
+
+@pytest.mark.parametrize("pad", [1, 5, 16])
+def test_padded_cascade_vs_reference(ref, pad):
+    # pipelines.cpp:76-92 (reflect_pad -> gradients -> filter -> solve -> crop)
+    g = ref.ref_natural_scene(30, 22, 3, 14)
+    gd = ref.ref_natural_scene(30, 22, 1, 15)
+    for guide in (None, gd):
+        a = ref.ref_blf_ls(g, guide, lam=700.0, sigma_s=1.5, sigma_r=0.1, iters=2, radius=3, pad=pad)
+        b = ref.blf_ls(g, guide, lam=700.0, sigma_s=1.5, sigma_r=0.1, iters=2, radius=3, pad=pad)
+        assert maxabs(a, b) < 1e-13
 
 
 # ------------------------------------------------------------- generator --

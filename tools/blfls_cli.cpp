@@ -2,14 +2,14 @@
 // reference CLI's hot-path subcommands (/root/reference/proj/tools/epls_main.cpp):
 //
 //   blfls smooth [--method blf-ls|ls] [--sigma-s S] [--sigma-r R] [--lambda L]
-//                [--pad 0] [--radius r] [--iters k] [--device d] input output
+//                [--pad 16] [--radius r] [--iters k] [--device d] input output
 //   blfls joint  --guide G [same flags] input output
 //
 // Defaults follow epls_main.cpp: sigma_s 12, sigma_r 0.04 (joint: 12 / 0.003,
 // its preparse defaults), lambda 1024.  Differences: the bilateral stage is
 // the brute-force filter (north star) with an explicit --radius (default
-// ceil(3 sigma_s) like bilateral.cpp:37); --iters cascades smooth() calls; the
-// GPU solve is periodic, so --pad defaults to 0 and pad > 0 is rejected.
+// ceil(3 sigma_s) like bilateral.cpp:37); --iters cascades smooth() calls;
+// --pad (reflect padding) defaults to 16 as in the reference.
 // Image formats: PFM (float, 'Pf' gray / 'PF' RGB, bottom-up, either endian)
 // and binary PGM/PPM (P5/P6, 8 or 16 bit) with the reference's conventions
 // (image_io.cpp: PNM values / maxval, PNM output clamped and rounded to 8 bit).
@@ -178,7 +178,7 @@ void save_image(const std::string& path, const blfls::Image& img)
 struct Options {
     std::string cmd, input, output, guide, method = "blf-ls";
     double sigma_s = 12.0, sigma_r = 0.04, lambda = -1.0;
-    int pad = 0, radius = -1, iters = 1, device = 0;
+    int pad = 16, radius = -1, iters = 1, device = 0;
 };
 
 double parse_double(const std::string& flag, const char* v)
@@ -252,7 +252,6 @@ Options parse(int argc, char** argv)
     if (o.cmd == "joint" && o.guide.empty()) throw UsageError("joint: --guide is required");
     o.input = pos[0];
     o.output = pos[1];
-    if (o.pad != 0) throw UsageError("--pad > 0: the GPU solve is periodic (pad 0 only)");
     return o;
 }
 
@@ -266,14 +265,14 @@ int run(const Options& o)
         // plain LS == lsgrad with a zero target (test_solver.cpp:129-134); the
         // reference normalises first (pipelines.cpp:64-68), a no-op for this
         // affine-equivariant solve
-        out = blfls::lsgrad_solve_fft(in, zero, zero, lam, o.device);
+        out = blfls::lsgrad_solve_fft(in, zero, zero, lam, o.device, o.pad);
     } else if (o.cmd == "joint") {
         const blfls::Image guide = load_image(o.guide);
         if (guide.width() != in.width() || guide.height() != in.height())
             throw std::invalid_argument("flash_no_flash: image shapes differ");
-        out = blfls::blf_ls(in, &guide, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device);
+        out = blfls::blf_ls(in, &guide, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device, o.pad);
     } else {
-        out = blfls::blf_ls(in, nullptr, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device);
+        out = blfls::blf_ls(in, nullptr, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device, o.pad);
     }
     save_image(o.output, out);
     return 0;
