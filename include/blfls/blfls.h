@@ -84,7 +84,15 @@ typedef struct blfls_params {
                              image.cpp:185-230); 0 = periodic boundary.  Besides
                              blfls_run, blfls_solve honours it; the other stage
                              entry points require pad == 0. */
+    int backend;          /* gradient filter: BLFLS_BACKEND_BRUTE (0, the north star:
+                             brute-force BLF over the (2r+1)^2 window) or
+                             BLFLS_BACKEND_GRID (1, the bilateral grid blf_grid that
+                             the reference's smooth() runs, bilateral.cpp:112-207,
+                             grid sampling = (sigma_s, sigma_r); radius unused) */
 } blfls_params;
+
+#define BLFLS_BACKEND_BRUTE 0
+#define BLFLS_BACKEND_GRID 1
 
 /* Validates like validate_params / validate_solve_params (bilateral.cpp:12-24,
  * solver.cpp:15-21) and caches twiddles, spectral denominators and workspaces. */

@@ -74,6 +74,7 @@ struct SmootherSpec {
     const Image* guidance = nullptr;
     int radius = -1;  // < 0: ceil(3 sigma_s) as bilateral.cpp:37
     int device = 0;
+    int backend = BLFLS_BACKEND_BRUTE;  // or BLFLS_BACKEND_GRID (the reference's blf_grid)
 };
 
 namespace detail {
@@ -96,9 +97,9 @@ struct PlanDeleter {
 using PlanPtr = std::unique_ptr<blfls_plan_s, PlanDeleter>;
 
 inline PlanPtr make_plan(int h, int w, int c, int gc, int radius, double ss, double sr, double lam,
-                         int batch, int device, int pad = 0)
+                         int batch, int device, int pad = 0, int backend = BLFLS_BACKEND_BRUTE)
 {
-    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device, pad};
+    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device, pad, backend};
     blfls_plan_t raw = nullptr;
     check(blfls_plan_create(&p, &raw));
     return PlanPtr(raw);
@@ -116,14 +117,15 @@ inline std::vector<float> to_f32(const Image& img)
 /// `iters` cascaded smooth() calls with the brute-force (joint) BLF, guide
 /// held fixed.  guide: nullptr, 1 channel, or img.channels() channels.
 inline Image blf_ls(const Image& img, const Image* guide, double lambda, double sigma_s,
-                    double sigma_r, int iters = 1, int radius = -1, int device = 0, int pad = 0)
+                    double sigma_r, int iters = 1, int radius = -1, int device = 0, int pad = 0,
+                    int backend = BLFLS_BACKEND_BRUTE)
 {
     if (guide && (guide->width() != img.width() || guide->height() != img.height() ||
                   (guide->channels() != 1 && guide->channels() != img.channels())))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
     auto plan = detail::make_plan(img.height(), img.width(), img.channels(),
                                   guide ? guide->channels() : 0, radius, sigma_s, sigma_r, lambda,
-                                  1, device, pad);
+                                  1, device, pad, backend);
     std::vector<float> in = detail::to_f32(img), out(img.size()), gd;
     if (guide) gd = detail::to_f32(*guide);
     detail::check(blfls_run(plan.get(), in.data(), guide ? gd.data() : nullptr, 1, iters,
@@ -139,7 +141,7 @@ inline Image smooth(const Image& g, const SmootherSpec& spec)
     if (spec.guidance && !spec.guidance->same_shape(g))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
     return blf_ls(g, spec.guidance, spec.solve.lambda, spec.blf.sigma_s, spec.blf.sigma_r, 1,
-                  spec.radius, spec.device, spec.solve.pad);
+                  spec.radius, spec.device, spec.solve.pad, spec.backend);
 }
 
 /// epls::flash_no_flash: joint smoothing of `noflash` guided by `flash`.

@@ -25,6 +25,8 @@ SYNC = 4
 NO_GRAPH = 8
 TIME_STAGES = 16
 ASYNC = 32
+BACKEND_BRUTE = 0
+BACKEND_GRID = 1
 
 # every symbol include/blfls/blfls.h declares
 EXPORTS = (
@@ -60,7 +62,7 @@ class Params(C.Structure):
         ("height", C.c_int), ("width", C.c_int), ("channels", C.c_int),
         ("guide_channels", C.c_int), ("radius", C.c_int), ("sigma_s", C.c_double),
         ("sigma_r", C.c_double), ("lambda_", C.c_double), ("max_batch", C.c_int),
-        ("device", C.c_int), ("pad", C.c_int),
+        ("device", C.c_int), ("pad", C.c_int), ("backend", C.c_int),
     ]
 
 
@@ -124,10 +126,10 @@ class Plan:
     """Owns a blfls_plan_t (one per host thread / stream, like the C ABI says)."""
 
     def __init__(self, height, width, channels, guide_channels, radius, sigma_s, sigma_r, lam,
-                 max_batch=1, device=0, pad=0):
+                 max_batch=1, device=0, pad=0, backend=0):
         self.params = Params(int(height), int(width), int(channels), int(guide_channels),
                              int(radius), float(sigma_s), float(sigma_r), float(lam),
-                             int(max_batch), int(device), int(pad))
+                             int(max_batch), int(device), int(pad), int(backend))
         h = C.c_void_p()
         check(lib().blfls_plan_create(C.byref(self.params), C.byref(h)))
         self.handle = h

@@ -79,6 +79,7 @@ class SmootherSpec:
     solve: SolveParams = field(default_factory=SolveParams)
     guidance: Any = None          # non-owning guide image of the same shape (or 1 channel)
     radius: int | None = None     # BLF window radius; None = ceil(3 sigma_s) (bilateral.cpp:37)
+    backend: str = "brute"        # "brute" (north star) or "grid" (the reference smooth()'s blf_grid)
 
 
 # ----------------------------------------------------------------- plans --
@@ -86,16 +87,27 @@ class SmootherSpec:
 _tls = threading.local()
 
 
-def get_plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, batch, device, pad=0) -> Plan:
+_BACKENDS = {"brute": _capi.BACKEND_BRUTE, "grid": _capi.BACKEND_GRID}
+
+
+def _backend(name) -> int:
+    if name not in _BACKENDS:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, f"unknown backend {name!r} (brute | grid)")
+    return _BACKENDS[name]
+
+
+def get_plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, batch, device, pad=0,
+             backend="brute") -> Plan:
     """Per-thread plan cache (plans are not thread-safe, blfls.h)."""
     cache = getattr(_tls, "plans", None)
     if cache is None:
         cache = _tls.plans = {}
-    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device, int(pad))
+    be = _backend(backend)
+    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device, int(pad), be)
     p = cache.get(key)
     if p is None or p.params.max_batch < batch:
         p = Plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, max_batch=max(batch, 1), device=device,
-                 pad=pad)
+                 pad=pad, backend=be)
         cache[key] = p
     return p
 
@@ -188,14 +200,17 @@ def _device(img: _Img, guide: _Img | None) -> int:
 
 def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, iters: int = 1,
            radius: int | None = None, check_finite: bool = True, use_graph: bool = True,
-           out=None, extra_flags: int = 0, wait: bool = True, pad: int = 0):
+           out=None, extra_flags: int = 0, wait: bool = True, pad: int = 0,
+           backend: str = "brute"):
     """BLF-LS: ``iters`` cascaded smooth() passes with the brute-force (joint) BLF.
 
     ``guide`` (optional) has 1 channel or the image's channel count and is held
     fixed over the iterations.  ``pad`` reflect-pads every smooth() input before
     the gradients and the solve and crops the result (SolveParams::pad,
     pipelines.cpp:76-92; the reference default is 16, the BASELINE configs
-    use 0 = periodic).  Returns the smoothed image in the input's type
+    use 0 = periodic).  ``backend="grid"`` filters the gradients with the
+    bilateral grid the reference's smooth() runs (bilateral.cpp:112-207)
+    instead of the brute-force window.  Returns the smoothed image in the input's type
     (written into ``out`` when given: an fp32 array/tensor of the image's shape
     in the same memory space, e.g. pinned host memory).
 
@@ -215,7 +230,7 @@ def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, ite
     if int(pad) < 0:
         raise InvalidArgument(_capi.BLFLS_EINVAL, "solver: pad must be >= 0")
     plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, lam,
-                    img.b, dev, pad=int(pad))
+                    img.b, dev, pad=int(pad), backend=backend)
     if out is None:
         out = img.empty_like()
         finish = True
@@ -262,7 +277,8 @@ def smooth(g, spec: SmootherSpec):
     including the reference's reflect padding ``spec.solve.pad`` (default 16)."""
     if spec.kind == SmootherKind.BLF_LS:
         return blf_ls(g, spec.guidance, lam=spec.solve.lam, sigma_s=spec.blf.sigma_s,
-                      sigma_r=spec.blf.sigma_r, iters=1, radius=spec.radius, pad=spec.solve.pad)
+                      sigma_r=spec.blf.sigma_r, iters=1, radius=spec.radius, pad=spec.solve.pad,
+                      backend=spec.backend)
     if spec.kind == SmootherKind.LS:
         # affine-equivariant, so normalise/denormalise (pipelines.cpp:64,68) is the identity
         return ls_solve_fft(g, spec.solve)
@@ -274,12 +290,12 @@ def flash_no_flash(noflash, flash, spec: SmootherSpec):
     a, b = _Img(noflash), _Img(flash, "guide")
     if a.shape != b.shape:
         raise InvalidArgument(_capi.BLFLS_EINVAL, "flash_no_flash: image shapes differ")
-    s = SmootherSpec(spec.kind, spec.blf, spec.solve, flash, spec.radius)
+    s = SmootherSpec(spec.kind, spec.blf, spec.solve, flash, spec.radius, spec.backend)
     return smooth(noflash, s)
 
 
 def filter_gradients(image, guide=None, *, sigma_s: float, sigma_r: float,
-                     radius: int | None = None):
+                     radius: int | None = None, backend: str = "brute"):
     """Gradient targets of one smooth() call (pipelines.cpp:33-53, brute-force BLF),
     in the reference's normalised units.  Returns (tx, ty)."""
     img = _Img(image)
@@ -287,7 +303,7 @@ def filter_gradients(image, guide=None, *, sigma_s: float, sigma_r: float,
     r = _radius(radius, sigma_s)
     dev = _device(img, gd)
     plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, 0.0,
-                    img.b, dev)
+                    img.b, dev, backend=backend)
     tx, ty = img.empty_like(), img.empty_like()
     stream, flags = _stream_and_flags(img)
     check(lib().blfls_filter_gradients(plan.handle, img.ptr, None if gd is None else gd.ptr, img.b,

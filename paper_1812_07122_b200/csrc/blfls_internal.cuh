@@ -90,6 +90,28 @@ struct BlfParams {
     float wrow[kMaxRadius + 1]; // exp2(cs[d]) : row factor
 };
 
+// bilateral-grid backend (k_grid.cu)
+struct GridParams {
+    const float* f;        // (padded) image, planes x H x W
+    const float* guide;    // (padded) guide or nullptr
+    float* tx;             // targets, raw units
+    float* ty;
+    const uint32_t* lohi;  // per image ordered (lo, hi) of f (fp32)
+    const uint32_t* glohi; // per image of the guide
+    double* wgrid;         // [slots][cells] splat targets
+    double* vgrid;
+    double* wtmp;          // blur ping-pong; the blurred grids end here
+    double* vtmp;
+    unsigned long long* erange;  // [slots][2] ordered (emin, emax) of guide01
+    int H, W, C, GC;
+    int plane0;            // first global plane of this launch
+    int slots;             // plane-axes in this launch
+    double ss, sr;         // grid sampling (sigma_s, sigma_r)
+    int gw, gh, gdmax;     // grid dims (gd per slot <= gdmax)
+    size_t cells;          // gw * gh * gdmax
+    int normalized;        // 1: targets of the [0,1]-normalised image (stage entry)
+};
+
 struct SolveParams {
     const float* f;      // image (batch x C x H x W)
     const float* tx;     // targets or nullptr

@@ -36,6 +36,7 @@ cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int
 cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz);
 cudaError_t launch_reflect_pad(const float* src, float* dst, int H, int W, int pad, size_t planes,
                                int nsm, cudaStream_t st);
+cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st);
 bool ct_geometry(bool cols, int n, int nvec, int planes, int nsm, int* V, int* threads);
 
 }  // namespace blfls
@@ -187,6 +188,9 @@ struct blfls_plan_s {
     size_t pplane = 0;
     float* fpad = nullptr;   // padded current image
     float* gpad = nullptr;   // padded guide
+    // bilateral-grid backend workspace (backend == BLFLS_BACKEND_GRID)
+    GridParams grid{};
+    int grid_planes = 0;     // planes per grid launch (2 slots each)
     float* buf[2] = {nullptr, nullptr};
     float* tx = nullptr;
     float* ty = nullptr;
@@ -338,10 +342,38 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
     return BLFLS_OK;
 }
 
+blfls_status enq_grid(blfls_plan_t p, const float* f, const float* guide, const uint32_t* lohi,
+                      float* tx, float* ty, int batch, int normalized, cudaStream_t st)
+{
+    GridParams g = p->grid;
+    g.f = f;
+    g.guide = guide;
+    g.tx = tx;
+    g.ty = ty;
+    g.lohi = lohi;
+    g.glohi = p->glohi;
+    g.normalized = normalized;
+    const int planes = batch * p->prm.channels;
+    stage_begin(p, 1, st);
+    for (int p0 = 0; p0 < planes; p0 += p->grid_planes) {
+        g.plane0 = p0;
+        g.slots = 2 * std::min(p->grid_planes, planes - p0);
+        CK(launch_grid_blf(g, p->nsm, st));
+        p->launches += 10;
+    }
+    stage_end(p, st);
+    p->stats.blf_launches++;
+    return BLFLS_OK;
+}
+
 blfls_status enq_blf(blfls_plan_t p, const float* f, const float* guide, const uint32_t* lohi,
                      float* tx, float* ty, int batch, int y0, int y1, int out_rows, int normalized,
                      cudaStream_t st)
 {
+    if (p->prm.backend == BLFLS_BACKEND_GRID) {
+        if (y0 != 0 || y1 != p->Hp) return fail(BLFLS_EUNSUPPORTED, "grid backend: no row bands");
+        return enq_grid(p, f, guide, lohi, tx, ty, batch, normalized, st);
+    }
     BlfParams b = p->blf;
     b.f = f;
     b.guide = guide;
@@ -471,7 +503,8 @@ void free_plan(blfls_plan_t p)
     }
     void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
-                    p->rowf.tw, p->colf.tw, p->fpad, p->gpad};
+                    p->rowf.tw, p->colf.tw, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
+                    p->grid.wtmp, p->grid.vtmp, p->grid.erange};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
@@ -513,7 +546,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     if (q.max_batch < 1) return fail(BLFLS_EINVAL, "plan: max_batch must be >= 1");
     if (q.pad < 0) return fail(BLFLS_EINVAL, "solver: pad must be >= 0");  // solver.cpp:19-20
     if (q.pad > 4096) return fail(BLFLS_EUNSUPPORTED, "plan: pad above 4096");
-    const int radius = q.radius < 0 ? (int)std::ceil(3.0 * q.sigma_s) : q.radius;
+    if (q.backend != BLFLS_BACKEND_BRUTE && q.backend != BLFLS_BACKEND_GRID)
+        return fail(BLFLS_EINVAL, "plan: unknown gradient-filter backend");
+    const bool grid = q.backend == BLFLS_BACKEND_GRID;
+    const int radius = grid ? 0 : (q.radius < 0 ? (int)std::ceil(3.0 * q.sigma_s) : q.radius);
     if (radius > kMaxRadius)
         return fail(BLFLS_EUNSUPPORTED, "plan: radius above " + std::to_string(kMaxRadius));
 
@@ -624,8 +660,36 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         // shared-memory envelope of the generic kernel
         const int narr = p->mode == 0 ? 2 : (p->mode == 1 ? 4 : 8);
         const size_t smem = (size_t)narr * (16 + 2 * radius) * (((64 + 2 * radius) + 3) & ~3) * 4;
-        if (smem > 227 * 1024)
+        if (!grid && smem > 227 * 1024)
             return bail(fail(BLFLS_EUNSUPPORTED, "plan: radius too large for the shared-memory tile"));
+    }
+    if (grid) {
+        // bilateral.cpp:126-134 with sampling = (sigma_s, sigma_r); guide01 in [0, 1]
+        GridParams& g = p->grid;
+        g.H = H;
+        g.W = W;
+        g.C = C;
+        g.GC = q.guide_channels;
+        g.ss = q.sigma_s;
+        g.sr = q.sigma_r;
+        g.gw = (int)std::floor((W - 1) / q.sigma_s) + 1 + 4;
+        g.gh = (int)std::floor((H - 1) / q.sigma_s) + 1 + 4;
+        const double gdmax = std::floor(1.0 / q.sigma_r) + 1 + 4 + 1;
+        if (gdmax > 1e6 || (double)g.gw * g.gh * gdmax > 2e9)
+            return bail(fail(BLFLS_EUNSUPPORTED, "grid backend: grid too large for these sigmas"));
+        g.gdmax = (int)gdmax;
+        g.cells = (size_t)g.gw * g.gh * g.gdmax;
+        const size_t per_plane = 2 * 4 * g.cells * sizeof(double);  // 2 slots x 4 grids
+        int np = (int)std::max<size_t>(1, (size_t)(1u << 30) / per_plane);
+        np = std::min(np, q.max_batch * C);
+        p->grid_planes = np;
+        const size_t n = (size_t)2 * np * g.cells;
+        if (cudaMalloc(&g.wgrid, sizeof(double) * n) != cudaSuccess ||
+            cudaMalloc(&g.vgrid, sizeof(double) * n) != cudaSuccess ||
+            cudaMalloc(&g.wtmp, sizeof(double) * n) != cudaSuccess ||
+            cudaMalloc(&g.vtmp, sizeof(double) * n) != cudaSuccess ||
+            cudaMalloc(&g.erange, sizeof(unsigned long long) * 4 * np) != cudaSuccess)
+            return bail(fail(BLFLS_ENOMEM, "plan: grid workspace allocation failed"));
     }
 
     // workspace
@@ -803,7 +867,8 @@ blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int
         p->stats.kernel_launches = p->launches;
     }
     const int G = p->mode == 2 ? 1 : p->prm.channels;
-    const double taps = (double)(2 * p->radius + 1) * (2 * p->radius + 1);
+    const double taps = p->prm.backend == BLFLS_BACKEND_GRID ? 0.0
+                                                            : (double)(2 * p->radius + 1) * (2 * p->radius + 1);
     p->stats.exps = taps * (double)p->pplane * 2.0 * batch * G * iters;
     p->stats.blf_launches = iters;
     if (!host) return join_out(p, us, flags);

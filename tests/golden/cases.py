@@ -33,3 +33,14 @@ CASES = [
     dict(name="rgb_32x24_joint_gray_pad4", w=32, h=24, c=3, scene="natural", seed=6,
          guide=("natural", 11, 1), sigma_s=1.0, sigma_r=0.1, lam=1000.0, iters=2, radius=3, pad=4),
 ]
+
+# The reference's own smooth() (bilateral grid, pipelines.cpp:47) cascaded
+# `iters` times with the guide fixed: the GPU grid backend's parity targets.
+GRID_CASES = [
+    dict(name="grid_gray_64x48_self", w=64, h=48, c=1, scene="natural", seed=21, guide=None,
+         sigma_s=4.0, sigma_r=0.1, lam=500.0, iters=1, pad=0),
+    dict(name="grid_rgb_48x40_self_pad16", w=48, h=40, c=3, scene="natural", seed=22, guide=None,
+         sigma_s=12.0, sigma_r=0.04, lam=1024.0, iters=1, pad=16),
+    dict(name="grid_rgb_56x40_joint_it2", w=56, h=40, c=3, scene="natural", seed=23,
+         guide=("natural", 24, 3), sigma_s=6.0, sigma_r=0.05, lam=800.0, iters=2, pad=0),
+]

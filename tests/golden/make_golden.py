@@ -16,7 +16,7 @@ HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parent.parent))
 sys.path.insert(0, str(HERE))
 
-from cases import CASES  # noqa: E402
+from cases import CASES, GRID_CASES  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
 
@@ -45,6 +45,22 @@ def main():
             arrays["guide"] = guide
         np.savez_compressed(HERE / f"{cs['name']}.npz", **arrays)
         print(cs["name"], out.shape, float(np.abs(out - img).max()))
+    for cs in GRID_CASES:
+        img = scene(cs["scene"], cs["w"], cs["h"], cs["c"], cs["seed"]).astype(np.float32)
+        guide = None
+        if cs["guide"] is not None:
+            kind, seed, gc = cs["guide"]
+            guide = scene(kind, cs["w"], cs["h"], gc, seed).astype(np.float32)
+        f = img.astype(np.float64)
+        for _ in range(cs["iters"]):
+            f = O.ref_smooth_grid(f, None if guide is None else guide.astype(np.float64),
+                                  lam=cs["lam"], sigma_s=cs["sigma_s"], sigma_r=cs["sigma_r"],
+                                  pad=cs["pad"])
+        arrays = dict(img=img, out=f)
+        if guide is not None:
+            arrays["guide"] = guide
+        np.savez_compressed(HERE / f"{cs['name']}.npz", **arrays)
+        print(cs["name"], f.shape, float(np.abs(f - img).max()))
 
 
 if __name__ == "__main__":

@@ -122,3 +122,18 @@ def test_reference_default_padding(gpu, cli, oracle, tmp_path):
     ref = oracle.blf_ls(img.astype(np.float64), lam=600.0, sigma_s=1.0, sigma_r=0.1, iters=1,
                         radius=3, pad=16)
     assert np.abs(read_pfm(tmp_path / "o.pfm") - ref).max() <= 1e-4
+
+
+@pytest.mark.gpu
+def test_grid_backend_reproduces_reference_cli_defaults(gpu, cli, oracle, tmp_path):
+    """`blfls smooth --blf grid in out` = `epls smooth in out` (method blf-ls,
+    sigma 12 / 0.04, lambda 1024, pad 16: the reference CLI's defaults)."""
+    if not oracle.REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    img = np.stack([oracle.gen_plane(970 + c, 40, 48, n_sites=12) for c in range(3)])
+    write_pfm(tmp_path / "in.pfm", img)
+    r = run(cli, "smooth", "--blf", "grid", tmp_path / "in.pfm", tmp_path / "o.pfm")
+    assert r.returncode == 0, r.stderr
+    ref = oracle.ref_smooth_grid(img.astype(np.float64), lam=1024.0, sigma_s=12.0, sigma_r=0.04,
+                                 pad=16)
+    assert np.abs(read_pfm(tmp_path / "o.pfm") - ref).max() <= 1e-4

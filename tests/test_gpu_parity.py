@@ -17,7 +17,7 @@ import pytest
 
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE / "golden"))
-from cases import CASES  # noqa: E402
+from cases import CASES, GRID_CASES  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -407,3 +407,26 @@ def test_solve_with_padding_vs_oracle(gpu, oracle, pad):
     assert maxabs(u, ref) <= 5e-5
     ls = gpu.ls_solve_fft(g, gpu.SolveParams(500.0, pad))
     assert maxabs(ls, oracle.lsgrad_solve_fft(g, None, None, lam=500.0, pad=pad)) <= 5e-5
+
+
+# ---------------------------------------------- bilateral-grid backend --
+
+@pytest.mark.parametrize("case", GRID_CASES, ids=[c["name"] for c in GRID_CASES])
+def test_grid_backend_golden_vectors(gpu, case):
+    """backend="grid" reproduces the reference's shipped smooth() (blf_grid)."""
+    d = np.load(HERE / "golden" / f"{case['name']}.npz")
+    guide = d["guide"] if "guide" in d else None
+    out = gpu.blf_ls(d["img"], guide, lam=case["lam"], sigma_s=case["sigma_s"],
+                     sigma_r=case["sigma_r"], iters=case["iters"], pad=case["pad"], backend="grid")
+    assert maxabs(out, d["out"]) <= TOL_OUT
+
+
+def test_grid_backend_vs_reference_live(gpu, oracle):
+    if not oracle.REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    img = _img(oracle, 3, 72, 96, 61)
+    for pad, ss, sr in ((0, 5.0, 0.05), (16, 12.0, 0.04), (3, 3.0, 0.2)):
+        ref = oracle.ref_smooth_grid(img.astype(np.float64), lam=1000.0, sigma_s=ss, sigma_r=sr, pad=pad)
+        out = gpu.smooth(img, gpu.SmootherSpec(blf=gpu.RangeSpatialParams(ss, sr),
+                                               solve=gpu.SolveParams(1000.0, pad), backend="grid"))
+        assert maxabs(out, ref) <= TOL_OUT

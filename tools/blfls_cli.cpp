@@ -9,7 +9,8 @@
 // its preparse defaults), lambda 1024.  Differences: the bilateral stage is
 // the brute-force filter (north star) with an explicit --radius (default
 // ceil(3 sigma_s) like bilateral.cpp:37); --iters cascades smooth() calls;
-// --pad (reflect padding) defaults to 16 as in the reference.
+// --pad (reflect padding) defaults to 16 as in the reference; --blf grid uses
+// the bilateral grid the reference's smooth() runs (default: brute force).
 // Image formats: PFM (float, 'Pf' gray / 'PF' RGB, bottom-up, either endian)
 // and binary PGM/PPM (P5/P6, 8 or 16 bit) with the reference's conventions
 // (image_io.cpp: PNM values / maxval, PNM output clamped and rounded to 8 bit).
@@ -178,7 +179,7 @@ void save_image(const std::string& path, const blfls::Image& img)
 struct Options {
     std::string cmd, input, output, guide, method = "blf-ls";
     double sigma_s = 12.0, sigma_r = 0.04, lambda = -1.0;
-    int pad = 16, radius = -1, iters = 1, device = 0;
+    int pad = 16, radius = -1, iters = 1, device = 0, backend = BLFLS_BACKEND_BRUTE;
 };
 
 double parse_double(const std::string& flag, const char* v)
@@ -236,6 +237,11 @@ Options parse(int argc, char** argv)
             if (o.iters < 1) throw UsageError("--iters must be >= 1");
         } else if (a == "--iterations") {
             next();  // domain-transform pass count of the reference; no effect on blf-ls
+        } else if (a == "--blf") {
+            const std::string b = next();
+            if (b == "grid") o.backend = BLFLS_BACKEND_GRID;
+            else if (b == "brute") o.backend = BLFLS_BACKEND_BRUTE;
+            else throw UsageError("--blf: brute or grid, got '" + b + "'");
         } else if (a == "--device") {
             o.device = parse_int(a, next());
         } else if (a == "--guide" && o.cmd == "joint") {
@@ -270,9 +276,11 @@ int run(const Options& o)
         const blfls::Image guide = load_image(o.guide);
         if (guide.width() != in.width() || guide.height() != in.height())
             throw std::invalid_argument("flash_no_flash: image shapes differ");
-        out = blfls::blf_ls(in, &guide, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device, o.pad);
+        out = blfls::blf_ls(in, &guide, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device, o.pad,
+                            o.backend);
     } else {
-        out = blfls::blf_ls(in, nullptr, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device, o.pad);
+        out = blfls::blf_ls(in, nullptr, lam, o.sigma_s, o.sigma_r, o.iters, o.radius, o.device, o.pad,
+                            o.backend);
     }
     save_image(o.output, out);
     return 0;
