@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--backend", default="brute", choices=["brute", "grid"],
+                    help="gradient filter: brute-force BLF (north star) or the reference's bilateral grid")
+    ap.add_argument("--pad", type=int, default=0, help="reflect padding (reference default 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -144,7 +147,7 @@ def config_json(cfg, n_gpus, extra=None):
     return d
 
 
-def cpu_sample(cfg, threads=None):
+def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
     """Reference CPU path on a bounded sample of the workload: the first image
     of the config, ONE iteration (of cfg.iters), through oracle/_ref
     (the reference's translation units + brute-force BLF with explicit r).
@@ -170,13 +173,24 @@ def cpu_sample(cfg, threads=None):
         crop = f", centred {side}x{side} crop"
     fn = O.ref_blf_ls if kind == "reference" else O.blf_ls
     t0 = time.perf_counter()
-    _, tb, ts = fn(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
-                   radius=cfg.radius, timed=True)
+    if backend == "grid" and kind == "reference":
+        # the reference's own smooth() (bilateral grid)
+        O.ref_smooth_grid(img, None if guide is None else np.repeat(guide, img.shape[0], axis=0),
+                          lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, pad=pad)
+        tb = ts = float("nan")
+    elif pad:
+        fn(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
+           radius=cfg.radius, pad=pad)
+        tb = ts = float("nan")
+    else:
+        _, tb, ts = fn(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
+                       radius=cfg.radius, timed=True)
     dt = time.perf_counter() - t0
     mp = img.shape[1] * img.shape[2] / 1e6
     return {"value": mp / dt, "unit": "MP/s", "cores": O.num_threads(), "kind": kind,
             "sample": f"1 image x 1 iteration of {cfg.name} ({cfg.height}x{cfg.width}x{cfg.channels}"
-                      f"{crop}), double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
+                      f"{crop}, {'grid' if backend == 'grid' else 'brute-force'} BLF, pad {pad}), "
+                      f"double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
             "seconds": dt, "mp": mp, "blf_s": tb, "solve_s": ts}
 
 
@@ -188,7 +202,7 @@ def run_reference(args, cfg):
         return
     res = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(cfg)
+        r = cpu_sample(cfg, pad=args.pad, backend=args.backend)
         if i >= args.warmup:
             res.append(r)
     secs = [r["seconds"] for r in res]
@@ -250,7 +264,7 @@ def run_ours(args, cfg):
                            n_sites=cfg.n_sites, device=dev).view(n, 1, cfg.height, cfg.width)
     out = torch.empty_like(img)
     kw = dict(lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=cfg.iters,
-              radius=cfg.radius, check_finite=False)
+              radius=cfg.radius, check_finite=False, pad=args.pad, backend=args.backend)
     in_bytes = img.numel() * 4 + (guide.numel() * 4 if guide is not None else 0)
     flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     l2_resident = in_bytes * 4 < 100e6
@@ -263,7 +277,7 @@ def run_ours(args, cfg):
         step()
     torch.cuda.synchronize()
     plan = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, cfg.radius,
-                      cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev)
+                      cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev, pad=args.pad, backend=args.backend)
 
     # ---- timed region: K steps, CUDA events per step, L2 flushed between steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -304,7 +318,7 @@ def run_ours(args, cfg):
     stage_ms, stage_n = plan.stage_times()
     blf_ms = stage_ms[1] / max(1, stage_n[1])
     solve_ms = sum(stage_ms[2:5]) / max(1, stage_n[2])  # per iteration (r2c + col + c2r)
-    exps_per_launch = stats.exps / max(1, stats.blf_launches)
+    exps_per_launch = stats.exps / max(1, stats.blf_launches)  # 0 for the grid backend
 
     mufu_rate, mufu_clk = _capi.mufu_peak(dev)
     # algorithmic exponentials per BLF launch / launch duration vs the SFU peak
@@ -343,7 +357,8 @@ def run_ours(args, cfg):
         # overlap step k's compute and D2H (two staging slots, copy streams).
         h_outs = [h_out, torch.empty(img.shape, dtype=torch.float32).pin_memory()]
         plan_e = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, cfg.radius,
-                            cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev)
+                            cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev, pad=args.pad,
+                            backend=args.backend)
         for k in range(2):
             P.blf_ls(h_img, h_guide, out=h_outs[k % 2], wait=False, **hkw)
         plan_e.sync()
@@ -368,7 +383,7 @@ def run_ours(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            c = cpu_sample(cfg)
+            c = cpu_sample(cfg, pad=args.pad, backend=args.backend)
             cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as exc:  # the baseline must not sink the bench line
             cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": None,
@@ -382,10 +397,11 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Voronoi + ramp + noise, BASELINE generator, generated on device)",
             "config": config_json(cfg, world, {
+                "backend": args.backend, "pad": args.pad,
                 "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2",
                 "decomposition": {"weak": "independent images per rank",
                                   "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]}),
-            "roofline": {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
+            "roofline": None if args.backend == "grid" else {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
                          "achieved": achieved / 1e9, "peak": mufu_rate / 1e9, "unit": "Gexp/s",
                          "frac": achieved / mufu_rate,
                          "peak_source": "measured MUFU.EX2 probe on this GPU "

@@ -677,6 +677,9 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         const double gdmax = std::floor(1.0 / q.sigma_r) + 1 + 4 + 1;
         if (gdmax > 1e6 || (double)g.gw * g.gh * gdmax > 2e9)
             return bail(fail(BLFLS_EUNSUPPORTED, "grid backend: grid too large for these sigmas"));
+        // a cell holds <= (sigma_s + 2)^2 pixels of 2^39-scaled fixed-point values
+        if (q.sigma_s > 4096.0)
+            return bail(fail(BLFLS_EUNSUPPORTED, "grid backend: sigma_s > 4096 overflows the splat"));
         g.gdmax = (int)gdmax;
         g.cells = (size_t)g.gw * g.gh * g.gdmax;
         const size_t per_plane = 2 * 4 * g.cells * sizeof(double);  // 2 slots x 4 grids

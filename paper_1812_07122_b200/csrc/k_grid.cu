@@ -9,7 +9,8 @@
 //      evaluated in double exactly as image.cpp:57-58, :89-90 and
 //      pipelines.cpp:21 do, so nearest-cell indices (std::lround) are
 //      bit-identical to the reference's; emin / emax of guide01 per slot.
-//   2. splat (bilateral.cpp:146-164): cell += {1, src01} (double atomics).
+//   2. splat (bilateral.cpp:146-164): cell += {1, src01}, integer (fixed
+//      point) accumulation so the result is independent of atomic order.
 //   3. separable 5-tap blur, sigma 1 cell, along y, x, range
 //      (bilateral.cpp:82-108, 166-173), out of place.
 //   4. trilinear slice (bilateral.cpp:175-205); T = 2 * out - 1
@@ -18,6 +19,8 @@
 // Grid geometry per slot: gw = floor((W-1)/ss)+5, gh = floor((H-1)/ss)+5,
 // gd = floor((emax-emin)/sr)+5 <= floor(1/sr)+5 (guide01 lies in [0, 1]); the
 // workspace is sized for the bound and each slot reads its own gd.
+#include <cmath>
+
 #include "blfls_internal.cuh"
 
 namespace blfls {
@@ -33,6 +36,17 @@ __device__ __forceinline__ double ordered_to_dbl(unsigned long long k)
 {
     const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
     return __longlong_as_double(b);
+}
+
+// Splat accumulators are integers so that the sums, and hence the output,
+// do not depend on atomic ordering (run-to-run byte-identical, the property
+// the reference gets from its serial splat, bilateral.cpp:142-145): counts
+// exactly, values src01 in [0, 1] in fixed point with 2^-39 resolution
+// (quantisation <= 1e-12, far below the float output's round-off).
+constexpr double kFixedScale = 549755813888.0;  // 2^39
+__device__ __forceinline__ unsigned long long to_fixed(double v)
+{
+    return (unsigned long long)__double2ll_rn(v * kFixedScale);
 }
 
 // slot -> (image b, channel c, axis a); slot = (plane0 + local plane) * 2 + axis
@@ -102,7 +116,7 @@ __global__ void k_grid_clear(GridParams p)
     }
 }
 
-// emin / emax of guide01 per slot; grid (blocks, slots)
+// emin / emax of guide01 per slot; grid (blocks, slots), rows grid-strided
 __global__ void k_grid_erange(GridParams p)
 {
     const Slot s = slot_of(p, blockIdx.y);
@@ -110,19 +124,17 @@ __global__ void k_grid_erange(GridParams p)
     double slo, ssc, glo, gsc;
     slot_images(p, s, src, gde, slo, ssc, glo, gsc);
     double lo = 1e300, hi = -1e300;
-    const size_t n = (size_t)p.H * p.W;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const int y = (int)(i / p.W), x = (int)(i - (size_t)y * p.W);
-        const double e = grad01(gde, p.H, p.W, y, x, s.axis, glo, gsc);
-        lo = fmin(lo, e);
-        hi = fmax(hi, e);
-    }
+    for (int y = blockIdx.x; y < p.H; y += gridDim.x)
+        for (int x = threadIdx.x; x < p.W; x += blockDim.x) {
+            const double e = grad01(gde, p.H, p.W, y, x, s.axis, glo, gsc);
+            lo = fmin(lo, e);
+            hi = fmax(hi, e);
+        }
     for (int o = 16; o > 0; o >>= 1) {
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    if ((threadIdx.x & 31) == 0) {
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
         atomicMin(&p.erange[2 * blockIdx.y], dbl_to_ordered(lo));
         atomicMax(&p.erange[2 * blockIdx.y + 1], dbl_to_ordered(hi));
     }
@@ -136,7 +148,8 @@ __device__ __forceinline__ int slot_gd(const GridParams& p, int z, double& emin)
     return gd > p.gdmax ? p.gdmax : gd;
 }
 
-// bilateral.cpp:146-164 (sy = gw*gd, sx = gd, sz = 1)
+// bilateral.cpp:146-164 (sy = gw*gd, sx = gd, sz = 1); global-atomic variant
+// for grids whose tile block does not fit in shared memory
 __global__ void k_grid_splat(GridParams p)
 {
     const int z = blockIdx.y;
@@ -146,51 +159,113 @@ __global__ void k_grid_splat(GridParams p)
     slot_images(p, s, src, gde, slo, ssc, glo, gsc);
     double emin;
     const int gd = slot_gd(p, z, emin);
-    double* wg = p.wgrid + (size_t)z * p.cells;
-    double* vg = p.vgrid + (size_t)z * p.cells;
-    const size_t n = (size_t)p.H * p.W;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const int y = (int)(i / p.W), x = (int)(i - (size_t)y * p.W);
+    unsigned long long* wg = reinterpret_cast<unsigned long long*>(p.wgrid) + (size_t)z * p.cells;
+    unsigned long long* vg = reinterpret_cast<unsigned long long*>(p.vgrid) + (size_t)z * p.cells;
+    for (int y = blockIdx.x; y < p.H; y += gridDim.x) {
         const int gy = (int)llround(y / p.ss) + 2;
-        const int gx = (int)llround(x / p.ss) + 2;
+        for (int x = threadIdx.x; x < p.W; x += blockDim.x) {
+            const int gx = (int)llround(x / p.ss) + 2;
+            const double e = grad01(gde, p.H, p.W, y, x, s.axis, glo, gsc);
+            const int gz = (int)llround(__ddiv_rn(__dsub_rn(e, emin), p.sr)) + 2;
+            const size_t cell = ((size_t)gy * p.gw + gx) * gd + gz;
+            atomicAdd(wg + cell, 1ull);
+            atomicAdd(vg + cell, to_fixed(grad01(src, p.H, p.W, y, x, s.axis, slo, ssc)));
+        }
+    }
+}
+
+// Tile-privatised splat: a CTA owns a TP x TP pixel tile (TP <= 64), whose
+// nearest cells span at most (TP/ss + 2)^2 x gd cells; it accumulates them in
+// shared memory with native 32-bit atomics (count, and the fixed-point value
+// split into 20-bit low and high words: a 4096-pixel tile cannot overflow
+// either) and flushes each non-empty cell with one 64-bit global atomic.
+// grid (tiles, slots); dynamic smem = 3 * ncx * ncy * gd words.
+__global__ void k_grid_splat_tiled(GridParams p, int lgTP, int ncx, int ncy)
+{
+    extern __shared__ unsigned sacc[];  // [3][ncy][ncx][gd]: count, value lo, value hi
+    __shared__ int tgx[64], tgy[64];    // tile-local nearest cells of each column / row
+    const int TP = 1 << lgTP;
+    const int z = blockIdx.y;
+    const Slot s = slot_of(p, z);
+    const float *src, *gde;
+    double slo, ssc, glo, gsc;
+    slot_images(p, s, src, gde, slo, ssc, glo, gsc);
+    double emin;
+    const int gd = slot_gd(p, z, emin);
+    const int tiles_x = (p.W + TP - 1) >> lgTP;
+    const int tx0 = (blockIdx.x % tiles_x) << lgTP, ty0 = (blockIdx.x / tiles_x) << lgTP;
+    const int cx0 = (int)llround(tx0 / p.ss) + 2, cy0 = (int)llround(ty0 / p.ss) + 2;
+    const int n = ncx * ncy * gd;
+    unsigned* scount = sacc;
+    unsigned* slo20 = sacc + n;
+    unsigned* shi = sacc + 2 * n;
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) sacc[i] = 0u;
+    if (threadIdx.x < TP) {
+        tgx[threadIdx.x] = (int)llround((tx0 + (int)threadIdx.x) / p.ss) + 2 - cx0;
+        tgy[threadIdx.x] = (int)llround((ty0 + (int)threadIdx.x) / p.ss) + 2 - cy0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < TP * TP; i += blockDim.x) {
+        const int ly = i >> lgTP, lx = i & (TP - 1);
+        const int y = ty0 + ly, x = tx0 + lx;
+        if (y >= p.H || x >= p.W) continue;
         const double e = grad01(gde, p.H, p.W, y, x, s.axis, glo, gsc);
         const int gz = (int)llround(__ddiv_rn(__dsub_rn(e, emin), p.sr)) + 2;
+        const int c = (tgy[ly] * ncx + tgx[lx]) * gd + gz;
+        const unsigned long long q = to_fixed(grad01(src, p.H, p.W, y, x, s.axis, slo, ssc));
+        atomicAdd(&scount[c], 1u);
+        atomicAdd(&slo20[c], (unsigned)(q & 0xfffffu));
+        atomicAdd(&shi[c], (unsigned)(q >> 20));
+    }
+    __syncthreads();
+    unsigned long long* wg = reinterpret_cast<unsigned long long*>(p.wgrid) + (size_t)z * p.cells;
+    unsigned long long* vg = reinterpret_cast<unsigned long long*>(p.vgrid) + (size_t)z * p.cells;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned w = scount[i];
+        if (w == 0u) continue;
+        const int gz = i % gd, r = i / gd;
+        const int gx = r % ncx + cx0, gy = r / ncx + cy0;
+        if (gx >= p.gw || gy >= p.gh) continue;
         const size_t cell = ((size_t)gy * p.gw + gx) * gd + gz;
-        atomicAdd(wg + cell, 1.0);
-        atomicAdd(vg + cell, grad01(src, p.H, p.W, y, x, s.axis, slo, ssc));
+        atomicAdd(wg + cell, (unsigned long long)w);
+        atomicAdd(vg + cell, ((unsigned long long)shi[i] << 20) + slo20[i]);
     }
 }
 
 // grid_blur_axis (bilateral.cpp:82-108) along axis `ax` (0 y, 1 x, 2 range),
 // out of place from `in` to `out`; the taps are summed in the reference's
 // order.  grid (blocks, slots).
-__global__ void k_grid_blur(GridParams p, const double* in, double* out, int ax)
+__global__ void k_grid_blur(GridParams p, const double* in, double* out, int ax, double in_scale)
 {
     const int z = blockIdx.y;
     double emin;
     const int gd = slot_gd(p, z, emin);
-    const size_t n = (size_t)p.gh * p.gw * gd;
     const double* g = in + (size_t)z * p.cells;
     double* o = out + (size_t)z * p.cells;
     const double r0 = exp(-2.0), r1 = exp(-0.5);
     const double ksum = r0 + r1 + 1.0 + r1 + r0;
     const double k[5] = {r0 / ksum, r1 / ksum, 1.0 / ksum, r1 / ksum, r0 / ksum};
     const int nlen = ax == 0 ? p.gh : (ax == 1 ? p.gw : gd);
-    const size_t stride = ax == 0 ? (size_t)p.gw * gd : (ax == 1 ? (size_t)gd : 1);
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const int iz = (int)(i % gd);
-        const size_t r = i / gd;
-        const int ix = (int)(r % p.gw), iy = (int)(r / p.gw);
-        const int pos = ax == 0 ? iy : (ax == 1 ? ix : iz);
-        double acc = 0.0;
+    const int stride = ax == 0 ? p.gw * gd : (ax == 1 ? gd : 1);
+    const int row = p.gw * gd;  // one grid row (iy fixed) is contiguous
+    for (int iy = blockIdx.x; iy < p.gh; iy += gridDim.x) {
+        const double* gr = g + (size_t)iy * row;
+        double* orow = o + (size_t)iy * row;
+        for (int j = threadIdx.x; j < row; j += blockDim.x) {
+            const int pos = ax == 0 ? iy : (ax == 1 ? j / gd : j % gd);
+            double acc = 0.0;
 #pragma unroll
-        for (int t = -2; t <= 2; ++t) {
-            const int j = pos + t;
-            if (j >= 0 && j < nlen) acc += k[t + 2] * g[i + (long long)t * (long long)stride];
+            for (int t = -2; t <= 2; ++t) {
+                const int q = pos + t;
+                if (q >= 0 && q < nlen) {
+                    double v = gr[j + t * stride];
+                    if (in_scale != 0.0)  // first pass: integer splat accumulators
+                        v = (double)__double_as_longlong(v) * in_scale;
+                    acc += k[t + 2] * v;
+                }
+            }
+            orow[j] = acc;
         }
-        o[i] = acc;
     }
 }
 
@@ -206,36 +281,47 @@ __global__ void k_grid_slice(GridParams p)
     const int gd = slot_gd(p, z, emin);
     const double* wg = p.wtmp + (size_t)z * p.cells;  // blurred (see launch_grid_blf)
     const double* vg = p.vtmp + (size_t)z * p.cells;
-    const size_t sy = (size_t)p.gw * gd, sx = gd;
+    const int sy = p.gw * gd, sx = gd;
     const size_t n = (size_t)p.H * p.W;
     const double range = ssc > 0.0 ? 1.0 / ssc : 1.0;
+    const double scale = 2.0 * (p.normalized ? 1.0 : range), shift = p.normalized ? 1.0 : range;
+    // The trilinear weights are continuous in (fy, fx, fz), so the cell
+    // coordinates are formed with reciprocals instead of the reference's
+    // divisions (bilateral.cpp:182-184): a 1-ulp coordinate change moves the
+    // output by ~1e-16, far inside the float output's tolerance.
+    const double inv_ss = 1.0 / p.ss, inv_sr = 1.0 / p.sr;
     float* dst = (s.axis == 0 ? p.tx : p.ty) + ((size_t)s.b * p.C + s.c) * n;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const int y = (int)(i / p.W), x = (int)(i - (size_t)y * p.W);
-        const double fy = y / p.ss + 2;
-        const double fx = x / p.ss + 2;
-        const double e = grad01(gde, p.H, p.W, y, x, s.axis, glo, gsc);
-        const double fz = (e - emin) / p.sr + 2;
+    for (int y = blockIdx.x; y < p.H; y += gridDim.x) {
+        const double fy = y * inv_ss + 2;
         const int iy = min((int)fy, p.gh - 2);
-        const int ix = min((int)fx, p.gw - 2);
-        const int iz = min((int)fz, gd - 2);
-        const double ay = fy - iy, ax = fx - ix, az = fz - iz;
-        double wsum = 0.0, vsum = 0.0;
+        const double ay = fy - iy;
+        for (int x = threadIdx.x; x < p.W; x += blockDim.x) {
+            const double fx = x * inv_ss + 2;
+            const double e = grad01(gde, p.H, p.W, y, x, s.axis, glo, gsc);
+            const double fz = (e - emin) * inv_sr + 2;
+            const int ix = min((int)fx, p.gw - 2);
+            const int iz = min((int)fz, gd - 2);
+            const double ax = fx - ix, az = fz - iz;
+            const double* wc = wg + sy * iy + sx * ix + iz;
+            const double* vc = vg + sy * iy + sx * ix + iz;
+            double wsum = 0.0, vsum = 0.0;
 #pragma unroll
-        for (int dy = 0; dy < 2; ++dy)
+            for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
-            for (int dx = 0; dx < 2; ++dx)
-#pragma unroll
-                for (int dz = 0; dz < 2; ++dz) {
-                    const double cw = (dy ? ay : 1.0 - ay) * (dx ? ax : 1.0 - ax) * (dz ? az : 1.0 - az);
-                    const size_t ci = sy * (iy + dy) + sx * (ix + dx) + (iz + dz);
-                    wsum += cw * wg[ci];
-                    vsum += cw * vg[ci];
+                for (int dx = 0; dx < 2; ++dx) {
+                    const double wyx = (dy ? ay : 1.0 - ay) * (dx ? ax : 1.0 - ax);
+                    const int o = sy * dy + sx * dx;
+                    const double w0 = wyx * (1.0 - az), w1 = wyx * az;
+                    wsum += w0 * wc[o] + w1 * wc[o + 1];
+                    vsum += w0 * vc[o] + w1 * vc[o + 1];
                 }
-        const double v = grad01(src, p.H, p.W, y, x, s.axis, slo, ssc);
-        const double out = wsum > 1e-12 ? vsum / wsum : v;
-        dst[i] = (float)((2.0 * out - 1.0) * (p.normalized ? 1.0 : range));
+            double out;
+            if (wsum > 1e-12)
+                out = vsum / wsum;
+            else
+                out = grad01(src, p.H, p.W, y, x, s.axis, slo, ssc);
+            dst[(size_t)y * p.W + x] = (float)(out * scale - shift);
+        }
     }
 }
 
@@ -245,14 +331,32 @@ cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st)
     k_grid_clear<<<blocks * p.slots, 256, 0, st>>>(p);
     dim3 g2(blocks, p.slots);
     k_grid_erange<<<g2, 256, 0, st>>>(p);
-    k_grid_splat<<<g2, 256, 0, st>>>(p);
+    // privatised splat when a pixel tile's cell block fits in 64 KB of smem
+    int TP = 0, lgTP = 0, ncx = 0;
+    for (int lg = 6; lg >= 3; --lg) {
+        const int nc = (int)std::ceil((1 << lg) / p.ss) + 2;
+        if ((size_t)nc * nc * p.gdmax * 3 * sizeof(unsigned) <= 64 * 1024) {
+            TP = 1 << lg;
+            lgTP = lg;
+            ncx = nc;
+            break;
+        }
+    }
+    if (TP) {
+        const size_t smem = (size_t)ncx * ncx * p.gdmax * 3 * sizeof(unsigned);
+        cudaFuncSetAttribute(k_grid_splat_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        dim3 gt((unsigned)(((p.W + TP - 1) / TP) * ((p.H + TP - 1) / TP)), p.slots);
+        k_grid_splat_tiled<<<gt, 256, smem, st>>>(p, lgTP, ncx, ncx);
+    } else {
+        k_grid_splat<<<g2, 256, 0, st>>>(p);
+    }
     // y, x, range (bilateral.cpp:166-173): grid -> tmp -> grid -> tmp
     for (int w = 0; w < 2; ++w) {
         double* g = w ? p.vgrid : p.wgrid;
         double* t = w ? p.vtmp : p.wtmp;
-        k_grid_blur<<<g2, 256, 0, st>>>(p, g, t, 0);
-        k_grid_blur<<<g2, 256, 0, st>>>(p, t, g, 1);
-        k_grid_blur<<<g2, 256, 0, st>>>(p, g, t, 2);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, g, t, 0, w ? 1.0 / kFixedScale : 1.0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, t, g, 1, 0.0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, g, t, 2, 0.0);
     }
     k_grid_slice<<<g2, 256, 0, st>>>(p);
     return cudaGetLastError();

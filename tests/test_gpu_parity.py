@@ -425,8 +425,27 @@ def test_grid_backend_vs_reference_live(gpu, oracle):
     if not oracle.REF_SO.exists():
         pytest.skip("oracle/_ref not built")
     img = _img(oracle, 3, 72, 96, 61)
-    for pad, ss, sr in ((0, 5.0, 0.05), (16, 12.0, 0.04), (3, 3.0, 0.2)):
+    # tile-privatised splat at TP 64 (12 / 0.04), 32 (5 / 0.05, 3 / 0.2), 16 (1.5 / 0.05),
+    # and the global-atomic splat when no tile fits (1 / 0.01: 105 range cells)
+    for pad, ss, sr in ((0, 5.0, 0.05), (16, 12.0, 0.04), (3, 3.0, 0.2), (0, 1.5, 0.05),
+                        (0, 1.0, 0.01)):
         ref = oracle.ref_smooth_grid(img.astype(np.float64), lam=1000.0, sigma_s=ss, sigma_r=sr, pad=pad)
         out = gpu.smooth(img, gpu.SmootherSpec(blf=gpu.RangeSpatialParams(ss, sr),
                                                solve=gpu.SolveParams(1000.0, pad), backend="grid"))
         assert maxabs(out, ref) <= TOL_OUT
+
+
+def test_grid_backend_is_deterministic(gpu, oracle):
+    """Integer splat accumulation: repeated runs are byte-identical, as the
+    reference's serial splat is (bilateral.cpp:142-145; test_cli.cpp:87-99)."""
+    img = _img(oracle, 3, 96, 128, 71)
+    spec = gpu.SmootherSpec(blf=gpu.RangeSpatialParams(4.0, 0.05), solve=gpu.SolveParams(800.0, 0),
+                            backend="grid")
+    outs = [gpu.smooth(img, spec) for _ in range(3)]
+    for o in outs[1:]:
+        assert o.tobytes() == outs[0].tobytes()
+    # fallback (global-atomic) splat too
+    spec2 = gpu.SmootherSpec(blf=gpu.RangeSpatialParams(1.0, 0.01), solve=gpu.SolveParams(800.0, 0),
+                             backend="grid")
+    a, b = gpu.smooth(img, spec2), gpu.smooth(img, spec2)
+    assert a.tobytes() == b.tobytes()

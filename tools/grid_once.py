@@ -1,0 +1,19 @@
+"""One grid-backend BLF-LS call at a BASELINE config (for ncu launch lists):
+python tools/grid_once.py [config] [images]."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_1812_07122_b200 as P  # noqa: E402
+from paper_1812_07122_b200 import configs  # noqa: E402
+
+cfg = configs.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+img = torch.rand(n, cfg.channels, cfg.height, cfg.width, device="cuda")
+guide = torch.rand(n, 1, cfg.height, cfg.width, device="cuda") if cfg.guide else None
+for _ in range(2):
+    P.blf_ls(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
+             radius=cfg.radius, backend="grid")
+torch.cuda.synchronize()
+print("ok")
