@@ -100,8 +100,8 @@ struct GridParams {
     const uint32_t* glohi; // per image of the guide
     double* wgrid;         // [slots][cells] splat targets
     double* vgrid;
-    double* wtmp;          // blur ping-pong; the blurred grids end here
-    double* vtmp;
+    double* blurred;       // [slots][cells] interleaved (w, v): the blurred grids
+                           // (also scratch of the per-axis fallback blur)
     unsigned long long* erange;  // [slots][2] ordered (emin, emax) of guide01
     int H, W, C, GC;
     int plane0;            // first global plane of this launch

@@ -504,7 +504,7 @@ void free_plan(blfls_plan_t p)
     void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
                     p->rowf.tw, p->colf.tw, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
-                    p->grid.wtmp, p->grid.vtmp, p->grid.erange};
+                    p->grid.blurred, p->grid.erange};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
@@ -689,8 +689,7 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         const size_t n = (size_t)2 * np * g.cells;
         if (cudaMalloc(&g.wgrid, sizeof(double) * n) != cudaSuccess ||
             cudaMalloc(&g.vgrid, sizeof(double) * n) != cudaSuccess ||
-            cudaMalloc(&g.wtmp, sizeof(double) * n) != cudaSuccess ||
-            cudaMalloc(&g.vtmp, sizeof(double) * n) != cudaSuccess ||
+            cudaMalloc(&g.blurred, sizeof(double) * 2 * n) != cudaSuccess ||
             cudaMalloc(&g.erange, sizeof(unsigned long long) * 4 * np) != cudaSuccess)
             return bail(fail(BLFLS_ENOMEM, "plan: grid workspace allocation failed"));
     }

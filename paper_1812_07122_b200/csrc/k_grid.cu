@@ -20,6 +20,7 @@
 // gd = floor((emax-emin)/sr)+5 <= floor(1/sr)+5 (guide01 lies in [0, 1]); the
 // workspace is sized for the bound and each slot reads its own gd.
 #include <cmath>
+#include <cstdlib>
 
 #include "blfls_internal.cuh"
 
@@ -235,13 +236,14 @@ __global__ void k_grid_splat_tiled(GridParams p, int lgTP, int ncx, int ncy)
 // grid_blur_axis (bilateral.cpp:82-108) along axis `ax` (0 y, 1 x, 2 range),
 // out of place from `in` to `out`; the taps are summed in the reference's
 // order.  grid (blocks, slots).
-__global__ void k_grid_blur(GridParams p, const double* in, double* out, int ax, double in_scale)
+__global__ void k_grid_blur(GridParams p, const double* in, double* out, int ax, double in_scale,
+                            int ostride, int ooff)
 {
     const int z = blockIdx.y;
     double emin;
     const int gd = slot_gd(p, z, emin);
     const double* g = in + (size_t)z * p.cells;
-    double* o = out + (size_t)z * p.cells;
+    double* o = out + (size_t)z * p.cells * ostride + ooff;
     const double r0 = exp(-2.0), r1 = exp(-0.5);
     const double ksum = r0 + r1 + 1.0 + r1 + r0;
     const double k[5] = {r0 / ksum, r1 / ksum, 1.0 / ksum, r1 / ksum, r0 / ksum};
@@ -250,7 +252,7 @@ __global__ void k_grid_blur(GridParams p, const double* in, double* out, int ax,
     const int row = p.gw * gd;  // one grid row (iy fixed) is contiguous
     for (int iy = blockIdx.x; iy < p.gh; iy += gridDim.x) {
         const double* gr = g + (size_t)iy * row;
-        double* orow = o + (size_t)iy * row;
+        double* orow = o + (size_t)iy * row * ostride;
         for (int j = threadIdx.x; j < row; j += blockDim.x) {
             const int pos = ax == 0 ? iy : (ax == 1 ? j / gd : j % gd);
             double acc = 0.0;
@@ -264,8 +266,93 @@ __global__ void k_grid_blur(GridParams p, const double* in, double* out, int ax,
                     acc += k[t + 2] * v;
                 }
             }
-            orow[j] = acc;
+            orow[(size_t)j * ostride] = acc;
         }
+    }
+}
+
+// The three blur passes fused (bilateral.cpp:166-173: y, then x, then range,
+// each grid_blur_axis): a CTA owns a B x B block of (y, x) cells with every
+// range cell, loads it with a 2-cell halo (converting the integer splat
+// accumulators), blurs y into T1 (B x (B+4) x gd), x into T2 (B x B x gd,
+// reusing the load buffer) and range on the way out to `out`.  Taps outside
+// the grid are dropped exactly as the reference's blur drops them.  Runs for
+// the count grid (w = 0) and then the value grid (w = 1).  grid (tiles, slots).
+__global__ void k_grid_blur3(GridParams p, int B)
+{
+    extern __shared__ double sm[];
+    const int z = blockIdx.y;
+    double emin;
+    const int gd = slot_gd(p, z, emin);
+    const double r0 = exp(-2.0), r1 = exp(-0.5);
+    const double ksum = r0 + r1 + 1.0 + r1 + r0;
+    const double k[5] = {r0 / ksum, r1 / ksum, 1.0 / ksum, r1 / ksum, r0 / ksum};
+    const int BH = B + 4;
+    const int tiles_x = (p.gw + B - 1) / B;
+    const int x0 = (blockIdx.x % tiles_x) * B, y0 = (blockIdx.x / tiles_x) * B;
+    const int rowL = BH * gd;  // one halo row of the load buffer
+    double* L = sm;                      // [BH][BH][gd], later T2 [B][B][gd]
+    double* T1 = sm + (size_t)BH * rowL;  // [B][BH][gd]
+    // Each phase walks a row offset j (x * gd + z within a tile row) per
+    // thread and loops over the tile rows, so the index divisions happen once
+    // per j rather than once per cell.
+    const int rowB = B * gd;
+    for (int w = 0; w < 2; ++w) {
+        const unsigned long long* in =
+            reinterpret_cast<const unsigned long long*>(w ? p.vgrid : p.wgrid) + (size_t)z * p.cells;
+        double* out = p.blurred + (size_t)z * p.cells * 2 + w;
+        const double scale = w ? 1.0 / kFixedScale : 1.0;
+        for (int j = threadIdx.x; j < rowL; j += blockDim.x) {  // load with halo
+            const int gx = x0 - 2 + j / gd;
+            const bool xin = gx >= 0 && gx < p.gw;
+            const long long off = (long long)(x0 - 2) * gd + j;
+            for (int ly = 0; ly < BH; ++ly) {
+                const int gy = y0 - 2 + ly;
+                double v = 0.0;
+                if (xin && gy >= 0 && gy < p.gh) v = (double)in[(size_t)gy * p.gw * gd + off] * scale;
+                L[ly * rowL + j] = v;
+            }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < rowL; j += blockDim.x)  // y
+            for (int ly = 0; ly < B; ++ly) {
+                const int gy = y0 + ly;
+                double acc = 0.0;
+#pragma unroll
+                for (int t = -2; t <= 2; ++t)
+                    if (gy + t >= 0 && gy + t < p.gh) acc += k[t + 2] * L[(ly + 2 + t) * rowL + j];
+                T1[ly * rowL + j] = acc;
+            }
+        __syncthreads();
+        for (int j = threadIdx.x; j < rowB; j += blockDim.x) {  // x
+            const int gx = x0 + j / gd;
+            unsigned ok = 0;
+#pragma unroll
+            for (int t = -2; t <= 2; ++t) ok |= (gx + t >= 0 && gx + t < p.gw) ? 1u << (t + 2) : 0u;
+            for (int ly = 0; ly < B; ++ly) {
+                const double* r = T1 + ly * rowL + j + 2 * gd;
+                double acc = 0.0;
+#pragma unroll
+                for (int t = -2; t <= 2; ++t)
+                    if (ok >> (t + 2) & 1u) acc += k[t + 2] * r[t * gd];
+                L[ly * rowB + j] = acc;
+            }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < rowB; j += blockDim.x) {  // range, store
+            const int lx = j / gd, iz = j - lx * gd;
+            const int gx = x0 + lx;
+            if (gx >= p.gw) continue;
+            for (int ly = 0; ly < B && y0 + ly < p.gh; ++ly) {
+                const double* r = L + ly * rowB + j;
+                double acc = 0.0;
+#pragma unroll
+                for (int t = -2; t <= 2; ++t)
+                    if (iz + t >= 0 && iz + t < gd) acc += k[t + 2] * r[t];
+                out[(((size_t)(y0 + ly) * p.gw + gx) * gd + iz) * 2] = acc;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -279,8 +366,7 @@ __global__ void k_grid_slice(GridParams p)
     slot_images(p, s, src, gde, slo, ssc, glo, gsc);
     double emin;
     const int gd = slot_gd(p, z, emin);
-    const double* wg = p.wtmp + (size_t)z * p.cells;  // blurred (see launch_grid_blf)
-    const double* vg = p.vtmp + (size_t)z * p.cells;
+    const double2* bg = reinterpret_cast<const double2*>(p.blurred) + (size_t)z * p.cells;
     const int sy = p.gw * gd, sx = gd;
     const size_t n = (size_t)p.H * p.W;
     const double range = ssc > 0.0 ? 1.0 / ssc : 1.0;
@@ -302,8 +388,7 @@ __global__ void k_grid_slice(GridParams p)
             const int ix = min((int)fx, p.gw - 2);
             const int iz = min((int)fz, gd - 2);
             const double ax = fx - ix, az = fz - iz;
-            const double* wc = wg + sy * iy + sx * ix + iz;
-            const double* vc = vg + sy * iy + sx * ix + iz;
+            const double2* c0 = bg + sy * iy + sx * ix + iz;
             double wsum = 0.0, vsum = 0.0;
 #pragma unroll
             for (int dy = 0; dy < 2; ++dy)
@@ -312,8 +397,9 @@ __global__ void k_grid_slice(GridParams p)
                     const double wyx = (dy ? ay : 1.0 - ay) * (dx ? ax : 1.0 - ax);
                     const int o = sy * dy + sx * dx;
                     const double w0 = wyx * (1.0 - az), w1 = wyx * az;
-                    wsum += w0 * wc[o] + w1 * wc[o + 1];
-                    vsum += w0 * vc[o] + w1 * vc[o + 1];
+                    const double2 a = c0[o], b = c0[o + 1];
+                    wsum += w0 * a.x + w1 * b.x;
+                    vsum += w0 * a.y + w1 * b.y;
                 }
             double out;
             if (wsum > 1e-12)
@@ -351,12 +437,36 @@ cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st)
         k_grid_splat<<<g2, 256, 0, st>>>(p);
     }
     // y, x, range (bilateral.cpp:166-173): grid -> tmp -> grid -> tmp
-    for (int w = 0; w < 2; ++w) {
-        double* g = w ? p.vgrid : p.wgrid;
-        double* t = w ? p.vtmp : p.wtmp;
-        k_grid_blur<<<g2, 256, 0, st>>>(p, g, t, 0, w ? 1.0 / kFixedScale : 1.0);
-        k_grid_blur<<<g2, 256, 0, st>>>(p, t, g, 1, 0.0);
-        k_grid_blur<<<g2, 256, 0, st>>>(p, g, t, 2, 0.0);
+    // fused 3-axis blur when a B x B cell block (+ halo, all range cells) fits
+    int B = 0;
+    size_t bsmem = 0;
+    static const int forced_b = [] {
+        const char* e = getenv("BLFLS_GRID_BLUR_B");
+        return e ? atoi(e) : 0;
+    }();
+    for (int b : {8, 16, 4}) {  // 8: best measured (c5: 3.83 vs 4.03 ms at 16)
+        if (forced_b && b != forced_b) continue;
+        const size_t need = (size_t)((b + 4) * (b + 4) + b * (b + 4)) * p.gdmax * sizeof(double);
+        if (need <= 112 * 1024) {
+            B = b;
+            bsmem = need;
+            break;
+        }
+    }
+    if (B) {
+        cudaFuncSetAttribute(k_grid_blur3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+        dim3 gb((unsigned)(((p.gw + B - 1) / B) * ((p.gh + B - 1) / B)), p.slots);
+        k_grid_blur3<<<gb, 256, bsmem, st>>>(p, B);
+    } else {
+        // y, x, range per grid; scratch: the (not yet written) blurred buffer
+        // for the counts, the dead count grid for the values
+        const double fs = 1.0 / kFixedScale;
+        k_grid_blur<<<g2, 256, 0, st>>>(p, p.wgrid, p.blurred, 0, 1.0, 1, 0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, p.blurred, p.wgrid, 1, 0.0, 1, 0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, p.wgrid, p.blurred, 2, 0.0, 2, 0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, p.vgrid, p.wgrid, 0, fs, 1, 0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, p.wgrid, p.vgrid, 1, 0.0, 1, 0);
+        k_grid_blur<<<g2, 256, 0, st>>>(p, p.vgrid, p.blurred, 2, 0.0, 2, 1);
     }
     k_grid_slice<<<g2, 256, 0, st>>>(p);
     return cudaGetLastError();

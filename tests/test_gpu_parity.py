@@ -426,9 +426,11 @@ def test_grid_backend_vs_reference_live(gpu, oracle):
         pytest.skip("oracle/_ref not built")
     img = _img(oracle, 3, 72, 96, 61)
     # tile-privatised splat at TP 64 (12 / 0.04), 32 (5 / 0.05, 3 / 0.2), 16 (1.5 / 0.05),
-    # and the global-atomic splat when no tile fits (1 / 0.01: 105 range cells)
+    # and the global-atomic splat when no tile fits (1 / 0.01: 105 range cells);
+    # fused 3-axis blur throughout except at 2 / 0.005 (205 range cells), which
+    # takes the global splat and the per-axis blur
     for pad, ss, sr in ((0, 5.0, 0.05), (16, 12.0, 0.04), (3, 3.0, 0.2), (0, 1.5, 0.05),
-                        (0, 1.0, 0.01)):
+                        (0, 1.0, 0.01), (0, 2.0, 0.005)):
         ref = oracle.ref_smooth_grid(img.astype(np.float64), lam=1000.0, sigma_s=ss, sigma_r=sr, pad=pad)
         out = gpu.smooth(img, gpu.SmootherSpec(blf=gpu.RangeSpatialParams(ss, sr),
                                                solve=gpu.SolveParams(1000.0, pad), backend="grid"))

@@ -17,3 +17,12 @@ for _ in range(2):
              radius=cfg.radius, backend="grid")
 torch.cuda.synchronize()
 print("ok")
+if len(sys.argv) > 3 and sys.argv[3] == "time":
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        P.blf_ls(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
+                 radius=cfg.radius, backend="grid")
+    b.record()
+    torch.cuda.synchronize()
+    print(f"{a.elapsed_time(b) / 5:.3f} ms per call ({n} images, 1 iteration)")
