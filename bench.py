@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--backend", default="brute", choices=["brute", "grid"],
+    ap.add_argument("--backend", default="brute", choices=["brute", "grid", "dt"],
                     help="gradient filter: brute-force BLF (north star) or the reference's bilateral grid")
     ap.add_argument("--pad", type=int, default=0, help="reflect padding (reference default 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -147,6 +147,9 @@ def config_json(cfg, n_gpus, extra=None):
     return d
 
 
+FILTER_NAMES = {"brute": "brute-force BLF", "grid": "grid BLF", "dt": "NC (domain transform, 3 passes)"}
+
+
 def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
     """Reference CPU path on a bounded sample of the workload: the first image
     of the config, ONE iteration (of cfg.iters), through oracle/_ref
@@ -178,6 +181,12 @@ def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
         O.ref_smooth_grid(img, None if guide is None else np.repeat(guide, img.shape[0], axis=0),
                           lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, pad=pad)
         tb = ts = float("nan")
+    elif backend == "dt":
+        # smooth() with SmootherKind::NC_LS, DtParams{sigma_s, sigma_r, 3}
+        nc = O.ref_smooth_nc if kind == "reference" else O.smooth_nc
+        nc(img, None if guide is None else np.repeat(guide, img.shape[0], axis=0), lam=cfg.lam,
+           sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, dt_iters=3, pad=pad)
+        tb = ts = float("nan")
     elif pad:
         fn(img, guide, lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=1,
            radius=cfg.radius, pad=pad)
@@ -189,7 +198,7 @@ def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
     mp = img.shape[1] * img.shape[2] / 1e6
     return {"value": mp / dt, "unit": "MP/s", "cores": O.num_threads(), "kind": kind,
             "sample": f"1 image x 1 iteration of {cfg.name} ({cfg.height}x{cfg.width}x{cfg.channels}"
-                      f"{crop}, {'grid' if backend == 'grid' else 'brute-force'} BLF, pad {pad}), "
+                      f"{crop}, {FILTER_NAMES[backend]}, pad {pad}), "
                       f"double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
             "seconds": dt, "mp": mp, "blf_s": tb, "solve_s": ts}
 
@@ -263,6 +272,7 @@ def run_ours(args, cfg):
         guide = P.generate(cfg.height, cfg.width, [cfg.guide_seed(first + i) for i in range(n)],
                            n_sites=cfg.n_sites, device=dev).view(n, 1, cfg.height, cfg.width)
     out = torch.empty_like(img)
+    radius = cfg.radius if args.backend == "brute" else 0  # the plan key blf_ls uses
     kw = dict(lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=cfg.iters,
               radius=cfg.radius, check_finite=False, pad=args.pad, backend=args.backend)
     in_bytes = img.numel() * 4 + (guide.numel() * 4 if guide is not None else 0)
@@ -276,7 +286,7 @@ def run_ours(args, cfg):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    plan = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, cfg.radius,
+    plan = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, radius,
                       cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev, pad=args.pad, backend=args.backend)
 
     # ---- timed region: K steps, CUDA events per step, L2 flushed between steps
@@ -356,7 +366,7 @@ def run_ours(args, cfg):
         # pinned memory and its result D2H; wait=False lets step k+1's H2D
         # overlap step k's compute and D2H (two staging slots, copy streams).
         h_outs = [h_out, torch.empty(img.shape, dtype=torch.float32).pin_memory()]
-        plan_e = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, cfg.radius,
+        plan_e = P.get_plan(cfg.height, cfg.width, cfg.channels, 1 if cfg.guide else 0, radius,
                             cfg.sigma_s, cfg.sigma_r, cfg.lam, n, dev, pad=args.pad,
                             backend=args.backend)
         for k in range(2):
@@ -401,7 +411,7 @@ def run_ours(args, cfg):
                 "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2",
                 "decomposition": {"weak": "independent images per rank",
                                   "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]}),
-            "roofline": None if args.backend == "grid" else {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
+            "roofline": None if args.backend != "brute" else {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
                          "achieved": achieved / 1e9, "peak": mufu_rate / 1e9, "unit": "Gexp/s",
                          "frac": achieved / mufu_rate,
                          "peak_source": "measured MUFU.EX2 probe on this GPU "

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define BLFLS_ABI_VERSION 1
+#define BLFLS_ABI_VERSION 2
 
 typedef enum blfls_status {
     BLFLS_OK = 0,
@@ -65,7 +65,8 @@ typedef enum blfls_status {
 typedef struct blfls_plan_s* blfls_plan_t;
 
 /* Everything a plan is specialised on.  Mirrors SmootherSpec
- * (pipelines.hpp:16-23) restricted to kind == BLF_LS. */
+ * (pipelines.hpp:16-23) for kind == BLF_LS (backends BRUTE, GRID) and
+ * kind == NC_LS (backend DT). */
 typedef struct blfls_params {
     int height, width;    /* image size, >= 2 each */
     int channels;         /* 1 or 3 (image.cpp:16-17) */
@@ -74,7 +75,8 @@ typedef struct blfls_params {
                              with SmootherSpec::guidance, pipelines.cpp:81-84) */
     int radius;           /* BLF window radius r; < 0 means ceil(3*sigma_s) as
                              bilateral.cpp:37 */
-    double sigma_s;       /* RangeSpatialParams (bilateral.hpp:10-13) */
+    double sigma_s;       /* RangeSpatialParams (bilateral.hpp:10-13), or DtParams
+                             (domain_transform.hpp:7-11) for BLFLS_BACKEND_DT */
     double sigma_r;
     double lambda;        /* SolveParams::lambda (solver.hpp:12-15); pad is 0 */
     int max_batch;        /* images per call the plan's workspace is sized for */
@@ -88,11 +90,18 @@ typedef struct blfls_params {
                              brute-force BLF over the (2r+1)^2 window) or
                              BLFLS_BACKEND_GRID (1, the bilateral grid blf_grid that
                              the reference's smooth() runs, bilateral.cpp:112-207,
-                             grid sampling = (sigma_s, sigma_r); radius unused) */
+                             grid sampling = (sigma_s, sigma_r); radius unused) or
+                             BLFLS_BACKEND_DT (2, nc_filter: normalized convolution
+                             over the domain transform, domain_transform.cpp:138-156,
+                             i.e. SmootherKind::NC_LS, pipelines.cpp:48; radius unused) */
+    int dt_iterations;    /* DtParams::iterations for BLFLS_BACKEND_DT: >= 1, 0 means
+                             the reference default 3 (pipelines.hpp:19); ignored by
+                             the other backends */
 } blfls_params;
 
 #define BLFLS_BACKEND_BRUTE 0
 #define BLFLS_BACKEND_GRID 1
+#define BLFLS_BACKEND_DT 2
 
 /* Validates like validate_params / validate_solve_params (bilateral.cpp:12-24,
  * solver.cpp:15-21) and caches twiddles, spectral denominators and workspaces. */
@@ -149,6 +158,16 @@ blfls_status blfls_irfft2(blfls_plan_t plan, const float* spec, int batch, float
 blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t* seeds,
                             int n_sites, double noise_sigma, double p_salt_pepper, float* out,
                             void* stream, int device);
+
+/* gaussian_blur (image.cpp:99-158): separable Gaussian of radius ceil(3 sigma),
+ * weights exp(-i^2 / (2 sigma^2)) normalised to sum 1, clamped borders,
+ * accumulated in double in the reference's tap order; `in` and `out` are
+ * channels x height x width float planes (distinct buffers).  DEVICE_PTRS /
+ * HOST_PTRS and SYNC as for blfls_run; stream NULL = legacy default stream.
+ * The initial guidance of rolling_nc_ls (pipelines.cpp:109). */
+blfls_status blfls_gaussian_blur(const float* in, int channels, int height, int width,
+                                 double sigma, float* out, int device, void* stream,
+                                 unsigned flags);
 
 /* Counters of the last blfls_run on this plan (for the bench's roofline). */
 typedef struct blfls_stats {

@@ -4,7 +4,9 @@
 //   blfls::Image                    ~ epls::PlanarImage (include/epls/image.hpp:9-41):
 //                                     planar doubles, channels in {1, 3}
 //   blfls::SmootherSpec             ~ epls::SmootherSpec (pipelines.hpp:16-23)
-//   blfls::smooth(g, spec)          ~ epls::smooth (pipelines.cpp:57-94), BLF_LS
+//   blfls::smooth(g, spec)          ~ epls::smooth (pipelines.cpp:57-94), BLF_LS / NC_LS
+//   blfls::rolling_nc_ls(...)       ~ epls::rolling_nc_ls (pipelines.cpp:96-117)
+//   blfls::gaussian_blur(img, s)    ~ epls::gaussian_blur (image.cpp:114-158)
 //   blfls::flash_no_flash(a, f, s)  ~ epls::flash_no_flash (applications.cpp:58-64)
 //   blfls::blf_ls(...)              the north-star cascade (iters smooth() calls)
 //   blfls::lsgrad_solve_fft(...)    ~ epls::lsgrad_solve_fft (solver.cpp:88-124)
@@ -68,8 +70,23 @@ struct SolveParams {
     int pad = 16;  // reflect padding (solver.hpp:12-15); 0 = periodic
 };
 
+struct DtParams {  // domain_transform.hpp:7-11
+    double sigma_s = 8.0;
+    double sigma_r = 0.1;
+    int iterations = 3;
+};
+
+struct RollingParams {  // pipelines.hpp:25-28
+    int n = 3;
+    double init_sigma = 2.5;
+};
+
+enum class SmootherKind { BLF_LS, NC_LS };  // the gradient-filter kinds of pipelines.hpp:11
+
 struct SmootherSpec {
+    SmootherKind kind = SmootherKind::BLF_LS;
     RangeSpatialParams blf{12.0, 0.04};
+    DtParams dt{12.0, 0.05, 3};
     SolveParams solve{};
     const Image* guidance = nullptr;
     int radius = -1;  // < 0: ceil(3 sigma_s) as bilateral.cpp:37
@@ -97,9 +114,10 @@ struct PlanDeleter {
 using PlanPtr = std::unique_ptr<blfls_plan_s, PlanDeleter>;
 
 inline PlanPtr make_plan(int h, int w, int c, int gc, int radius, double ss, double sr, double lam,
-                         int batch, int device, int pad = 0, int backend = BLFLS_BACKEND_BRUTE)
+                         int batch, int device, int pad = 0, int backend = BLFLS_BACKEND_BRUTE,
+                         int dt_iterations = 0)
 {
-    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device, pad, backend};
+    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device, pad, backend, dt_iterations};
     blfls_plan_t raw = nullptr;
     check(blfls_plan_create(&p, &raw));
     return PlanPtr(raw);
@@ -118,14 +136,14 @@ inline std::vector<float> to_f32(const Image& img)
 /// held fixed.  guide: nullptr, 1 channel, or img.channels() channels.
 inline Image blf_ls(const Image& img, const Image* guide, double lambda, double sigma_s,
                     double sigma_r, int iters = 1, int radius = -1, int device = 0, int pad = 0,
-                    int backend = BLFLS_BACKEND_BRUTE)
+                    int backend = BLFLS_BACKEND_BRUTE, int dt_iterations = 0)
 {
     if (guide && (guide->width() != img.width() || guide->height() != img.height() ||
                   (guide->channels() != 1 && guide->channels() != img.channels())))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
     auto plan = detail::make_plan(img.height(), img.width(), img.channels(),
                                   guide ? guide->channels() : 0, radius, sigma_s, sigma_r, lambda,
-                                  1, device, pad, backend);
+                                  1, device, pad, backend, dt_iterations);
     std::vector<float> in = detail::to_f32(img), out(img.size()), gd;
     if (guide) gd = detail::to_f32(*guide);
     detail::check(blfls_run(plan.get(), in.data(), guide ? gd.data() : nullptr, 1, iters,
@@ -135,13 +153,52 @@ inline Image blf_ls(const Image& img, const Image* guide, double lambda, double 
     return res;
 }
 
-/// epls::smooth for kind BLF_LS (brute-force BLF), including reflect padding.
+/// `iters` cascaded smooth() calls of kind NC_LS (nc_filter, domain_transform.cpp:138-156).
+inline Image nc_ls(const Image& img, const Image* guide, double lambda, const DtParams& dt,
+                   int iters = 1, int device = 0, int pad = 0)
+{
+    if (dt.iterations < 1) throw std::invalid_argument("nc_filter: iterations must be >= 1");
+    return blf_ls(img, guide, lambda, dt.sigma_s, dt.sigma_r, iters, 0, device, pad,
+                  BLFLS_BACKEND_DT, dt.iterations);
+}
+
+/// epls::smooth for kinds BLF_LS (brute-force BLF, or the grid via spec.backend)
+/// and NC_LS, including reflect padding.
 inline Image smooth(const Image& g, const SmootherSpec& spec)
 {
     if (spec.guidance && !spec.guidance->same_shape(g))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
+    if (spec.kind == SmootherKind::NC_LS)
+        return nc_ls(g, spec.guidance, spec.solve.lambda, spec.dt, 1, spec.device, spec.solve.pad);
     return blf_ls(g, spec.guidance, spec.solve.lambda, spec.blf.sigma_s, spec.blf.sigma_r, 1,
                   spec.radius, spec.device, spec.solve.pad, spec.backend);
+}
+
+/// epls::gaussian_blur (image.cpp:114-158) on the GPU.
+inline Image gaussian_blur(const Image& img, double sigma, int device = 0)
+{
+    std::vector<float> in = detail::to_f32(img), out(img.size());
+    detail::check(blfls_gaussian_blur(in.data(), img.channels(), img.height(), img.width(), sigma,
+                                      out.data(), device, nullptr, BLFLS_HOST_PTRS | BLFLS_SYNC));
+    Image res(img.width(), img.height(), img.channels());
+    for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
+    return res;
+}
+
+/// epls::rolling_nc_ls (pipelines.cpp:96-117).
+inline Image rolling_nc_ls(const Image& g, const DtParams& dt, const SolveParams& sp,
+                           const RollingParams& rp, int device = 0)
+{
+    if (rp.n < 1) throw std::invalid_argument("rolling_nc_ls: n must be >= 1");
+    if (!(rp.init_sigma > 0.0))
+        throw std::invalid_argument("rolling_nc_ls: init_sigma must be positive");
+    Image guide = gaussian_blur(g, rp.init_sigma, device);
+    Image u;
+    for (int k = 0; k < rp.n; ++k) {
+        u = nc_ls(g, &guide, sp.lambda, dt, 1, device, sp.pad);
+        guide = u;
+    }
+    return u;
 }
 
 /// epls::flash_no_flash: joint smoothing of `noflash` guided by `flash`.

@@ -547,9 +547,12 @@ int orc_dense_solve(const double* g, const double* tx, const double* ty, int c, 
 
 /* ------------------------------------------------------ pipelines.cpp -- */
 
-static int smooth_core(const double* g, int c, int h, int w, const double* guide, int radius,
-                       double sigma_s, double sigma_r, double lambda, int pad, double* out,
-                       double* t_blf, double* t_solve)
+/* gradient filter of smooth(): dt_iters == 0 -> brute-force BLF with `radius`
+ * (north star, for blf_grid at pipelines.cpp:47); dt_iters > 0 -> nc_filter
+ * with DtParams{sigma_s, sigma_r, dt_iters} (pipelines.cpp:48) */
+static int smooth_core_k(const double* g, int c, int h, int w, const double* guide, int radius,
+                         int dt_iters, double sigma_s, double sigma_r, double lambda, int pad,
+                         double* out, double* t_blf, double* t_solve)
 {
     const size_t n = (size_t)c * h * w;
     /* pipelines.cpp:59 */
@@ -602,7 +605,10 @@ static int smooth_core(const double* g, int c, int h, int w, const double* guide
                 s01[i] = (src[ch * pp + i] + 1.0) * 0.5;
                 g01[i] = (gd[ch * pp + i] + 1.0) * 0.5;
             }
-            orc_blf_brute_r(s01, 1, g01, 1, hp, wp, radius, sigma_s, sigma_r, f01);
+            if (dt_iters > 0)
+                orc_nc_filter(s01, 1, g01, 1, hp, wp, sigma_s, sigma_r, dt_iters, f01);
+            else
+                orc_blf_brute_r(s01, 1, g01, 1, hp, wp, radius, sigma_s, sigma_r, f01);
             /* from_unit_range_into, pipelines.cpp:25-31 */
             for (size_t i = 0; i < pp; ++i) dst[ch * pp + i] = 2.0 * f01[i] - 1.0;
         }
@@ -629,15 +635,23 @@ static int smooth_core(const double* g, int c, int h, int w, const double* guide
     return st;
 }
 
+static int smooth_core(const double* g, int c, int h, int w, const double* guide, int radius,
+                       double sigma_s, double sigma_r, double lambda, int pad, double* out,
+                       double* t_blf, double* t_solve)
+{
+    return smooth_core_k(g, c, h, w, guide, radius, 0, sigma_s, sigma_r, lambda, pad, out, t_blf,
+                         t_solve);
+}
+
 int orc_smooth_brute(const double* g, int c, int h, int w, const double* guide, int radius,
                      double sigma_s, double sigma_r, double lambda, int pad, double* out)
 {
     return smooth_core(g, c, h, w, guide, radius, sigma_s, sigma_r, lambda, pad, out, NULL, NULL);
 }
 
-static int blf_ls_core(const double* g, int c, int h, int w, const double* guide, int guide_c,
-                       int radius, double sigma_s, double sigma_r, double lambda, int iters, int pad,
-                       double* out, double* t_blf, double* t_solve)
+static int cascade_core(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                        int radius, int dt_iters, double sigma_s, double sigma_r, double lambda,
+                        int iters, int pad, double* out, double* t_blf, double* t_solve)
 {
     if (c != 1 && c != 3) return ORC_EINVAL;
     if (h < 1 || w < 1 || iters < 1) return ORC_EINVAL;
@@ -656,13 +670,21 @@ static int blf_ls_core(const double* g, int c, int h, int w, const double* guide
     if (t_solve) *t_solve = 0.0;
     int st = ORC_OK;
     for (int k = 0; k < iters && st == ORC_OK; ++k) {
-        st = smooth_core(f, c, h, w, guide_rep, radius, sigma_s, sigma_r, lambda, pad, out, t_blf,
-                         t_solve);
+        st = smooth_core_k(f, c, h, w, guide_rep, radius, dt_iters, sigma_s, sigma_r, lambda, pad,
+                           out, t_blf, t_solve);
         memcpy(f, out, sizeof(double) * n);
     }
     free(f);
     free(guide_rep);
     return st;
+}
+
+static int blf_ls_core(const double* g, int c, int h, int w, const double* guide, int guide_c,
+                       int radius, double sigma_s, double sigma_r, double lambda, int iters, int pad,
+                       double* out, double* t_blf, double* t_solve)
+{
+    return cascade_core(g, c, h, w, guide, guide_c, radius, 0, sigma_s, sigma_r, lambda, iters, pad,
+                        out, t_blf, t_solve);
 }
 
 int orc_blf_ls_timed(const double* g, int c, int h, int w, const double* guide, int guide_c,
@@ -687,6 +709,178 @@ int orc_blf_ls_pad(const double* g, int c, int h, int w, const double* guide, in
     if (pad < 0) return ORC_EINVAL;
     return blf_ls_core(g, c, h, w, guide, guide_c, radius, sigma_s, sigma_r, lambda, iters, pad, out,
                        NULL, NULL);
+}
+
+/* ------------------------------------------------- domain_transform.cpp -- */
+
+double orc_nc_box_radius(double sigma_s, int iter, int total)
+{
+    /* domain_transform.cpp:9-17: per-pass Gaussian bandwidth, box of equal variance */
+    const double sigma_i =
+        sigma_s * sqrt(3.0) * pow(2.0, total - iter) / sqrt(pow(4.0, total) - 1.0);
+    return sqrt(3.0) * sigma_i;
+}
+
+/* One scanline of n samples at stride `st`: normalized box over the warped
+ * coordinates t (domain_transform.cpp:72-103 / 105-134).  The sliding bounds
+ * and the prefix sums are evaluated in the reference's order. */
+static void nc_box_line(double* v, size_t st, int n, const double* t, size_t tst, double radius,
+                        double* prefix)
+{
+    prefix[0] = 0.0;
+    for (int k = 0; k < n; ++k) prefix[k + 1] = prefix[k] + v[k * st];
+    int lo = 0, hi = 0;
+    for (int k = 0; k < n; ++k) {
+        const double tk = t[k * tst];
+        while (t[lo * tst] < tk - radius) ++lo;
+        if (hi < k) hi = k;
+        while (hi + 1 < n && t[(hi + 1) * tst] <= tk + radius) ++hi;
+        const double inv = 1.0 / (hi - lo + 1);
+        v[k * st] = (prefix[hi + 1] - prefix[lo]) * inv;
+    }
+}
+
+int orc_nc_filter(const double* src, int cs, const double* guide, int cg, int h, int w,
+                  double sigma_s, double sigma_r, int iters, double* out)
+{
+    /* domain_transform.cpp:21-29 (validate) */
+    if (!(sigma_s > 0.0) || !(sigma_r > 0.0) || !isfinite(sigma_s) || !isfinite(sigma_r))
+        return ORC_EINVAL;
+    if (iters < 1 || h < 1 || w < 1 || cs < 1 || cg < 1) return ORC_EINVAL;
+    const size_t pp = (size_t)h * w;
+    if (!all_finite(src, cs * pp) || !all_finite(guide, cg * pp)) return ORC_ENONFINITE;
+    const double ratio = sigma_s / sigma_r;
+    /* transform_rows / transform_cols, domain_transform.cpp:31-68 */
+    double* cth = (double*)malloc(sizeof(double) * pp);
+    double* ctv = (double*)malloc(sizeof(double) * pp);
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < h; ++y) {
+        double acc = 1.0;
+        cth[(size_t)y * w] = acc;
+        for (int x = 1; x < w; ++x) {
+            double d = 0.0;
+            for (int c = 0; c < cg; ++c)
+                d += fabs(guide[c * pp + (size_t)y * w + x] - guide[c * pp + (size_t)y * w + x - 1]);
+            acc += 1.0 + ratio * d;
+            cth[(size_t)y * w + x] = acc;
+        }
+    }
+#pragma omp parallel for schedule(static)
+    for (int x = 0; x < w; ++x) {
+        double acc = 1.0;
+        ctv[x] = acc;
+        for (int y = 1; y < h; ++y) {
+            double d = 0.0;
+            for (int c = 0; c < cg; ++c)
+                d += fabs(guide[c * pp + (size_t)y * w + x] - guide[c * pp + (size_t)(y - 1) * w + x]);
+            acc += 1.0 + ratio * d;
+            ctv[(size_t)y * w + x] = acc;
+        }
+    }
+    memcpy(out, src, sizeof(double) * cs * pp);
+    /* nc_filter, domain_transform.cpp:138-156: rows then columns per pass */
+    for (int it = 1; it <= iters; ++it) {
+        const double radius = orc_nc_box_radius(sigma_s, it, iters);
+#pragma omp parallel
+        {
+            double* prefix = (double*)malloc(sizeof(double) * ((h > w ? h : w) + 1));
+#pragma omp for schedule(static)
+            for (int y = 0; y < h; ++y)
+                for (int c = 0; c < cs; ++c)
+                    nc_box_line(out + c * pp + (size_t)y * w, 1, w, cth + (size_t)y * w, 1, radius,
+                                prefix);
+#pragma omp for schedule(static)
+            for (int x = 0; x < w; ++x)
+                for (int c = 0; c < cs; ++c)
+                    nc_box_line(out + c * pp + x, (size_t)w, h, ctv + x, (size_t)w, radius, prefix);
+            free(prefix);
+        }
+    }
+    free(cth);
+    free(ctv);
+    return ORC_OK;
+}
+
+int orc_smooth_nc(const double* g, int c, int h, int w, const double* guide, double sigma_s,
+                  double sigma_r, int dt_iters, double lambda, int pad, double* out)
+{
+    if (dt_iters < 1) return ORC_EINVAL;
+    return smooth_core_k(g, c, h, w, guide, 0, dt_iters, sigma_s, sigma_r, lambda, pad, out, NULL,
+                         NULL);
+}
+
+int orc_nc_ls(const double* g, int c, int h, int w, const double* guide, int guide_c,
+              double sigma_s, double sigma_r, int dt_iters, double lambda, int iters, int pad,
+              double* out)
+{
+    if (dt_iters < 1 || pad < 0) return ORC_EINVAL;
+    return cascade_core(g, c, h, w, guide, guide_c, 0, dt_iters, sigma_s, sigma_r, lambda, iters,
+                        pad, out, NULL, NULL);
+}
+
+/* image.cpp:99-158: separable Gaussian, radius ceil(3 sigma), clamped borders */
+int orc_gaussian_blur(const double* img, int c, int h, int w, double sigma, double* out)
+{
+    if (!(sigma > 0.0) || !isfinite(sigma)) return ORC_EINVAL;
+    const int r = (int)ceil(3.0 * sigma);
+    double* k = (double*)malloc(sizeof(double) * (2 * r + 1));
+    double sum = 0.0;
+    for (int i = -r; i <= r; ++i) {
+        k[i + r] = exp(-((double)i * i) / (2.0 * sigma * sigma));
+        sum += k[i + r];
+    }
+    for (int i = 0; i <= 2 * r; ++i) k[i] /= sum;
+    const size_t pp = (size_t)h * w;
+    double* tmp = (double*)malloc(sizeof(double) * c * pp);
+    for (int ch = 0; ch < c; ++ch) {
+        const double* src = img + ch * pp;
+        double* dst = tmp + ch * pp;
+#pragma omp parallel for schedule(static)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                double acc = 0.0;
+                for (int i = -r; i <= r; ++i) {
+                    int xi = x + i;
+                    xi = xi < 0 ? 0 : (xi > w - 1 ? w - 1 : xi);
+                    acc += k[i + r] * src[(size_t)y * w + xi];
+                }
+                dst[(size_t)y * w + x] = acc;
+            }
+    }
+    for (int ch = 0; ch < c; ++ch) {
+        const double* src = tmp + ch * pp;
+        double* dst = out + ch * pp;
+#pragma omp parallel for schedule(static)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                double acc = 0.0;
+                for (int i = -r; i <= r; ++i) {
+                    int yi = y + i;
+                    yi = yi < 0 ? 0 : (yi > h - 1 ? h - 1 : yi);
+                    acc += k[i + r] * src[(size_t)yi * w + x];
+                }
+                dst[(size_t)y * w + x] = acc;
+            }
+    }
+    free(tmp);
+    free(k);
+    return ORC_OK;
+}
+
+/* pipelines.cpp:96-117: guide <- blur(g); n times u <- smooth_nc(g, guide), guide <- u */
+int orc_rolling_nc_ls(const double* g, int c, int h, int w, double sigma_s, double sigma_r,
+                      int dt_iters, double lambda, int pad, int n, double init_sigma, double* out)
+{
+    if (n < 1 || !(init_sigma > 0.0)) return ORC_EINVAL;
+    const size_t nn = (size_t)c * h * w;
+    double* guide = (double*)malloc(sizeof(double) * nn);
+    int st = orc_gaussian_blur(g, c, h, w, init_sigma, guide);
+    for (int k = 0; k < n && st == ORC_OK; ++k) {
+        st = orc_smooth_nc(g, c, h, w, guide, sigma_s, sigma_r, dt_iters, lambda, pad, out);
+        memcpy(guide, out, sizeof(double) * nn);
+    }
+    free(guide);
+    return st;
 }
 
 /* ------------------------------------------------------------ generator -- */

@@ -100,6 +100,26 @@ int orc_blf_ls_timed(const double* g, int c, int h, int w, const double* guide, 
                      int radius, double sigma_s, double sigma_r, double lambda, int iters,
                      double* out, double* t_blf, double* t_solve);
 
+/* domain_transform.cpp:9-17 */
+double orc_nc_box_radius(double sigma_s, int iter, int total);
+/* domain_transform.cpp:21-156: normalized convolution over the domain
+ * transform; guide has cg channels (L1 distance summed over them). */
+int orc_nc_filter(const double* src, int cs, const double* guide, int cg, int h, int w,
+                  double sigma_s, double sigma_r, int iters, double* out);
+/* pipelines.cpp:57-94 with SmootherKind::NC_LS (nc_filter at pipelines.cpp:48);
+ * guide NULL or c channels. */
+int orc_smooth_nc(const double* g, int c, int h, int w, const double* guide, double sigma_s,
+                  double sigma_r, int dt_iters, double lambda, int pad, double* out);
+/* NC-LS cascade (iters smooth_nc calls, guide fixed, 1-channel guide replicated). */
+int orc_nc_ls(const double* g, int c, int h, int w, const double* guide, int guide_c,
+              double sigma_s, double sigma_r, int dt_iters, double lambda, int iters, int pad,
+              double* out);
+/* image.cpp:99-158 */
+int orc_gaussian_blur(const double* img, int c, int h, int w, double sigma, double* out);
+/* pipelines.cpp:96-117 */
+int orc_rolling_nc_ls(const double* g, int c, int h, int w, double sigma_s, double sigma_r,
+                      int dt_iters, double lambda, int pad, int n, double init_sigma, double* out);
+
 /* SplitMix64 draw j (0-based) of the stream seeded with `seed`
  * (testimage.cpp:11-21: state += gamma, then mix). */
 uint64_t orc_splitmix64_at(uint64_t seed, uint64_t j);

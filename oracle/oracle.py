@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
         _lib.orc_splitmix64_at.restype = C.c_uint64
         _lib.orc_splitmix64_at.argtypes = [C.c_uint64, C.c_uint64]
         _lib.orc_diff_gain_sq.restype = C.c_double
+        _lib.orc_nc_box_radius.restype = C.c_double
+        _lib.orc_nc_box_radius.argtypes = [C.c_double, C.c_int, C.c_int]
         _lib.orc_gen_plane.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _fp]
         for name in ("orc_blf_ls", "orc_blf_ls_timed", "orc_blf_ls_pad", "orc_smooth_brute", "orc_blf_brute_r",
                      "orc_lsgrad_solve_fft", "orc_dense_solve"):
@@ -84,6 +86,8 @@ def ref() -> C.CDLL:
     if _ref is None:
         _ref = _load(REF_SO)
         _ref.ref_max_abs_gradient.restype = C.c_double
+        _ref.ref_nc_box_radius.restype = C.c_double
+        _ref.ref_nc_box_radius.argtypes = [C.c_double, C.c_int, C.c_int]
         _ref.ref_random_image.argtypes = [C.c_int, C.c_int, C.c_int, C.c_ulonglong, C.c_double,
                                           C.c_double, _dp]
         _ref.ref_natural_scene.argtypes = [C.c_int, C.c_int, C.c_int, C.c_ulonglong, _dp]
@@ -234,6 +238,67 @@ def naive_dft2(img):
     return spec
 
 
+def nc_box_radius(sigma_s, it, total) -> float:
+    return lib().orc_nc_box_radius(sigma_s, it, total)
+
+
+def nc_filter(src, guide, *, sigma_s, sigma_r, iters=3):
+    """orc_nc_filter (domain_transform.cpp:138-156)."""
+    s_ = _f64(src)
+    gd = _f64(guide)
+    cs, h, w = _shape3(s_)
+    out = np.empty((cs, h, w))
+    _check("orc_nc_filter", lib().orc_nc_filter(_d(s_), cs, _d(gd), _shape3(gd)[0], h, w,
+                                                C.c_double(sigma_s), C.c_double(sigma_r), int(iters),
+                                                _d(out)))
+    return out
+
+
+def smooth_nc(img, guide=None, *, lam, sigma_s, sigma_r, dt_iters=3, pad=0):
+    """One smooth() call with SmootherKind::NC_LS (pipelines.cpp:57-94)."""
+    g = _f64(img)
+    c, h, w = _shape3(g)
+    out = np.empty((c, h, w))
+    gd = None if guide is None else _f64(guide)
+    _check("orc_smooth_nc", lib().orc_smooth_nc(_d(g), c, h, w, _d(gd), C.c_double(sigma_s),
+                                                C.c_double(sigma_r), int(dt_iters), C.c_double(lam),
+                                                int(pad), _d(out)))
+    return out
+
+
+def nc_ls(img, guide=None, *, lam, sigma_s, sigma_r, dt_iters=3, iters=1, pad=0):
+    """NC-LS cascade: `iters` smooth_nc calls, guide fixed (1-channel guide replicated)."""
+    g = _f64(img)
+    c, h, w = _shape3(g)
+    out = np.empty((c, h, w))
+    gd = None if guide is None else _f64(guide)
+    gc = 0 if gd is None else _shape3(gd)[0]
+    _check("orc_nc_ls", lib().orc_nc_ls(_d(g), c, h, w, _d(gd), gc, C.c_double(sigma_s),
+                                        C.c_double(sigma_r), int(dt_iters), C.c_double(lam),
+                                        int(iters), int(pad), _d(out)))
+    return out
+
+
+def gaussian_blur(img, sigma):
+    g = _f64(img)
+    c, h, w = _shape3(g)
+    out = np.empty((c, h, w))
+    _check("orc_gaussian_blur", lib().orc_gaussian_blur(_d(g), c, h, w, C.c_double(sigma), _d(out)))
+    return out
+
+
+def rolling_nc_ls(img, *, lam, sigma_s, sigma_r, dt_iters=3, pad=0, n=3, init_sigma=2.5):
+    """pipelines.cpp:96-117."""
+    g = _f64(img)
+    c, h, w = _shape3(g)
+    out = np.empty((c, h, w))
+    _check("orc_rolling_nc_ls",
+           lib().orc_rolling_nc_ls(_d(g), c, h, w, C.c_double(sigma_s), C.c_double(sigma_r),
+                                   int(dt_iters), C.c_double(lam), int(pad), int(n),
+                                   C.c_double(init_sigma), _d(out)))
+    return out
+
+
 def gen_plane(seed, h, w, *, n_sites, noise_sigma=0.03, p_sp=0.0) -> np.ndarray:
     out = np.empty((h, w), dtype=np.float32)
     lib().orc_gen_plane(C.c_uint64(seed), h, w, n_sites, C.c_double(noise_sigma), C.c_double(p_sp),
@@ -345,6 +410,43 @@ def ref_blf_ls(img, guide=None, *, lam, sigma_s, sigma_r, iters, radius, timed=F
                                 C.byref(tb), C.byref(ts)))
     if timed:
         return out, tb.value, ts.value
+    return out
+
+
+def ref_nc_box_radius(sigma_s, it, total) -> float:
+    return ref().ref_nc_box_radius(sigma_s, it, total)
+
+
+def ref_nc_filter(src, guide, *, sigma_s, sigma_r, iters=3, serial=False):
+    s_ = _f64(src)
+    gd = _f64(guide)
+    cs, h, w = _shape3(s_)
+    out = np.empty((cs, h, w))
+    fn = "ref_serial_nc_filter" if serial else "ref_nc_filter"
+    _check(fn, getattr(ref(), fn)(_d(s_), cs, _d(gd), _shape3(gd)[0], h, w, C.c_double(sigma_s),
+                                  C.c_double(sigma_r), int(iters), _d(out)))
+    return out
+
+
+def ref_smooth_nc(img, guide=None, *, lam, sigma_s, sigma_r, dt_iters=3, pad=0):
+    g = _f64(img)
+    c, h, w = _shape3(g)
+    out = np.empty((c, h, w))
+    gd = None if guide is None else _f64(guide)
+    _check("ref_smooth_nc", ref().ref_smooth_nc(_d(g), c, h, w, _d(gd), C.c_double(sigma_s),
+                                                C.c_double(sigma_r), int(dt_iters), C.c_double(lam),
+                                                int(pad), _d(out)))
+    return out
+
+
+def ref_rolling_nc_ls(img, *, lam, sigma_s, sigma_r, dt_iters=3, pad=0, n=3, init_sigma=2.5):
+    g = _f64(img)
+    c, h, w = _shape3(g)
+    out = np.empty((c, h, w))
+    _check("ref_rolling_nc_ls",
+           ref().ref_rolling_nc_ls(_d(g), c, h, w, C.c_double(sigma_s), C.c_double(sigma_r),
+                                   int(dt_iters), C.c_double(lam), int(pad), int(n),
+                                   C.c_double(init_sigma), _d(out)))
     return out
 
 

@@ -294,6 +294,55 @@ int ref_blf_ls(const double* g, int c, int h, int w, const double* guide, int gu
                           t_blf, t_solve);
 }
 
+int ref_nc_filter(const double* src, int cs, const double* guide, int cg, int h, int w,
+                  double sigma_s, double sigma_r, int iters, double* out)
+{
+    return guarded([&] {
+        unwrap(nc_filter(wrap(src, cs, h, w), wrap(guide, cg, h, w), {sigma_s, sigma_r, iters}), out);
+    });
+}
+
+int ref_serial_nc_filter(const double* src, int cs, const double* guide, int cg, int h, int w,
+                         double sigma_s, double sigma_r, int iters, double* out)
+{
+    return guarded([&] {
+        unwrap(serial::nc_filter(wrap(src, cs, h, w), wrap(guide, cg, h, w), {sigma_s, sigma_r, iters}),
+               out);
+    });
+}
+
+double ref_nc_box_radius(double sigma_s, int iter, int total)
+{
+    return nc_box_radius(sigma_s, iter, total);
+}
+
+int ref_smooth_nc(const double* g, int c, int h, int w, const double* guide, double sigma_s,
+                  double sigma_r, int dt_iters, double lambda, int pad, double* out)
+{
+    return guarded([&] {
+        SmootherSpec s;
+        s.kind = SmootherKind::NC_LS;
+        s.dt = {sigma_s, sigma_r, dt_iters};
+        s.solve = {lambda, pad};
+        PlanarImage gd;
+        if (guide) {
+            gd = wrap(guide, c, h, w);
+            s.guidance = &gd;
+        }
+        unwrap(smooth(wrap(g, c, h, w), s), out);
+    });
+}
+
+int ref_rolling_nc_ls(const double* g, int c, int h, int w, double sigma_s, double sigma_r,
+                      int dt_iters, double lambda, int pad, int n, double init_sigma, double* out)
+{
+    return guarded([&] {
+        unwrap(rolling_nc_ls(wrap(g, c, h, w), {sigma_s, sigma_r, dt_iters}, {lambda, pad},
+                             {n, init_sigma}),
+               out);
+    });
+}
+
 int ref_random_image(int w, int h, int c, unsigned long long seed, double lo, double hi, double* out)
 {
     return guarded([&] { unwrap(testimage::random_image(w, h, c, seed, lo, hi), out); });

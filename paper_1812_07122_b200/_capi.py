@@ -27,13 +27,14 @@ TIME_STAGES = 16
 ASYNC = 32
 BACKEND_BRUTE = 0
 BACKEND_GRID = 1
+BACKEND_DT = 2
 
 # every symbol include/blfls/blfls.h declares
 EXPORTS = (
     "blfls_plan_create", "blfls_plan_destroy", "blfls_run", "blfls_sync", "blfls_filter_gradients",
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
     "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
-    "blfls_version", "blfls_abi_version",
+    "blfls_version", "blfls_abi_version", "blfls_gaussian_blur",
 )
 
 
@@ -63,6 +64,7 @@ class Params(C.Structure):
         ("guide_channels", C.c_int), ("radius", C.c_int), ("sigma_s", C.c_double),
         ("sigma_r", C.c_double), ("lambda_", C.c_double), ("max_batch", C.c_int),
         ("device", C.c_int), ("pad", C.c_int), ("backend", C.c_int),
+        ("dt_iterations", C.c_int),
     ]
 
 
@@ -102,6 +104,7 @@ def lib() -> C.CDLL:
             L.blfls_stage_times.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
             L.blfls_debug_ranges.argtypes = [vp, C.POINTER(C.c_float)]
             L.blfls_mufu_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+            L.blfls_gaussian_blur.argtypes = [fp, ip, ip, ip, C.c_double, fp, ip, vp, C.c_uint]
             L.blfls_last_error.restype = C.c_char_p
             L.blfls_version.restype = C.c_char_p
             for name in EXPORTS:
@@ -126,10 +129,11 @@ class Plan:
     """Owns a blfls_plan_t (one per host thread / stream, like the C ABI says)."""
 
     def __init__(self, height, width, channels, guide_channels, radius, sigma_s, sigma_r, lam,
-                 max_batch=1, device=0, pad=0, backend=0):
+                 max_batch=1, device=0, pad=0, backend=0, dt_iterations=0):
         self.params = Params(int(height), int(width), int(channels), int(guide_channels),
                              int(radius), float(sigma_s), float(sigma_r), float(lam),
-                             int(max_batch), int(device), int(pad), int(backend))
+                             int(max_batch), int(device), int(pad), int(backend),
+                             int(dt_iterations))
         h = C.c_void_p()
         check(lib().blfls_plan_create(C.byref(self.params), C.byref(h)))
         self.handle = h

@@ -9,7 +9,14 @@ this module                reference
 ``SmootherSpec``           ``SmootherSpec`` (include/epls/pipelines.hpp:16-23)
 ``RangeSpatialParams``     ``RangeSpatialParams`` (bilateral.hpp:10-13)
 ``SolveParams``            ``SolveParams`` (solver.hpp:12-15)
-``smooth(g, spec)``        ``smooth`` (pipelines.cpp:57-94), BLF_LS and LS
+``smooth(g, spec)``        ``smooth`` (pipelines.cpp:57-94), BLF_LS, NC_LS and LS
+``DtParams``               ``DtParams`` (domain_transform.hpp:7-11)
+``RollingParams``          ``RollingParams`` (pipelines.hpp:25-28)
+``nc_ls``                  NC_LS cascade: ``iters`` smooth() calls (nc_filter)
+``rolling_nc_ls``          ``rolling_nc_ls`` (pipelines.cpp:96-117)
+``texture_removal``        ``texture_removal`` (applications.cpp:66-70)
+``clipart_cleanup``        ``clipart_cleanup`` (applications.cpp:72-76)
+``gaussian_blur``          ``gaussian_blur`` (image.cpp:114-158)
 ``flash_no_flash``         ``flash_no_flash`` (applications.cpp:58-64)
 ``blf_ls``                 the north-star cascade: ``iters`` smooth() calls
 ``filter_gradients``       ``filter_gradients`` (pipelines.cpp:33-53)
@@ -20,9 +27,10 @@ this module                reference
 
 Differences, all deliberate and documented in DESIGN.md: the bilateral stage
 is the brute-force filter (the north star) where the reference's smooth()
-runs the bilateral grid; the window radius is explicit (``radius``; ``None``
-means the reference's ceil(3 sigma_s)); arithmetic is fp32 on the GPU; only
-``pad == 0`` (periodic boundary) is supported.
+runs the bilateral grid (``backend="grid"`` runs the grid too); the window
+radius is explicit (``radius``; ``None`` means the reference's
+ceil(3 sigma_s)); images cross the API as fp32 (the filters evaluate the
+gradients in double, the FFT solve in fp32).
 
 Images are numpy arrays (host memory; copied through the C ABI with
 ``BLFLS_HOST_PTRS``) or CUDA torch tensors (device memory, current stream).
@@ -47,7 +55,8 @@ from ._capi import (ASYNC, CHECK_FINITE, DEVICE_PTRS, HOST_PTRS, NO_GRAPH, SYNC,
 
 __all__ = [
     "SmootherKind", "RangeSpatialParams", "SolveParams", "SmootherSpec", "smooth",
-    "flash_no_flash", "blf_ls", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
+    "flash_no_flash", "blf_ls", "nc_ls", "rolling_nc_ls", "texture_removal", "clipart_cleanup",
+    "gaussian_blur", "DtParams", "RollingParams", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
     "rfft2", "irfft2", "generate", "get_plan", "sync_plans", "InvalidArgument", "CudaError",
     "Unsupported",
 ]
@@ -73,6 +82,19 @@ class SolveParams:
 
 
 @dataclass
+class DtParams:
+    sigma_s: float = 8.0
+    sigma_r: float = 0.1
+    iterations: int = 3
+
+
+@dataclass
+class RollingParams:
+    n: int = 3
+    init_sigma: float = 2.5
+
+
+@dataclass
 class SmootherSpec:
     kind: SmootherKind = SmootherKind.BLF_LS
     blf: RangeSpatialParams = field(default_factory=lambda: RangeSpatialParams(12.0, 0.04))
@@ -80,6 +102,7 @@ class SmootherSpec:
     guidance: Any = None          # non-owning guide image of the same shape (or 1 channel)
     radius: int | None = None     # BLF window radius; None = ceil(3 sigma_s) (bilateral.cpp:37)
     backend: str = "brute"        # "brute" (north star) or "grid" (the reference smooth()'s blf_grid)
+    dt: DtParams = field(default_factory=lambda: DtParams(12.0, 0.05, 3))  # NC_LS filter
 
 
 # ----------------------------------------------------------------- plans --
@@ -87,27 +110,28 @@ class SmootherSpec:
 _tls = threading.local()
 
 
-_BACKENDS = {"brute": _capi.BACKEND_BRUTE, "grid": _capi.BACKEND_GRID}
+_BACKENDS = {"brute": _capi.BACKEND_BRUTE, "grid": _capi.BACKEND_GRID, "dt": _capi.BACKEND_DT}
 
 
 def _backend(name) -> int:
     if name not in _BACKENDS:
-        raise InvalidArgument(_capi.BLFLS_EINVAL, f"unknown backend {name!r} (brute | grid)")
+        raise InvalidArgument(_capi.BLFLS_EINVAL, f"unknown backend {name!r} (brute | grid | dt)")
     return _BACKENDS[name]
 
 
 def get_plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, batch, device, pad=0,
-             backend="brute") -> Plan:
+             backend="brute", dt_iterations=0) -> Plan:
     """Per-thread plan cache (plans are not thread-safe, blfls.h)."""
     cache = getattr(_tls, "plans", None)
     if cache is None:
         cache = _tls.plans = {}
     be = _backend(backend)
-    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device, int(pad), be)
+    key = (h, w, c, gc, radius, float(sigma_s), float(sigma_r), float(lam), device, int(pad), be,
+           int(dt_iterations))
     p = cache.get(key)
     if p is None or p.params.max_batch < batch:
         p = Plan(h, w, c, gc, radius, sigma_s, sigma_r, lam, max_batch=max(batch, 1), device=device,
-                 pad=pad, backend=be)
+                 pad=pad, backend=be, dt_iterations=dt_iterations)
         cache[key] = p
     return p
 
@@ -201,7 +225,7 @@ def _device(img: _Img, guide: _Img | None) -> int:
 def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, iters: int = 1,
            radius: int | None = None, check_finite: bool = True, use_graph: bool = True,
            out=None, extra_flags: int = 0, wait: bool = True, pad: int = 0,
-           backend: str = "brute"):
+           backend: str = "brute", dt_iterations: int = 0):
     """BLF-LS: ``iters`` cascaded smooth() passes with the brute-force (joint) BLF.
 
     ``guide`` (optional) has 1 channel or the image's channel count and is held
@@ -225,12 +249,12 @@ def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, ite
         if (gd.h, gd.w) != (img.h, img.w) or gd.b != img.b or gd.c not in (1, img.c):
             raise InvalidArgument(_capi.BLFLS_EINVAL,
                                   "smooth: guidance image shape does not match input")
-    r = _radius(radius, sigma_s)
+    r = _radius(radius, sigma_s) if backend == "brute" else 0
     dev = _device(img, gd)
     if int(pad) < 0:
         raise InvalidArgument(_capi.BLFLS_EINVAL, "solver: pad must be >= 0")
     plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, lam,
-                    img.b, dev, pad=int(pad), backend=backend)
+                    img.b, dev, pad=int(pad), backend=backend, dt_iterations=dt_iterations)
     if out is None:
         out = img.empty_like()
         finish = True
@@ -272,13 +296,68 @@ def sync_plans() -> None:
         p.sync()
 
 
+def nc_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float,
+          dt_iterations: int = 3, iters: int = 1, pad: int = 0, **kw):
+    """NC-LS: ``iters`` cascaded smooth() passes with SmootherKind::NC_LS, i.e.
+    the gradients filtered by nc_filter (domain_transform.cpp:138-156) with
+    DtParams{sigma_s, sigma_r, dt_iterations}; otherwise as ``blf_ls``."""
+    if int(dt_iterations) < 1:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "nc_filter: iterations must be >= 1")
+    return blf_ls(image, guide, lam=lam, sigma_s=sigma_s, sigma_r=sigma_r, iters=iters, pad=pad,
+                  backend="dt", dt_iterations=int(dt_iterations), **kw)
+
+
+def gaussian_blur(img, sigma: float):
+    """``gaussian_blur`` (image.cpp:114-158) on the GPU: radius ceil(3 sigma),
+    clamped borders, double accumulation; fp32 in and out."""
+    im = _Img(img)
+    out = im.empty_like()
+    stream, flags = _stream_and_flags(im)
+    dev = im.device if im.torch else 0
+    check(lib().blfls_gaussian_blur(im.ptr, im.b * im.c, im.h, im.w, float(sigma), _ptr(out), dev,
+                                    stream, flags))
+    return im.finish(out)
+
+
+def rolling_nc_ls(g, dt: DtParams, sp: SolveParams, rp: RollingParams):
+    """``rolling_nc_ls`` (pipelines.cpp:96-117): NC_LS smoothing of the original
+    input guided first by a Gaussian-blurred copy, then by the previous
+    round's output."""
+    if rp.n < 1:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "rolling_nc_ls: n must be >= 1")
+    if not rp.init_sigma > 0.0:
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "rolling_nc_ls: init_sigma must be positive")
+    guide = gaussian_blur(g, rp.init_sigma)
+    u = None
+    for _ in range(rp.n):
+        u = nc_ls(g, guide, lam=sp.lam, sigma_s=dt.sigma_s, sigma_r=dt.sigma_r,
+                  dt_iterations=dt.iterations, pad=sp.pad)
+        guide = u
+    return u
+
+
+def texture_removal(g, dt: DtParams, rp: RollingParams, sp: SolveParams):
+    """applications.cpp:66-70."""
+    return rolling_nc_ls(g, dt, sp, rp)
+
+
+def clipart_cleanup(g, dt: DtParams, rp: RollingParams, sp: SolveParams):
+    """applications.cpp:72-76."""
+    return rolling_nc_ls(g, dt, sp, rp)
+
+
 def smooth(g, spec: SmootherSpec):
-    """``epls::smooth`` (pipelines.cpp:57-94) for kind BLF_LS (brute-force BLF) and LS,
-    including the reference's reflect padding ``spec.solve.pad`` (default 16)."""
+    """``epls::smooth`` (pipelines.cpp:57-94) for kinds BLF_LS (brute-force BLF,
+    or the grid with ``backend="grid"``), NC_LS and LS, including the
+    reference's reflect padding ``spec.solve.pad`` (default 16)."""
     if spec.kind == SmootherKind.BLF_LS:
         return blf_ls(g, spec.guidance, lam=spec.solve.lam, sigma_s=spec.blf.sigma_s,
                       sigma_r=spec.blf.sigma_r, iters=1, radius=spec.radius, pad=spec.solve.pad,
                       backend=spec.backend)
+    if spec.kind == SmootherKind.NC_LS:
+        return nc_ls(g, spec.guidance, lam=spec.solve.lam, sigma_s=spec.dt.sigma_s,
+                     sigma_r=spec.dt.sigma_r, dt_iterations=spec.dt.iterations,
+                     pad=spec.solve.pad)
     if spec.kind == SmootherKind.LS:
         # affine-equivariant, so normalise/denormalise (pipelines.cpp:64,68) is the identity
         return ls_solve_fft(g, spec.solve)
@@ -290,20 +369,21 @@ def flash_no_flash(noflash, flash, spec: SmootherSpec):
     a, b = _Img(noflash), _Img(flash, "guide")
     if a.shape != b.shape:
         raise InvalidArgument(_capi.BLFLS_EINVAL, "flash_no_flash: image shapes differ")
-    s = SmootherSpec(spec.kind, spec.blf, spec.solve, flash, spec.radius, spec.backend)
+    s = SmootherSpec(spec.kind, spec.blf, spec.solve, flash, spec.radius, spec.backend, spec.dt)
     return smooth(noflash, s)
 
 
 def filter_gradients(image, guide=None, *, sigma_s: float, sigma_r: float,
-                     radius: int | None = None, backend: str = "brute"):
-    """Gradient targets of one smooth() call (pipelines.cpp:33-53, brute-force BLF),
-    in the reference's normalised units.  Returns (tx, ty)."""
+                     radius: int | None = None, backend: str = "brute", dt_iterations: int = 0):
+    """Gradient targets of one smooth() call (pipelines.cpp:33-53: brute-force BLF,
+    ``backend="grid"`` blf_grid, ``backend="dt"`` nc_filter with
+    ``dt_iterations``), in the reference's normalised units.  Returns (tx, ty)."""
     img = _Img(image)
     gd = None if guide is None else _Img(guide, "guide")
-    r = _radius(radius, sigma_s)
+    r = _radius(radius, sigma_s) if backend == "brute" else 0
     dev = _device(img, gd)
     plan = get_plan(img.h, img.w, img.c, 0 if gd is None else gd.c, r, sigma_s, sigma_r, 0.0,
-                    img.b, dev, backend=backend)
+                    img.b, dev, backend=backend, dt_iterations=dt_iterations)
     tx, ty = img.empty_like(), img.empty_like()
     stream, flags = _stream_and_flags(img)
     check(lib().blfls_filter_gradients(plan.handle, img.ptr, None if gd is None else gd.ptr, img.b,

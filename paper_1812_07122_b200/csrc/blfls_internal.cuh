@@ -1,6 +1,8 @@
 // blfls_internal.cuh -- shared definitions of the sm_100a BLF-LS library.
 #pragma once
 
+#include <vector>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -111,6 +113,34 @@ struct GridParams {
     size_t cells;          // gw * gh * gdmax
     int normalized;        // 1: targets of the [0,1]-normalised image (stage entry)
 };
+
+// domain-transform backend (k_dt.cu): nc_filter per slot
+struct DtParams {
+    const float* f;        // (padded) image, planes x H x W
+    const float* guide;    // (padded) guide or nullptr
+    float* tx;             // targets, raw units
+    float* ty;
+    const uint32_t* lohi;  // per image ordered (lo, hi) of f
+    const uint32_t* glohi; // per image of the guide
+    double* cth;           // [slots][H][W] warped row coordinates
+    double* ctv;           // [slots][H][W] warped column coordinates
+    double* pc;            // [slots][pcplane] prefix sums of the current pass
+    double* x;             // [slots][H][W] signal between passes
+    size_t plane;          // H * W
+    size_t pcplane;        // (H + 1) * (W + 1)
+    int H, W, C, GC;
+    int plane0;            // first global plane of this launch
+    int slots;             // plane-axes in this launch
+    int normalized;        // targets in normalised units (else raw)
+    double ratio;          // sigma_s / sigma_r (domain_transform.cpp:142)
+};
+
+double nc_box_radius(double sigma_s, int iter, int total);
+// returns the number of kernels launched, or -1 on a launch error
+int launch_dt_filter(const DtParams& p, int iterations, double sigma_s, cudaStream_t st);
+std::vector<double> gaussian_weights(double sigma);
+cudaError_t launch_gaussian_blur(const float* in, float* out, double* tmp, const double* k, int r,
+                                 int C, int H, int W, int nsm, cudaStream_t st);
 
 struct SolveParams {
     const float* f;      // image (batch x C x H x W)

@@ -36,7 +36,7 @@ cudaError_t launch_generate(int H, int W, int planes, const uint64_t* seeds, int
 cudaError_t measure_mufu(int device, double* ex2_per_s, double* clock_hz);
 cudaError_t launch_reflect_pad(const float* src, float* dst, int H, int W, int pad, size_t planes,
                                int nsm, cudaStream_t st);
-cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st);
+cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st, int* launches);
 bool ct_geometry(bool cols, int n, int nvec, int planes, int nsm, int* V, int* threads);
 
 }  // namespace blfls
@@ -191,6 +191,10 @@ struct blfls_plan_s {
     // bilateral-grid backend workspace (backend == BLFLS_BACKEND_GRID)
     GridParams grid{};
     int grid_planes = 0;     // planes per grid launch (2 slots each)
+    // domain-transform backend workspace (backend == BLFLS_BACKEND_DT)
+    DtParams dt{};
+    int dt_planes = 0;       // planes per DT launch group (2 slots each)
+    int dt_iters = 0;
     float* buf[2] = {nullptr, nullptr};
     float* tx = nullptr;
     float* ty = nullptr;
@@ -358,8 +362,34 @@ blfls_status enq_grid(blfls_plan_t p, const float* f, const float* guide, const 
     for (int p0 = 0; p0 < planes; p0 += p->grid_planes) {
         g.plane0 = p0;
         g.slots = 2 * std::min(p->grid_planes, planes - p0);
-        CK(launch_grid_blf(g, p->nsm, st));
-        p->launches += 10;
+        int n = 0;
+        CK(launch_grid_blf(g, p->nsm, st, &n));
+        p->launches += n;
+    }
+    stage_end(p, st);
+    p->stats.blf_launches++;
+    return BLFLS_OK;
+}
+
+blfls_status enq_dt(blfls_plan_t p, const float* f, const float* guide, const uint32_t* lohi,
+                    float* tx, float* ty, int batch, int normalized, cudaStream_t st)
+{
+    DtParams d = p->dt;
+    d.f = f;
+    d.guide = guide;
+    d.tx = tx;
+    d.ty = ty;
+    d.lohi = lohi;
+    d.glohi = p->glohi;
+    d.normalized = normalized;
+    const int planes = batch * p->prm.channels;
+    stage_begin(p, 1, st);
+    for (int p0 = 0; p0 < planes; p0 += p->dt_planes) {
+        d.plane0 = p0;
+        d.slots = 2 * std::min(p->dt_planes, planes - p0);
+        const int n = launch_dt_filter(d, p->dt_iters, p->prm.sigma_s, st);
+        if (n < 0) CK(cudaGetLastError());
+        p->launches += n;
     }
     stage_end(p, st);
     p->stats.blf_launches++;
@@ -370,6 +400,10 @@ blfls_status enq_blf(blfls_plan_t p, const float* f, const float* guide, const u
                      float* tx, float* ty, int batch, int y0, int y1, int out_rows, int normalized,
                      cudaStream_t st)
 {
+    if (p->prm.backend == BLFLS_BACKEND_DT) {
+        if (y0 != 0 || y1 != p->Hp) return fail(BLFLS_EUNSUPPORTED, "dt backend: no row bands");
+        return enq_dt(p, f, guide, lohi, tx, ty, batch, normalized, st);
+    }
     if (p->prm.backend == BLFLS_BACKEND_GRID) {
         if (y0 != 0 || y1 != p->Hp) return fail(BLFLS_EUNSUPPORTED, "grid backend: no row bands");
         return enq_grid(p, f, guide, lohi, tx, ty, batch, normalized, st);
@@ -504,7 +538,7 @@ void free_plan(blfls_plan_t p)
     void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
                     p->rowf.tw, p->colf.tw, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
-                    p->grid.blurred, p->grid.erange};
+                    p->grid.blurred, p->grid.erange, p->dt.cth, p->dt.ctv, p->dt.pc, p->dt.x};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
@@ -546,10 +580,14 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
     if (q.max_batch < 1) return fail(BLFLS_EINVAL, "plan: max_batch must be >= 1");
     if (q.pad < 0) return fail(BLFLS_EINVAL, "solver: pad must be >= 0");  // solver.cpp:19-20
     if (q.pad > 4096) return fail(BLFLS_EUNSUPPORTED, "plan: pad above 4096");
-    if (q.backend != BLFLS_BACKEND_BRUTE && q.backend != BLFLS_BACKEND_GRID)
+    if (q.backend != BLFLS_BACKEND_BRUTE && q.backend != BLFLS_BACKEND_GRID &&
+        q.backend != BLFLS_BACKEND_DT)
         return fail(BLFLS_EINVAL, "plan: unknown gradient-filter backend");
+    if (q.backend == BLFLS_BACKEND_DT && q.dt_iterations < 0)  // domain_transform.cpp:27-28
+        return fail(BLFLS_EINVAL, "nc_filter: iterations must be >= 1");
     const bool grid = q.backend == BLFLS_BACKEND_GRID;
-    const int radius = grid ? 0 : (q.radius < 0 ? (int)std::ceil(3.0 * q.sigma_s) : q.radius);
+    const bool brute = q.backend == BLFLS_BACKEND_BRUTE;  // the only one with a window radius
+    const int radius = !brute ? 0 : (q.radius < 0 ? (int)std::ceil(3.0 * q.sigma_s) : q.radius);
     if (radius > kMaxRadius)
         return fail(BLFLS_EUNSUPPORTED, "plan: radius above " + std::to_string(kMaxRadius));
 
@@ -660,7 +698,7 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         // shared-memory envelope of the generic kernel
         const int narr = p->mode == 0 ? 2 : (p->mode == 1 ? 4 : 8);
         const size_t smem = (size_t)narr * (16 + 2 * radius) * (((64 + 2 * radius) + 3) & ~3) * 4;
-        if (!grid && smem > 227 * 1024)
+        if (brute && smem > 227 * 1024)
             return bail(fail(BLFLS_EUNSUPPORTED, "plan: radius too large for the shared-memory tile"));
     }
     if (grid) {
@@ -692,6 +730,27 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
             cudaMalloc(&g.blurred, sizeof(double) * 2 * n) != cudaSuccess ||
             cudaMalloc(&g.erange, sizeof(unsigned long long) * 4 * np) != cudaSuccess)
             return bail(fail(BLFLS_ENOMEM, "plan: grid workspace allocation failed"));
+    }
+    if (q.backend == BLFLS_BACKEND_DT) {
+        DtParams& d = p->dt;
+        d.H = p->Hp;
+        d.W = p->Wp;
+        d.C = C;
+        d.GC = q.guide_channels;
+        d.ratio = q.sigma_s / q.sigma_r;
+        d.plane = (size_t)p->Hp * p->Wp;
+        d.pcplane = (size_t)(p->Hp + 1) * (p->Wp + 1);
+        p->dt_iters = q.dt_iterations == 0 ? 3 : q.dt_iterations;
+        const size_t per_plane = 2 * sizeof(double) * (3 * d.plane + d.pcplane);  // 2 slots
+        int np = (int)std::max<size_t>(1, (size_t)(1u << 30) / per_plane);
+        np = std::min(np, q.max_batch * C);
+        p->dt_planes = np;
+        const size_t ns = (size_t)2 * np;
+        if (cudaMalloc(&d.cth, sizeof(double) * ns * d.plane) != cudaSuccess ||
+            cudaMalloc(&d.ctv, sizeof(double) * ns * d.plane) != cudaSuccess ||
+            cudaMalloc(&d.x, sizeof(double) * ns * d.plane) != cudaSuccess ||
+            cudaMalloc(&d.pc, sizeof(double) * ns * d.pcplane) != cudaSuccess)
+            return bail(fail(BLFLS_ENOMEM, "plan: domain-transform workspace allocation failed"));
     }
 
     // workspace
@@ -1099,6 +1158,54 @@ blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t*
     CK(launch_generate(height, width, n_planes, dseeds, n_sites, noise_sigma, p_sp, out, st));
     CK(cudaFreeAsync(dseeds, st));
     CK(cudaStreamSynchronize(st));
+    return BLFLS_OK;
+}
+
+blfls_status blfls_gaussian_blur(const float* in, int channels, int height, int width, double sigma,
+                                 float* out, int device, void* stream, unsigned flags)
+{
+    // image.cpp:116-117
+    if (!(sigma > 0.0) || !std::isfinite(sigma))
+        return fail(BLFLS_EINVAL, "gaussian_blur: sigma must be positive and finite");
+    if (!in || !out || channels < 1 || height < 1 || width < 1 || in == out)
+        return fail(BLFLS_EINVAL, "gaussian_blur: bad arguments");
+    if ((size_t)std::ceil(3.0 * sigma) > (size_t)1 << 20)
+        return fail(BLFLS_EUNSUPPORTED, "gaussian_blur: sigma too large");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(BLFLS_ECUDA, "no CUDA device (this library has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(BLFLS_EINVAL, "gaussian_blur: bad device ordinal");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const std::vector<double> k = gaussian_weights(sigma);
+    const int r = (int)(k.size() / 2);
+    const size_t n = (size_t)channels * height * width;
+    const bool host = flags & BLFLS_HOST_PTRS;
+    double* dk = nullptr;
+    double* tmp = nullptr;
+    float *din = nullptr, *dout = nullptr;
+    CK(cudaMallocAsync(&dk, sizeof(double) * k.size(), st));
+    CK(cudaMallocAsync(&tmp, sizeof(double) * n, st));
+    CK(cudaMemcpyAsync(dk, k.data(), sizeof(double) * k.size(), cudaMemcpyHostToDevice, st));
+    const float* src = in;
+    float* dst = out;
+    if (host) {
+        CK(cudaMallocAsync(&din, sizeof(float) * n, st));
+        CK(cudaMallocAsync(&dout, sizeof(float) * n, st));
+        CK(cudaMemcpyAsync(din, in, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        src = din;
+        dst = dout;
+    }
+    CK(launch_gaussian_blur(src, dst, tmp, dk, r, channels, height, width,
+                            prop.multiProcessorCount, st));
+    if (host) CK(cudaMemcpyAsync(out, dout, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(dk, st));
+    CK(cudaFreeAsync(tmp, st));
+    if (din) CK(cudaFreeAsync(din, st));
+    if (dout) CK(cudaFreeAsync(dout, st));
+    if (host || (flags & BLFLS_SYNC)) CK(cudaStreamSynchronize(st));
     return BLFLS_OK;
 }
 

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "blfls_internal.cuh"
+#include "slot_common.cuh"
 
 namespace blfls {
 
@@ -48,58 +49,6 @@ constexpr double kFixedScale = 549755813888.0;  // 2^39
 __device__ __forceinline__ unsigned long long to_fixed(double v)
 {
     return (unsigned long long)__double2ll_rn(v * kFixedScale);
-}
-
-// slot -> (image b, channel c, axis a); slot = (plane0 + local plane) * 2 + axis
-struct Slot {
-    int b, c, axis;
-};
-__device__ __forceinline__ Slot slot_of(const GridParams& p, int z)
-{
-    const int gp = p.plane0 * 2 + z;
-    Slot s;
-    s.axis = gp & 1;
-    const int plane = gp >> 1;
-    s.b = plane / p.C;
-    s.c = plane - s.b * p.C;
-    return s;
-}
-
-// normalisation (lo, scale) of an image in double, image.cpp:46-60
-__device__ __forceinline__ void norm_of(const uint32_t* lohi, int b, double& lo, double& scale)
-{
-    const double l = (double)ordered_to_float(lohi[2 * b]);
-    const double h = (double)ordered_to_float(lohi[2 * b + 1]);
-    lo = l;
-    scale = h > l ? 1.0 / (h - l) : 0.0;  // constant image -> zeros
-}
-
-// ((gn[next] - gn[here]) + 1) * 0.5, every operation rounded as the reference's
-__device__ __forceinline__ double grad01(const float* img, int H, int W, int y, int x, int axis,
-                                         double lo, double scale)
-{
-    const int xn = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
-    const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
-    const double a = __dmul_rn(__dsub_rn((double)__ldg(img + (size_t)yn * W + xn), lo), scale);
-    const double b = __dmul_rn(__dsub_rn((double)__ldg(img + (size_t)y * W + x), lo), scale);
-    return __dmul_rn(__dadd_rn(__dsub_rn(a, b), 1.0), 0.5);
-}
-
-__device__ __forceinline__ void slot_images(const GridParams& p, const Slot& s, const float*& src,
-                                            const float*& gde, double& slo, double& ssc, double& glo,
-                                            double& gsc)
-{
-    const size_t plane = (size_t)p.H * p.W;
-    src = p.f + ((size_t)s.b * p.C + s.c) * plane;
-    norm_of(p.lohi, s.b, slo, ssc);
-    if (p.guide) {
-        gde = p.guide + ((size_t)s.b * p.GC + (p.GC == 1 ? 0 : s.c)) * plane;
-        norm_of(p.glohi, s.b, glo, gsc);
-    } else {
-        gde = src;
-        glo = slo;
-        gsc = ssc;
-    }
 }
 
 __global__ void k_grid_clear(GridParams p)
@@ -411,8 +360,9 @@ __global__ void k_grid_slice(GridParams p)
     }
 }
 
-cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st)
+cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st, int* launches)
 {
+    *launches = 4;  // clear, erange, splat, slice (+ blur below)
     const unsigned blocks = (unsigned)(nsm * 4);
     k_grid_clear<<<blocks * p.slots, 256, 0, st>>>(p);
     dim3 g2(blocks, p.slots);
@@ -457,6 +407,7 @@ cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st)
         cudaFuncSetAttribute(k_grid_blur3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
         dim3 gb((unsigned)(((p.gw + B - 1) / B) * ((p.gh + B - 1) / B)), p.slots);
         k_grid_blur3<<<gb, 256, bsmem, st>>>(p, B);
+        *launches += 1;
     } else {
         // y, x, range per grid; scratch: the (not yet written) blurred buffer
         // for the counts, the dead count grid for the values
@@ -467,6 +418,7 @@ cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st)
         k_grid_blur<<<g2, 256, 0, st>>>(p, p.vgrid, p.wgrid, 0, fs, 1, 0);
         k_grid_blur<<<g2, 256, 0, st>>>(p, p.wgrid, p.vgrid, 1, 0.0, 1, 0);
         k_grid_blur<<<g2, 256, 0, st>>>(p, p.vgrid, p.blurred, 2, 0.0, 2, 1);
+        *launches += 6;
     }
     k_grid_slice<<<g2, 256, 0, st>>>(p);
     return cudaGetLastError();

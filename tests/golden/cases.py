@@ -44,3 +44,24 @@ GRID_CASES = [
     dict(name="grid_rgb_56x40_joint_it2", w=56, h=40, c=3, scene="natural", seed=23,
          guide=("natural", 24, 3), sigma_s=6.0, sigma_r=0.05, lam=800.0, iters=2, pad=0),
 ]
+
+# The reference's smooth() with SmootherKind::NC_LS (nc_filter,
+# pipelines.cpp:48) and rolling_nc_ls (pipelines.cpp:96-117): the GPU
+# domain-transform backend's parity targets.  guide = None (self) or a
+# same-channel guide image like the reference requires.
+NC_CASES = [
+    dict(name="nc_gray_48x40_self", w=48, h=40, c=1, scene="natural", seed=31, guide=None,
+         sigma_s=6.0, sigma_r=0.05, dt_iters=3, lam=800.0, pad=0),
+    dict(name="nc_rgb_40x32_self_pad16", w=40, h=32, c=3, scene="natural", seed=32, guide=None,
+         sigma_s=12.0, sigma_r=0.05, dt_iters=3, lam=1024.0, pad=16),
+    dict(name="nc_rgb_36x28_joint_it2", w=36, h=28, c=3, scene="natural", seed=33,
+         guide=("natural", 34, 3), sigma_s=4.0, sigma_r=0.1, dt_iters=2, lam=600.0, pad=3),
+    dict(name="nc_gray_33x25_random", w=33, h=25, c=1, scene="random", seed=35, guide=None,
+         sigma_s=3.0, sigma_r=0.2, dt_iters=1, lam=50.0, pad=0),
+    dict(name="rolling_rgb_40x32_texture", w=40, h=32, c=3, scene="natural", seed=36, guide=None,
+         sigma_s=8.0, sigma_r=0.02, dt_iters=3, lam=1024.0, pad=16, rolling=True, n=3,
+         init_sigma=2.5),
+    dict(name="rolling_gray_32x32_clipart", w=32, h=32, c=1, scene="natural", seed=37, guide=None,
+         sigma_s=6.0, sigma_r=0.02, dt_iters=3, lam=1024.0, pad=16, rolling=True, n=2,
+         init_sigma=0.75),
+]

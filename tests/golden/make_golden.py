@@ -16,7 +16,7 @@ HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parent.parent))
 sys.path.insert(0, str(HERE))
 
-from cases import CASES, GRID_CASES  # noqa: E402
+from cases import CASES, GRID_CASES, NC_CASES  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
 
@@ -61,6 +61,26 @@ def main():
             arrays["guide"] = guide
         np.savez_compressed(HERE / f"{cs['name']}.npz", **arrays)
         print(cs["name"], f.shape, float(np.abs(f - img).max()))
+    for cs in NC_CASES:
+        img = scene(cs["scene"], cs["w"], cs["h"], cs["c"], cs["seed"]).astype(np.float32)
+        arrays = {"img": img}
+        if cs.get("rolling"):
+            out = O.ref_rolling_nc_ls(img.astype(np.float64), lam=cs["lam"], sigma_s=cs["sigma_s"],
+                                      sigma_r=cs["sigma_r"], dt_iters=cs["dt_iters"], pad=cs["pad"],
+                                      n=cs["n"], init_sigma=cs["init_sigma"])
+        else:
+            guide = None
+            if cs["guide"] is not None:
+                kind, seed, gc = cs["guide"]
+                guide = scene(kind, cs["w"], cs["h"], gc, seed).astype(np.float32)
+                arrays["guide"] = guide
+            out = O.ref_smooth_nc(img.astype(np.float64),
+                                  None if guide is None else guide.astype(np.float64),
+                                  lam=cs["lam"], sigma_s=cs["sigma_s"], sigma_r=cs["sigma_r"],
+                                  dt_iters=cs["dt_iters"], pad=cs["pad"])
+        arrays["out"] = out
+        np.savez_compressed(HERE / f"{cs['name']}.npz", **arrays)
+        print(cs["name"], out.shape, float(np.abs(out - img).max()))
 
 
 if __name__ == "__main__":

@@ -45,7 +45,7 @@ def test_python_binding_lists_all_exports():
 def test_abi_version_and_strings(lib):
     lib.blfls_abi_version.restype = ctypes.c_int
     lib.blfls_version.restype = ctypes.c_char_p
-    assert lib.blfls_abi_version() == 1
+    assert lib.blfls_abi_version() == 2
     assert b"sm_100a" in lib.blfls_version()
 
 
