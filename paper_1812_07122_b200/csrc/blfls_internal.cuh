@@ -126,6 +126,7 @@ struct DtParams {
     double* ctv;           // [slots][H][W] warped column coordinates
     double* pc;            // [slots][pcplane] prefix sums of the current pass
     double* x;             // [slots][H][W] signal between passes
+    double* g01;           // [slots][H][W] guide01 (the DT guide) of each slot
     size_t plane;          // H * W
     size_t pcplane;        // (H + 1) * (W + 1)
     int H, W, C, GC;
@@ -137,7 +138,8 @@ struct DtParams {
 
 double nc_box_radius(double sigma_s, int iter, int total);
 // returns the number of kernels launched, or -1 on a launch error
-int launch_dt_filter(const DtParams& p, int iterations, double sigma_s, cudaStream_t st);
+bool dt_configure(int iterations, double sigma_s);
+int launch_dt_filter(const DtParams& p, int iterations, double sigma_s, int nsm, cudaStream_t st);
 std::vector<double> gaussian_weights(double sigma);
 cudaError_t launch_gaussian_blur(const float* in, float* out, double* tmp, const double* k, int r,
                                  int C, int H, int W, int nsm, cudaStream_t st);

@@ -387,7 +387,7 @@ blfls_status enq_dt(blfls_plan_t p, const float* f, const float* guide, const ui
     for (int p0 = 0; p0 < planes; p0 += p->dt_planes) {
         d.plane0 = p0;
         d.slots = 2 * std::min(p->dt_planes, planes - p0);
-        const int n = launch_dt_filter(d, p->dt_iters, p->prm.sigma_s, st);
+        const int n = launch_dt_filter(d, p->dt_iters, p->prm.sigma_s, p->nsm, st);
         if (n < 0) CK(cudaGetLastError());
         p->launches += n;
     }
@@ -538,7 +538,7 @@ void free_plan(blfls_plan_t p)
     void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
                     p->rowf.tw, p->colf.tw, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
-                    p->grid.blurred, p->grid.erange, p->dt.cth, p->dt.ctv, p->dt.pc, p->dt.x};
+                    p->grid.blurred, p->grid.erange, p->dt.cth, p->dt.ctv, p->dt.pc, p->dt.x, p->dt.g01};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
@@ -732,6 +732,8 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
             return bail(fail(BLFLS_ENOMEM, "plan: grid workspace allocation failed"));
     }
     if (q.backend == BLFLS_BACKEND_DT) {
+        if (p->Hp > 65535)  // window grid rows
+            return bail(fail(BLFLS_EUNSUPPORTED, "dt backend: padded height above 65535"));
         DtParams& d = p->dt;
         d.H = p->Hp;
         d.W = p->Wp;
@@ -741,7 +743,9 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         d.plane = (size_t)p->Hp * p->Wp;
         d.pcplane = (size_t)(p->Hp + 1) * (p->Wp + 1);
         p->dt_iters = q.dt_iterations == 0 ? 3 : q.dt_iterations;
-        const size_t per_plane = 2 * sizeof(double) * (3 * d.plane + d.pcplane);  // 2 slots
+        if (!dt_configure(p->dt_iters, q.sigma_s))
+            return bail(fail(BLFLS_EUNSUPPORTED, "dt backend: sigma_s too large for the window tile"));
+        const size_t per_plane = 2 * sizeof(double) * (4 * d.plane + d.pcplane);  // 2 slots
         int np = (int)std::max<size_t>(1, (size_t)(1u << 30) / per_plane);
         np = std::min(np, q.max_batch * C);
         p->dt_planes = np;
@@ -749,6 +753,7 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         if (cudaMalloc(&d.cth, sizeof(double) * ns * d.plane) != cudaSuccess ||
             cudaMalloc(&d.ctv, sizeof(double) * ns * d.plane) != cudaSuccess ||
             cudaMalloc(&d.x, sizeof(double) * ns * d.plane) != cudaSuccess ||
+            cudaMalloc(&d.g01, sizeof(double) * ns * d.plane) != cudaSuccess ||
             cudaMalloc(&d.pc, sizeof(double) * ns * d.pcplane) != cudaSuccess)
             return bail(fail(BLFLS_ENOMEM, "plan: domain-transform workspace allocation failed"));
     }

@@ -380,7 +380,8 @@ cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st, int* 
     }
     if (TP) {
         const size_t smem = (size_t)ncx * ncx * p.gdmax * 3 * sizeof(unsigned);
-        cudaFuncSetAttribute(k_grid_splat_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_grid_splat_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         dim3 gt((unsigned)(((p.W + TP - 1) / TP) * ((p.H + TP - 1) / TP)), p.slots);
         k_grid_splat_tiled<<<gt, 256, smem, st>>>(p, lgTP, ncx, ncx);
     } else {
@@ -404,7 +405,8 @@ cudaError_t launch_grid_blf(const GridParams& p, int nsm, cudaStream_t st, int* 
         }
     }
     if (B) {
-        cudaFuncSetAttribute(k_grid_blur3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+        if (bsmem > 48 * 1024)
+            cudaFuncSetAttribute(k_grid_blur3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
         dim3 gb((unsigned)(((p.gw + B - 1) / B) * ((p.gh + B - 1) / B)), p.slots);
         k_grid_blur3<<<gb, 256, bsmem, st>>>(p, B);
         *launches += 1;
