@@ -76,6 +76,35 @@ int main()
         threw = true;
     }
     EXPECT(threw);
+    {
+        // NC_LS keeps constants (test_pipelines.cpp:33-38) and rolling keeps them too
+        // (test_pipelines.cpp:113-118); bad DtParams / RollingParams throw
+        blfls::SmootherSpec s3;
+        s3.kind = blfls::SmootherKind::NC_LS;
+        s3.dt = {6.0, 0.05, 3};
+        blfls::Image u3 = blfls::smooth(c, s3);
+        double m3 = 0.0;
+        for (std::size_t i = 0; i < u3.size(); ++i) m3 = std::fmax(m3, std::fabs(u3.data()[i] - 0.55));
+        EXPECT(m3 < 1e-6);
+        blfls::Image cst(24, 24, 1, 0.8);
+        blfls::Image r3 = blfls::rolling_nc_ls(cst, {8.0, 0.02, 3}, {}, {2, 2.5});
+        double m4 = 0.0;
+        for (std::size_t i = 0; i < r3.size(); ++i) m4 = std::fmax(m4, std::fabs(r3.data()[i] - 0.8));
+        EXPECT(m4 < 1e-6);
+        bool t1 = false, t2 = false;
+        try {
+            blfls::rolling_nc_ls(cst, {8.0, 0.02, 3}, {}, {0, 2.5});
+        } catch (const std::invalid_argument&) {
+            t1 = true;
+        }
+        try {
+            blfls::gaussian_blur(cst, -1.0);
+        } catch (const std::invalid_argument&) {
+            t2 = true;
+        }
+        EXPECT(t1);
+        EXPECT(t2);
+    }
     if (fails == 0) std::printf("OK\n");
     return fails == 0 ? 0 : 1;
 }

@@ -57,6 +57,10 @@ def test_usage_errors_exit_2(cli, tmp_path):
     assert run(cli, "smooth", "--sigma-s", "-1", "in.pfm", "out.pfm").returncode == 2
     assert run(cli, "smooth", "--pad", "-1", "in.pfm", "out.pfm").returncode == 2
     assert run(cli, "joint", "in.pfm", "out.pfm").returncode == 2  # --guide required
+    assert run(cli, "smooth", "--method", "nc-ls", "--iterations", "0", "in.pfm", "o.pfm").returncode == 2
+    assert run(cli, "texture", "--n", "0", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "clipart", "--init-sigma", "-1", "in.pfm", "out.pfm").returncode == 2
+    assert run(cli, "texture", "--method", "ls", "in.pfm", "out.pfm").returncode == 2  # no --method
 
 
 def test_unreadable_input_exits_1(cli, tmp_path):
@@ -137,3 +141,33 @@ def test_grid_backend_reproduces_reference_cli_defaults(gpu, cli, oracle, tmp_pa
     ref = oracle.ref_smooth_grid(img.astype(np.float64), lam=1024.0, sigma_s=12.0, sigma_r=0.04,
                                  pad=16)
     assert np.abs(read_pfm(tmp_path / "o.pfm") - ref).max() <= 1e-4
+
+
+@pytest.mark.gpu
+def test_nc_ls_method(gpu, cli, oracle, tmp_path):
+    """`smooth --method nc-ls` = smooth() with SmootherKind::NC_LS (make_spec,
+    epls_main.cpp:48-63): DtParams{sigma_s, sigma_r, --iterations}."""
+    img = np.stack([oracle.gen_plane(930 + c, 44, 52, n_sites=12) for c in range(3)])
+    write_pfm(tmp_path / "in.pfm", img)
+    r = run(cli, "smooth", "--method", "nc-ls", "--sigma-s", "6", "--sigma-r", "0.05",
+            "--iterations", "2", "--lambda", "700", tmp_path / "in.pfm", tmp_path / "o.pfm")
+    assert r.returncode == 0, r.stderr
+    ref = oracle.smooth_nc(img.astype(np.float64), lam=700.0, sigma_s=6.0, sigma_r=0.05, dt_iters=2,
+                           pad=16)
+    assert np.abs(read_pfm(tmp_path / "o.pfm") - ref).max() <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cmd,ss,sr,n,s0", [("texture", 8.0, 0.02, 3, 2.5),
+                                            ("clipart", 6.0, 0.02, 2, 0.75)])
+def test_rolling_subcommands_use_reference_defaults(gpu, cli, oracle, tmp_path, cmd, ss, sr, n, s0):
+    """`texture` / `clipart` with no flags = texture_removal / clipart_cleanup
+    with the reference CLI's preparse defaults (epls_main.cpp:181-192)."""
+    img = np.stack([oracle.gen_plane(960 + c, 40, 48, n_sites=12) for c in range(3)])
+    write_pfm(tmp_path / "in.pfm", img)
+    r = run(cli, cmd, tmp_path / "in.pfm", tmp_path / "o.pfm")
+    assert r.returncode == 0, r.stderr
+    ref = oracle.rolling_nc_ls(img.astype(np.float64), lam=1024.0, sigma_s=ss, sigma_r=sr,
+                               dt_iters=3, pad=16, n=n, init_sigma=s0)
+    d = np.abs(read_pfm(tmp_path / "o.pfm") - ref)
+    assert d.max() <= 5e-3 and d.mean() <= 5e-5

@@ -1,9 +1,17 @@
 // blfls_cli.cpp -- command-line front end over the C ABI, mirroring the
 // reference CLI's hot-path subcommands (/root/reference/proj/tools/epls_main.cpp):
 //
-//   blfls smooth [--method blf-ls|ls] [--sigma-s S] [--sigma-r R] [--lambda L]
-//                [--pad 16] [--radius r] [--iters k] [--device d] input output
+//   blfls smooth [--method blf-ls|nc-ls|ls] [--sigma-s S] [--sigma-r R] [--lambda L]
+//                [--pad 16] [--radius r] [--iters k] [--iterations t] [--device d] input output
 //   blfls joint  --guide G [same flags] input output
+//   blfls texture|clipart [--sigma-s S] [--sigma-r R] [--lambda L] [--n N]
+//                [--init-sigma s] [--pad 16] [--device d] input output
+//
+// texture / clipart are rolling-guidance NC-LS (texture_removal /
+// clipart_cleanup, applications.cpp:66-76) with the reference's preparse
+// defaults (texture 8 / 0.02, n 3, init 2.5; clipart 6 / 0.02, n 2, init 0.75).
+// --method nc-ls filters the gradients with nc_filter, DtParams{sigma_s,
+// sigma_r, --iterations (default 3)}.
 //
 // Defaults follow epls_main.cpp: sigma_s 12, sigma_r 0.04 (joint: 12 / 0.003,
 // its preparse defaults), lambda 1024.  Differences: the bilateral stage is
@@ -178,8 +186,9 @@ void save_image(const std::string& path, const blfls::Image& img)
 
 struct Options {
     std::string cmd, input, output, guide, method = "blf-ls";
-    double sigma_s = 12.0, sigma_r = 0.04, lambda = -1.0;
+    double sigma_s = 12.0, sigma_r = 0.04, lambda = -1.0, init_sigma = 2.5;
     int pad = 16, radius = -1, iters = 1, device = 0, backend = BLFLS_BACKEND_BRUTE;
+    int iterations = 3, n = 3;
 };
 
 double parse_double(const std::string& flag, const char* v)
@@ -200,13 +209,25 @@ int parse_int(const std::string& flag, const char* v)
 
 Options parse(int argc, char** argv)
 {
-    if (argc < 2) throw UsageError("a subcommand is required: smooth | joint");
+    if (argc < 2) throw UsageError("a subcommand is required: smooth | joint | texture | clipart");
     Options o;
     o.cmd = argv[1];
-    if (o.cmd != "smooth" && o.cmd != "joint") throw UsageError("unknown subcommand '" + o.cmd + "'");
+    if (o.cmd != "smooth" && o.cmd != "joint" && o.cmd != "texture" && o.cmd != "clipart")
+        throw UsageError("unknown subcommand '" + o.cmd + "'");
+    const bool rolling = o.cmd == "texture" || o.cmd == "clipart";
     if (o.cmd == "joint") {  // epls_main.cpp preparse defaults of `joint`
         o.sigma_s = 12.0;
         o.sigma_r = 0.003;
+    } else if (o.cmd == "texture") {  // ... of `texture`
+        o.sigma_s = 8.0;
+        o.sigma_r = 0.02;
+        o.n = 3;
+        o.init_sigma = 2.5;
+    } else if (o.cmd == "clipart") {  // ... of `clipart`
+        o.sigma_s = 6.0;
+        o.sigma_r = 0.02;
+        o.n = 2;
+        o.init_sigma = 0.75;
     }
     std::vector<std::string> pos;
     for (int i = 2; i < argc; ++i) {
@@ -215,10 +236,10 @@ Options parse(int argc, char** argv)
             if (i + 1 >= argc) throw UsageError(a + " needs a value");
             return argv[++i];
         };
-        if (a == "--method") {
+        if (a == "--method" && !rolling) {
             o.method = next();
-            if (o.method != "blf-ls" && o.method != "ls")
-                throw UsageError("--method: GPU build supports blf-ls and ls, got '" + o.method + "'");
+            if (o.method != "blf-ls" && o.method != "nc-ls" && o.method != "ls")
+                throw UsageError("--method: GPU build supports blf-ls, nc-ls and ls, got '" + o.method + "'");
         } else if (a == "--sigma-s") {
             o.sigma_s = parse_double(a, next());
             if (!(o.sigma_s > 0)) throw UsageError("--sigma-s must be positive");
@@ -235,8 +256,15 @@ Options parse(int argc, char** argv)
         } else if (a == "--iters") {
             o.iters = parse_int(a, next());
             if (o.iters < 1) throw UsageError("--iters must be >= 1");
-        } else if (a == "--iterations") {
-            next();  // domain-transform pass count of the reference; no effect on blf-ls
+        } else if (a == "--iterations" && !rolling) {
+            o.iterations = parse_int(a, next());  // DtParams::iterations (nc-ls)
+            if (o.iterations < 1) throw UsageError("--iterations must be positive");
+        } else if (a == "--n" && rolling) {
+            o.n = parse_int(a, next());
+            if (o.n < 1) throw UsageError("--n must be positive");
+        } else if (a == "--init-sigma" && rolling) {
+            o.init_sigma = parse_double(a, next());
+            if (!(o.init_sigma > 0)) throw UsageError("--init-sigma must be positive");
         } else if (a == "--blf") {
             const std::string b = next();
             if (b == "grid") o.backend = BLFLS_BACKEND_GRID;
@@ -265,8 +293,19 @@ int run(const Options& o)
 {
     const blfls::Image in = load_image(o.input);
     const double lam = o.lambda >= 0.0 ? o.lambda : 1024.0;
+    const blfls::DtParams dt{o.sigma_s, o.sigma_r, o.iterations};
     blfls::Image out;
-    if (o.method == "ls") {
+    if (o.cmd == "texture" || o.cmd == "clipart") {
+        out = blfls::rolling_nc_ls(in, dt, blfls::SolveParams{lam, o.pad},
+                                   blfls::RollingParams{o.n, o.init_sigma}, o.device);
+    } else if (o.method == "nc-ls") {
+        blfls::Image guide;
+        if (o.cmd == "joint") {
+            guide = load_image(o.guide);
+            if (!guide.same_shape(in)) throw std::invalid_argument("flash_no_flash: image shapes differ");
+        }
+        out = blfls::nc_ls(in, o.cmd == "joint" ? &guide : nullptr, lam, dt, o.iters, o.device, o.pad);
+    } else if (o.method == "ls") {
         blfls::Image zero(in.width(), in.height(), in.channels(), 0.0);
         // plain LS == lsgrad with a zero target (test_solver.cpp:129-134); the
         // reference normalises first (pipelines.cpp:64-68), a no-op for this
