@@ -34,6 +34,77 @@ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2
 __device__ __forceinline__ float2 cmuli(float2 a, float sg) { return make_float2(-sg * a.y, sg * a.x); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
+// Compile-time cos / sin of 2 pi m / P (Taylor series in double; the
+// arguments are reduced to [0, pi]) for the odd-prime radices of the
+// compile-time engine: they become FFMA immediates, not table loads.
+constexpr double ct_pi = 3.14159265358979323846;
+constexpr double ct_taylor_sin(double x)
+{
+    double term = x, sum = x;
+    for (int k = 1; k < 30; ++k) {
+        term *= -x * x / ((2.0 * k) * (2.0 * k + 1.0));
+        sum += term;
+    }
+    return sum;
+}
+constexpr double ct_taylor_cos(double x)
+{
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 30; ++k) {
+        term *= -x * x / ((2.0 * k - 1.0) * (2.0 * k));
+        sum += term;
+    }
+    return sum;
+}
+template <int P>
+struct DftConst {
+    float c[P], s[P];  // cos, sin of 2 pi m / P
+    constexpr DftConst() : c(), s()
+    {
+        for (int m = 0; m < P; ++m) {
+            c[m] = (float)ct_taylor_cos(2.0 * ct_pi * m / P);
+            s[m] = (float)ct_taylor_sin(2.0 * ct_pi * m / P);
+        }
+    }
+};
+
+// Direct DFT of odd prime length P (7, 11, 13, 17) with the conjugate-pair
+// symmetry: s_r = a_r + a_{P-r}, d_r = a_r - a_{P-r} (r = 1..h, h = (P-1)/2);
+// A_t = a_0 + sum_r s_r cos(2 pi rt/P), B_t = sum_r d_r sin(2 pi rt/P);
+// y_t = A_t + i sg B_t, y_{P-t} = A_t - i sg B_t: 4 h^2 real FMAs per P outputs.
+template <int P>
+__device__ __forceinline__ void dft_prime(float2 (&a)[P], float sg)
+{
+    constexpr int h = (P - 1) / 2;
+    constexpr DftConst<P> K{};
+    float2 sr[h + 1], dr[h + 1];
+    float2 y0 = a[0];
+#pragma unroll
+    for (int r = 1; r <= h; ++r) {
+        sr[r] = cadd(a[r], a[P - r]);
+        dr[r] = csub(a[r], a[P - r]);
+        y0 = cadd(y0, sr[r]);
+    }
+    float2 out[P];
+    out[0] = y0;
+#pragma unroll
+    for (int t = 1; t <= h; ++t) {
+        float2 A = a[0], B = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 1; r <= h; ++r) {
+            const int m = (r * t) % P;
+            const float c = K.c[m], sn = K.s[m];  // cos / sin of 2 pi m / P (sin odd in m)
+            A = make_float2(fmaf(sr[r].x, c, A.x), fmaf(sr[r].y, c, A.y));
+            B = make_float2(fmaf(dr[r].x, sn, B.x), fmaf(dr[r].y, sn, B.y));
+        }
+        const float2 jb = cmuli(B, sg);
+        out[t] = cadd(A, jb);
+        out[P - t] = csub(A, jb);
+    }
+#pragma unroll
+    for (int t = 0; t < P; ++t) a[t] = out[t];
+}
+
 template <int P>
 __device__ __forceinline__ void dft_small(float2 (&a)[P], float sg /* -1 fwd, +1 inv */)
 {
@@ -91,6 +162,8 @@ __device__ __forceinline__ void dft_small(float2 (&a)[P], float sg /* -1 fwd, +1
         a[4] = csub(m1, j1);
         a[2] = cadd(m2, j2);
         a[3] = csub(m2, j2);
+    } else {
+        dft_prime<P>(a, sg);
     }
 }
 
@@ -257,12 +330,14 @@ __device__ void fft_run(float2* buf, const FftDesc& d, int V, int log2V, bool in
 namespace blfls {
 
 constexpr int ct_count(int n, int p) { return n % p == 0 ? 1 + ct_count(n / p, p) : 0; }
-// power-of-two part as radix 8s, then one 4 or 2; then 3s, then 5s
+// power-of-two part as radix 8s, then one 4 or 2; then 3s, 5s, and the odd
+// primes 7, 11, 13, 17 (reflect-padded sizes, e.g. 1056 = 2^5 3 11)
 constexpr int ct_n8(int n) { return ct_count(n, 2) / 3; }
 constexpr int ct_rest(int n) { return ct_count(n, 2) % 3; }  // 0, 1 (radix 2) or 2 (radix 4)
 constexpr int ct_nstages(int n)
 {
-    return ct_n8(n) + (ct_rest(n) ? 1 : 0) + ct_count(n, 3) + ct_count(n, 5);
+    return ct_n8(n) + (ct_rest(n) ? 1 : 0) + ct_count(n, 3) + ct_count(n, 5) + ct_count(n, 7) +
+           ct_count(n, 11) + ct_count(n, 13) + ct_count(n, 17);
 }
 constexpr int ct_radix(int n, int i)
 {
@@ -272,8 +347,11 @@ constexpr int ct_radix(int n, int i)
         if (i == 0) return ct_rest(n) == 2 ? 4 : 2;
         i -= 1;
     }
-    if (i < ct_count(n, 3)) return 3;
-    return 5;
+    for (int p : {3, 5, 7, 11, 13, 17}) {
+        if (i < ct_count(n, p)) return p;
+        i -= ct_count(n, p);
+    }
+    return 1;
 }
 constexpr int ct_stride(int n, int i)
 {
@@ -284,7 +362,7 @@ constexpr int ct_stride(int n, int i)
 constexpr bool ct_supported(int n)
 {
     int m = n;
-    for (int p : {2, 3, 5})
+    for (int p : {2, 3, 5, 7, 11, 13, 17})
         while (m % p == 0) m /= p;
     return m == 1;
 }

@@ -453,9 +453,15 @@ static void launch_pass(int which, const SolveParams& p, const F& f, int V, int 
 // V*8 >= 32-byte row segments, H in {512, 1024, 1080, 2048, 4096}.  Narrow
 // variants (small V) keep small images from running a handful of CTAs.
 #define BLFLS_CT_ROWS(X) X(256, 8, 32) X(256, 2, 32) X(512, 4, 64) X(512, 1, 64) X(960, 2, 128) \
-    X(1024, 2, 128) X(2048, 1, 256)
+    X(1024, 2, 128) X(2048, 1, 256) BLFLS_CT_ROWS_PAD16(X)
 #define BLFLS_CT_COLS(X) X(512, 16, 32) X(512, 2, 64) X(1024, 8, 64) X(1024, 2, 128) \
-    X(1080, 4, 128) X(2048, 4, 128) X(4096, 4, 256)
+    X(1080, 4, 128) X(2048, 4, 128) X(4096, 4, 256) BLFLS_CT_COLS_PAD16(X)
+// the reference's default reflect padding (pad 16) of the power-of-two
+// BASELINE sizes: 544 = 2^5 17, 1056 = 2^5 3 11, 2080 = 2^5 5 13 (rows: half)
+#define BLFLS_CT_ROWS_PAD16(X) X(272, 8, 32) X(272, 2, 32) X(528, 4, 64) X(528, 1, 64) \
+    X(1040, 2, 128) X(1040, 1, 128)
+#define BLFLS_CT_COLS_PAD16(X) X(544, 16, 32) X(544, 2, 64) X(1056, 8, 64) X(1056, 2, 128) \
+    X(2080, 4, 128)
 
 // Largest-V geometry that still launches >= 2 CTAs per SM for `planes`
 // planes; otherwise the narrowest one.

@@ -129,7 +129,10 @@ def test_solve_fixed_point_and_identity(gpu, oracle):
     assert maxabs(gpu.ls_solve_fft(g, gpu.SolveParams(0.0, 0)), g) <= 1e-6
 
 
-@pytest.mark.parametrize("h,w", [(32, 32), (54, 96), (13, 9), (30, 18), (120, 1920 // 8)])
+@pytest.mark.parametrize("h,w", [(32, 32), (54, 96), (13, 9), (30, 18), (120, 1920 // 8),
+                                 # compile-time engine with the odd-prime radices of the
+                                 # pad-16 sizes: rows 272 / 528 / 1040, columns 544 / 1056 / 2080
+                                 (544, 544), (1056, 1056), (2080, 96), (64, 2080)])
 def test_rfft2_roundtrip_vs_numpy(gpu, h, w):
     rng = np.random.default_rng(h * w)
     x = rng.random((1, h, w)).astype(np.float32)
@@ -451,3 +454,25 @@ def test_grid_backend_is_deterministic(gpu, oracle):
                              backend="grid")
     a, b = gpu.smooth(img, spec2), gpu.smooth(img, spec2)
     assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("h,w", [(1056, 1056), (544, 544), (2080, 96), (64, 2080)])
+def test_solve_prime_radix_sizes_vs_oracle(gpu, oracle, h, w):
+    """The FFT solve on the compile-time geometries with radix 11 / 17 / 13
+    stages (the reference-default pad-16 grids of the BASELINE sizes)."""
+    rng = np.random.default_rng(h + w)
+    g = rng.random((1, h, w)).astype(np.float32)
+    tx, ty = rng.uniform(-0.2, 0.2, (2, 1, h, w)).astype(np.float32)
+    u = gpu.lsgrad_solve_fft(g, (tx, ty), gpu.SolveParams(1000.0, 0))
+    ref = oracle.lsgrad_solve_fft(g, tx, ty, lam=1000.0)
+    assert maxabs(u, ref) <= TOL_SOLVE * 10.0
+
+
+def test_c2_reference_default_padding_vs_oracle(gpu, oracle):
+    """c2's image at the reference default pad 16 (1056 x 1056 grid: radix-11
+    rows and columns), one BLF-LS iteration against the oracle."""
+    img = np.stack([oracle.gen_plane(2000 + c, 1024, 1024, n_sites=12) for c in range(3)])
+    out = gpu.blf_ls(img, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=1, radius=7, pad=16)
+    ref = oracle.blf_ls(img.astype(np.float64), lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=1,
+                        radius=7, pad=16)
+    assert maxabs(out, ref) <= TOL_OUT
