@@ -267,30 +267,52 @@ __device__ void fft_stage_generic(float2* buf, const FftLane& l, int n, int V, i
 }
 
 // Direct DFT stage for primes above 13 (reflect-padded sizes such as
-// 1952 = 2^5 * 61 or 1112 = 2^3 * 139): every output sums its p inputs from
-// shared memory (p complex MACs per element) into `scratch`, then the stage
-// result is copied back.  Only sizes with such a factor take this path.
+// 1952 = 2^5 * 61 or 1112 = 2^3 * 139).  The P outputs t of a butterfly group
+// (k, q) share the P inputs a_r, so a work item is a group and a block of
+// kDirT consecutive t: every input is read from shared memory once per block
+// and the roots w^{r t} of the block come from one table load w^{r t0} and
+// the step w^r (kDirT - 1 complex products: no long recurrences).  Results go
+// to `scratch`, then the stage is copied back.  Only sizes with such a factor
+// take this path.
+constexpr int kDirT = 8;
 template <bool COLS>
 __device__ void fft_stage_direct(float2* buf, float2* scratch, const FftLane& l, int n, int V, int s,
                                  int P, const float2* __restrict__ tw, bool inv)
 {
     const int nbp = n / P;
-    for (int o = l.t; o < n; o += l.TV) {
-        const int k = o % s, rest = o / s;
-        const int t = rest % P, q = rest / P;
-        const int bb = q * s + k;
-        float2 acc = make_float2(0.f, 0.f);
-        int e = 0;  // (r * t) mod P
+    const int nblk = (P + kDirT - 1) / kDirT;
+    for (int item = l.t; item < nbp * nblk; item += l.TV) {
+        const int bb = item / nblk, t0 = (item - bb * nblk) * kDirT;
+        const int q = bb / s, k = bb - q * s;
+        float2 acc[kDirT];
+#pragma unroll
+        for (int j = 0; j < kDirT; ++j) acc[j] = make_float2(0.f, 0.f);
+        int e0 = 0;  // (r * t0) mod P
         for (int r = 0; r < P; ++r) {
-            float2 w = __ldg(&tw[e * nbp]);
-            if (inv) w.y = -w.y;
-            acc = cadd(acc, cmul(buf[fft_addr<COLS>(l, bb + r * nbp, n, V)], w));
-            e += t;
-            if (e >= P) e -= P;
+            const float2 a = buf[fft_addr<COLS>(l, bb + r * nbp, n, V)];
+            float2 w = __ldg(&tw[e0 * nbp]);
+            float2 w1 = __ldg(&tw[r * nbp]);  // w_P^r
+            if (inv) {
+                w.y = -w.y;
+                w1.y = -w1.y;
+            }
+#pragma unroll
+            for (int j = 0; j < kDirT; ++j) {
+                acc[j] = cadd(acc[j], cmul(a, w));
+                w = cmul(w, w1);
+            }
+            e0 += t0;
+            while (e0 >= P) e0 -= P;
         }
-        float2 w2 = __ldg(&tw[q * t * s]);
-        if (inv) w2.y = -w2.y;
-        scratch[fft_addr<COLS>(l, o, n, V)] = cmul(acc, w2);
+#pragma unroll
+        for (int j = 0; j < kDirT; ++j) {
+            const int t = t0 + j;
+            if (t < P) {
+                float2 w2 = __ldg(&tw[q * t * s]);
+                if (inv) w2.y = -w2.y;
+                scratch[fft_addr<COLS>(l, k + s * (P * q + t), n, V)] = cmul(acc[j], w2);
+            }
+        }
     }
     __syncthreads();
     for (int o = l.t; o < n; o += l.TV) buf[fft_addr<COLS>(l, o, n, V)] = scratch[fft_addr<COLS>(l, o, n, V)];

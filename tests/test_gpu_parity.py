@@ -456,7 +456,9 @@ def test_grid_backend_is_deterministic(gpu, oracle):
     assert a.tobytes() == b.tobytes()
 
 
-@pytest.mark.parametrize("h,w", [(1056, 1056), (544, 544), (2080, 96), (64, 2080)])
+@pytest.mark.parametrize("h,w", [(1056, 1056), (544, 544), (2080, 96), (64, 2080),
+                                 # runtime engine, blocked direct-DFT stages: c3 / c4 at pad 16
+                                 (1112, 1952), (4128, 64)])
 def test_solve_prime_radix_sizes_vs_oracle(gpu, oracle, h, w):
     """The FFT solve on the compile-time geometries with radix 11 / 17 / 13
     stages (the reference-default pad-16 grids of the BASELINE sizes)."""
