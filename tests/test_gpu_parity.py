@@ -478,3 +478,19 @@ def test_c2_reference_default_padding_vs_oracle(gpu, oracle):
     ref = oracle.blf_ls(img.astype(np.float64), lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=1,
                         radius=7, pad=16)
     assert maxabs(out, ref) <= TOL_OUT
+
+
+def test_grid_backend_batch_gray_guide_vs_reference(gpu, oracle):
+    """Grid backend, batch of 2 RGB images with one shared grayscale guide each
+    (replicated to the reference's per-channel guide), pad 4, two cascade steps."""
+    if not oracle.REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    imgs = np.stack([_img(oracle, 3, 40, 56, 500 + b) for b in range(2)]).astype(np.float32)
+    gds = np.stack([_img(oracle, 1, 40, 56, 600 + b) for b in range(2)]).astype(np.float32)
+    out = gpu.blf_ls(imgs, gds, lam=700.0, sigma_s=4.0, sigma_r=0.06, iters=2, pad=4, backend="grid")
+    for b in range(2):
+        f = imgs[b].astype(np.float64)
+        g3 = np.repeat(gds[b].astype(np.float64), 3, axis=0)
+        for _ in range(2):
+            f = oracle.ref_smooth_grid(f, g3, lam=700.0, sigma_s=4.0, sigma_r=0.06, pad=4)
+        assert maxabs(out[b], f) <= TOL_OUT

@@ -234,3 +234,28 @@ def test_rolling_nc_ls(gpu, oracle):
                                         gpu.RollingParams(n, 2.5)), cst) < 1e-6
     with pytest.raises(gpu.InvalidArgument):
         gpu.rolling_nc_ls(cst, dt, sp, gpu.RollingParams(0, 2.5))
+
+
+@pytest.mark.gpu
+def test_dt_batch_rgb_guide_odd_pad(gpu, oracle):
+    """Batched NC-LS with a per-channel RGB guide (mode 1), odd sizes and
+    reflect padding: every image of the batch matches its own oracle run."""
+    imgs = np.stack([_img(oracle, 3, 37, 53, 300 + b) for b in range(2)]).astype(np.float32)
+    gds = np.stack([_img(oracle, 3, 37, 53, 400 + b) for b in range(2)]).astype(np.float32)
+    out = gpu.nc_ls(imgs, gds, lam=600.0, sigma_s=5.0, sigma_r=0.05, dt_iterations=2, iters=2, pad=5)
+    for b in range(2):
+        ref = oracle.nc_ls(imgs[b].astype(np.float64), gds[b].astype(np.float64), lam=600.0,
+                           sigma_s=5.0, sigma_r=0.05, dt_iters=2, iters=2, pad=5)
+        assert maxabs(out[b], ref) <= TOL_OUT
+
+
+@pytest.mark.gpu
+def test_dt_gray_guide_shared_by_rgb(gpu, oracle):
+    """One grayscale guide for an RGB image: replicated per channel exactly as
+    the oracle's cascade does (the reference requires equal channel counts)."""
+    img = _img(oracle, 3, 48, 40, 310)
+    gd = _img(oracle, 1, 48, 40, 311)
+    out = gpu.nc_ls(img, gd, lam=800.0, sigma_s=6.0, sigma_r=0.04)
+    ref = oracle.nc_ls(img.astype(np.float64), gd.astype(np.float64), lam=800.0, sigma_s=6.0,
+                       sigma_r=0.04)
+    assert maxabs(out, ref) <= TOL_OUT
