@@ -105,9 +105,11 @@ def band_blf_ls(f0, guide, iters: int, *, filter_rows: Callable, solve: Callable
 
 
 def batch_blf_ls(images, guides, *, lam, sigma_s, sigma_r, iters, radius, group=None,
-                 gather=False):
+                 gather=False, **kw):
     """Batch-sharded BLF-LS: rank r smooths images[i0:i1] of the full batch
-    (every rank passes the same full batch, or only needs its shard)."""
+    (every rank passes the same full batch, or only needs its shard).  Extra
+    keywords go to ``blf_ls`` (``pad``, ``backend="grid"|"dt"``,
+    ``dt_iterations``): images are independent under every gradient filter."""
     import torch
     import torch.distributed as dist
 
@@ -116,7 +118,7 @@ def batch_blf_ls(images, guides, *, lam, sigma_s, sigma_r, iters, radius, group=
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     i0, i1 = batch_shard(images.shape[0], world, rank)
     out = blf_ls(images[i0:i1], None if guides is None else guides[i0:i1], lam=lam,
-                 sigma_s=sigma_s, sigma_r=sigma_r, iters=iters, radius=radius)
+                 sigma_s=sigma_s, sigma_r=sigma_r, iters=iters, radius=radius, **kw)
     if not gather or world == 1:
         return out, (i0, i1)
     per = math.ceil(images.shape[0] / world)

@@ -149,3 +149,40 @@ def test_batch_sharding_world2(oracle):
     for i in range(3):
         ref = oracle.blf_ls(imgs[i], iters=1, **PRM)
         assert np.abs(res[0][i] - ref).max() == 0.0
+
+
+def _batch_api_worker(rank, world, port, imgs, q):
+    """Runs the real multigpu.batch_blf_ls host path (shard, all_gather over
+    gloo, reassembly); the per-shard device call is replaced by the oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_1812_07122_b200 import blfls
+        from paper_1812_07122_b200.multigpu import batch_blf_ls
+
+        def fake_blf_ls(images, guides, *, lam, sigma_s, sigma_r, iters, radius, backend="brute",
+                        dt_iterations=0, pad=0):
+            assert backend == "dt" and dt_iterations == 2 and guides is None
+            outs = [O.nc_ls(images[i].numpy(), lam=lam, sigma_s=sigma_s, sigma_r=sigma_r,
+                            dt_iters=dt_iterations, iters=iters, pad=pad)
+                    for i in range(images.shape[0])]
+            return torch.from_numpy(np.stack(outs))
+
+        blfls.blf_ls = fake_blf_ls
+        out, span = batch_blf_ls(torch.from_numpy(imgs), None, lam=500.0, sigma_s=3.0, sigma_r=0.1,
+                                 iters=1, radius=0, gather=True, backend="dt", dt_iterations=2, pad=2)
+        assert span == (0, imgs.shape[0])
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_blf_ls_api_world2_dt_backend(oracle):
+    rng = np.random.default_rng(9)
+    imgs = rng.random((3, 1, 18, 22))
+    res = _run(2, _batch_api_worker, imgs)
+    for r in range(2):
+        for i in range(3):
+            ref = oracle.nc_ls(imgs[i], lam=500.0, sigma_s=3.0, sigma_r=0.1, dt_iters=2, pad=2)
+            assert np.abs(res[r][i] - ref).max() == 0.0
