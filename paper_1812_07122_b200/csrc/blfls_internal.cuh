@@ -64,6 +64,7 @@ struct FftGeom {
     int E;         // complex values per thread across a stage barrier (8 or 16)
     bool generic;  // a radix other than 2/3/4/5 occurs
     bool direct;   // a prime factor above 13 (direct DFT stage, 2x shared memory)
+    int pmax;      // largest prime factor (root table of the direct stage)
     bool ct;       // a compile-time specialised engine exists for (n, V, threads)
 };
 

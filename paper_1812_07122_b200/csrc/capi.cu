@@ -106,9 +106,11 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
 {
     if (!factorize(n, radix)) return false;
     bool generic = false, direct = false;
+    int pmax = 1;
     for (int p : radix) {
         generic |= p > 5;
         direct |= p > 13;
+        pmax = std::max(pmax, p);
     }
     int cv = 0, ct = 0;
     if (!odd && ct_geometry(cols, n, nvec, planes, nsm, &cv, &ct)) {
@@ -124,7 +126,8 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
         return true;
     }
     for (int V = Vmax; V >= 1; V >>= 1) {
-        if ((size_t)V * n * 8 * (direct ? 2 : 1) > smem_cap) continue;
+        // direct stages: strip + scratch copy + root table of the largest prime
+        if ((size_t)V * n * 8 * (direct ? 2 : 1) + (direct ? (size_t)pmax * 8 : 0) > smem_cap) continue;
         for (int E : {8, 16}) {
             int tv = threads_per_vector(radix, n, E);
             // whole warps per CTA: the block reductions shuffle over full warps
@@ -138,6 +141,7 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
             g.E = E;
             g.generic = generic;
             g.direct = direct;
+            g.pmax = pmax;
             g.ct = false;
             return true;
         }

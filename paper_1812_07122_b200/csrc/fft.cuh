@@ -267,50 +267,82 @@ __device__ void fft_stage_generic(float2* buf, const FftLane& l, int n, int V, i
 }
 
 // Direct DFT stage for primes above 13 (reflect-padded sizes such as
-// 1952 = 2^5 * 61 or 1112 = 2^3 * 139).  The P outputs t of a butterfly group
-// (k, q) share the P inputs a_r, so a work item is a group and a block of
-// kDirT consecutive t: every input is read from shared memory once per block
-// and the roots w^{r t} of the block come from one table load w^{r t0} and
-// the step w^r (kDirT - 1 complex products: no long recurrences).  Results go
-// to `scratch`, then the stage is copied back.  Only sizes with such a factor
-// take this path.
-constexpr int kDirT = 8;
+// 1952 = 2^5 * 61 or 1112 = 2^3 * 139): a batched P x P matrix product
+// y[t][g] = sum_r w^{(r t) mod P} a[r][g] over the V * n / P butterfly
+// groups g of the CTA.  Register tiling: a work item is kDirG groups x kDirT
+// outputs t; per r it loads kDirG inputs and kDirT roots (a shared table of
+// the P roots, indices advanced incrementally) for kDirG * kDirT complex
+// MACs.  The outer twiddle and the Stockham placement are applied on the way
+// to `scratch`; the stage is then copied back.  The root table sits after
+// the scratch buffer (RtFft::smem_bytes).
+constexpr int kDirT = 4;  // outputs t per item
+constexpr int kDirG = 4;  // groups per item
 template <bool COLS>
 __device__ void fft_stage_direct(float2* buf, float2* scratch, const FftLane& l, int n, int V, int s,
                                  int P, const float2* __restrict__ tw, bool inv)
 {
     const int nbp = n / P;
-    const int nblk = (P + kDirT - 1) / kDirT;
-    for (int item = l.t; item < nbp * nblk; item += l.TV) {
-        const int bb = item / nblk, t0 = (item - bb * nblk) * kDirT;
-        const int q = bb / s, k = bb - q * s;
-        float2 acc[kDirT];
+    float2* roots = scratch + (size_t)V * n;  // [P]
+    for (int m = threadIdx.x; m < P; m += blockDim.x) {
+        float2 w = __ldg(&tw[m * nbp]);  // w_P^m
+        if (inv) w.y = -w.y;
+        roots[m] = w;
+    }
+    __syncthreads();
+    const int groups = V * nbp;  // g -> (vector g / nbp, butterfly g % nbp)
+    const int ngb = (groups + kDirG - 1) / kDirG, ntb = (P + kDirT - 1) / kDirT;
+    for (int item = threadIdx.x; item < ngb * ntb; item += blockDim.x) {
+        const int gb = item % ngb, tb = item / ngb;
+        const int t0 = tb * kDirT;
+        int addr_in[kDirG];
 #pragma unroll
-        for (int j = 0; j < kDirT; ++j) acc[j] = make_float2(0.f, 0.f);
-        int e0 = 0;  // (r * t0) mod P
+        for (int j = 0; j < kDirG; ++j) {
+            const int g = min(gb * kDirG + j, groups - 1);
+            const int v = g / nbp, bb = g - v * nbp;
+            addr_in[j] = COLS ? bb * V + v : v * n + bb;
+        }
+        const int rstep = COLS ? nbp * V : nbp;  // address step of r
+        float2 acc[kDirG][kDirT];
+#pragma unroll
+        for (int j = 0; j < kDirG; ++j)
+#pragma unroll
+            for (int i = 0; i < kDirT; ++i) acc[j][i] = make_float2(0.f, 0.f);
+        int e[kDirT];  // (r * t) mod P
+#pragma unroll
+        for (int i = 0; i < kDirT; ++i) e[i] = 0;
         for (int r = 0; r < P; ++r) {
-            const float2 a = buf[fft_addr<COLS>(l, bb + r * nbp, n, V)];
-            float2 w = __ldg(&tw[e0 * nbp]);
-            float2 w1 = __ldg(&tw[r * nbp]);  // w_P^r
-            if (inv) {
-                w.y = -w.y;
-                w1.y = -w1.y;
+            float2 a[kDirG], w[kDirT];
+#pragma unroll
+            for (int j = 0; j < kDirG; ++j) a[j] = buf[addr_in[j] + r * rstep];
+#pragma unroll
+            for (int i = 0; i < kDirT; ++i) {
+                w[i] = roots[e[i]];
+                e[i] += min(t0 + i, P - 1);
+                if (e[i] >= P) e[i] -= P;
             }
 #pragma unroll
-            for (int j = 0; j < kDirT; ++j) {
-                acc[j] = cadd(acc[j], cmul(a, w));
-                w = cmul(w, w1);
-            }
-            e0 += t0;
-            while (e0 >= P) e0 -= P;
+            for (int j = 0; j < kDirG; ++j)
+#pragma unroll
+                for (int i = 0; i < kDirT; ++i) {
+                    acc[j][i].x = fmaf(a[j].x, w[i].x, fmaf(-a[j].y, w[i].y, acc[j][i].x));
+                    acc[j][i].y = fmaf(a[j].x, w[i].y, fmaf(a[j].y, w[i].x, acc[j][i].y));
+                }
         }
 #pragma unroll
-        for (int j = 0; j < kDirT; ++j) {
-            const int t = t0 + j;
-            if (t < P) {
-                float2 w2 = __ldg(&tw[q * t * s]);
-                if (inv) w2.y = -w2.y;
-                scratch[fft_addr<COLS>(l, k + s * (P * q + t), n, V)] = cmul(acc[j], w2);
+        for (int j = 0; j < kDirG; ++j) {
+            const int g = gb * kDirG + j;
+            if (g >= groups) break;
+            const int v = g / nbp, bb = g - v * nbp;
+            const int q = bb / s, k = bb - q * s;
+#pragma unroll
+            for (int i = 0; i < kDirT; ++i) {
+                const int t = t0 + i;
+                if (t < P) {
+                    float2 w2 = __ldg(&tw[q * t * s]);
+                    if (inv) w2.y = -w2.y;
+                    const int o = k + s * (P * q + t);
+                    scratch[COLS ? o * V + v : v * n + o] = cmul(acc[j][i], w2);
+                }
             }
         }
     }
@@ -491,10 +523,16 @@ struct RtFft {
     __device__ __forceinline__ int n() const { return d.n; }
     __device__ __forceinline__ int vecs() const { return V; }
     bool direct;  // a prime factor above 13: the direct stage needs a scratch buffer
+    int pmax;     // largest prime factor (the direct stage's root table)
     template <bool COLS>
     __device__ __forceinline__ int pad(int flat) const { return flat; }
     __device__ __forceinline__ int threads() const { return blockDim.x; }
-    size_t smem_bytes(bool) const { return (size_t)V * d.n * sizeof(float2) * (direct ? 2 : 1); }
+    size_t smem_bytes(bool) const
+    {
+        // direct stages: a scratch copy of the strip plus the root table
+        return (size_t)V * d.n * sizeof(float2) * (direct ? 2 : 1) +
+               (direct ? (size_t)pmax * sizeof(float2) : 0);
+    }
     template <bool COLS>
     __device__ __forceinline__ void run(float2* buf, bool inv) const
     {
