@@ -445,13 +445,29 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
     constexpr bool PRED = NB * TV != NBP;
     constexpr float sg = INV ? 1.0f : -1.0f;
     auto addr = [&](int j) { return ct_pad<V, COLS>(COLS ? j * V + v : v * N + j); };
+    // ct_pad adds one pad slot per 8 (rows) / per 8 V (columns) elements, so
+    // indices j + m D with D a multiple of 8 map to addr(j) + m D (9/8) (x V
+    // for columns): the butterfly's P inputs (D = NBP) and, when the stage
+    // stride S is a multiple of 8 (or S = 1 with P | 8, outputs inside one
+    // 8-block), its P outputs are a base address plus compile-time offsets.
+    constexpr bool LIN_IN = NBP % 8 == 0;
+    constexpr bool LIN_OUT = S % 8 == 0 || (S == 1 && 8 % P == 0);
+    constexpr int VS = COLS ? V : 1;
+    constexpr int STR_IN = LIN_IN ? NBP / 8 * 9 * VS : 0;
+    constexpr int STR_OUT = S == 1 ? VS : (LIN_OUT ? S / 8 * 9 * VS : 0);
     float2 a[NB][P];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int bb = t + i * TV;
         if (!PRED || bb < NBP) {
+            if constexpr (LIN_IN) {
+                const float2* src = buf + addr(bb);
 #pragma unroll
-            for (int r = 0; r < P; ++r) a[i][r] = buf[addr(bb + r * NBP)];
+                for (int r = 0; r < P; ++r) a[i][r] = src[r * STR_IN];
+            } else {
+#pragma unroll
+                for (int r = 0; r < P; ++r) a[i][r] = buf[addr(bb + r * NBP)];
+            }
         }
     }
     __syncthreads();
@@ -462,7 +478,14 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
             const int q = bb / S, k = bb - q * S;
             dft_small<P>(a[i], sg);
             const int obase = k + S * P * q;
-            buf[addr(obase)] = a[i][0];
+            float2* dst = buf + addr(obase);
+            auto out_at = [&](int tt) -> float2& {
+                if constexpr (LIN_OUT)
+                    return dst[tt * STR_OUT];
+                else
+                    return buf[addr(obase + S * tt)];
+            };
+            out_at(0) = a[i][0];
             // twiddles w^t, w = tw[q S]: one coalesced load, powers by complex
             // multiplication (relative error <= (P-1) ulp-level products)
             float2 w1 = __ldg(&tw[q * S]);
@@ -470,7 +493,7 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
             float2 wt = w1;
 #pragma unroll
             for (int tt = 1; tt < P; ++tt) {
-                buf[addr(obase + S * tt)] = cmul(a[i][tt], wt);
+                out_at(tt) = cmul(a[i][tt], wt);
                 if (tt + 1 < P) wt = cmul(wt, w1);  // w^(t+1)
             }
         }
