@@ -1192,9 +1192,23 @@ blfls_status blfls_gaussian_blur(const float* in, int channels, int height, int 
     const int r = (int)(k.size() / 2);
     const size_t n = (size_t)channels * height * width;
     const bool host = flags & BLFLS_HOST_PTRS;
-    double* dk = nullptr;
-    double* tmp = nullptr;
-    float *din = nullptr, *dout = nullptr;
+    // temporaries are stream-ordered and released on every exit path
+    struct Tmp {
+        cudaStream_t st;
+        double* dk = nullptr;
+        double* tmp = nullptr;
+        float* din = nullptr;
+        float* dout = nullptr;
+        ~Tmp()
+        {
+            for (void* q : {(void*)dk, (void*)tmp, (void*)din, (void*)dout})
+                if (q) cudaFreeAsync(q, st);
+        }
+    } t{st};
+    double*& dk = t.dk;
+    double*& tmp = t.tmp;
+    float*& din = t.din;
+    float*& dout = t.dout;
     CK(cudaMallocAsync(&dk, sizeof(double) * k.size(), st));
     CK(cudaMallocAsync(&tmp, sizeof(double) * n, st));
     CK(cudaMemcpyAsync(dk, k.data(), sizeof(double) * k.size(), cudaMemcpyHostToDevice, st));
@@ -1210,10 +1224,6 @@ blfls_status blfls_gaussian_blur(const float* in, int channels, int height, int 
     CK(launch_gaussian_blur(src, dst, tmp, dk, r, channels, height, width,
                             prop.multiProcessorCount, st));
     if (host) CK(cudaMemcpyAsync(out, dout, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaFreeAsync(dk, st));
-    CK(cudaFreeAsync(tmp, st));
-    if (din) CK(cudaFreeAsync(din, st));
-    if (dout) CK(cudaFreeAsync(dout, st));
     if (host || (flags & BLFLS_SYNC)) CK(cudaStreamSynchronize(st));
     return BLFLS_OK;
 }
