@@ -1161,11 +1161,17 @@ blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t*
         return fail(BLFLS_EINVAL, "generate: bad arguments");
     CK(cudaSetDevice(device));
     cudaStream_t st = (cudaStream_t)stream;
-    uint64_t* dseeds = nullptr;
-    CK(cudaMallocAsync(&dseeds, sizeof(uint64_t) * n_planes, st));
-    CK(cudaMemcpyAsync(dseeds, seeds, sizeof(uint64_t) * n_planes, cudaMemcpyHostToDevice, st));
-    CK(launch_generate(height, width, n_planes, dseeds, n_sites, noise_sigma, p_sp, out, st));
-    CK(cudaFreeAsync(dseeds, st));
+    struct Seeds {  // released on every exit path (stream-ordered)
+        cudaStream_t st;
+        uint64_t* d = nullptr;
+        ~Seeds()
+        {
+            if (d) cudaFreeAsync(d, st);
+        }
+    } ds{st};
+    CK(cudaMallocAsync(&ds.d, sizeof(uint64_t) * n_planes, st));
+    CK(cudaMemcpyAsync(ds.d, seeds, sizeof(uint64_t) * n_planes, cudaMemcpyHostToDevice, st));
+    CK(launch_generate(height, width, n_planes, ds.d, n_sites, noise_sigma, p_sp, out, st));
     CK(cudaStreamSynchronize(st));
     return BLFLS_OK;
 }
