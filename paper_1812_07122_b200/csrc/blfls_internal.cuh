@@ -57,9 +57,22 @@ struct FftDesc {
     const float2* tw;  // n entries, device
 };
 
+// Bluestein transform of a length whose prime factors include one above the
+// direct-stage threshold: chirp c_j = exp(-pi i j^2 / n) (n entries), the
+// 5-smooth convolution length M >= 2n - 1 and its FFT (m), and the spectra of
+// the chirp kernel for the forward / inverse direction with 1/M folded in.
+struct BlueDesc {
+    FftDesc m;
+    const float2* chirp;
+    const float2* hf;
+    const float2* hi;
+};
+
 // launch geometry of one FFT pass: V vectors per CTA, threads = V * TV
 struct FftGeom {
     FftDesc desc;
+    bool bluestein = false;  // run the length-n transform as a length-M convolution
+    BlueDesc blue{};
     int V, log2V, threads;
     int E;         // complex values per thread across a stage barrier (8 or 16)
     bool generic;  // a radix other than 2/3/4/5 occurs

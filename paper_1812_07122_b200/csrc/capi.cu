@@ -7,6 +7,7 @@
 //
 // replayed as a cached CUDA graph on the plan's own stream.
 #include <algorithm>
+#include <complex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -68,7 +69,51 @@ blfls_status cuda_fail(cudaError_t e, const char* where)
 struct DevFft {
     FftGeom g{};
     float2* tw = nullptr;
+    // Bluestein tables (device): chirp (n), M-point twiddles, kernel spectra
+    float2* chirp = nullptr;
+    float2* btw = nullptr;
+    float2* hf = nullptr;
+    float2* hi = nullptr;
 };
+
+// Bluestein for lengths with a prime factor above this (the direct stage
+// below it); BLFLS_BLUESTEIN_MINP overrides (0 disables Bluestein)
+int bluestein_min_prime()
+{
+    static const int v = [] {
+        const char* e = std::getenv("BLFLS_BLUESTEIN_MINP");
+        return e ? std::atoi(e) : 150;  // measured: P = 61, 43 faster direct, P = 139 a tie
+    }();
+    return v;
+}
+
+bool smooth235(int m)
+{
+    for (int p : {2, 3, 5})
+        while (m % p == 0) m /= p;
+    return m == 1;
+}
+
+// host mixed-radix (2, 3, 5) FFT in double, sign -1 forward (table setup only)
+void host_fft(std::vector<std::complex<double>>& a, int sign)
+{
+    const int n = (int)a.size();
+    if (n == 1) return;
+    int p = n % 2 == 0 ? 2 : (n % 3 == 0 ? 3 : 5);
+    const int m = n / p;
+    std::vector<std::vector<std::complex<double>>> sub(p, std::vector<std::complex<double>>(m));
+    for (int j = 0; j < m; ++j)
+        for (int r = 0; r < p; ++r) sub[r][j] = a[(size_t)j * p + r];
+    for (auto& v : sub) host_fft(v, sign);
+    for (int k = 0; k < n; ++k) {
+        std::complex<double> acc = 0.0;
+        for (int r = 0; r < p; ++r) {
+            const double ang = sign * 2.0 * M_PI * (double)(((long long)r * k) % n) / n;
+            acc += sub[r][k % m] * std::complex<double>(std::cos(ang), std::sin(ang));
+        }
+        a[k] = acc;
+    }
+}
 
 bool factorize(int n, std::vector<int>& radix)
 {
@@ -124,6 +169,37 @@ bool plan_fft(int n, int Vmax, size_t smem_cap, bool cols, bool odd, int nvec, i
         g.direct = false;
         g.ct = true;
         return true;
+    }
+    const int bmin = bluestein_min_prime();
+    if (bmin > 0 && pmax > bmin) {
+        // Bluestein: the transform becomes a cyclic convolution of 5-smooth length M
+        int M = 2 * n - 1;
+        while (!smooth235(M)) ++M;
+        std::vector<int> mrad;
+        factorize(M, mrad);
+        for (int V = Vmax; V >= 1; V >>= 1) {
+            if ((size_t)V * (n + M) * 8 > smem_cap) continue;
+            for (int E : {8, 16}) {
+                int tv = threads_per_vector(mrad, M, E);
+                while ((tv * V) % 32 != 0) ++tv;
+                if ((long)tv * V > 1024) continue;
+                FftGeom& g = out.g;
+                g.V = V;
+                g.log2V = 0;
+                while ((1 << g.log2V) < V) ++g.log2V;
+                g.threads = tv * V;
+                g.E = E;
+                g.generic = false;
+                g.direct = false;
+                g.pmax = pmax;
+                g.ct = false;
+                g.bluestein = true;
+                g.blue.m.n = M;
+                g.blue.m.nstages = (int)mrad.size();
+                for (size_t i = 0; i < mrad.size(); ++i) g.blue.m.radix[i] = mrad[i];
+                return true;
+            }
+        }
     }
     for (int V = Vmax; V >= 1; V >>= 1) {
         // direct stages: strip + scratch copy + root table of the largest prime
@@ -541,7 +617,8 @@ void free_plan(blfls_plan_t p)
     }
     void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
-                    p->rowf.tw, p->colf.tw, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
+                    p->rowf.tw, p->colf.tw, p->rowf.chirp, p->rowf.btw, p->rowf.hf, p->rowf.hi,
+                    p->colf.chirp, p->colf.btw, p->colf.hf, p->colf.hi, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
                     p->grid.blurred, p->grid.erange, p->dt.cth, p->dt.ctv, p->dt.pc, p->dt.x, p->dt.g01};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -636,6 +713,12 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: height " + std::to_string(H) +
                                                  " too large for the shared-memory column FFT"));
 
+    if (std::getenv("BLFLS_DEBUG_FFT")) {
+        for (const DevFft* f : {&p->rowf, &p->colf})
+            std::fprintf(stderr, "blfls fft n=%d ct=%d bluestein=%d (M=%d) direct=%d pmax=%d V=%d threads=%d E=%d\n",
+                         f->g.desc.n, (int)f->g.ct, (int)f->g.bluestein, f->g.blue.m.n, (int)f->g.direct,
+                         f->g.pmax, f->g.V, f->g.threads, f->g.E);
+    }
     // tables (double -> float)
     {
         auto tr = twiddles(nrow);
@@ -671,6 +754,44 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         };
         fill(p->rowf, nrow, rrad);
         fill(p->colf, H, crad);
+        for (DevFft* f : {&p->rowf, &p->colf}) {
+            if (!f->g.bluestein) continue;
+            const int n = f->g.desc.n, M = f->g.blue.m.n;
+            std::vector<float2> ch(n);
+            std::vector<std::complex<double>> hk(M, 0.0), hk_inv(M, 0.0);
+            for (int j = 0; j < n; ++j) {  // c_j = exp(-pi i j^2 / n), angle reduced mod 2 pi
+                const double a = -M_PI * (double)(((long long)j * j) % (2LL * n)) / n;
+                const std::complex<double> c(std::cos(a), std::sin(a));
+                ch[j] = make_float2((float)c.real(), (float)c.imag());
+                hk[j] = std::conj(c);  // forward kernel h = conj(c); inverse: c
+                hk_inv[j] = c;
+                if (j) {
+                    hk[M - j] = std::conj(c);
+                    hk_inv[M - j] = c;
+                }
+            }
+            host_fft(hk, -1);
+            host_fft(hk_inv, -1);
+            std::vector<float2> hf(M), hi(M);
+            for (int k = 0; k < M; ++k) {
+                hf[k] = make_float2((float)(hk[k].real() / M), (float)(hk[k].imag() / M));
+                hi[k] = make_float2((float)(hk_inv[k].real() / M), (float)(hk_inv[k].imag() / M));
+            }
+            auto tm = twiddles(M);
+            if (cudaMalloc(&f->chirp, sizeof(float2) * n) != cudaSuccess ||
+                cudaMalloc(&f->btw, sizeof(float2) * M) != cudaSuccess ||
+                cudaMalloc(&f->hf, sizeof(float2) * M) != cudaSuccess ||
+                cudaMalloc(&f->hi, sizeof(float2) * M) != cudaSuccess)
+                return bail(fail(BLFLS_ENOMEM, "plan: Bluestein table allocation failed"));
+            cudaMemcpy(f->chirp, ch.data(), sizeof(float2) * n, cudaMemcpyHostToDevice);
+            cudaMemcpy(f->btw, tm.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+            cudaMemcpy(f->hf, hf.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+            cudaMemcpy(f->hi, hi.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+            f->g.blue.m.tw = f->btw;
+            f->g.blue.chirp = f->chirp;
+            f->g.blue.hf = f->hf;
+            f->g.blue.hi = f->hi;
+        }
     }
 
     // BLF constants

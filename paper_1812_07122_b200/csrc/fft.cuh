@@ -375,6 +375,41 @@ __device__ void fft_run(float2* buf, const FftDesc& d, int V, int log2V, bool in
     }
 }
 
+// Bluestein: X_k = c_k sum_j (x_j c_j) h_{k-j}, c_m = exp(sg pi i m^2 / n),
+// h = conj(c) -- a cyclic convolution of length M computed with two M-point
+// transforms of the runtime engine in `work` (V * M complex after the strip).
+template <int E, bool COLS>
+__device__ void fft_bluestein(float2* buf, float2* work, const FftDesc& d, const BlueDesc& b, int V,
+                              int log2V, bool inv)
+{
+    const FftLane l = fft_lane<COLS>(V, log2V);
+    const int n = d.n, M = b.m.n;
+    for (int j = l.t; j < M; j += l.TV) {
+        float2 a = make_float2(0.f, 0.f);
+        if (j < n) {
+            float2 c = __ldg(&b.chirp[j]);
+            if (inv) c.y = -c.y;
+            a = cmul(buf[fft_addr<COLS>(l, j, n, V)], c);
+        }
+        work[fft_addr<COLS>(l, j, M, V)] = a;
+    }
+    __syncthreads();
+    fft_run<E, COLS, false>(work, b.m, V, log2V, false);
+    const float2* H = inv ? b.hi : b.hf;
+    for (int j = l.t; j < M; j += l.TV) {
+        const int o = fft_addr<COLS>(l, j, M, V);
+        work[o] = cmul(work[o], __ldg(&H[j]));
+    }
+    __syncthreads();
+    fft_run<E, COLS, false>(work, b.m, V, log2V, true);
+    for (int k = l.t; k < n; k += l.TV) {
+        float2 c = __ldg(&b.chirp[k]);
+        if (inv) c.y = -c.y;
+        buf[fft_addr<COLS>(l, k, n, V)] = cmul(work[fft_addr<COLS>(l, k, M, V)], c);
+    }
+    __syncthreads();
+}
+
 }  // namespace blfls
 
 // ===================================================================
@@ -547,19 +582,26 @@ struct RtFft {
     __device__ __forceinline__ int vecs() const { return V; }
     bool direct;  // a prime factor above 13: the direct stage needs a scratch buffer
     int pmax;     // largest prime factor (the direct stage's root table)
+    bool bluestein;
+    BlueDesc blue;
     template <bool COLS>
     __device__ __forceinline__ int pad(int flat) const { return flat; }
     __device__ __forceinline__ int threads() const { return blockDim.x; }
     size_t smem_bytes(bool) const
     {
-        // direct stages: a scratch copy of the strip plus the root table
+        // Bluestein: the strip plus the length-M work vectors; direct stages:
+        // a scratch copy of the strip plus the root table
+        if (bluestein) return (size_t)V * (d.n + blue.m.n) * sizeof(float2);
         return (size_t)V * d.n * sizeof(float2) * (direct ? 2 : 1) +
                (direct ? (size_t)pmax * sizeof(float2) : 0);
     }
     template <bool COLS>
     __device__ __forceinline__ void run(float2* buf, bool inv) const
     {
-        fft_run<E, COLS, GENERIC>(buf, d, V, log2V, inv);
+        if (bluestein)
+            fft_bluestein<E, COLS>(buf, buf + (size_t)V * d.n, d, blue, V, log2V, inv);
+        else
+            fft_run<E, COLS, GENERIC>(buf, d, V, log2V, inv);
     }
 };
 

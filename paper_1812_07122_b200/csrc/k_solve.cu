@@ -520,14 +520,14 @@ static cudaError_t launch_fft_pass(int which, const SolveParams& p, const FftGeo
     }
     if (g.E == 16) {
         if (g.generic)
-            launch_pass(which, p, RtFft<16, true>{g.desc, g.V, g.log2V, g.direct, g.pmax}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<16, true>{g.desc, g.V, g.log2V, g.direct, g.pmax, g.bluestein, g.blue}, g.V, n, g.threads, planes, odd, st);
         else
-            launch_pass(which, p, RtFft<16, false>{g.desc, g.V, g.log2V, false, 0}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<16, false>{g.desc, g.V, g.log2V, false, 0, g.bluestein, g.blue}, g.V, n, g.threads, planes, odd, st);
     } else {
         if (g.generic)
-            launch_pass(which, p, RtFft<8, true>{g.desc, g.V, g.log2V, g.direct, g.pmax}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<8, true>{g.desc, g.V, g.log2V, g.direct, g.pmax, g.bluestein, g.blue}, g.V, n, g.threads, planes, odd, st);
         else
-            launch_pass(which, p, RtFft<8, false>{g.desc, g.V, g.log2V, false, 0}, g.V, n, g.threads, planes, odd, st);
+            launch_pass(which, p, RtFft<8, false>{g.desc, g.V, g.log2V, false, 0, g.bluestein, g.blue}, g.V, n, g.threads, planes, odd, st);
     }
     return cudaGetLastError();
 }

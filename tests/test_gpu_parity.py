@@ -458,7 +458,9 @@ def test_grid_backend_is_deterministic(gpu, oracle):
 
 @pytest.mark.parametrize("h,w", [(1056, 1056), (544, 544), (2080, 96), (64, 2080),
                                  # runtime engine, blocked direct-DFT stages: c3 / c4 at pad 16
-                                 (1112, 1952), (4128, 64)])
+                                 (1112, 1952), (4128, 64),
+                                 # Bluestein (prime factors above 150): 1021 prime, 634 = 2 * 317
+                                 (1021, 634), (634, 1021)])
 def test_solve_prime_radix_sizes_vs_oracle(gpu, oracle, h, w):
     """The FFT solve on the compile-time geometries with radix 11 / 17 / 13
     stages (the reference-default pad-16 grids of the BASELINE sizes)."""
