@@ -159,6 +159,18 @@ blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t*
                             int n_sites, double noise_sigma, double p_salt_pepper, float* out,
                             void* stream, int device);
 
+/* blf_brute (bilateral.cpp:28-77): the standalone brute-force (joint)
+ * bilateral filter of `batch` images of cs planes (1 or 3), guided by cg
+ * planes (1 or cs; guide == NULL: guided by src itself, cg ignored).  Weights
+ * exp(-|dxy|^2 / (2 sigma_s^2)) * exp(-|g(s) - g(t)|^2 / (2 sigma_r^2)) with the
+ * Euclidean norm over the guide channels, window |dx|, |dy| <= radius clipped at
+ * the border; radius < 0 means ceil(3 sigma_s) as the reference (bilateral.cpp:37).
+ * fp32 in and out; flags DEVICE_PTRS / HOST_PTRS, CHECK_FINITE, SYNC as for
+ * blfls_run.  BLFLS_EUNSUPPORTED when the tile (radius) exceeds shared memory. */
+blfls_status blfls_blf_brute(const float* src, int cs, const float* guide, int cg, int height,
+                             int width, int batch, int radius, double sigma_s, double sigma_r,
+                             float* out, int device, void* stream, unsigned flags);
+
 /* gaussian_blur (image.cpp:99-158): separable Gaussian of radius ceil(3 sigma),
  * weights exp(-i^2 / (2 sigma^2)) normalised to sum 1, clamped borders,
  * accumulated in double in the reference's tap order; `in` and `out` are

@@ -7,6 +7,7 @@
 //   blfls::smooth(g, spec)          ~ epls::smooth (pipelines.cpp:57-94), BLF_LS / NC_LS
 //   blfls::rolling_nc_ls(...)       ~ epls::rolling_nc_ls (pipelines.cpp:96-117)
 //   blfls::gaussian_blur(img, s)    ~ epls::gaussian_blur (image.cpp:114-158)
+//   blfls::blf_brute(src, guide, p) ~ epls::blf_brute (bilateral.cpp:28-77)
 //   blfls::flash_no_flash(a, f, s)  ~ epls::flash_no_flash (applications.cpp:58-64)
 //   blfls::blf_ls(...)              the north-star cascade (iters smooth() calls)
 //   blfls::lsgrad_solve_fft(...)    ~ epls::lsgrad_solve_fft (solver.cpp:88-124)
@@ -181,6 +182,22 @@ inline Image gaussian_blur(const Image& img, double sigma, int device = 0)
     detail::check(blfls_gaussian_blur(in.data(), img.channels(), img.height(), img.width(), sigma,
                                       out.data(), device, nullptr, BLFLS_HOST_PTRS | BLFLS_SYNC));
     Image res(img.width(), img.height(), img.channels());
+    for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
+    return res;
+}
+
+/// epls::blf_brute (bilateral.cpp:28-77): standalone (joint) bilateral filter;
+/// radius < 0 is the reference's ceil(3 sigma_s).
+inline Image blf_brute(const Image& src, const Image& guide, const RangeSpatialParams& p,
+                       int radius = -1, int device = 0)
+{
+    if (src.width() != guide.width() || src.height() != guide.height())
+        throw std::invalid_argument("bilateral: src and guide dimensions differ");
+    std::vector<float> s = detail::to_f32(src), g = detail::to_f32(guide), out(src.size());
+    detail::check(blfls_blf_brute(s.data(), src.channels(), g.data(), guide.channels(), src.height(),
+                                  src.width(), 1, radius, p.sigma_s, p.sigma_r, out.data(), device,
+                                  nullptr, BLFLS_HOST_PTRS | BLFLS_CHECK_FINITE | BLFLS_SYNC));
+    Image res(src.width(), src.height(), src.channels());
     for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
     return res;
 }

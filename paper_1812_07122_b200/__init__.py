@@ -9,7 +9,7 @@ mirror of the reference's ``epls`` entry points
 (see :mod:`paper_1812_07122_b200.blfls`).
 """
 from .blfls import (CudaError, DtParams, InvalidArgument, RangeSpatialParams, RollingParams,
-                    SmootherKind, SmootherSpec, SolveParams, Unsupported, blf_ls, clipart_cleanup,
+                    SmootherKind, SmootherSpec, SolveParams, Unsupported, blf_brute, blf_ls, clipart_cleanup,
                     filter_gradients, flash_no_flash, gaussian_blur, generate, get_plan, irfft2,
                     ls_solve_fft, lsgrad_solve_fft, nc_ls, rfft2, rolling_nc_ls, smooth, sync_plans,
                     texture_removal)
@@ -17,7 +17,8 @@ from .configs import CONFIGS, Config
 
 __all__ = [
     "CudaError", "DtParams", "InvalidArgument", "RangeSpatialParams", "RollingParams",
-    "SmootherKind", "SmootherSpec", "SolveParams", "Unsupported", "blf_ls", "clipart_cleanup",
+    "SmootherKind", "SmootherSpec", "SolveParams", "Unsupported", "blf_brute", "blf_ls",
+    "clipart_cleanup",
     "filter_gradients", "flash_no_flash", "gaussian_blur", "generate", "get_plan", "irfft2",
     "ls_solve_fft", "lsgrad_solve_fft", "nc_ls", "rfft2", "rolling_nc_ls", "smooth", "sync_plans",
     "texture_removal", "CONFIGS", "Config",

@@ -34,7 +34,7 @@ EXPORTS = (
     "blfls_plan_create", "blfls_plan_destroy", "blfls_run", "blfls_sync", "blfls_filter_gradients",
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
     "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
-    "blfls_version", "blfls_abi_version", "blfls_gaussian_blur",
+    "blfls_version", "blfls_abi_version", "blfls_gaussian_blur", "blfls_blf_brute",
 )
 
 
@@ -105,6 +105,8 @@ def lib() -> C.CDLL:
             L.blfls_debug_ranges.argtypes = [vp, C.POINTER(C.c_float)]
             L.blfls_mufu_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
             L.blfls_gaussian_blur.argtypes = [fp, ip, ip, ip, C.c_double, fp, ip, vp, C.c_uint]
+            L.blfls_blf_brute.argtypes = [fp, ip, fp, ip, ip, ip, ip, ip, C.c_double, C.c_double, fp,
+                                          ip, vp, C.c_uint]
             L.blfls_last_error.restype = C.c_char_p
             L.blfls_version.restype = C.c_char_p
             for name in EXPORTS:

@@ -17,6 +17,7 @@ this module                reference
 ``texture_removal``        ``texture_removal`` (applications.cpp:66-70)
 ``clipart_cleanup``        ``clipart_cleanup`` (applications.cpp:72-76)
 ``gaussian_blur``          ``gaussian_blur`` (image.cpp:114-158)
+``blf_brute``              ``blf_brute`` (bilateral.cpp:28-77), standalone filter
 ``flash_no_flash``         ``flash_no_flash`` (applications.cpp:58-64)
 ``blf_ls``                 the north-star cascade: ``iters`` smooth() calls
 ``filter_gradients``       ``filter_gradients`` (pipelines.cpp:33-53)
@@ -56,7 +57,7 @@ from ._capi import (ASYNC, CHECK_FINITE, DEVICE_PTRS, HOST_PTRS, NO_GRAPH, SYNC,
 __all__ = [
     "SmootherKind", "RangeSpatialParams", "SolveParams", "SmootherSpec", "smooth",
     "flash_no_flash", "blf_ls", "nc_ls", "rolling_nc_ls", "texture_removal", "clipart_cleanup",
-    "gaussian_blur", "DtParams", "RollingParams", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
+    "gaussian_blur", "blf_brute", "DtParams", "RollingParams", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
     "rfft2", "irfft2", "generate", "get_plan", "sync_plans", "InvalidArgument", "CudaError",
     "Unsupported",
 ]
@@ -317,6 +318,27 @@ def gaussian_blur(img, sigma: float):
     check(lib().blfls_gaussian_blur(im.ptr, im.b * im.c, im.h, im.w, float(sigma), _ptr(out), dev,
                                     stream, flags))
     return im.finish(out)
+
+
+def blf_brute(src, guide=None, params: RangeSpatialParams = None, *, radius: int | None = None):
+    """``blf_brute`` (bilateral.cpp:28-77): the brute-force (joint) bilateral
+    filter of arbitrary planes.  ``guide`` has 1 channel or ``src``'s count
+    (None: ``src`` guides itself); the range distance is the Euclidean norm
+    over the guide channels; ``radius`` None is the reference's ceil(3 sigma_s)."""
+    params = params or RangeSpatialParams()
+    img = _Img(src)
+    gd = None if guide is None else _Img(guide, "guide")
+    if gd is not None and ((gd.h, gd.w) != (img.h, img.w) or gd.b != img.b):
+        raise InvalidArgument(_capi.BLFLS_EINVAL, "bilateral: src and guide dimensions differ")
+    dev = _device(img, gd)
+    out = img.empty_like()
+    stream, flags = _stream_and_flags(img)
+    check(lib().blfls_blf_brute(img.ptr, img.c, None if gd is None else gd.ptr,
+                                img.c if gd is None else gd.c, img.h, img.w, img.b,
+                                -1 if radius is None else int(radius), float(params.sigma_s),
+                                float(params.sigma_r), _ptr(out), dev, stream,
+                                flags | CHECK_FINITE))
+    return img.finish(out)
 
 
 def rolling_nc_ls(g, dt: DtParams, sp: SolveParams, rp: RollingParams):

@@ -153,6 +153,10 @@ struct DtParams {
 double nc_box_radius(double sigma_s, int iter, int total);
 // returns the number of kernels launched, or -1 on a launch error
 bool dt_configure(int iterations, double sigma_s);
+size_t blf_plain_smem(int cg, int cs, int R);
+cudaError_t launch_blf_plain(const float* src, int cs, const float* guide, int cg, float* out, int batch,
+                             int H, int W, int R, double sigma_s, double sigma_r, const float* tables,
+                             cudaStream_t st);
 int launch_dt_filter(const DtParams& p, int iterations, double sigma_s, int nsm, cudaStream_t st);
 std::vector<double> gaussian_weights(double sigma);
 cudaError_t launch_gaussian_blur(const float* in, float* out, double* tmp, const double* k, int r,

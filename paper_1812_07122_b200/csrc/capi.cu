@@ -1297,6 +1297,85 @@ blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t*
     return BLFLS_OK;
 }
 
+blfls_status blfls_blf_brute(const float* src, int cs, const float* guide, int cg, int height,
+                             int width, int batch, int radius, double sigma_s, double sigma_r,
+                             float* out, int device, void* stream, unsigned flags)
+{
+    // bilateral.cpp:12-24 (validate_params / validate_pair)
+    if (!(sigma_s > 0.0) || !std::isfinite(sigma_s) || !(sigma_r > 0.0) || !std::isfinite(sigma_r))
+        return fail(BLFLS_EINVAL, "bilateral: sigma_s and sigma_r must be positive and finite");
+    if (!src || !out || height < 1 || width < 1 || batch < 1 || (cs != 1 && cs != 3))
+        return fail(BLFLS_EINVAL, "blf_brute: bad arguments");
+    if (!guide) cg = cs;
+    if (cg != 1 && cg != cs)
+        return fail(BLFLS_EINVAL, "bilateral: guide channels must be 1 or match src");
+    const int R = radius < 0 ? (int)std::ceil(3.0 * sigma_s) : radius;
+    if (R > 4096 || blf_plain_smem(cg, cs, R) > 227 * 1024)
+        return fail(BLFLS_EUNSUPPORTED, "blf_brute: radius " + std::to_string(R) +
+                                            " exceeds the shared-memory tile");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(BLFLS_ECUDA, "no CUDA device (this library has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(BLFLS_EINVAL, "blf_brute: bad device ordinal");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t ns = (size_t)batch * cs * height * width, ng = (size_t)batch * cg * height * width;
+    const bool host = flags & BLFLS_HOST_PTRS;
+    std::vector<float> tab(2 * (R + 1));
+    for (int d = 0; d <= R; ++d) {  // bilateral.cpp:42-47 in the exp2 domain
+        const double c = -(double)d * d / (2.0 * sigma_s * sigma_s) * 1.4426950408889634;
+        tab[d] = (float)c;
+        tab[R + 1 + d] = (float)std::exp2(c);
+    }
+    struct Tmp {  // stream-ordered temporaries, released on every exit path
+        cudaStream_t st;
+        float* tab = nullptr;
+        float* s = nullptr;
+        float* g = nullptr;
+        float* o = nullptr;
+        unsigned* bad = nullptr;
+        ~Tmp()
+        {
+            for (void* q : {(void*)tab, (void*)s, (void*)g, (void*)o, (void*)bad})
+                if (q) cudaFreeAsync(q, st);
+        }
+    } t{st};
+    CK(cudaMallocAsync(&t.tab, sizeof(float) * tab.size(), st));
+    CK(cudaMemcpyAsync(t.tab, tab.data(), sizeof(float) * tab.size(), cudaMemcpyHostToDevice, st));
+    const float* ds = src;
+    const float* dg = guide ? guide : src;
+    float* dout = out;
+    if (host) {
+        CK(cudaMallocAsync(&t.s, sizeof(float) * ns, st));
+        CK(cudaMallocAsync(&t.o, sizeof(float) * ns, st));
+        CK(cudaMemcpyAsync(t.s, src, sizeof(float) * ns, cudaMemcpyHostToDevice, st));
+        ds = t.s;
+        dg = t.s;
+        if (guide) {
+            CK(cudaMallocAsync(&t.g, sizeof(float) * ng, st));
+            CK(cudaMemcpyAsync(t.g, guide, sizeof(float) * ng, cudaMemcpyHostToDevice, st));
+            dg = t.g;
+        }
+        dout = t.o;
+    }
+    if (flags & BLFLS_CHECK_FINITE) {  // bilateral.cpp:31-32 (require_finite)
+        CK(cudaMallocAsync(&t.bad, sizeof(unsigned), st));
+        CK(cudaMemsetAsync(t.bad, 0, sizeof(unsigned), st));
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        CK(launch_count_nonfinite(ds, ns, t.bad, prop.multiProcessorCount, st));
+        if (guide) CK(launch_count_nonfinite(dg, ng, t.bad, prop.multiProcessorCount, st));
+        unsigned nbad = 0;
+        CK(cudaMemcpyAsync(&nbad, t.bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (nbad) return fail(BLFLS_ENONFINITE, "blf_brute: image contains non-finite values");
+    }
+    CK(launch_blf_plain(ds, cs, dg, cg, dout, batch, height, width, R, sigma_s, sigma_r, t.tab, st));
+    if (host) CK(cudaMemcpyAsync(out, t.o, sizeof(float) * ns, cudaMemcpyDeviceToHost, st));
+    if (host || (flags & BLFLS_SYNC)) CK(cudaStreamSynchronize(st));
+    return BLFLS_OK;
+}
+
 blfls_status blfls_gaussian_blur(const float* in, int channels, int height, int width, double sigma,
                                  float* out, int device, void* stream, unsigned flags)
 {

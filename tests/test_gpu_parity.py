@@ -496,3 +496,45 @@ def test_grid_backend_batch_gray_guide_vs_reference(gpu, oracle):
         for _ in range(2):
             f = oracle.ref_smooth_grid(f, g3, lam=700.0, sigma_s=4.0, sigma_r=0.06, pad=4)
         assert maxabs(out[b], f) <= TOL_OUT
+
+
+# -------------------------------------------- standalone blf_brute (a7) --
+
+@pytest.mark.parametrize("cs,cg,h,w,ss,sr,r", [
+    (1, 1, 37, 53, 2.0, 0.1, None),   # self-guided gray, reference radius ceil(3 ss) = 6
+    (3, 3, 40, 48, 1.5, 0.08, None),  # self-guided RGB: Euclidean colour distance
+    (3, 1, 33, 70, 3.0, 0.05, 4),     # gray guide shared by RGB, explicit radius
+    (3, 3, 29, 31, 1.0, 0.2, 11),     # joint RGB guide
+    (1, 1, 64, 64, 4.0, 0.1, 0),      # radius 0: the identity
+])
+def test_blf_brute_standalone_vs_oracle(gpu, oracle, cs, cg, h, w, ss, sr, r):
+    src = _img(oracle, cs, h, w, 700 + h)
+    guide = None if (cg == cs and r is None) else _img(oracle, cg, h, w, 800 + w)
+    out = gpu.blf_brute(src, guide, gpu.RangeSpatialParams(ss, sr), radius=r)
+    g = src if guide is None else guide
+    ref = oracle.blf_brute_r(src.astype(np.float64), g.astype(np.float64), sigma_s=ss, sigma_r=sr,
+                             radius=-1 if r is None else r)
+    assert maxabs(out, ref) <= 2e-5
+    if r is None and oracle.REF_SO.exists():  # the reference's own blf_brute
+        ref2 = oracle.ref_blf_brute(src.astype(np.float64), g.astype(np.float64), sigma_s=ss,
+                                    sigma_r=sr)
+        assert maxabs(out, ref2) <= 2e-5
+
+
+def test_blf_brute_standalone_batch_and_errors(gpu, oracle):
+    import torch
+    srcs = np.stack([_img(oracle, 3, 24, 40, 900 + b) for b in range(3)]).astype(np.float32)
+    out = gpu.blf_brute(torch.from_numpy(srcs).cuda(), None, gpu.RangeSpatialParams(2.0, 0.1)).cpu()
+    for b in range(3):
+        ref = oracle.blf_brute_r(srcs[b].astype(np.float64), srcs[b].astype(np.float64), sigma_s=2.0,
+                                 sigma_r=0.1)
+        assert maxabs(out[b].numpy(), ref) <= 2e-5
+    img = _img(oracle, 1, 16, 16, 5)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_brute(img, None, gpu.RangeSpatialParams(0.0, 0.1))
+    bad = img.copy()
+    bad[0, 3, 3] = np.nan
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_brute(bad, None, gpu.RangeSpatialParams(1.0, 0.1))
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.blf_brute(img, _img(oracle, 1, 16, 17, 6), gpu.RangeSpatialParams(1.0, 0.1))
