@@ -159,6 +159,12 @@ blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t*
                             int n_sites, double noise_sigma, double p_salt_pepper, float* out,
                             void* stream, int device);
 
+/* forward_gradients (image.cpp:72-95): circular forward differences of
+ * `planes` planes, gx = f[y][(x+1) mod W] - f[y][x], gy = f[(y+1) mod H][x] -
+ * f[y][x]; fp32, flags DEVICE_PTRS / HOST_PTRS and SYNC as for blfls_run. */
+blfls_status blfls_forward_gradients(const float* img, int planes, int height, int width, float* gx,
+                                     float* gy, int device, void* stream, unsigned flags);
+
 /* blf_brute (bilateral.cpp:28-77): the standalone brute-force (joint)
  * bilateral filter of `batch` images of cs planes (1 or 3), guided by cg
  * planes (1 or cs; guide == NULL: guided by src itself, cg ignored).  Weights

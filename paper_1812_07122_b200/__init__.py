@@ -10,7 +10,7 @@ mirror of the reference's ``epls`` entry points
 """
 from .blfls import (CudaError, DtParams, InvalidArgument, RangeSpatialParams, RollingParams,
                     SmootherKind, SmootherSpec, SolveParams, Unsupported, blf_brute, blf_ls, clipart_cleanup,
-                    filter_gradients, flash_no_flash, gaussian_blur, generate, get_plan, irfft2,
+                    filter_gradients, flash_no_flash, forward_gradients, gaussian_blur, generate, get_plan, irfft2,
                     ls_solve_fft, lsgrad_solve_fft, nc_ls, rfft2, rolling_nc_ls, smooth, sync_plans,
                     texture_removal)
 from .configs import CONFIGS, Config
@@ -19,7 +19,7 @@ __all__ = [
     "CudaError", "DtParams", "InvalidArgument", "RangeSpatialParams", "RollingParams",
     "SmootherKind", "SmootherSpec", "SolveParams", "Unsupported", "blf_brute", "blf_ls",
     "clipart_cleanup",
-    "filter_gradients", "flash_no_flash", "gaussian_blur", "generate", "get_plan", "irfft2",
+    "filter_gradients", "flash_no_flash", "forward_gradients", "gaussian_blur", "generate", "get_plan", "irfft2",
     "ls_solve_fft", "lsgrad_solve_fft", "nc_ls", "rfft2", "rolling_nc_ls", "smooth", "sync_plans",
     "texture_removal", "CONFIGS", "Config",
 ]

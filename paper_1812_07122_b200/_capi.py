@@ -35,6 +35,7 @@ EXPORTS = (
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
     "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
     "blfls_version", "blfls_abi_version", "blfls_gaussian_blur", "blfls_blf_brute",
+    "blfls_forward_gradients",
 )
 
 
@@ -105,6 +106,7 @@ def lib() -> C.CDLL:
             L.blfls_debug_ranges.argtypes = [vp, C.POINTER(C.c_float)]
             L.blfls_mufu_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
             L.blfls_gaussian_blur.argtypes = [fp, ip, ip, ip, C.c_double, fp, ip, vp, C.c_uint]
+            L.blfls_forward_gradients.argtypes = [fp, ip, ip, ip, fp, fp, ip, vp, C.c_uint]
             L.blfls_blf_brute.argtypes = [fp, ip, fp, ip, ip, ip, ip, ip, C.c_double, C.c_double, fp,
                                           ip, vp, C.c_uint]
             L.blfls_last_error.restype = C.c_char_p

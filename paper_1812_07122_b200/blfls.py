@@ -18,6 +18,7 @@ this module                reference
 ``clipart_cleanup``        ``clipart_cleanup`` (applications.cpp:72-76)
 ``gaussian_blur``          ``gaussian_blur`` (image.cpp:114-158)
 ``blf_brute``              ``blf_brute`` (bilateral.cpp:28-77), standalone filter
+``forward_gradients``      ``forward_gradients`` (image.cpp:72-95)
 ``flash_no_flash``         ``flash_no_flash`` (applications.cpp:58-64)
 ``blf_ls``                 the north-star cascade: ``iters`` smooth() calls
 ``filter_gradients``       ``filter_gradients`` (pipelines.cpp:33-53)
@@ -57,7 +58,7 @@ from ._capi import (ASYNC, CHECK_FINITE, DEVICE_PTRS, HOST_PTRS, NO_GRAPH, SYNC,
 __all__ = [
     "SmootherKind", "RangeSpatialParams", "SolveParams", "SmootherSpec", "smooth",
     "flash_no_flash", "blf_ls", "nc_ls", "rolling_nc_ls", "texture_removal", "clipart_cleanup",
-    "gaussian_blur", "blf_brute", "DtParams", "RollingParams", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
+    "gaussian_blur", "blf_brute", "forward_gradients", "DtParams", "RollingParams", "filter_gradients", "lsgrad_solve_fft", "ls_solve_fft",
     "rfft2", "irfft2", "generate", "get_plan", "sync_plans", "InvalidArgument", "CudaError",
     "Unsupported",
 ]
@@ -318,6 +319,18 @@ def gaussian_blur(img, sigma: float):
     check(lib().blfls_gaussian_blur(im.ptr, im.b * im.c, im.h, im.w, float(sigma), _ptr(out), dev,
                                     stream, flags))
     return im.finish(out)
+
+
+def forward_gradients(img):
+    """``forward_gradients`` (image.cpp:72-95): circular forward differences
+    per channel; returns (gx, gy) in the input's type."""
+    im = _Img(img)
+    gx, gy = im.empty_like(), im.empty_like()
+    stream, flags = _stream_and_flags(im)
+    dev = im.device if im.torch else 0
+    check(lib().blfls_forward_gradients(im.ptr, im.b * im.c, im.h, im.w, _ptr(gx), _ptr(gy), dev,
+                                        stream, flags))
+    return im.finish(gx), im.finish(gy)
 
 
 def blf_brute(src, guide=None, params: RangeSpatialParams = None, *, radius: int | None = None):

@@ -154,6 +154,8 @@ double nc_box_radius(double sigma_s, int iter, int total);
 // returns the number of kernels launched, or -1 on a launch error
 bool dt_configure(int iterations, double sigma_s);
 size_t blf_plain_smem(int cg, int cs, int R);
+cudaError_t launch_forward_gradients(const float* img, float* gx, float* gy, int planes, int H, int W,
+                                     int nsm, cudaStream_t st);
 cudaError_t launch_blf_plain(const float* src, int cs, const float* guide, int cg, float* out, int batch,
                              int H, int W, int R, double sigma_s, double sigma_r, const float* tables,
                              cudaStream_t st);

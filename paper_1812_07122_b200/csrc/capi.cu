@@ -1297,6 +1297,48 @@ blfls_status blfls_generate(int height, int width, int n_planes, const uint64_t*
     return BLFLS_OK;
 }
 
+blfls_status blfls_forward_gradients(const float* img, int planes, int height, int width, float* gx,
+                                     float* gy, int device, void* stream, unsigned flags)
+{
+    if (!img || !gx || !gy || planes < 1 || height < 1 || width < 1)
+        return fail(BLFLS_EINVAL, "forward_gradients: bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(BLFLS_ECUDA, "no CUDA device (this library has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(BLFLS_EINVAL, "forward_gradients: bad device ordinal");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)planes * height * width;
+    struct Tmp {
+        cudaStream_t st;
+        float* v[3] = {nullptr, nullptr, nullptr};
+        ~Tmp()
+        {
+            for (float* q : v)
+                if (q) cudaFreeAsync(q, st);
+        }
+    } t{st};
+    const float* src = img;
+    float *ox = gx, *oy = gy;
+    const bool host = flags & BLFLS_HOST_PTRS;
+    if (host) {
+        for (float*& q : t.v) CK(cudaMallocAsync(&q, sizeof(float) * n, st));
+        CK(cudaMemcpyAsync(t.v[0], img, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        src = t.v[0];
+        ox = t.v[1];
+        oy = t.v[2];
+    }
+    CK(launch_forward_gradients(src, ox, oy, planes, height, width, prop.multiProcessorCount, st));
+    if (host) {
+        CK(cudaMemcpyAsync(gx, ox, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(gy, oy, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    }
+    if (host || (flags & BLFLS_SYNC)) CK(cudaStreamSynchronize(st));
+    return BLFLS_OK;
+}
+
 blfls_status blfls_blf_brute(const float* src, int cs, const float* guide, int cg, int height,
                              int width, int batch, int radius, double sigma_s, double sigma_r,
                              float* out, int device, void* stream, unsigned flags)

@@ -16,6 +16,7 @@
 // (P + 2R of them, one shared-memory read per guide / source channel) and
 // updates each output whose window contains the column.  Any radius (runtime
 // R); shared memory holds (CG + CS) planes of (16 + 2R) x (64 + 2R) floats.
+#include <algorithm>
 #include <cmath>
 
 #include "blfls_internal.cuh"
@@ -142,7 +143,31 @@ __global__ void __launch_bounds__(256) k_blf_plain(PlainParams p)
     }
 }
 
+// forward_gradients (image.cpp:72-95): circular forward differences per plane
+__global__ void k_forward_gradients(const float* img, float* gx, float* gy, int H, int W, size_t n)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const size_t plane = (size_t)H * W;
+        const size_t pl = i / plane, r = i - pl * plane;
+        const int y = (int)(r / W), x = (int)(r - (size_t)y * W);
+        const float* base = img + pl * plane;
+        const float v = base[r];
+        gx[i] = base[(size_t)y * W + (x + 1 == W ? 0 : x + 1)] - v;
+        gy[i] = base[(size_t)(y + 1 == H ? 0 : y + 1) * W + x] - v;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_forward_gradients(const float* img, float* gx, float* gy, int planes, int H, int W,
+                                     int nsm, cudaStream_t st)
+{
+    const size_t n = (size_t)planes * H * W;
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)nsm * 8);
+    k_forward_gradients<<<blocks, 256, 0, st>>>(img, gx, gy, H, W, n);
+    return cudaGetLastError();
+}
 
 size_t blf_plain_smem(int cg, int cs, int R)
 {

@@ -538,3 +538,14 @@ def test_blf_brute_standalone_batch_and_errors(gpu, oracle):
         gpu.blf_brute(bad, None, gpu.RangeSpatialParams(1.0, 0.1))
     with pytest.raises(gpu.InvalidArgument):
         gpu.blf_brute(img, _img(oracle, 1, 16, 17, 6), gpu.RangeSpatialParams(1.0, 0.1))
+
+
+def test_forward_gradients_standalone(gpu, oracle):
+    """forward_gradients (image.cpp:72-95), exact in fp32 (one subtraction)."""
+    import torch
+    img = _img(oracle, 3, 19, 23, 42).astype(np.float32)
+    gx, gy = gpu.forward_gradients(img)
+    rx, ry = oracle.forward_gradients(img.astype(np.float64))
+    assert maxabs(gx, rx.astype(np.float32)) == 0.0 and maxabs(gy, ry.astype(np.float32)) == 0.0
+    tx, ty = gpu.forward_gradients(torch.from_numpy(img).cuda())
+    assert maxabs(tx.cpu().numpy(), gx) == 0.0 and maxabs(ty.cpu().numpy(), gy) == 0.0
