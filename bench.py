@@ -340,6 +340,24 @@ def run_ours(args, cfg):
     S = 8 * cfg.height * (cfg.width // 2 + 1)
     solve_bytes = planes * (16 * cfg.height * cfg.width + 4 * S)
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof_dt = None
+    if args.backend == "dt":
+        # DT filter design traffic per slot (plane-axis) pixel and smooth, T = 3
+        # DT iterations (k_dt.cu): prep reads the two fp32 source planes and
+        # writes x, g01 (24 B); the two ct scans read g01 and write ct (32 B);
+        # per iteration and direction a prefix scan (16 B) and a window
+        # (ct + pc read, x written: 24 B) = 80 B.  Padded grid when pad > 0.
+        hp, wp = cfg.height + 2 * args.pad, cfg.width + 2 * args.pad
+        slots = 2 * n * cfg.channels
+        dt_bytes = slots * hp * wp * (24 + 32 + 80 * 3)
+        roof_dt = {"bound": "hbm", "kernel": "k_dt_* (the domain-transform filter stage)",
+                   "achieved": dt_bytes / (blf_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                   "frac": dt_bytes / (blf_ms * 1e-3) / 1e9 / hbm_peak,
+                   "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                   "bytes_per_launch": dt_bytes, "launch_ms": blf_ms,
+                   "note": "design traffic of the scan / window kernels (296 B per slot pixel); "
+                           "the reference algorithm's minimum (read src + guide, write target) "
+                           "is 12 B"}
 
     mp_step = cfg.height * cfg.width * n * cfg.iters / 1e6
     if mode == "shard":
@@ -411,7 +429,7 @@ def run_ours(args, cfg):
                 "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2",
                 "decomposition": {"weak": "independent images per rank",
                                   "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]}),
-            "roofline": None if args.backend != "brute" else {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
+            "roofline": roof_dt if args.backend != "brute" else {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
                          "achieved": achieved / 1e9, "peak": mufu_rate / 1e9, "unit": "Gexp/s",
                          "frac": achieved / mufu_rate,
                          "peak_source": "measured MUFU.EX2 probe on this GPU "
