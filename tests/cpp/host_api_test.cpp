@@ -105,6 +105,21 @@ int main()
         EXPECT(t1);
         EXPECT(t2);
     }
+    {
+        // blf_brute: constants are fixed points; a guide of the wrong shape throws
+        blfls::Image cst(20, 12, 3, 0.25), gd(20, 12, 1, 0.5), bad(21, 12, 1, 0.5);
+        blfls::Image f = blfls::blf_brute(cst, gd, {2.0, 0.1});
+        double m5 = 0.0;
+        for (std::size_t i = 0; i < f.size(); ++i) m5 = std::fmax(m5, std::fabs(f.data()[i] - 0.25));
+        EXPECT(m5 < 1e-6);
+        bool t3 = false;
+        try {
+            blfls::blf_brute(cst, bad, {2.0, 0.1});
+        } catch (const std::invalid_argument&) {
+            t3 = true;
+        }
+        EXPECT(t3);
+    }
     if (fails == 0) std::printf("OK\n");
     return fails == 0 ? 0 : 1;
 }
