@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--band-exchange", default="peer", choices=["peer", "allgather"],
+                    help="row-band mode (c4, N > 1): fused peer stores or an NCCL all_gather")
     ap.add_argument("--backend", default="brute", choices=["brute", "grid", "dt"],
                     help="gradient filter: brute-force BLF (north star) or the reference's bilateral grid")
     ap.add_argument("--pad", type=int, default=0, help="reflect padding (reference default 16)")
@@ -464,14 +466,18 @@ def run_band(args, cfg, world, rank, dev, peaks, peak_src):
     import torch.distributed as dist
 
     import paper_1812_07122_b200 as P
-    from paper_1812_07122_b200.multigpu import band_blf_ls, gpu_band_ops
+    from paper_1812_07122_b200.multigpu import GpuBandPeers, band_blf_ls, gpu_band_ops
     img = P.generate(cfg.height, cfg.width, cfg.seeds(0), n_sites=cfg.n_sites,
                      p_salt_pepper=cfg.p_salt_pepper, device=dev).view(cfg.channels, cfg.height,
                                                                        cfg.width)
     fr, so = gpu_band_ops(cfg.height, cfg.width, cfg.channels, 0, lam=cfg.lam, sigma_s=cfg.sigma_s,
-                          sigma_r=cfg.sigma_r, radius=cfg.radius, device=dev)
+                          sigma_r=cfg.sigma_r, radius=cfg.radius, device=dev,
+                          fused=args.band_exchange == "peer")
+    fused = isinstance(fr, GpuBandPeers)
 
     def step():
+        if fused:
+            return band_blf_ls(img, None, cfg.iters, peers=fr, solve=so)
         return band_blf_ls(img, None, cfg.iters, filter_rows=fr, solve=so)
 
     for _ in range(max(3, args.warmup)):
@@ -503,8 +509,11 @@ def run_band(args, cfg, world, rank, dev, peaks, peak_src):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded Voronoi + ramp + noise, BASELINE generator, generated on device)",
                 "config": config_json(cfg, world, {
-                    "decomposition": f"one image in {world} row bands; all_gather of band targets "
-                                     "over NCCL; redundant full FFT solve per rank",
+                    "decomposition": f"one image in {world} row bands; " + (
+                        "band targets stored into every rank's symmetric-memory buffers by the "
+                        "filter kernel (NVLink peer stores) + device barrier"
+                        if fused else "all_gather of band targets over NCCL") +
+                        "; redundant full FFT solve per rank",
                     "l2": "inputs larger than L2"}),
                 "gpu_launches": None, "clocks": clocks.summary(), "e2e": None, "cpu_baseline": None}
         print(json.dumps(line), flush=True)

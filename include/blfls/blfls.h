@@ -136,6 +136,17 @@ blfls_status blfls_filter_gradients(blfls_plan_t plan, const float* img, const f
 blfls_status blfls_filter_gradients_rows(blfls_plan_t plan, const float* img, const float* guide,
                                          int y0, int y1, float* tx, float* ty, void* stream,
                                          unsigned flags);
+/* Fused band exchange for multi-GPU row bands: as blfls_filter_gradients_rows,
+ * but every target of rows [y0, y1) is stored at its global position in the
+ * full-height (channels x H x W) tx / ty buffers of all `npeers` ranks (1..8,
+ * NVLink peer-mapped device pointers, e.g. symmetric-memory buffers) by the
+ * filter kernel itself, so no separate all-gather follows; the caller makes
+ * the stores visible with a device barrier before the solve.  Brute-force
+ * backend, pad 0, device pointers. */
+blfls_status blfls_filter_gradients_rows_peers(blfls_plan_t plan, const float* img,
+                                               const float* guide, int y0, int y1,
+                                               float* const* tx_peers, float* const* ty_peers,
+                                               int npeers, void* stream, unsigned flags);
 
 /* lsgrad_solve_fft(g, {tx, ty}, {lambda, pad}) (solver.cpp:88-124) with the
  * plan's pad (image and targets reflect-padded as plain rasters, result

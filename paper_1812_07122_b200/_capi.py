@@ -35,7 +35,7 @@ EXPORTS = (
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
     "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
     "blfls_version", "blfls_abi_version", "blfls_gaussian_blur", "blfls_blf_brute",
-    "blfls_forward_gradients",
+    "blfls_forward_gradients", "blfls_filter_gradients_rows_peers",
 )
 
 
@@ -106,6 +106,8 @@ def lib() -> C.CDLL:
             L.blfls_debug_ranges.argtypes = [vp, C.POINTER(C.c_float)]
             L.blfls_mufu_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
             L.blfls_gaussian_blur.argtypes = [fp, ip, ip, ip, C.c_double, fp, ip, vp, C.c_uint]
+            L.blfls_filter_gradients_rows_peers.argtypes = [vp, fp, fp, ip, ip, C.POINTER(C.c_void_p),
+                                                            C.POINTER(C.c_void_p), ip, vp, C.c_uint]
             L.blfls_forward_gradients.argtypes = [fp, ip, ip, ip, fp, fp, ip, vp, C.c_uint]
             L.blfls_blf_brute.argtypes = [fp, ip, fp, ip, ip, ip, ip, ip, C.c_double, C.c_double, fp,
                                           ip, vp, C.c_uint]

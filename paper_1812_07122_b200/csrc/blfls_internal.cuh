@@ -11,6 +11,7 @@
 namespace blfls {
 
 constexpr int kMaxRadius = 48;     // smem tile envelope (radius <= 48)
+constexpr int kMaxPeers = 8;       // fused band exchange: ranks of one NVLink domain
 constexpr int kMaxFftRadices = 32;
 constexpr int kMaxGenericRadix = 31;
 
@@ -104,6 +105,12 @@ struct BlfParams {
                            // gradients of a unit-range image
     float cs[kMaxRadius + 1];  // log2 spatial weight -d^2/(2 sigma_s^2) * log2(e)
     float wrow[kMaxRadius + 1]; // exp2(cs[d]) : row factor
+    // fused band exchange (multi-GPU row bands): npeers > 0 writes every target
+    // into the full-height tx / ty of each peer (NVLink peer-mapped pointers,
+    // rank order) instead of tx / ty -- the all-gather done by the epilogue
+    int npeers;
+    float* peer_tx[kMaxPeers];
+    float* peer_ty[kMaxPeers];
 };
 
 // bilateral-grid backend (k_grid.cu)

@@ -1162,6 +1162,56 @@ blfls_status blfls_filter_gradients_rows(blfls_plan_t p, const float* img, const
     return join_out(p, us, flags);
 }
 
+blfls_status blfls_filter_gradients_rows_peers(blfls_plan_t p, const float* img, const float* guide,
+                                               int y0, int y1, float* const* tx_peers,
+                                               float* const* ty_peers, int npeers, void* stream,
+                                               unsigned flags)
+{
+    blfls_status r = validate_batch(p, 1);
+    if (r) return r;
+    if (p->pad) return fail(BLFLS_EUNSUPPORTED, "stage entry points require pad == 0");
+    if (p->prm.backend != BLFLS_BACKEND_BRUTE)
+        return fail(BLFLS_EUNSUPPORTED, "rows: row bands need the brute-force backend");
+    if (npeers < 1 || npeers > kMaxPeers || !tx_peers || !ty_peers)
+        return fail(BLFLS_EINVAL, "rows_peers: 1..8 peer buffers");
+    if (y0 < 0 || y1 > p->prm.height || y0 >= y1) return fail(BLFLS_EINVAL, "rows: bad row range");
+    if ((p->prm.guide_channels == 0) != (guide == nullptr))
+        return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
+    if (flags & BLFLS_HOST_PTRS) return fail(BLFLS_EINVAL, "rows: device pointers only");
+    for (int j = 0; j < npeers; ++j)
+        if (!tx_peers[j] || !ty_peers[j]) return fail(BLFLS_EINVAL, "rows_peers: null peer buffer");
+    if ((r = set_device(p))) return r;
+    cudaStream_t us = (cudaStream_t)stream;
+    if ((r = fork_in(p, us))) return r;
+    cudaStream_t st = p->ps;
+    if (guide && (r = enq_minmax(p, guide, (size_t)p->prm.guide_channels * p->plane, 1, p->glohi, st)))
+        return r;
+    if ((r = enq_minmax(p, img, (size_t)p->prm.channels * p->plane, 1, p->lohi, st))) return r;
+    // the band's targets go straight to every rank's full-height buffers
+    BlfParams b = p->blf;
+    b.f = img;
+    b.guide = guide;
+    b.tx = nullptr;
+    b.ty = nullptr;
+    b.lohi = p->lohi;
+    b.glohi = p->glohi;
+    b.y0 = y0;
+    b.y1 = y1;
+    b.out_rows = p->Hp;
+    b.normalized_out = 0;
+    b.x2_poly = -1;  // the experiment kernels have no peer epilogue
+    b.legacy_joint3 = 0;
+    b.npeers = npeers;
+    for (int j = 0; j < npeers; ++j) {
+        b.peer_tx[j] = tx_peers[j];
+        b.peer_ty[j] = ty_peers[j];
+    }
+    CK(launch_grad_blf(b, p->mode, 1, st));
+    p->launches++;
+    p->stats.blf_launches++;
+    return join_out(p, us, flags);
+}
+
 blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const float* ty, int batch,
                          float* u, void* stream, unsigned flags)
 {

@@ -55,6 +55,17 @@ __device__ __forceinline__ float poly_ex2(float x)
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// one target value: the local band buffer, or (fused band exchange) the
+// same offset of every peer's full-height buffer over NVLink
+__device__ __forceinline__ void store_target(const BlfParams& p, int axis, size_t off, float v)
+{
+    if (p.npeers == 0) {
+        (axis == 0 ? p.tx : p.ty)[off] = v;
+        return;
+    }
+    for (int j = 0; j < p.npeers; ++j) (axis == 0 ? p.peer_tx[j] : p.peer_ty[j])[off] = v;
+}
+
 __device__ __forceinline__ void decode_range(const uint32_t* lohi, int b, float coef, float& s,
                                              float& range)
 {
@@ -225,14 +236,13 @@ __global__ void __launch_bounds__(16 * TH) k_grad_blf(const BlfParams p)
         }
         // ---- epilogue
         if (oy < p.y1) {
-            float* dst = axis == 0 ? p.tx : p.ty;
             const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                float* o = dst + ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow;
+                const size_t o = ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow + ox;
 #pragma unroll
                 for (int q = 0; q < P; ++q)
-                    if (ox + q < W) o[ox + q] = num[c][q] / z[q] * oscale;
+                    if (ox + q < W) store_target(p, axis, o + q, num[c][q] / z[q] * oscale);
             }
         }
     }
@@ -679,12 +689,11 @@ __global__ void __launch_bounds__(256) k_grad_blf_any(const BlfParams p)
             }
         }
         if (oy < p.y1) {
-            float* dst = axis == 0 ? p.tx : p.ty;
             const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
             for (int c = 0; c < NC; ++c) {
-                float* o = dst + ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow;
+                const size_t o = ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow + ox;
                 for (int q = 0; q < P; ++q)
-                    if (ox + q < W) o[ox + q] = num[c][q] / z[q] * oscale;
+                    if (ox + q < W) store_target(p, axis, o + q, num[c][q] / z[q] * oscale);
             }
         }
     }

@@ -67,13 +67,19 @@ def batch_shard(batch: int, world: int, rank: int) -> tuple[int, int]:
     return i0, i0 + base + (1 if rank < extra else 0)
 
 
-def band_blf_ls(f0, guide, iters: int, *, filter_rows: Callable, solve: Callable, group=None,
-                xp=None):
+def band_blf_ls(f0, guide, iters: int, *, filter_rows: Callable = None, solve: Callable,
+                group=None, xp=None, peers=None):
     """Band-decomposed BLF-LS cascade.
 
     f0: the full image (C, H, W) on this rank (every rank holds it).
     filter_rows(f, guide, y0, y1) -> (tx_band, ty_band) of shape (C, y1-y0, W)
-        targets of the band in RAW units (blfls_filter_gradients_rows).
+        targets of the band in RAW units (blfls_filter_gradients_rows); the
+        bands are then all-gathered (NCCL over NVLink / NVSwitch, gloo on CPU).
+    peers: the fused exchange instead (blfls_filter_gradients_rows_peers): an
+        object with .filter(f, guide, y0, y1) that stores the band's targets
+        straight into every rank's full-height buffers, .barrier() (all ranks'
+        stores visible / all ranks done reading) and .targets() -> (tx, ty)
+        of this rank; no separate collective.
     solve(f, tx, ty) -> next full image (blfls_solve).
     Returns the final full image (identical on every rank).
     """
@@ -88,6 +94,13 @@ def band_blf_ls(f0, guide, iters: int, *, filter_rows: Callable, solve: Callable
     f = f0
     for _ in range(iters):
         y0, y1 = bands[rank]
+        if peers is not None:
+            peers.barrier()  # every rank finished reading the previous targets
+            peers.filter(f, guide, y0, y1)
+            peers.barrier()  # every band's targets landed in every rank's buffers
+            tx, ty = peers.targets()
+            f = solve(f, tx, ty)
+            continue
         tx_b, ty_b = filter_rows(f, guide, y0, y1)
         # pad to the common band height so all ranks contribute equal chunks
         pad = torch.zeros((2, C_, hb, W), dtype=f.dtype, device=f.device)
@@ -102,6 +115,46 @@ def band_blf_ls(f0, guide, iters: int, *, filter_rows: Callable, solve: Callable
         ty = torch.cat([gathered[b, 1, :, : y1b - y0b] for b, (y0b, y1b) in enumerate(bands)], dim=1)
         f = solve(f, tx.contiguous(), ty.contiguous())
     return f
+
+
+class GpuBandPeers:
+    """Fused band exchange on CUDA: tx / ty live in symmetric memory
+    (torch.distributed._symmetric_memory: every rank maps every peer's
+    buffer over NVLink), blfls_filter_gradients_rows_peers stores each band's
+    targets into all of them from the filter kernel's epilogue, and the
+    symmetric-memory device barrier orders the stores against the solve."""
+
+    def __init__(self, plan, channels, height, width, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        from . import _capi
+        self.plan, self.lib, self._capi = plan, _capi.lib(), _capi
+        self.device = device
+        group = group or dist.group.WORLD
+        n = channels * height * width
+        self.buf = symm.empty((2, channels, height, width), dtype=torch.float32, device=device)
+        self.hdl = symm.rendezvous(self.buf, group)
+        ptrs = list(self.hdl.buffer_ptrs)
+        self.np = len(ptrs)
+        self.txp = (C.c_void_p * self.np)(*[p for p in ptrs])
+        self.typ = (C.c_void_p * self.np)(*[p + 4 * n for p in ptrs])
+
+    def _stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def filter(self, f, guide, y0, y1):
+        self._capi.check(self.lib.blfls_filter_gradients_rows_peers(
+            self.plan.handle, f.data_ptr(), None if guide is None else guide.data_ptr(), y0, y1,
+            self.txp, self.typ, self.np, self._stream(), self._capi.DEVICE_PTRS))
+
+    def barrier(self):
+        self.hdl.barrier(channel=0)
+
+    def targets(self):
+        return self.buf[0], self.buf[1]
 
 
 def batch_blf_ls(images, guides, *, lam, sigma_s, sigma_r, iters, radius, group=None,
@@ -132,8 +185,10 @@ def batch_blf_ls(images, guides, *, lam, sigma_s, sigma_r, iters, radius, group=
 
 
 def gpu_band_ops(height, width, channels, guide_channels, *, lam, sigma_s, sigma_r, radius,
-                 device):
-    """(filter_rows, solve) bound to the C ABI on CUDA `device` for band_blf_ls."""
+                 device, fused=False, group=None):
+    """(filter_rows, solve) bound to the C ABI on CUDA `device` for band_blf_ls;
+    fused=True returns (GpuBandPeers, solve) for the fused peer-store exchange
+    (falls back to the all-gather pair when symmetric memory is unavailable)."""
     import torch
 
     from . import _capi
@@ -160,4 +215,9 @@ def gpu_band_ops(height, width, channels, guide_channels, *, lam, sigma_s, sigma
                                   u.data_ptr(), stream(), _capi.DEVICE_PTRS))
         return u
 
+    if fused:
+        try:
+            return GpuBandPeers(plan, channels, height, width, device, group), solve
+        except Exception:  # no symmetric memory / NVLink P2P here: keep the collective
+            pass
     return filter_rows, solve

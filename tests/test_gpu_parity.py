@@ -549,3 +549,45 @@ def test_forward_gradients_standalone(gpu, oracle):
     assert maxabs(gx, rx.astype(np.float32)) == 0.0 and maxabs(gy, ry.astype(np.float32)) == 0.0
     tx, ty = gpu.forward_gradients(torch.from_numpy(img).cuda())
     assert maxabs(tx.cpu().numpy(), gx) == 0.0 and maxabs(ty.cpu().numpy(), gy) == 0.0
+
+
+@pytest.mark.parametrize("nbands,npeers,guided", [(2, 2, False), (3, 4, True), (1, 1, False)])
+def test_band_peer_stores_match_band_filter(gpu, oracle, nbands, npeers, guided):
+    """The fused band exchange's epilogue (blfls_filter_gradients_rows_peers):
+    every band's targets land at their global rows in all `npeers` destination
+    buffers (local stand-ins for NVLink peer buffers: no rank waits on another),
+    bit-identical to the plain band filter; then the solve matches the
+    single-GPU cascade exactly."""
+    import ctypes as C
+
+    import torch
+    from paper_1812_07122_b200 import _capi
+    from paper_1812_07122_b200.multigpu import band_rows, gpu_band_ops
+    c, h, w = 3, 72, 96
+    img = torch.from_numpy(_img(oracle, c, h, w, 31)).cuda()
+    guide = torch.from_numpy(_img(oracle, 1, h, w, 32)).cuda() if guided else None
+    kw = dict(lam=1500.0, sigma_s=5.0, sigma_r=0.08, radius=5)
+    fr, so = gpu_band_ops(h, w, c, 1 if guided else 0, device=0, **kw)
+    from paper_1812_07122_b200.blfls import get_plan
+    plan = get_plan(h, w, c, 1 if guided else 0, 5, 5.0, 0.08, 1500.0, 1, 0)
+    bufs = [torch.full((2, c, h, w), float("nan"), device="cuda") for _ in range(npeers)]
+    txp = (C.c_void_p * npeers)(*[b[0].data_ptr() for b in bufs])
+    typ = (C.c_void_p * npeers)(*[b[1].data_ptr() for b in bufs])
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for y0, y1 in band_rows(h, nbands):
+        _capi.check(_capi.lib().blfls_filter_gradients_rows_peers(
+            plan.handle, img.data_ptr(), None if guide is None else guide.data_ptr(), y0, y1, txp,
+            typ, npeers, stream, _capi.DEVICE_PTRS))
+    parts = [fr(img, guide, y0, y1) for y0, y1 in band_rows(h, nbands)]
+    tx = torch.cat([p[0] for p in parts], dim=1)
+    ty = torch.cat([p[1] for p in parts], dim=1)
+    torch.cuda.synchronize()
+    for b in bufs:
+        assert torch.equal(b[0], tx) and torch.equal(b[1], ty)
+    u = so(img, bufs[-1][0].contiguous(), bufs[-1][1].contiguous())
+    ref = gpu.blf_ls(img, guide, iters=1, **kw)
+    assert (u - ref).abs().max().item() == 0.0
+    with pytest.raises(gpu.InvalidArgument):
+        _capi.check(_capi.lib().blfls_filter_gradients_rows_peers(
+            plan.handle, img.data_ptr(), None if guide is None else guide.data_ptr(), 0, h, txp,
+            typ, 9, stream, _capi.DEVICE_PTRS))

@@ -186,3 +186,51 @@ def test_batch_blf_ls_api_world2_dt_backend(oracle):
         for i in range(3):
             ref = oracle.nc_ls(imgs[i], lam=500.0, sigma_s=3.0, sigma_r=0.1, dt_iters=2, pad=2)
             assert np.abs(res[r][i] - ref).max() == 0.0
+
+
+class _SharedPeers:
+    """CPU stand-in for GpuBandPeers: every rank's full-height targets live in
+    shared-memory tensors all processes map (like NVLink peer buffers); the
+    filter writes its band into all of them, dist.barrier is the device
+    barrier."""
+
+    def __init__(self, bufs, rank):
+        self.bufs, self.rank = bufs, rank
+
+    def filter(self, f, guide, y0, y1):
+        fr, _ = oracle_ops()
+        tx_b, ty_b = fr(f, guide, y0, y1)
+        for b in self.bufs:
+            b[0, :, y0:y1] = tx_b
+            b[1, :, y0:y1] = ty_b
+
+    def barrier(self):
+        dist.barrier()
+
+    def targets(self):
+        b = self.bufs[self.rank]
+        return b[0].clone(), b[1].clone()
+
+
+def _band_peer_worker(rank, world, port, img, bufs, iters, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, so = oracle_ops()
+        out = band_blf_ls(torch.from_numpy(img), None, iters, solve=so,
+                          peers=_SharedPeers(bufs, rank))
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_band_driver_peer_exchange_world2(oracle):
+    """The fused-exchange band driver (peer stores + barriers, no collective)
+    equals the single-process cascade on every rank."""
+    rng = np.random.default_rng(11)
+    img = rng.random((1, 24, 20))
+    bufs = [torch.zeros((2, 1, 24, 20), dtype=torch.float64).share_memory_() for _ in range(2)]
+    res = _run(2, _band_peer_worker, img, bufs, 2)
+    ref = oracle.blf_ls(img, iters=2, **PRM)
+    for r in range(2):
+        assert np.abs(res[r] - ref).max() <= 1e-12
