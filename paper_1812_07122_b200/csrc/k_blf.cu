@@ -82,7 +82,9 @@ __device__ __forceinline__ void decode_range(const uint32_t* lohi, int b, float 
 //         exponential per tap serves all three channels.
 // POLY: every POLY-th tap of a row evaluates its exponential with poly_ex2
 // on the FMA pipe instead of MUFU.EX2 (0 = never), balancing the two pipes.
-template <int R, int P, int MODE, int POLY, int TH = 16>
+// PEERS: the fused band exchange (multi-GPU row bands, p.npeers > 0) -- a
+// separate instantiation so the single-GPU kernels carry no peer code.
+template <int R, int P, int MODE, int POLY, int TH = 16, bool PEERS = false>
 __global__ void __launch_bounds__(16 * TH) k_grad_blf(const BlfParams p)
 {
     constexpr int TW = 16 * P;
@@ -241,8 +243,14 @@ __global__ void __launch_bounds__(16 * TH) k_grad_blf(const BlfParams p)
             for (int c = 0; c < NC; ++c) {
                 const size_t o = ((size_t)b * C + c0 + c) * ((size_t)p.out_rows * W) + orow + ox;
 #pragma unroll
-                for (int q = 0; q < P; ++q)
-                    if (ox + q < W) store_target(p, axis, o + q, num[c][q] / z[q] * oscale);
+                for (int q = 0; q < P; ++q) {
+                    if (ox + q >= W) continue;
+                    const float v = num[c][q] / z[q] * oscale;
+                    if constexpr (PEERS)
+                        store_target(p, axis, o + q, v);
+                    else
+                        (axis == 0 ? p.tx : p.ty)[o + q] = v;
+                }
             }
         }
     }
@@ -701,7 +709,7 @@ __global__ void __launch_bounds__(256) k_grad_blf_any(const BlfParams p)
 
 // ------------------------------------------------------------- dispatch --
 
-template <int R, int P, int MODE, int POLY, int TH>
+template <int R, int P, int MODE, int POLY, int TH, bool PEERS = false>
 static cudaError_t launch_fixed_th(const BlfParams& p, int nz, cudaStream_t st)
 {
     constexpr int TW = 16 * P;
@@ -709,11 +717,11 @@ static cudaError_t launch_fixed_th(const BlfParams& p, int nz, cudaStream_t st)
     constexpr int NARR = MODE == 0 ? 2 : (MODE == 1 ? 4 : 8);
     const size_t smem = (size_t)NARR * ROWS * PITCH * sizeof(float);
     // not a stream operation: legal while the stream is being captured
-    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE, POLY, TH>,
+    cudaError_t e = cudaFuncSetAttribute(k_grad_blf<R, P, MODE, POLY, TH, PEERS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + TW - 1) / TW, (p.y1 - p.y0 + TH - 1) / TH, nz);
-    k_grad_blf<R, P, MODE, POLY, TH><<<grid, 16 * TH, smem, st>>>(p);
+    k_grad_blf<R, P, MODE, POLY, TH, PEERS><<<grid, 16 * TH, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -823,6 +831,18 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 {
     constexpr int P = 4;
     constexpr int D = kPolyDefault<MODE>;
+    if (p.npeers > 0) {
+        // fused band exchange: peer-storing instantiations at the BASELINE radii
+        // (16-row tiles: a band is a fraction of a large image), any other radius
+        // through the generic-radius kernel
+        switch (p.radius) {
+            case 3: return launch_fixed_th<3, P, MODE, 0, 16, true>(p, nz, st);
+            case 5: return launch_fixed_th<5, P, MODE, 0, 16, true>(p, nz, st);
+            case 7: return launch_fixed_th<7, P, MODE, 0, 16, true>(p, nz, st);
+            case 15: return launch_fixed_th<15, P, MODE, 0, 16, true>(p, nz, st);
+            default: return launch_any<MODE>(p, nz, st);
+        }
+    }
     if constexpr (MODE == 0) {
         if (p.x2_poly >= 0) {
             switch (p.radius) {
