@@ -191,4 +191,18 @@ struct SolveParams {
     int mode;            // column pass: 1 fwd, 2 inv, 3 fwd+scale+inv
 };
 
+// high-radix solve passes (k_solve2.cu): false when no geometry exists for n
+bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,
+                    cudaStream_t st);
+
+// persistent bulk-copy-pipelined row passes (k_solve3.cu): which 0 r2c, 2 c2r
+bool launch_v3_row_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,
+                        cudaStream_t st, cudaError_t* err);
+
+// pair-symmetric brute-force filter (k_blf_sym.cu); false: not covered
+bool launch_grad_blf_sym(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err);
+
+// shared-gray-guide filter with packed accumulation (k_blf_j3.cu); false: not covered
+bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
+
 }  // namespace blfls

@@ -890,6 +890,9 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 // mode: 0 self, 1 joint per-channel / single-channel, 2 joint shared gray guide (C == 3)
 cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st)
 {
+    cudaError_t e = cudaSuccess;
+    if (launch_grad_blf_sym(p, mode, batch, st, &e)) return e;
+    if (mode == 2 && launch_grad_blf_j3(p, batch, st, &e)) return e;
     switch (mode) {
         case 0: return dispatch_mode<0>(p, batch * p.C, st);
         case 1: return dispatch_mode<1>(p, batch * p.C, st);

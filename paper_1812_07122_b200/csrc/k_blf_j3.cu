@@ -1,0 +1,263 @@
+// k_blf_j3.cu -- shared-grayscale-guide brute-force BLF (MODE 2: three image
+// channels filtered with one guide, the joint variant of bilateral.cpp:28-77
+// as filter_gradients calls it per channel with the same guide,
+// pipelines.cpp:33-53), one gradient axis per CTA.
+//
+// One exponential per tap serves the three channels; the four sums it feeds
+// (three numerators and the normaliser) are updated by two packed FFMA2
+// (sm_100 f32x2 with the weight as a broadcast scalar operand): the sources
+// are interleaved in shared memory as {g0, g1} and {g2, 1}.  Per tap:
+//   FADD (guide difference), FFMA (exponent: cs[|dy|] + cs[|dx|] - d^2),
+//   MUFU.EX2, 2 x FFMA2
+// against FADD, FFMA, MUFU.EX2, FADD, 3 x FFMA in k_grad_blf<MODE 2>, which
+// is issue-bound at ~8.8 instructions per MUFU.EX2.  The window is streamed
+// column by column (LDS.128 = two columns of one interleaved array) instead
+// of being held in registers, so the kernel stays at 4 CTAs per SM; the
+// interleaved rows are chunk-swizzled (j3_sw) so the LDS.128 are conflict-free.
+#include <cstdlib>
+
+#include "blfls_internal.cuh"
+
+namespace blfls {
+
+namespace {
+
+constexpr float kJ3Sentinel = 1.0e15f;
+
+__device__ __forceinline__ float j3_ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// d.xy = {a, a} * b.xy + c.xy
+__device__ __forceinline__ unsigned long long j3_ffma2(float a, unsigned long long b, unsigned long long c)
+{
+    unsigned long long aa, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float2 j3_unpack(unsigned long long r)
+{
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+// 16-byte chunk swizzle of the interleaved source rows: a thread's 4 output
+// columns make consecutive lanes read chunks 2 apart, so quarter-warps would
+// hit each 128-byte bank line twice; flipping bit 0 of the chunk index in
+// every odd group of 8 chunks spreads the 8 reads over the 8 bank groups
+__device__ __forceinline__ int j3_sw(int col)
+{
+    const int k = col >> 1;
+    return ((k ^ ((k >> 3) & 1)) << 1) | (col & 1);
+}
+__device__ __forceinline__ void j3_decode(const uint32_t* lohi, int b, float coef, float& s, float& range)
+{
+    const float lo = ordered_to_float(lohi[2 * b]);
+    const float hi = ordered_to_float(lohi[2 * b + 1]);
+    range = hi - lo;
+    s = range > 0.f ? coef / range : coef;
+}
+
+}  // namespace
+
+// TH output rows x 64 output columns, 16 threads per row, P = 4 columns per
+// thread; blockIdx.z = image * 2 + axis
+template <int R, int TH>
+struct J3Geom {
+    static constexpr int P = 4, TW = 64, NT = 16 * TH;
+    static constexpr int ROWS = TH + 2 * R;
+    static constexpr int COLS = TW + 2 * R;
+    static constexpr int VN = P + 2 * R;                      // window columns per thread
+    static constexpr int VN4 = (VN + 3) & ~3;                 // rounded to column quads
+    static constexpr int GP = ((COLS + 3) & ~3) + 4;          // guide pitch (floats)
+    static constexpr int SP = (COLS + 3 + 15) & ~15;          // source pitch (float2, 128-byte rows)
+    static constexpr size_t smem_bytes()
+    {
+        return (size_t)ROWS * GP * sizeof(float) + (size_t)2 * ROWS * SP * sizeof(float2);
+    }
+};
+
+// PEERS: fused band exchange (multi-GPU row bands): every target is stored
+// into the full-height buffers of all p.npeers ranks (NVLink peer pointers)
+template <int R, int TH, bool PEERS, int MINB>
+__global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
+{
+    using Gm = J3Geom<R, TH>;
+    constexpr int P = Gm::P, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
+    constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
+    extern __shared__ __align__(16) float smj[];
+    float* G = smj;                                                   // [ROWS][GP]
+    float2* S01 = reinterpret_cast<float2*>(smj + ROWS * GP);         // [ROWS][SP] {g0, g1}
+    float2* S2 = S01 + ROWS * SP;                                     // [ROWS][SP] {g2, 1}
+
+    const int H = p.H, W = p.W;
+    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range, sg, grange;
+    j3_decode(p.lohi, b, p.range_coef, s, range);
+    j3_decode(p.glohi, b, p.range_coef, sg, grange);
+    const float* fimg = p.f + (size_t)b * 3 * plane;
+    const float* gimg = p.guide + (size_t)b * p.GC * plane;
+
+    // ---- prologue: this axis' circular gradients of guide and channels
+    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += NT) {
+        const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
+        const int y = ty0 - R + i, x = tx0 - R + j;
+        const int og = i * GP + j, o = i * SP + j3_sw(j);
+        if (y >= 0 && y < H && x >= 0 && x < W) {
+            const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+            const int y1 = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+            const size_t r0 = (size_t)y * W + x, r1 = (size_t)y1 * W + x1;
+            G[og] = (__ldg(gimg + r1) - __ldg(gimg + r0)) * sg;
+            float g[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float* fc = fimg + (size_t)c * plane;
+                g[c] = __ldg(fc + r1) - __ldg(fc + r0);
+            }
+            S01[o] = make_float2(g[0], g[1]);
+            S2[o] = make_float2(g[2], 1.0f);
+        } else {
+            G[og] = kJ3Sentinel;
+            S01[o] = make_float2(0.f, 0.f);
+            S2[o] = make_float2(0.f, 0.f);
+        }
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int ox = tx0 + tx * P, oy = ty0 + ty;
+    float gs[P];
+    unsigned long long acc01[P], acc2z[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        gs[q] = G[(ty + R) * GP + tx * P + q + R];
+        acc01[q] = 0ull;
+        acc2z[q] = 0ull;
+    }
+#pragma unroll 1
+    for (int dy = -R; dy <= R; ++dy) {
+        const int ady = dy < 0 ? -dy : dy;
+        float ce[R + 1];  // log2 spatial weight of (dy, |dx|)
+#pragma unroll
+        for (int k = 0; k <= R; ++k) ce[k] = p.cs[ady] + p.cs[k];
+        const float* grow = G + (ty + R + dy) * GP + tx * P;
+        const float2* s01 = S01 + (ty + R + dy) * SP;
+        const float2* s2 = S2 + (ty + R + dy) * SP;
+#pragma unroll
+        for (int j4 = 0; j4 < VN4; j4 += 4) {
+            const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+            const float gt[4] = {g4.x, g4.y, g4.z, g4.w};
+            unsigned long long v01[4], v2z[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                // columns tx P + j4 + 2h, + 1: one swizzled 16-byte chunk per array
+                const int pc = j3_sw(tx * P + j4 + 2 * h);
+                const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
+                const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
+                asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
+                asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
+                asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
+                asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h + 1]) : "f"(c.z), "f"(c.w));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j4 + u;
+                if (j >= VN) break;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int dx = j - q - R;
+                    if (dx < -R || dx > R) continue;
+                    const float d = gs[q] - gt[u];
+                    const float w = j3_ex2(fmaf(-d, d, ce[dx < 0 ? -dx : dx]));
+                    acc01[q] = j3_ffma2(w, v01[u], acc01[q]);
+                    acc2z[q] = j3_ffma2(w, v2z[u], acc2z[q]);
+                }
+            }
+        }
+    }
+    if (oy < p.y1) {
+        const float oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
+        float* dst = axis == 0 ? p.tx : p.ty;
+        const size_t pl = (size_t)p.out_rows * W;
+        const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
+        float t[3][P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const float2 n01 = j3_unpack(acc01[q]);
+            const float2 n2z = j3_unpack(acc2z[q]);
+            const float inv = oscale / n2z.y;
+            t[0][q] = n01.x * inv;
+            t[1][q] = n01.y * inv;
+            t[2][q] = n2z.x * inv;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const size_t off = ((size_t)b * 3 + c) * pl + orow + ox;
+            if constexpr (PEERS) {
+                for (int k = 0; k < p.npeers; ++k) {
+                    float* d = (axis == 0 ? p.peer_tx[k] : p.peer_ty[k]) + off;
+                    for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[c][q];
+                }
+            } else if (ox + P <= W && (off & 3) == 0) {
+                *reinterpret_cast<float4*>(dst + off) = make_float4(t[c][0], t[c][1], t[c][2], t[c][3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (ox + q < W) dst[off + q] = t[c][q];
+            }
+        }
+    }
+}
+
+template <int R, int TH, bool PEERS, int MINB>
+static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
+{
+    using Gm = J3Geom<R, TH>;
+    constexpr size_t smem = Gm::smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * batch);
+    k_blf_j3<R, TH, PEERS, MINB><<<grid, Gm::NT, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int R, int TH>
+static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
+{
+    // register cap: 4 CTAs per SM (64 registers, a few spills) or 3 (no spills)
+    static const int minb = [] {
+        const char* e = std::getenv("BLFLS_J3_MINB");
+        return e ? std::atoi(e) : 4;
+    }();
+    if (p.npeers > 0) return launch_j3_t<R, TH, true, 3>(p, batch, st);
+    if (minb == 3) return launch_j3_t<R, TH, false, 3>(p, batch, st);
+    return launch_j3_t<R, TH, false, 4>(p, batch, st);
+}
+
+// Shared-gray-guide filter (mode 2) on the packed kernel at the radii it is
+// instantiated for; false otherwise (the caller runs k_grad_blf<MODE 2>).
+// BLFLS_J3=0 selects the unpacked kernel (A/B experiments).
+bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
+{
+    static const bool enabled = [] {
+        const char* e = std::getenv("BLFLS_J3");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    if (!enabled || p.C != 3) return false;
+    switch (p.radius) {
+        case 3: *err = launch_j3<3, 16>(p, batch, st); return true;
+        case 5: *err = launch_j3<5, 16>(p, batch, st); return true;
+        case 7: *err = launch_j3<7, 16>(p, batch, st); return true;
+        case 15: *err = launch_j3<15, 16>(p, batch, st); return true;
+        default: return false;
+    }
+}
+
+}  // namespace blfls

@@ -506,6 +506,14 @@ static cudaError_t launch_fft_pass(int which, const SolveParams& p, const FftGeo
                                    bool odd, cudaStream_t st)
 {
     const int n = g.desc.n;
+    if (!odd && !g.bluestein) {  // high-radix engine (k_solve2.cu) where a geometry exists
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e3 = cudaSuccess;
+        if (which != 1 && launch_v3_row_pass(which, p, n, g.desc.tw, planes, nsm, st, &e3)) return e3;
+        if (launch_v2_pass(which, p, n, g.desc.tw, planes, nsm, st)) return cudaGetLastError();
+    }
     if (g.ct && !odd) {
 #define BLFLS_CT_LAUNCH(N, VV, TV)                                                          \
     if (n == N && g.V == VV) {                                                             \

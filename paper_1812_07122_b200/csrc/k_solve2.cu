@@ -1,0 +1,303 @@
+// k_solve2.cu -- the periodic least-squares solve (solver.cpp:88-124) on the
+// high-radix engine of fft2.cuh.  Same three passes and the same arithmetic
+// contract as k_solve.cu (divergence fold, 1/(H W den) with a correctly
+// rounded reciprocal, min/max epilogue), but each pass touches shared memory
+// only between its FFT stages:
+//
+//   row r2c : stage 0 reads the fold r = f + lambda (Dx^T Tx + Dy^T Ty)
+//             straight from global; the even/odd split reads the last stage
+//             from shared memory and writes the half spectrum
+//   column  : forward stage 0 reads the spectrum column strip from global;
+//             the inverse's stage 0 applies 1 / (H W den) to its inputs; the
+//             inverse's last stage writes the strip back to global
+//   row c2r : stage 0 builds the half-length complex row from the spectrum
+//             (global); the last stage writes the pixels (crop for padded
+//             grids) and reduces the next iteration's min/max
+//
+// Geometries exist for the even-width BASELINE sizes; every other size (and
+// the stage entry points' forward-only / inverse-only column modes) runs the
+// kernels of k_solve.cu.
+#include "blfls_internal.cuh"
+#include <cstdlib>
+
+#include "fft2.cuh"
+
+namespace blfls {
+
+__device__ __forceinline__ void block_minmax_atomic2(float lo, float hi, uint32_t* slot)
+{
+    __shared__ float slo[32], shi[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        slo[warp] = lo;
+        shi[warp] = hi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        lo = lane < nw ? slo[lane] : INFINITY;
+        hi = lane < nw ? shi[lane] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            atomicMin(slot, float_to_ordered(lo));
+            atomicMax(slot + 1, float_to_ordered(hi));
+        }
+    }
+}
+
+// grid (ceil(H / V), planes); n = W / 2 complex points per row
+template <class G>
+__global__ void __launch_bounds__(G::THREADS) k2_row_r2c(const SolveParams p, const float2* __restrict__ tw)
+{
+    extern __shared__ __align__(16) float2 buf[];
+    constexpr int n = G::N;
+    const int v = threadIdx.x / G::TV, t = threadIdx.x - v * G::TV;
+    const int plane = blockIdx.y;
+    const int y = blockIdx.x * G::V + v;
+    const bool live = y < p.H;
+    const int W = p.W;
+    const size_t poff = (size_t)plane * p.H * W;
+    const size_t roff = poff + (size_t)(live ? y : 0) * W;
+    const size_t rprev = poff + (size_t)(live ? (y == 0 ? p.H - 1 : y - 1) : 0) * W;
+    const float L = p.lambda;
+    const bool fold = p.tx != nullptr;
+    auto ld = [&](int j) -> float2 {
+        if (!live) return make_float2(0.f, 0.f);
+        float2 r = __ldg(reinterpret_cast<const float2*>(p.f + roff) + j);
+        if (fold) {
+            const float2 a = __ldg(reinterpret_cast<const float2*>(p.tx + roff) + j);
+            const float2 b = __ldg(reinterpret_cast<const float2*>(p.ty + roff) + j);
+            const float2 c = __ldg(reinterpret_cast<const float2*>(p.ty + rprev) + j);
+            const float am = __ldg(p.tx + roff + (j == 0 ? W - 1 : 2 * j - 1));
+            r.x = fmaf(L, (am - a.x) + (c.x - b.x), r.x);
+            r.y = fmaf(L, (a.x - a.y) + (c.y - b.y), r.y);
+        }
+        return r;
+    };
+    auto st = [&](int j, float2 z) { buf[G::ra(v, j)] = z; };
+    s2_stage<G, false, 0, false>(t, tw, ld, st);
+    __syncthreads();
+    s2_smem_stages<G, false, false, 1, G::NST>(buf, v, t, tw);
+    // even/odd split: X_k = (Z_k + conj Z_{n-k}) / 2 + e^{-2 pi i k / W} (Z_k - conj Z_{n-k}) / (2i)
+    const int wc = p.wc;
+    for (int idx = threadIdx.x; idx < G::V * wc; idx += G::THREADS) {
+        const int vv = idx / wc, k = idx - vv * wc;
+        const int yy = blockIdx.x * G::V + vv;
+        if (yy >= p.H) continue;
+        const float2 zk = buf[G::ra(vv, k == n ? 0 : k)];
+        const float2 zn = cconj(buf[G::ra(vv, k == 0 ? 0 : n - k)]);
+        const float2 e = cscale(cadd(zk, zn), 0.5f);
+        const float2 o = cscale(cmuli(csub(zk, zn), -1.0f), 0.5f);
+        p.spec[((size_t)plane * p.H + yy) * p.spitch + k] = cadd(e, cmul(__ldg(&p.post[k]), o));
+    }
+}
+
+// grid (ceil(wc / V), planes): V adjacent spectrum columns, forward FFT,
+// 1 / (H W (1 + lambda (4 sin^2(pi u/H) + 4 sin^2(pi v/W)))), inverse FFT
+template <class G>
+__global__ void __launch_bounds__(G::THREADS) k2_col(const SolveParams p, const float2* __restrict__ tw)
+{
+    extern __shared__ __align__(16) float2 buf[];
+    const int v = threadIdx.x % G::V, t = threadIdx.x / G::V;
+    const int plane = blockIdx.y;
+    const int vc = blockIdx.x * G::V + v;
+    const bool live = vc < p.wc;
+    float2* spec = p.spec + (size_t)plane * G::N * p.spitch + (live ? vc : 0);
+    const size_t sp = p.spitch;
+    auto ldg = [&](int u) -> float2 { return live ? __ldcg(spec + (size_t)u * sp) : make_float2(0.f, 0.f); };
+    auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
+    auto lds = [&](int u) { return buf[G::ca(v, u)]; };
+    s2_stage<G, false, 0, false>(t, tw, ldg, sts);
+    __syncthreads();
+    s2_smem_stages<G, true, false, 1, G::NST>(buf, v, t, tw);
+    const float gx = live ? __ldg(&p.gain_x[vc]) : 0.f;
+    const float L = p.lambda, ihw = p.inv_hw;
+    auto lds_scaled = [&](int u) {
+        const float sc = ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f));
+        return cscale(buf[G::ca(v, u)], sc);
+    };
+    auto stg = [&](int u, float2 z) {
+        if (live) spec[(size_t)u * sp] = z;
+    };
+    if constexpr (G::NST == 1) {
+        s2_stage<G, true, 0, false>(t, tw, lds_scaled, stg);
+    } else {
+        s2_stage<G, true, 0, true>(t, tw, lds_scaled, sts);
+        __syncthreads();
+        s2_smem_stages<G, true, true, 1, G::NST - 1>(buf, v, t, tw);
+        s2_stage<G, true, G::NST - 1, false>(t, tw, lds, stg);
+    }
+}
+
+// grid (ceil(H / V), planes)
+template <class G>
+__global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, const float2* __restrict__ tw)
+{
+    extern __shared__ __align__(16) float2 buf[];
+    constexpr int n = G::N;
+    const int v = threadIdx.x / G::TV, t = threadIdx.x - v * G::TV;
+    const int plane = blockIdx.y;
+    const int y = blockIdx.x * G::V + v;
+    const bool live = y < p.H;
+    const float2* srow = p.spec + ((size_t)plane * p.H + (live ? y : 0)) * p.spitch;
+    // Z_k = (X_k + conj X_{n-k}) + i e^{+2 pi i k / W} (X_k - conj X_{n-k}); c2r
+    // ignores Im of DC and Nyquist
+    auto ldg = [&](int k) -> float2 {
+        if (!live) return make_float2(0.f, 0.f);
+        float2 xk = __ldcg(srow + k);
+        float2 xn = __ldcg(srow + (n - k));
+        if (k == 0) {
+            xk.y = 0.f;
+            xn.y = 0.f;
+        }
+        const float2 xnc = cconj(xn);
+        const float2 a = cadd(xk, xnc);
+        const float2 bb = cmul(csub(xk, xnc), cconj(__ldg(&p.post[k])));
+        return cadd(a, cmuli(bb, 1.0f));
+    };
+    auto sts = [&](int j, float2 z) { buf[G::ra(v, j)] = z; };
+    auto lds = [&](int j) { return buf[G::ra(v, j)]; };
+    float lo = INFINITY, hi = -INFINITY;
+    const int yo = y - p.opad;
+    const bool out_row = live && yo >= 0 && yo < p.oH;
+    float* orow = p.out + (size_t)plane * p.oH * p.oW + (size_t)(out_row ? yo : 0) * p.oW;
+    auto sto = [&](int j, float2 z) {
+        if (!out_row) return;
+        if (p.opad == 0) {
+            *reinterpret_cast<float2*>(orow + 2 * j) = z;
+            lo = fminf(lo, fminf(z.x, z.y));
+            hi = fmaxf(hi, fmaxf(z.x, z.y));
+        } else {
+            const int x0 = 2 * j - p.opad;
+            if (x0 >= 0 && x0 < p.oW) {
+                orow[x0] = z.x;
+                lo = fminf(lo, z.x);
+                hi = fmaxf(hi, z.x);
+            }
+            if (x0 + 1 >= 0 && x0 + 1 < p.oW) {
+                orow[x0 + 1] = z.y;
+                lo = fminf(lo, z.y);
+                hi = fmaxf(hi, z.y);
+            }
+        }
+    };
+    if constexpr (G::NST == 1) {
+        s2_stage<G, true, 0, false>(t, tw, ldg, sto);
+    } else {
+        s2_stage<G, true, 0, false>(t, tw, ldg, sts);
+        __syncthreads();
+        s2_smem_stages<G, false, true, 1, G::NST - 1>(buf, v, t, tw);
+        s2_stage<G, true, G::NST - 1, false>(t, tw, lds, sto);
+    }
+    if (p.lohi_out != nullptr) block_minmax_atomic2(lo, hi, p.lohi_out + 2 * ((p.plane0 + plane) / p.C));
+}
+
+// ------------------------------------------------------------ launchers --
+
+// Row geometries (N = W/2, V rows, TV threads per row, PMAX) and column
+// geometries (N = H, V columns, TV threads per column, PMAX).
+#define BLFLS_V2_ROWS(X) X(256, 16, 8, 32) X(256, 4, 8, 32) X(512, 8, 16, 32) X(512, 2, 16, 32) \
+    X(960, 8, 32, 32) X(960, 2, 32, 32) X(1024, 8, 32, 32) X(1024, 2, 32, 32) X(2048, 4, 64, 32) \
+    X(2048, 1, 64, 32) \
+    X(256, 8, 16, 16) X(512, 8, 32, 16) X(512, 2, 32, 16) X(960, 4, 64, 16) X(960, 1, 64, 16) \
+    X(1024, 4, 64, 16) X(1024, 1, 64, 16) X(2048, 2, 128, 16) X(2048, 1, 128, 16)
+#define BLFLS_V2_COLS(X) X(512, 8, 16, 32) X(512, 2, 16, 32) X(1024, 4, 32, 32) X(1024, 2, 32, 32) \
+    X(1080, 8, 36, 32) X(1080, 4, 40, 32) X(2048, 4, 64, 32) X(2048, 2, 64, 32) X(4096, 4, 128, 32) \
+    X(4096, 2, 128, 32) \
+    X(512, 8, 32, 16) X(512, 2, 32, 16) X(1024, 4, 64, 16) X(1024, 2, 64, 16) X(1080, 4, 72, 16) \
+    X(2048, 4, 128, 16) X(2048, 2, 128, 16) X(4096, 2, 256, 16) X(4096, 4, 256, 16)
+
+template <class K>
+static void set_smem2(K kernel, size_t smem)
+{
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <class G>
+static void launch2(int which, const SolveParams& p, const float2* tw, int planes, cudaStream_t st)
+{
+    constexpr size_t smem = G::smem_bytes();
+    if (which == 1) {
+        dim3 grid((p.wc + G::V - 1) / G::V, planes);
+        set_smem2(k2_col<G>, smem);
+        k2_col<G><<<grid, G::THREADS, smem, st>>>(p, tw);
+    } else if (which == 0) {
+        dim3 grid((p.H + G::V - 1) / G::V, planes);
+        set_smem2(k2_row_r2c<G>, smem);
+        k2_row_r2c<G><<<grid, G::THREADS, smem, st>>>(p, tw);
+    } else {
+        dim3 grid((p.H + G::V - 1) / G::V, planes);
+        set_smem2(k2_row_c2r<G>, smem);
+        k2_row_c2r<G><<<grid, G::THREADS, smem, st>>>(p, tw);
+    }
+}
+
+// Runs pass `which` (0 row r2c, 1 column, 2 row c2r) on the high-radix
+// engine when a geometry exists for length n; returns false otherwise.  The
+// widest geometry that still launches >= 2 CTAs per SM is chosen.
+bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,
+                    cudaStream_t st)
+{
+    static const bool disabled = [] {
+        const char* e = std::getenv("BLFLS_FFT_V1");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    if (disabled) return false;
+    if (which == 1 && p.mode != 3) return false;
+    // passes routed here (bit 0 row r2c, bit 1 column, bit 2 row c2r)
+    static const int passes = [] {
+        const char* e = std::getenv("BLFLS_V2_PASSES");
+        return e ? std::atoi(e) : 6;  // column + row c2r (streaming ncu, r01)
+    }();
+    if (!((passes >> which) & 1)) return false;
+    // radix cap of the row / column engines (experiment knob; default 32)
+    static const int pmax_rows = [] {
+        const char* e = std::getenv("BLFLS_V2_PMAX_ROWS");
+        return e ? std::atoi(e) : 16;
+    }();
+    static const int pmax_cols = [] {
+        const char* e = std::getenv("BLFLS_V2_PMAX_COLS");
+        return e ? std::atoi(e) : 16;
+    }();
+    const int pmax = which == 1 ? pmax_cols : pmax_rows;
+    const int nvec = which == 1 ? p.wc : p.H;
+    int bestV = 0, narrowV = 1 << 30;
+    auto consider = [&](int N, int V, int PM) {
+        if (N != n || PM != pmax) return;
+        const long ctas = (long)planes * ((nvec + V - 1) / V);
+        if (ctas >= 2L * nsm && V > bestV) bestV = V;
+        if (V < narrowV) narrowV = V;
+    };
+#define BLFLS_V2_CONSIDER(N, V, TV, PM) consider(N, V, PM);
+    if (which == 1) {
+        BLFLS_V2_COLS(BLFLS_V2_CONSIDER)
+    } else {
+        BLFLS_V2_ROWS(BLFLS_V2_CONSIDER)
+    }
+#undef BLFLS_V2_CONSIDER
+    const int V = bestV ? bestV : narrowV;
+    if (V == 1 << 30) return false;
+#define BLFLS_V2_GO(N, VV, TV, PM)                                  \
+    if (n == N && V == VV && pmax == PM) {                          \
+        launch2<Fft2<N, VV, TV, PM>>(which, p, tw, planes, st);     \
+        return true;                                                \
+    }
+    if (which == 1) {
+        BLFLS_V2_COLS(BLFLS_V2_GO)
+    } else {
+        BLFLS_V2_ROWS(BLFLS_V2_GO)
+    }
+#undef BLFLS_V2_GO
+    return false;
+}
+
+}  // namespace blfls
