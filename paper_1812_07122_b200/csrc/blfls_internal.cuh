@@ -205,4 +205,7 @@ bool launch_grad_blf_sym(const BlfParams& p, int mode, int batch, cudaStream_t s
 // shared-gray-guide filter with packed accumulation (k_blf_j3.cu); false: not covered
 bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
 
+// self / per-channel-joint filter with packed accumulation (k_blf_p2.cu); false: not covered
+bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err);
+
 }  // namespace blfls

@@ -893,6 +893,7 @@ cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_
     cudaError_t e = cudaSuccess;
     if (launch_grad_blf_sym(p, mode, batch, st, &e)) return e;
     if (mode == 2 && launch_grad_blf_j3(p, batch, st, &e)) return e;
+    if (mode != 2 && launch_grad_blf_p2(p, mode, batch, st, &e)) return e;
     switch (mode) {
         case 0: return dispatch_mode<0>(p, batch * p.C, st);
         case 1: return dispatch_mode<1>(p, batch * p.C, st);

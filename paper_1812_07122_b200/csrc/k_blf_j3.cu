@@ -231,10 +231,11 @@ static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
 template <int R, int TH>
 static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
 {
-    // register cap: 4 CTAs per SM (64 registers, a few spills) or 3 (no spills)
+    // register cap: 3 CTAs per SM (no spills; c5 0.764 of MUFU) or 4 (64
+    // registers, a few spills; 0.755)
     static const int minb = [] {
         const char* e = std::getenv("BLFLS_J3_MINB");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : 3;
     }();
     if (p.npeers > 0) return launch_j3_t<R, TH, true, 3>(p, batch, st);
     if (minb == 3) return launch_j3_t<R, TH, false, 3>(p, batch, st);

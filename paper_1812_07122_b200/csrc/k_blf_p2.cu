@@ -1,0 +1,295 @@
+// k_blf_p2.cu -- self-guided / per-channel-joint brute-force BLF (MODE 0 / 1)
+// with packed accumulation, one gradient axis per CTA (bilateral.cpp:28-77
+// semantics, driven per channel and axis as filter_gradients does,
+// pipelines.cpp:33-53).
+//
+// The two sums of an output (numerator and normaliser) are one f32x2 pair
+// updated by a single FFMA2 with the weight as broadcast scalar: the source
+// is staged interleaved as {v, 1}, so per tap
+//   FADD (guide difference), FFMA (exponent cs[|dy|] + cs[|dx|] - d^2),
+//   MUFU.EX2, FFMA2
+// four instructions against five in k_grad_blf (FADD, FFMA, MUFU, FADD,
+// FFMA).  The freed issue slots let every POLY-th exponential run on the FMA
+// pipe (poly_ex2 of k_blf.cu) next to MUFU.EX2.  Rows of {v, 1} are
+// chunk-swizzled like k_blf_j3.cu so the LDS.128 of a quarter-warp (8 lanes,
+// each 4 columns apart) hit 8 different bank groups.
+#include <cstdlib>
+
+#include "blfls_internal.cuh"
+
+namespace blfls {
+
+namespace {
+
+constexpr float kP2Sentinel = 1.0e15f;
+
+__device__ __forceinline__ float p2_ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// exp2 on the FMA pipe (same polynomial as k_blf.cu poly_ex2)
+__device__ __forceinline__ float p2_poly_ex2(float x)
+{
+    x = fmaxf(x, -125.0f);
+    const float t = x + 12582912.0f;
+    const float j = t - 12582912.0f;
+    const float f = x - j;
+    float p = fmaf(0.001327647129073739f, f, 0.009675541892647743f);
+    p = fmaf(p, f, 0.05550713092088699f);
+    p = fmaf(p, f, 0.24022120237350464f);
+    p = fmaf(p, f, 0.6931469440460205f);
+    p = fmaf(p, f, 1.0000001192092896f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+__device__ __forceinline__ unsigned long long p2_ffma2(float a, unsigned long long b, unsigned long long c)
+{
+    unsigned long long aa, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float2 p2_unpack(unsigned long long r)
+{
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ int p2_sw(int col)
+{
+    const int k = col >> 1;
+    return ((k ^ ((k >> 3) & 1)) << 1) | (col & 1);
+}
+__device__ __forceinline__ void p2_decode(const uint32_t* lohi, int b, float coef, float& s, float& range)
+{
+    const float lo = ordered_to_float(lohi[2 * b]);
+    const float hi = ordered_to_float(lohi[2 * b + 1]);
+    range = hi - lo;
+    s = range > 0.f ? coef / range : coef;
+}
+
+}  // namespace
+
+template <int R, int TH, int MODE>
+struct P2Geom {
+    static constexpr int P = 4, TW = 64, NT = 16 * TH;
+    static constexpr int ROWS = TH + 2 * R;
+    static constexpr int COLS = TW + 2 * R;
+    static constexpr int VN = P + 2 * R;
+    static constexpr int VN4 = (VN + 3) & ~3;
+    static constexpr int GP = MODE == 1 ? ((COLS + 3) & ~3) + 4 : 0;  // planar guide (MODE 1)
+    static constexpr int SP = (COLS + 3 + 15) & ~15;                  // {v, 1} pitch (float2)
+    static constexpr size_t smem_bytes()
+    {
+        return (size_t)ROWS * GP * sizeof(float) + (size_t)ROWS * SP * sizeof(float2);
+    }
+};
+
+// blockIdx.z = plane * 2 + axis, plane = image * C + channel
+template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB>
+__global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
+{
+    using Gm = P2Geom<R, TH, MODE>;
+    constexpr int P = Gm::P, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
+    constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
+    extern __shared__ __align__(16) float smp[];
+    float* G = smp;                                                  // [ROWS][GP] (MODE 1)
+    float2* SV = reinterpret_cast<float2*>(smp + ROWS * GP);         // [ROWS][SP] {v, 1}
+
+    const int H = p.H, W = p.W, C = p.C;
+    const int pl = blockIdx.z >> 1, axis = blockIdx.z & 1;
+    const int b = pl / C, c0 = pl - (pl / C) * C;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range;
+    p2_decode(p.lohi, b, p.range_coef, s, range);
+    float sg = s, grange = range;
+    if (MODE == 1) p2_decode(p.glohi, b, p.range_coef, sg, grange);
+    const float* fimg = p.f + ((size_t)b * C + c0) * plane;
+    const float* gimg = MODE == 0 ? fimg : p.guide + ((size_t)b * p.GC + (p.GC == 1 ? 0 : c0)) * plane;
+
+    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += NT) {
+        const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
+        const int y = ty0 - R + i, x = tx0 - R + j;
+        const int o = i * SP + p2_sw(j);
+        if (y >= 0 && y < H && x >= 0 && x < W) {
+            const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+            const int y1 = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+            const size_t r0 = (size_t)y * W + x, r1 = (size_t)y1 * W + x1;
+            const float v = __ldg(fimg + r1) - __ldg(fimg + r0);
+            if (MODE == 0) {
+                SV[o] = make_float2(v * s, 1.0f);  // source = guide (scaled)
+            } else {
+                G[i * GP + j] = (__ldg(gimg + r1) - __ldg(gimg + r0)) * sg;
+                SV[o] = make_float2(v, 1.0f);
+            }
+        } else {
+            SV[o] = make_float2(MODE == 0 ? kP2Sentinel : 0.f, 0.f);
+            if (MODE == 1) G[i * GP + j] = kP2Sentinel;
+        }
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int ox = tx0 + tx * P, oy = ty0 + ty;
+    float gs[P];
+    unsigned long long acc[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        gs[q] = MODE == 0 ? SV[(ty + R) * SP + p2_sw(tx * P + q + R)].x : G[(ty + R) * GP + tx * P + q + R];
+        acc[q] = 0ull;
+    }
+#pragma unroll 1
+    for (int dy = -R; dy <= R; ++dy) {
+        const int ady = dy < 0 ? -dy : dy;
+        float ce[R + 1];
+#pragma unroll
+        for (int k = 0; k <= R; ++k) ce[k] = p.cs[ady] + p.cs[k];
+        const float2* sv = SV + (ty + R + dy) * SP;
+        const float* grow = G + (ty + R + dy) * GP + tx * P;
+#pragma unroll
+        for (int j4 = 0; j4 < VN4; j4 += 4) {
+            float gt[4];
+            unsigned long long v1[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 a = *reinterpret_cast<const float4*>(sv + p2_sw(tx * P + j4 + 2 * h));
+                asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h]) : "f"(a.x), "f"(a.y));
+                asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h + 1]) : "f"(a.z), "f"(a.w));
+                if (MODE == 0) {
+                    gt[2 * h] = a.x;
+                    gt[2 * h + 1] = a.z;
+                }
+            }
+            if (MODE == 1) {
+                const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+                gt[0] = g4.x;
+                gt[1] = g4.y;
+                gt[2] = g4.z;
+                gt[3] = g4.w;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j4 + u;
+                if (j >= VN) break;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int dx = j - q - R;
+                    if (dx < -R || dx > R) continue;
+                    const float d = gs[q] - gt[u];
+                    const float e = fmaf(-d, d, ce[dx < 0 ? -dx : dx]);
+                    const int tap = (dx + R) * P + q;
+                    const float w = (POLY > 0 && tap % POLY == POLY - 1) ? p2_poly_ex2(e) : p2_ex2(e);
+                    acc[q] = p2_ffma2(w, v1[u], acc[q]);
+                }
+            }
+        }
+    }
+    if (oy < p.y1) {
+        float oscale;
+        if (MODE == 0)
+            oscale = p.normalized_out ? 1.f / p.range_coef : 1.f / s;
+        else
+            oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
+        float t[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const float2 nz = p2_unpack(acc[q]);
+            t[q] = nz.x / nz.y * oscale;
+        }
+        const size_t off = ((size_t)b * C + c0) * ((size_t)p.out_rows * W) +
+                           (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W + ox;
+        if constexpr (PEERS) {
+            for (int k = 0; k < p.npeers; ++k) {
+                float* d = (axis == 0 ? p.peer_tx[k] : p.peer_ty[k]) + off;
+                for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[q];
+            }
+        } else {
+            float* dst = (axis == 0 ? p.tx : p.ty) + off;
+            if (ox + P <= W && (off & 3) == 0) {
+                *reinterpret_cast<float4*>(dst) = make_float4(t[0], t[1], t[2], t[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (ox + q < W) dst[q] = t[q];
+            }
+        }
+    }
+}
+
+template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB>
+static cudaError_t launch_p2_t(const BlfParams& p, int nplanes, cudaStream_t st)
+{
+    using Gm = P2Geom<R, TH, MODE>;
+    constexpr size_t smem = Gm::smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k_blf_p2<R, TH, MODE, POLY, PEERS, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * nplanes);
+    k_blf_p2<R, TH, MODE, POLY, PEERS, MINB><<<grid, Gm::NT, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// tile height: 16 rows, or 8 when the 16-row grid would fill fewer than ~6
+// waves (small images: c1); every 5th exponential on the FMA pipe by default
+template <int R, int MODE>
+static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
+{
+    // default: every 7th exponential on the FMA pipe for the large window
+    // (r = 15: c4 0.966 of MUFU against 0.945 unpacked), none otherwise
+    static const int poly_env = [] {
+        const char* e = std::getenv("BLFLS_P2_POLY");
+        return e ? std::atoi(e) : -1;
+    }();
+    const int poly = poly_env >= 0 ? poly_env : (R >= 12 ? 7 : 0);
+    // peer-storing epilogue (fused band exchange) with the default offload, so
+    // its targets equal the plain band filter's bit for bit
+    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, (R >= 12 ? 7 : 0), true, 3>(p, nplanes, st);
+    const long ctas16 = (long)((p.W + 63) / 64) * ((p.y1 - p.y0 + 15) / 16) * 2 * nplanes;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const bool small = ctas16 < 6L * 4 * nsm;
+    switch (poly) {
+        case 4:
+            return small ? launch_p2_t<R, 8, MODE, 4, false, 8>(p, nplanes, st)
+                         : launch_p2_t<R, 16, MODE, 4, false, 4>(p, nplanes, st);
+        case 5:
+            return small ? launch_p2_t<R, 8, MODE, 5, false, 8>(p, nplanes, st)
+                         : launch_p2_t<R, 16, MODE, 5, false, 4>(p, nplanes, st);
+        case 7:
+            return small ? launch_p2_t<R, 8, MODE, 7, false, 8>(p, nplanes, st)
+                         : launch_p2_t<R, 16, MODE, 7, false, 4>(p, nplanes, st);
+        default:
+            return small ? launch_p2_t<R, 8, MODE, 0, false, 8>(p, nplanes, st)
+                         : launch_p2_t<R, 16, MODE, 0, false, 4>(p, nplanes, st);
+    }
+}
+
+// Packed self / per-channel-joint filter; false when not selected (the caller
+// runs k_grad_blf).  Default: the self-guided large window (r = 15, c4),
+// where the freed issue slots carry the FMA-pipe exp2 offload.  At r <= 7
+// the unpacked kernel is as fast or faster (r01 B200: c2 1.059 vs 1.062 ms,
+// c3 1.172 vs 1.107 ms, poly offload slower there).  BLFLS_P2=1 forces it
+// for every instantiated radius and both modes, BLFLS_P2=0 disables it.
+bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err)
+{
+    static const int sel = [] {
+        const char* e = std::getenv("BLFLS_P2");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (sel == 0 || mode == 2) return false;
+    if (sel < 0 && !(mode == 0 && p.radius == 15)) return false;
+    const int np = batch * p.C;
+    switch (p.radius) {
+        case 3: *err = mode == 0 ? launch_p2<3, 0>(p, np, st) : launch_p2<3, 1>(p, np, st); return true;
+        case 5: *err = mode == 0 ? launch_p2<5, 0>(p, np, st) : launch_p2<5, 1>(p, np, st); return true;
+        case 7: *err = mode == 0 ? launch_p2<7, 0>(p, np, st) : launch_p2<7, 1>(p, np, st); return true;
+        case 15: *err = mode == 0 ? launch_p2<15, 0>(p, np, st) : launch_p2<15, 1>(p, np, st); return true;
+        default: return false;
+    }
+}
+
+}  // namespace blfls

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_r2c(const SolveParams p, co
 // grid (ceil(wc / V), planes): V adjacent spectrum columns, forward FFT,
 // 1 / (H W (1 + lambda (4 sin^2(pi u/H) + 4 sin^2(pi v/W)))), inverse FFT
 template <class G>
-__global__ void __launch_bounds__(G::THREADS) k2_col(const SolveParams p, const float2* __restrict__ tw)
+__global__ void __launch_bounds__(G::THREADS, G::THREADS <= 512 ? 65536 / (64 * G::THREADS) : 1) k2_col(const SolveParams p, const float2* __restrict__ tw)
 {
     extern __shared__ __align__(16) float2 buf[];
     const int v = threadIdx.x % G::V, t = threadIdx.x / G::V;
