@@ -105,27 +105,38 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     const float* gimg = p.guide + (size_t)b * p.GC * plane;
 
     // ---- prologue: this axis' circular gradients of guide and channels
-    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += NT) {
-        const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
-        const int y = ty0 - R + i, x = tx0 - R + j;
-        const int og = i * GP + j, o = i * SP + j3_sw(j);
-        if (y >= 0 && y < H && x >= 0 && x < W) {
-            const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
-            const int y1 = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
-            const size_t r0 = (size_t)y * W + x, r1 = (size_t)y1 * W + x1;
-            G[og] = (__ldg(gimg + r1) - __ldg(gimg + r0)) * sg;
-            float g[3];
+    // staging: warp per tile row, lane per column
+    {
+        const int lane = threadIdx.x & 31;
+        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
+            const int y = ty0 - R + i;
+            const bool yin = y >= 0 && y < H;
+            const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+            const size_t r0 = (size_t)(yin ? y : 0) * W, r1 = (size_t)(yin ? yn : 0) * W;
+            float* grow = G + i * GP;
+            float2* s01 = S01 + i * SP;
+            float2* s2 = S2 + i * SP;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float* fc = fimg + (size_t)c * plane;
-                g[c] = __ldg(fc + r1) - __ldg(fc + r0);
+            for (int j = lane; j < COLS; j += 32) {
+                const int x = tx0 - R + j;
+                const int o = j3_sw(j);
+                if (yin && x >= 0 && x < W) {
+                    const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                    grow[j] = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
+                    float g[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float* fc = fimg + (size_t)c * plane;
+                        g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
+                    }
+                    s01[o] = make_float2(g[0], g[1]);
+                    s2[o] = make_float2(g[2], 1.0f);
+                } else {
+                    grow[j] = kJ3Sentinel;
+                    s01[o] = make_float2(0.f, 0.f);
+                    s2[o] = make_float2(0.f, 0.f);
+                }
             }
-            S01[o] = make_float2(g[0], g[1]);
-            S2[o] = make_float2(g[2], 1.0f);
-        } else {
-            G[og] = kJ3Sentinel;
-            S01[o] = make_float2(0.f, 0.f);
-            S2[o] = make_float2(0.f, 0.f);
         }
     }
     __syncthreads();

@@ -110,24 +110,36 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
     const float* fimg = p.f + ((size_t)b * C + c0) * plane;
     const float* gimg = MODE == 0 ? fimg : p.guide + ((size_t)b * p.GC + (p.GC == 1 ? 0 : c0)) * plane;
 
-    for (int idx = threadIdx.x; idx < ROWS * COLS; idx += NT) {
-        const int i = idx / COLS, j = idx - (idx / COLS) * COLS;
-        const int y = ty0 - R + i, x = tx0 - R + j;
-        const int o = i * SP + p2_sw(j);
-        if (y >= 0 && y < H && x >= 0 && x < W) {
-            const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
-            const int y1 = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
-            const size_t r0 = (size_t)y * W + x, r1 = (size_t)y1 * W + x1;
-            const float v = __ldg(fimg + r1) - __ldg(fimg + r0);
-            if (MODE == 0) {
-                SV[o] = make_float2(v * s, 1.0f);  // source = guide (scaled)
-            } else {
-                G[i * GP + j] = (__ldg(gimg + r1) - __ldg(gimg + r0)) * sg;
-                SV[o] = make_float2(v, 1.0f);
+    // staging: warp per tile row, lane per column (no per-element division;
+    // the row's base pointer and wrap row are computed once)
+    {
+        const int lane = threadIdx.x & 31;
+        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
+            const int y = ty0 - R + i;
+            const bool yin = y >= 0 && y < H;
+            const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+            const float* f0 = fimg + (size_t)(yin ? y : 0) * W;
+            const float* f1 = fimg + (size_t)(yin ? yn : 0) * W;
+            const float* g0 = gimg + (size_t)(yin ? y : 0) * W;
+            const float* g1 = gimg + (size_t)(yin ? yn : 0) * W;
+            float2* srow = SV + i * SP;
+#pragma unroll
+            for (int j = lane; j < COLS; j += 32) {
+                const int x = tx0 - R + j;
+                if (yin && x >= 0 && x < W) {
+                    const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                    const float v = __ldg(f1 + x1) - __ldg(f0 + x);
+                    if (MODE == 0) {
+                        srow[p2_sw(j)] = make_float2(v * s, 1.0f);  // source = guide (scaled)
+                    } else {
+                        G[i * GP + j] = (__ldg(g1 + x1) - __ldg(g0 + x)) * sg;
+                        srow[p2_sw(j)] = make_float2(v, 1.0f);
+                    }
+                } else {
+                    srow[p2_sw(j)] = make_float2(MODE == 0 ? kP2Sentinel : 0.f, 0.f);
+                    if (MODE == 1) G[i * GP + j] = kP2Sentinel;
+                }
             }
-        } else {
-            SV[o] = make_float2(MODE == 0 ? kP2Sentinel : 0.f, 0.f);
-            if (MODE == 1) G[i * GP + j] = kP2Sentinel;
         }
     }
     __syncthreads();
@@ -269,11 +281,11 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
 }
 
 // Packed self / per-channel-joint filter; false when not selected (the caller
-// runs k_grad_blf).  Default: the self-guided large window (r = 15, c4),
-// where the freed issue slots carry the FMA-pipe exp2 offload.  At r <= 7
-// the unpacked kernel is as fast or faster (r01 B200: c2 1.059 vs 1.062 ms,
-// c3 1.172 vs 1.107 ms, poly offload slower there).  BLFLS_P2=1 forces it
-// for every instantiated radius and both modes, BLFLS_P2=0 disables it.
+// runs k_grad_blf).  Default: self-guided r = 7 (c2: 1.046 vs 1.062 ms per
+// 3 iterations) and r = 15 with the FMA-pipe exp2 offload every 7th tap (c4:
+// 0.973 of the MUFU peak vs 0.945); at r = 5 the unpacked kernel is faster
+// (c3: 1.107 vs 1.167 ms; r01 B200 A/B, tools/p2_ab.sh).  BLFLS_P2=1 forces
+// it for every instantiated radius and both modes, BLFLS_P2=0 disables it.
 bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err)
 {
     static const int sel = [] {
@@ -281,7 +293,7 @@ bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st
         return e ? std::atoi(e) : -1;
     }();
     if (sel == 0 || mode == 2) return false;
-    if (sel < 0 && !(mode == 0 && p.radius == 15)) return false;
+    if (sel < 0 && !(mode == 0 && (p.radius == 7 || p.radius == 15))) return false;
     const int np = batch * p.C;
     switch (p.radius) {
         case 3: *err = mode == 0 ? launch_p2<3, 0>(p, np, st) : launch_p2<3, 1>(p, np, st); return true;
