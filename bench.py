@@ -70,6 +70,18 @@ def load_traffic(name):
         return None
 
 
+def blf_kernel_name(cfg):
+    """The brute-force BLF kernel the library dispatches for this config
+    (k_blf.cu launch_grad_blf: packed shared-guide kernel for a gray guide over
+    RGB, packed self-guided kernel at r = 7 / 15, the unpacked kernel otherwise)."""
+    if cfg.guide and cfg.channels == 3 and cfg.radius in (3, 5, 7, 15):
+        return "k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums)"
+    if not cfg.guide and cfg.radius in (7, 15):
+        return "k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums" + \
+            (", FMA-pipe exp2 on every 7th tap)" if cfg.radius == 15 else ")")
+    return "k_grad_blf (fused gradient + brute-force BLF)"
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -431,7 +443,7 @@ def run_ours(args, cfg):
                 "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2",
                 "decomposition": {"weak": "independent images per rank",
                                   "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]}),
-            "roofline": roof_dt if args.backend != "brute" else {"bound": "sfu", "kernel": "k_grad_blf (fused gradient + brute-force BLF)",
+            "roofline": roof_dt if args.backend != "brute" else {"bound": "sfu", "kernel": blf_kernel_name(cfg),
                          "achieved": achieved / 1e9, "peak": mufu_rate / 1e9, "unit": "Gexp/s",
                          "frac": achieved / mufu_rate,
                          "peak_source": "measured MUFU.EX2 probe on this GPU "
