@@ -105,6 +105,10 @@ struct BlfParams {
                            // gradients of a unit-range image
     float cs[kMaxRadius + 1];  // log2 spatial weight -d^2/(2 sigma_s^2) * log2(e)
     float wrow[kMaxRadius + 1]; // exp2(cs[d]) : row factor
+    // column-spatial pairs of two adjacent outputs (q, q + 1) at one source
+    // column: cep[i] = (cs[|i - r|], cs[|i - r - 1|]), i in [0, 2r + 1]
+    // (entries outside the window hold cs[r]; k_blf_p2.cu pair exponents)
+    float2 cep[2 * kMaxRadius + 2];
     // fused band exchange (multi-GPU row bands): npeers > 0 writes every target
     // into the full-height tx / ty of each peer (NVLink peer-mapped pointers,
     // rank order) instead of tx / ty -- the all-gather done by the epilogue

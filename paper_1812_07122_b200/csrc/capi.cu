@@ -820,6 +820,10 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
             b.cs[d] = (float)c;
             b.wrow[d] = (float)std::exp2(c);
         }
+        for (int i = 0; i < 2 * kMaxRadius + 2; ++i) {
+            const int a = std::min(std::abs(i - radius), radius), c = std::min(std::abs(i - radius - 1), radius);
+            b.cep[i] = make_float2(b.cs[a], b.cs[c]);
+        }
         // shared-memory envelope of the generic kernel
         const int narr = p->mode == 0 ? 2 : (p->mode == 1 ? 4 : 8);
         const size_t smem = (size_t)narr * (16 + 2 * radius) * (((64 + 2 * radius) + 3) & ~3) * 4;

@@ -87,7 +87,11 @@ struct P2Geom {
 };
 
 // blockIdx.z = plane * 2 + axis, plane = image * C + channel
-template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB>
+// PX: the guide difference and exponent of two adjacent outputs (q, q + 1)
+// at one source column as one FFMA2 each (the weight's column-spatial term
+// from the cep pair table; the row term applied to per-row partial sums), so
+// a tap costs 1 + 0.5 + 0.5 instructions next to its MUFU.EX2
+template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX = false>
 __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
 {
     using Gm = P2Geom<R, TH, MODE>;
@@ -153,48 +157,118 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
         gs[q] = MODE == 0 ? SV[(ty + R) * SP + p2_sw(tx * P + q + R)].x : G[(ty + R) * GP + tx * P + q + R];
         acc[q] = 0ull;
     }
+    if constexpr (PX) {
+        unsigned long long gsp[2];
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[0]) : "f"(gs[0]), "f"(gs[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[1]) : "f"(gs[2]), "f"(gs[3]));
+        unsigned long long m1;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(m1) : "f"(-1.0f));
 #pragma unroll 1
-    for (int dy = -R; dy <= R; ++dy) {
-        const int ady = dy < 0 ? -dy : dy;
-        float ce[R + 1];
+        for (int dy = -R; dy <= R; ++dy) {
+            const float2* sv = SV + (ty + R + dy) * SP;
+            const float* grow = G + (ty + R + dy) * GP + tx * P;
+            unsigned long long accr[P];
 #pragma unroll
-        for (int k = 0; k <= R; ++k) ce[k] = p.cs[ady] + p.cs[k];
-        const float2* sv = SV + (ty + R + dy) * SP;
-        const float* grow = G + (ty + R + dy) * GP + tx * P;
+            for (int q = 0; q < P; ++q) accr[q] = 0ull;
 #pragma unroll
-        for (int j4 = 0; j4 < VN4; j4 += 4) {
-            float gt[4];
-            unsigned long long v1[4];
+            for (int j4 = 0; j4 < VN4; j4 += 4) {
+                float gt[4];
+                unsigned long long v1[4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const float4 a = *reinterpret_cast<const float4*>(sv + p2_sw(tx * P + j4 + 2 * h));
-                asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h]) : "f"(a.x), "f"(a.y));
-                asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h + 1]) : "f"(a.z), "f"(a.w));
-                if (MODE == 0) {
-                    gt[2 * h] = a.x;
-                    gt[2 * h + 1] = a.z;
+                for (int h = 0; h < 2; ++h) {
+                    const float4 a = *reinterpret_cast<const float4*>(sv + p2_sw(tx * P + j4 + 2 * h));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h]) : "f"(a.x), "f"(a.y));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h + 1]) : "f"(a.z), "f"(a.w));
+                    if (MODE == 0) {
+                        gt[2 * h] = a.x;
+                        gt[2 * h + 1] = a.z;
+                    }
+                }
+                if (MODE == 1) {
+                    const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+                    gt[0] = g4.x;
+                    gt[1] = g4.y;
+                    gt[2] = g4.z;
+                    gt[3] = g4.w;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j4 + u;
+                    if (j >= VN) break;
+#pragma unroll
+                    for (int h = 0; h < P / 2; ++h) {
+                        const int q0 = 2 * h, dx0 = j - q0 - R;
+                        const bool ok0 = dx0 >= -R && dx0 <= R, ok1 = dx0 - 1 >= -R && dx0 - 1 <= R;
+                        if (!ok0 && !ok1) continue;
+                        unsigned long long gtt, d, nd, ce, e;
+                        asm("mov.b64 %0, {%1, %1};" : "=l"(gtt) : "f"(gt[u]));
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[h]));
+                        const float2 dd = p2_unpack(d);
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(ce) : "f"(p.cep[dx0 + R].x), "f"(p.cep[dx0 + R].y));
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                        const float2 ee = p2_unpack(e);
+                        if (ok0) {
+                            const int tap = (dx0 + R) * P + q0;
+                            const float w = (POLY > 0 && tap % POLY == POLY - 1) ? p2_poly_ex2(ee.x) : p2_ex2(ee.x);
+                            accr[q0] = p2_ffma2(w, v1[u], accr[q0]);
+                        }
+                        if (ok1) {
+                            const int tap = (dx0 - 1 + R) * P + q0 + 1;
+                            const float w = (POLY > 0 && tap % POLY == POLY - 1) ? p2_poly_ex2(ee.y) : p2_ex2(ee.y);
+                            accr[q0 + 1] = p2_ffma2(w, v1[u], accr[q0 + 1]);
+                        }
+                    }
                 }
             }
-            if (MODE == 1) {
-                const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
-                gt[0] = g4.x;
-                gt[1] = g4.y;
-                gt[2] = g4.z;
-                gt[3] = g4.w;
-            }
+            const float wy = p.wrow[dy < 0 ? -dy : dy];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j4 + u;
-                if (j >= VN) break;
-#pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    const int dx = j - q - R;
-                    if (dx < -R || dx > R) continue;
-                    const float d = gs[q] - gt[u];
-                    const float e = fmaf(-d, d, ce[dx < 0 ? -dx : dx]);
-                    const int tap = (dx + R) * P + q;
-                    const float w = (POLY > 0 && tap % POLY == POLY - 1) ? p2_poly_ex2(e) : p2_ex2(e);
-                    acc[q] = p2_ffma2(w, v1[u], acc[q]);
+            for (int q = 0; q < P; ++q) acc[q] = p2_ffma2(wy, accr[q], acc[q]);
+        }
+    } else {
+#pragma unroll 1
+        for (int dy = -R; dy <= R; ++dy) {
+            const int ady = dy < 0 ? -dy : dy;
+            float ce[R + 1];
+    #pragma unroll
+            for (int k = 0; k <= R; ++k) ce[k] = p.cs[ady] + p.cs[k];
+            const float2* sv = SV + (ty + R + dy) * SP;
+            const float* grow = G + (ty + R + dy) * GP + tx * P;
+    #pragma unroll
+            for (int j4 = 0; j4 < VN4; j4 += 4) {
+                float gt[4];
+                unsigned long long v1[4];
+    #pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float4 a = *reinterpret_cast<const float4*>(sv + p2_sw(tx * P + j4 + 2 * h));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h]) : "f"(a.x), "f"(a.y));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h + 1]) : "f"(a.z), "f"(a.w));
+                    if (MODE == 0) {
+                        gt[2 * h] = a.x;
+                        gt[2 * h + 1] = a.z;
+                    }
+                }
+                if (MODE == 1) {
+                    const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+                    gt[0] = g4.x;
+                    gt[1] = g4.y;
+                    gt[2] = g4.z;
+                    gt[3] = g4.w;
+                }
+    #pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j4 + u;
+                    if (j >= VN) break;
+    #pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int dx = j - q - R;
+                        if (dx < -R || dx > R) continue;
+                        const float d = gs[q] - gt[u];
+                        const float e = fmaf(-d, d, ce[dx < 0 ? -dx : dx]);
+                        const int tap = (dx + R) * P + q;
+                        const float w = (POLY > 0 && tap % POLY == POLY - 1) ? p2_poly_ex2(e) : p2_ex2(e);
+                        acc[q] = p2_ffma2(w, v1[u], acc[q]);
+                    }
                 }
             }
         }
@@ -231,52 +305,69 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
     }
 }
 
-template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB>
+template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX>
 static cudaError_t launch_p2_t(const BlfParams& p, int nplanes, cudaStream_t st)
 {
     using Gm = P2Geom<R, TH, MODE>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_p2<R, TH, MODE, POLY, PEERS, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * nplanes);
-    k_blf_p2<R, TH, MODE, POLY, PEERS, MINB><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-// tile height: 16 rows, or 8 when the 16-row grid would fill fewer than ~6
-// waves (small images: c1); every 5th exponential on the FMA pipe by default
-template <int R, int MODE>
-static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
+template <int R, int MODE, int POLY, bool PX>
+static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t st)
 {
-    // default: every 7th exponential on the FMA pipe for the large window
-    // (r = 15: c4 0.966 of MUFU against 0.945 unpacked), none otherwise
-    static const int poly_env = [] {
-        const char* e = std::getenv("BLFLS_P2_POLY");
-        return e ? std::atoi(e) : -1;
-    }();
-    const int poly = poly_env >= 0 ? poly_env : (R >= 12 ? 7 : 0);
-    // peer-storing epilogue (fused band exchange) with the default offload, so
-    // its targets equal the plain band filter's bit for bit
-    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, (R >= 12 ? 7 : 0), true, 3>(p, nplanes, st);
+    // tile height: 16 rows, or 8 when the 16-row grid would fill fewer than
+    // ~6 waves of 4 CTAs per SM (small images: c1)
     const long ctas16 = (long)((p.W + 63) / 64) * ((p.y1 - p.y0 + 15) / 16) * 2 * nplanes;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const bool small = ctas16 < 6L * 4 * nsm;
+    static const int th = [] {  // experiment override: 8, 16 or 32 rows per tile
+        const char* e = std::getenv("BLFLS_P2_TH");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (th == 32 && PX) return launch_p2_t<R, 32, MODE, POLY, false, 2, PX>(p, nplanes, st);
+    if (th == 8 || (th == 0 && ctas16 < 6L * 4 * nsm))
+        return launch_p2_t<R, 8, MODE, POLY, false, 8, PX>(p, nplanes, st);
+    return launch_p2_t<R, 16, MODE, POLY, false, 4, PX>(p, nplanes, st);
+}
+
+template <int R, int MODE>
+static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
+{
+    // default: every 7th exponential on the FMA pipe for the large window
+    // (r = 15: c4 0.973 of MUFU against 0.945 unpacked), none otherwise
+    static const int poly_env = [] {
+        const char* e = std::getenv("BLFLS_P2_POLY");
+        return e ? std::atoi(e) : -1;
+    }();
+    static const int px = [] {
+        const char* e = std::getenv("BLFLS_P2X");
+        return e ? std::atoi(e) : 1;
+    }();
+    // pair exponents (PX) free enough issue slots for the offload at r = 7 too
+    const int poly = poly_env >= 0 ? poly_env : (px || R >= 12 ? 7 : 0);
+    // peer-storing epilogue (fused band exchange) with the default offload, so
+    // its targets equal the plain band filter's bit for bit
+    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, 7, true, 3, true>(p, nplanes, st);
+    if (px) {
+        switch (poly) {
+            case 5: return launch_p2_sized<R, MODE, 5, true>(p, nplanes, st);
+            case 6: return launch_p2_sized<R, MODE, 6, true>(p, nplanes, st);
+            case 7: return launch_p2_sized<R, MODE, 7, true>(p, nplanes, st);
+            case 8: return launch_p2_sized<R, MODE, 8, true>(p, nplanes, st);
+            case 10: return launch_p2_sized<R, MODE, 10, true>(p, nplanes, st);
+            default: return launch_p2_sized<R, MODE, 0, true>(p, nplanes, st);
+        }
+    }
     switch (poly) {
-        case 4:
-            return small ? launch_p2_t<R, 8, MODE, 4, false, 8>(p, nplanes, st)
-                         : launch_p2_t<R, 16, MODE, 4, false, 4>(p, nplanes, st);
-        case 5:
-            return small ? launch_p2_t<R, 8, MODE, 5, false, 8>(p, nplanes, st)
-                         : launch_p2_t<R, 16, MODE, 5, false, 4>(p, nplanes, st);
-        case 7:
-            return small ? launch_p2_t<R, 8, MODE, 7, false, 8>(p, nplanes, st)
-                         : launch_p2_t<R, 16, MODE, 7, false, 4>(p, nplanes, st);
-        default:
-            return small ? launch_p2_t<R, 8, MODE, 0, false, 8>(p, nplanes, st)
-                         : launch_p2_t<R, 16, MODE, 0, false, 4>(p, nplanes, st);
+        case 7: return launch_p2_sized<R, MODE, 7, false>(p, nplanes, st);
+        default: return launch_p2_sized<R, MODE, 0, false>(p, nplanes, st);
     }
 }
 
