@@ -908,11 +908,12 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         cudaMalloc(&p->nonfinite, sizeof(unsigned)) != cudaSuccess)
         return bail(fail(BLFLS_ENOMEM, "plan: workspace allocation failed"));
     {
-        // group planes when all spectra together would not stay in L2
-        const double spec_plane = (double)H * p->spitch * sizeof(float2);
-        const double total = spec_plane * q.max_batch * C;
+        // one launch per pass over all planes: with the high-radix column /
+        // c2r passes the streaming solve beats plane groups that keep each
+        // spectrum L2-resident (c5: 7.64 ms per iteration vs 7.8-9.1 for
+        // groups of 6..1 planes, r01 B200); BLFLS_SOLVE_GROUP=n (experiment)
+        // runs groups of n planes on two streams
         int grp = 0;
-        if (total > 64e6) grp = std::max(1, (int)(24e6 / spec_plane));
         if (const char* ev = std::getenv("BLFLS_SOLVE_GROUP")) grp = std::atoi(ev);
         p->solve_group = grp;
     }

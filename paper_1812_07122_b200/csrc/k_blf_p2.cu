@@ -321,9 +321,11 @@ static cudaError_t launch_p2_t(const BlfParams& p, int nplanes, cudaStream_t st)
 template <int R, int MODE, int POLY, bool PX>
 static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t st)
 {
-    // tile height: 16 rows, or 8 when the 16-row grid would fill fewer than
-    // ~6 waves of 4 CTAs per SM (small images: c1)
+    // tile height: 32 rows (512 threads, 2 CTAs per SM: the staged halo rows
+    // amortised over more outputs; c2 -1%) when that grid still fills ~6
+    // waves, else 16, else 8 (small images: c1)
     const long ctas16 = (long)((p.W + 63) / 64) * ((p.y1 - p.y0 + 15) / 16) * 2 * nplanes;
+    const long ctas32 = (long)((p.W + 63) / 64) * ((p.y1 - p.y0 + 31) / 32) * 2 * nplanes;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -331,7 +333,8 @@ static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t
         const char* e = std::getenv("BLFLS_P2_TH");
         return e ? std::atoi(e) : 0;
     }();
-    if (th == 32 && PX) return launch_p2_t<R, 32, MODE, POLY, false, 2, PX>(p, nplanes, st);
+    if (PX && (th == 32 || (th == 0 && ctas32 >= 6L * 2 * nsm)))
+        return launch_p2_t<R, 32, MODE, POLY, false, 2, PX>(p, nplanes, st);
     if (th == 8 || (th == 0 && ctas16 < 6L * 4 * nsm))
         return launch_p2_t<R, 8, MODE, POLY, false, 8, PX>(p, nplanes, st);
     return launch_p2_t<R, 16, MODE, POLY, false, 4, PX>(p, nplanes, st);
