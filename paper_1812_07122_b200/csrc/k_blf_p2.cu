@@ -354,10 +354,12 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
         return e ? std::atoi(e) : 1;
     }();
     // pair exponents (PX) free enough issue slots for the offload at r = 7 too
-    const int poly = poly_env >= 0 ? poly_env : (px || R >= 12 ? 7 : 0);
+    // (r = 5: every 10th; with 32-row tiles it ties the unpacked kernel at
+    // c3 and beats it at c1)
+    const int poly = poly_env >= 0 ? poly_env : (px ? (R == 5 ? 10 : 7) : (R >= 12 ? 7 : 0));
     // peer-storing epilogue (fused band exchange) with the default offload, so
     // its targets equal the plain band filter's bit for bit
-    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, 7, true, 3, true>(p, nplanes, st);
+    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, (R == 5 ? 10 : 7), true, 3, true>(p, nplanes, st);
     if (px) {
         switch (poly) {
             case 5: return launch_p2_sized<R, MODE, 5, true>(p, nplanes, st);
@@ -365,6 +367,7 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
             case 7: return launch_p2_sized<R, MODE, 7, true>(p, nplanes, st);
             case 8: return launch_p2_sized<R, MODE, 8, true>(p, nplanes, st);
             case 10: return launch_p2_sized<R, MODE, 10, true>(p, nplanes, st);
+            case 12: return launch_p2_sized<R, MODE, 12, true>(p, nplanes, st);
             default: return launch_p2_sized<R, MODE, 0, true>(p, nplanes, st);
         }
     }
@@ -375,11 +378,11 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
 }
 
 // Packed self / per-channel-joint filter; false when not selected (the caller
-// runs k_grad_blf).  Default: self-guided r = 7 (c2: 1.046 vs 1.062 ms per
-// 3 iterations) and r = 15 with the FMA-pipe exp2 offload every 7th tap (c4:
-// 0.973 of the MUFU peak vs 0.945); at r = 5 the unpacked kernel is faster
-// (c3: 1.107 vs 1.167 ms; r01 B200 A/B, tools/p2_ab.sh).  BLFLS_P2=1 forces
-// it for every instantiated radius and both modes, BLFLS_P2=0 disables it.
+// runs k_grad_blf).  Default: self-guided r = 5, 7, 15 with pair exponents
+// and the FMA-pipe exp2 offload (r01 B200 A/B, tools/p2_ab.sh, p2x_ab.sh:
+// c2 BLF 1.062 -> 0.970 ms per 3 iterations, c4 14.72 -> 13.50 ms, c1
+// 28.2 -> 25.8 us, c3 tie).  BLFLS_P2=1 forces it for every instantiated
+// radius and both modes, BLFLS_P2=0 disables it.
 bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err)
 {
     static const int sel = [] {
@@ -387,7 +390,7 @@ bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st
         return e ? std::atoi(e) : -1;
     }();
     if (sel == 0 || mode == 2) return false;
-    if (sel < 0 && !(mode == 0 && (p.radius == 7 || p.radius == 15))) return false;
+    if (sel < 0 && !(mode == 0 && (p.radius == 5 || p.radius == 7 || p.radius == 15))) return false;
     const int np = batch * p.C;
     switch (p.radius) {
         case 3: *err = mode == 0 ? launch_p2<3, 0>(p, np, st) : launch_p2<3, 1>(p, np, st); return true;

@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, co
 // Row geometries (N = W/2, V rows, TV threads per row, PMAX) and column
 // geometries (N = H, V columns, TV threads per column, PMAX).  No radix-16
 // row geometry for n = 960 (c3): its 15 x 16 x 4 c2r measured slower than
-// the radix-8 engine's (31 vs 27 us per iteration).
+// the radix-8 engine's (31 vs 27 us per iteration); no radix-16 column
+// geometry for H = 512 (c1: 15.9 vs 12.1 us).
 #define BLFLS_V2_ROWS(X) X(256, 16, 8, 32) X(256, 4, 8, 32) X(512, 8, 16, 32) X(512, 2, 16, 32) \
     X(960, 8, 32, 32) X(960, 2, 32, 32) X(1024, 8, 32, 32) X(1024, 2, 32, 32) X(2048, 4, 64, 32) \
     X(2048, 1, 64, 32) \
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, co
 #define BLFLS_V2_COLS(X) X(512, 8, 16, 32) X(512, 2, 16, 32) X(1024, 4, 32, 32) X(1024, 2, 32, 32) \
     X(1080, 8, 36, 32) X(1080, 4, 40, 32) X(2048, 4, 64, 32) X(2048, 2, 64, 32) X(4096, 4, 128, 32) \
     X(4096, 2, 128, 32) \
-    X(512, 8, 32, 16) X(512, 2, 32, 16) X(1024, 4, 64, 16) X(1024, 2, 64, 16) X(1080, 4, 72, 16) \
+    X(1024, 4, 64, 16) X(1024, 2, 64, 16) X(1080, 4, 72, 16) \
     X(2048, 4, 128, 16) X(2048, 2, 128, 16) X(4096, 2, 256, 16) X(4096, 4, 256, 16)
 
 template <class K>
