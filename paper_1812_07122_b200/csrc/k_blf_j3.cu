@@ -82,7 +82,9 @@ struct J3Geom {
 
 // PEERS: fused band exchange (multi-GPU row bands): every target is stored
 // into the full-height buffers of all p.npeers ranks (NVLink peer pointers)
-template <int R, int TH, bool PEERS, int MINB>
+// PX: guide difference and exponent of two adjacent outputs as one FFMA2
+// each (column-spatial pair table p.cep, row factor on per-row partial sums)
+template <int R, int TH, bool PEERS, int MINB, bool PX = false>
 __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
 {
     using Gm = J3Geom<R, TH>;
@@ -151,43 +153,113 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
         acc01[q] = 0ull;
         acc2z[q] = 0ull;
     }
+    if constexpr (PX) {
+        unsigned long long gsp[2], m1;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[0]) : "f"(gs[0]), "f"(gs[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[1]) : "f"(gs[2]), "f"(gs[3]));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(m1) : "f"(-1.0f));
 #pragma unroll 1
-    for (int dy = -R; dy <= R; ++dy) {
-        const int ady = dy < 0 ? -dy : dy;
-        float ce[R + 1];  // log2 spatial weight of (dy, |dx|)
+        for (int dy = -R; dy <= R; ++dy) {
+            const float* grow = G + (ty + R + dy) * GP + tx * P;
+            const float2* s01 = S01 + (ty + R + dy) * SP;
+            const float2* s2 = S2 + (ty + R + dy) * SP;
+            unsigned long long r01[P], r2z[P];
 #pragma unroll
-        for (int k = 0; k <= R; ++k) ce[k] = p.cs[ady] + p.cs[k];
-        const float* grow = G + (ty + R + dy) * GP + tx * P;
-        const float2* s01 = S01 + (ty + R + dy) * SP;
-        const float2* s2 = S2 + (ty + R + dy) * SP;
-#pragma unroll
-        for (int j4 = 0; j4 < VN4; j4 += 4) {
-            const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
-            const float gt[4] = {g4.x, g4.y, g4.z, g4.w};
-            unsigned long long v01[4], v2z[4];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                // columns tx P + j4 + 2h, + 1: one swizzled 16-byte chunk per array
-                const int pc = j3_sw(tx * P + j4 + 2 * h);
-                const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
-                const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
-                asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
-                asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
-                asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
-                asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h + 1]) : "f"(c.z), "f"(c.w));
+            for (int q = 0; q < P; ++q) {
+                r01[q] = 0ull;
+                r2z[q] = 0ull;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j4 + u;
-                if (j >= VN) break;
+            for (int j4 = 0; j4 < VN4; j4 += 4) {
+                const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+                const float gt[4] = {g4.x, g4.y, g4.z, g4.w};
+                unsigned long long v01[4], v2z[4];
 #pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    const int dx = j - q - R;
-                    if (dx < -R || dx > R) continue;
-                    const float d = gs[q] - gt[u];
-                    const float w = j3_ex2(fmaf(-d, d, ce[dx < 0 ? -dx : dx]));
-                    acc01[q] = j3_ffma2(w, v01[u], acc01[q]);
-                    acc2z[q] = j3_ffma2(w, v2z[u], acc2z[q]);
+                for (int h = 0; h < 2; ++h) {
+                    const int pc = j3_sw(tx * P + j4 + 2 * h);
+                    const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
+                    const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h + 1]) : "f"(c.z), "f"(c.w));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j4 + u;
+                    if (j >= VN) break;
+#pragma unroll
+                    for (int h = 0; h < P / 2; ++h) {
+                        const int q0 = 2 * h, dx0 = j - q0 - R;
+                        const bool ok0 = dx0 >= -R && dx0 <= R, ok1 = dx0 - 1 >= -R && dx0 - 1 <= R;
+                        if (!ok0 && !ok1) continue;
+                        unsigned long long gtt, d, nd, ce, e;
+                        asm("mov.b64 %0, {%1, %1};" : "=l"(gtt) : "f"(gt[u]));
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[h]));
+                        const float2 dd = j3_unpack(d);
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(ce) : "f"(p.cep[dx0 + R].x), "f"(p.cep[dx0 + R].y));
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                        const float2 ee = j3_unpack(e);
+                        if (ok0) {
+                            const float w = j3_ex2(ee.x);
+                            r01[q0] = j3_ffma2(w, v01[u], r01[q0]);
+                            r2z[q0] = j3_ffma2(w, v2z[u], r2z[q0]);
+                        }
+                        if (ok1) {
+                            const float w = j3_ex2(ee.y);
+                            r01[q0 + 1] = j3_ffma2(w, v01[u], r01[q0 + 1]);
+                            r2z[q0 + 1] = j3_ffma2(w, v2z[u], r2z[q0 + 1]);
+                        }
+                    }
+                }
+            }
+            const float wy = p.wrow[dy < 0 ? -dy : dy];
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                acc01[q] = j3_ffma2(wy, r01[q], acc01[q]);
+                acc2z[q] = j3_ffma2(wy, r2z[q], acc2z[q]);
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int dy = -R; dy <= R; ++dy) {
+            const int ady = dy < 0 ? -dy : dy;
+            float ce[R + 1];  // log2 spatial weight of (dy, |dx|)
+    #pragma unroll
+            for (int k = 0; k <= R; ++k) ce[k] = p.cs[ady] + p.cs[k];
+            const float* grow = G + (ty + R + dy) * GP + tx * P;
+            const float2* s01 = S01 + (ty + R + dy) * SP;
+            const float2* s2 = S2 + (ty + R + dy) * SP;
+    #pragma unroll
+            for (int j4 = 0; j4 < VN4; j4 += 4) {
+                const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+                const float gt[4] = {g4.x, g4.y, g4.z, g4.w};
+                unsigned long long v01[4], v2z[4];
+    #pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    // columns tx P + j4 + 2h, + 1: one swizzled 16-byte chunk per array
+                    const int pc = j3_sw(tx * P + j4 + 2 * h);
+                    const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
+                    const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h + 1]) : "f"(c.z), "f"(c.w));
+                }
+    #pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j4 + u;
+                    if (j >= VN) break;
+    #pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int dx = j - q - R;
+                        if (dx < -R || dx > R) continue;
+                        const float d = gs[q] - gt[u];
+                        const float w = j3_ex2(fmaf(-d, d, ce[dx < 0 ? -dx : dx]));
+                        acc01[q] = j3_ffma2(w, v01[u], acc01[q]);
+                        acc2z[q] = j3_ffma2(w, v2z[u], acc2z[q]);
+                    }
                 }
             }
         }
@@ -226,16 +298,16 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     }
 }
 
-template <int R, int TH, bool PEERS, int MINB>
+template <int R, int TH, bool PEERS, int MINB, bool PX = false>
 static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J3Geom<R, TH>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB, PX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * batch);
-    k_blf_j3<R, TH, PEERS, MINB><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_j3<R, TH, PEERS, MINB, PX><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -248,7 +320,16 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
         const char* e = std::getenv("BLFLS_J3_MINB");
         return e ? std::atoi(e) : 3;
     }();
-    if (p.npeers > 0) return launch_j3_t<R, TH, true, 3>(p, batch, st);
+    static const int px = [] {
+        const char* e = std::getenv("BLFLS_J3X");  // 0: per-tap exponents (A/B)
+        return e ? std::atoi(e) : 2;
+    }();
+    // pair exponents at 2 CTAs per SM by default (c5: 0.786 of the MUFU peak,
+    // 0.781 at 3 CTAs, 0.765 without); the peer-storing epilogue uses the
+    // same arithmetic so band exchange targets match the plain band filter
+    if (p.npeers > 0) return launch_j3_t<R, TH, true, 2, true>(p, batch, st);
+    if (px == 2) return launch_j3_t<R, TH, false, 2, true>(p, batch, st);
+    if (px == 3) return launch_j3_t<R, TH, false, 3, true>(p, batch, st);
     if (minb == 3) return launch_j3_t<R, TH, false, 3>(p, batch, st);
     return launch_j3_t<R, TH, false, 4>(p, batch, st);
 }
