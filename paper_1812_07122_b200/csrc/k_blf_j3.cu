@@ -14,6 +14,8 @@
 // column by column (LDS.128 = two columns of one interleaved array) instead
 // of being held in registers, so the kernel stays at 4 CTAs per SM; the
 // interleaved rows are chunk-swizzled (j3_sw) so the LDS.128 are conflict-free.
+#include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 
 #include "blfls_internal.cuh"
@@ -80,69 +82,19 @@ struct J3Geom {
     }
 };
 
-// PEERS: fused band exchange (multi-GPU row bands): every target is stored
-// into the full-height buffers of all p.npeers ranks (NVLink peer pointers)
-// PX: guide difference and exponent of two adjacent outputs as one FFMA2
-// each (column-spatial pair table p.cep, row factor on per-row partial sums)
-template <int R, int TH, bool PEERS, int MINB, bool PX = false>
-__global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
+// The filter of one staged tile (G: scaled guide gradients, S01 / S2: the
+// interleaved channel gradients, all [ROWS] rows from tile row -R)
+// and its epilogue: targets of output rows [ty0, ty0 + TH) x columns
+// [tx0, tx0 + 64).  row_hook(i) runs at the start of window row i (the
+// persistent kernel issues its next-tile copies there).
+template <int R, int TH, bool PEERS, bool PX, class Hook>
+__device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* __restrict__ G,
+                                               const float2* __restrict__ S01, const float2* __restrict__ S2,
+                                               int b, int axis, int tx0, int ty0, float range, Hook&& row_hook)
 {
     using Gm = J3Geom<R, TH>;
-    constexpr int P = Gm::P, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
-    constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
-    extern __shared__ __align__(16) float smj[];
-    float* G = smj;                                                   // [ROWS][GP]
-    float2* S01 = reinterpret_cast<float2*>(smj + ROWS * GP);         // [ROWS][SP] {g0, g1}
-    float2* S2 = S01 + ROWS * SP;                                     // [ROWS][SP] {g2, 1}
-
+    constexpr int P = Gm::P, VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
     const int H = p.H, W = p.W;
-    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
-    const int tx0 = blockIdx.x * TW;
-    const int ty0 = p.y0 + blockIdx.y * TH;
-    const size_t plane = (size_t)H * W;
-    float s, range, sg, grange;
-    j3_decode(p.lohi, b, p.range_coef, s, range);
-    j3_decode(p.glohi, b, p.range_coef, sg, grange);
-    const float* fimg = p.f + (size_t)b * 3 * plane;
-    const float* gimg = p.guide + (size_t)b * p.GC * plane;
-
-    // ---- prologue: this axis' circular gradients of guide and channels
-    // staging: warp per tile row, lane per column
-    {
-        const int lane = threadIdx.x & 31;
-        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
-            const int y = ty0 - R + i;
-            const bool yin = y >= 0 && y < H;
-            const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
-            const size_t r0 = (size_t)(yin ? y : 0) * W, r1 = (size_t)(yin ? yn : 0) * W;
-            float* grow = G + i * GP;
-            float2* s01 = S01 + i * SP;
-            float2* s2 = S2 + i * SP;
-#pragma unroll
-            for (int j = lane; j < COLS; j += 32) {
-                const int x = tx0 - R + j;
-                const int o = j3_sw(j);
-                if (yin && x >= 0 && x < W) {
-                    const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
-                    grow[j] = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
-                    float g[3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float* fc = fimg + (size_t)c * plane;
-                        g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
-                    }
-                    s01[o] = make_float2(g[0], g[1]);
-                    s2[o] = make_float2(g[2], 1.0f);
-                } else {
-                    grow[j] = kJ3Sentinel;
-                    s01[o] = make_float2(0.f, 0.f);
-                    s2[o] = make_float2(0.f, 0.f);
-                }
-            }
-        }
-    }
-    __syncthreads();
-
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int ox = tx0 + tx * P, oy = ty0 + ty;
     float gs[P];
@@ -160,6 +112,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
         asm("mov.b64 %0, {%1, %1};" : "=l"(m1) : "f"(-1.0f));
 #pragma unroll 1
         for (int dy = -R; dy <= R; ++dy) {
+            row_hook(dy + R);
             const float* grow = G + (ty + R + dy) * GP + tx * P;
             const float2* s01 = S01 + (ty + R + dy) * SP;
             const float2* s2 = S2 + (ty + R + dy) * SP;
@@ -224,6 +177,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     } else {
 #pragma unroll 1
         for (int dy = -R; dy <= R; ++dy) {
+            row_hook(dy + R);
             const int ady = dy < 0 ? -dy : dy;
             float ce[R + 1];  // log2 spatial weight of (dy, |dx|)
     #pragma unroll
@@ -298,6 +252,254 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     }
 }
 
+// PEERS: fused band exchange (multi-GPU row bands): every target is stored
+// into the full-height buffers of all p.npeers ranks (NVLink peer pointers)
+// PX: guide difference and exponent of two adjacent outputs as one FFMA2
+// each (column-spatial pair table p.cep, row factor on per-row partial sums)
+template <int R, int TH, bool PEERS, int MINB, bool PX = false>
+__global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
+{
+    using Gm = J3Geom<R, TH>;
+    constexpr int P = Gm::P, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
+    constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
+    extern __shared__ __align__(16) float smj[];
+    float* G = smj;                                                   // [ROWS][GP]
+    float2* S01 = reinterpret_cast<float2*>(smj + ROWS * GP);         // [ROWS][SP] {g0, g1}
+    float2* S2 = S01 + ROWS * SP;                                     // [ROWS][SP] {g2, 1}
+
+    const int H = p.H, W = p.W;
+    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range, sg, grange;
+    j3_decode(p.lohi, b, p.range_coef, s, range);
+    j3_decode(p.glohi, b, p.range_coef, sg, grange);
+    const float* fimg = p.f + (size_t)b * 3 * plane;
+    const float* gimg = p.guide + (size_t)b * p.GC * plane;
+
+    // ---- prologue: this axis' circular gradients of guide and channels
+    // staging: warp per tile row, lane per column
+    {
+        const int lane = threadIdx.x & 31;
+        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
+            const int y = ty0 - R + i;
+            const bool yin = y >= 0 && y < H;
+            const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+            const size_t r0 = (size_t)(yin ? y : 0) * W, r1 = (size_t)(yin ? yn : 0) * W;
+            float* grow = G + i * GP;
+            float2* s01 = S01 + i * SP;
+            float2* s2 = S2 + i * SP;
+#pragma unroll
+            for (int j = lane; j < COLS; j += 32) {
+                const int x = tx0 - R + j;
+                const int o = j3_sw(j);
+                if (yin && x >= 0 && x < W) {
+                    const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                    grow[j] = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
+                    float g[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float* fc = fimg + (size_t)c * plane;
+                        g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
+                    }
+                    s01[o] = make_float2(g[0], g[1]);
+                    s2[o] = make_float2(g[2], 1.0f);
+                } else {
+                    grow[j] = kJ3Sentinel;
+                    s01[o] = make_float2(0.f, 0.f);
+                    s2[o] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    j3_filter_tile<R, TH, PEERS, PX>(p, G, S01, S2, b, axis, tx0, ty0, range, [](int) {});
+}
+
+// Persistent variant: gridDim.x CTAs stride over the tiles (same order as
+// k_blf_j3's grid: tile column, tile row, image x axis).  The raw samples of
+// the NEXT tile (guide + 3 channels, rows [-R, TH + R] and the 16-byte
+// aligned columns [-R - 1, TW + R + 1) around it, index H / W wrapped to 0
+// for the periodic +1 neighbour) are copied into a shared staging area by
+// 16-byte cp.async, a few per thread at the start of each window row while
+// the current tile is filtered; the gradient prologue then reads shared
+// memory instead of waiting on global loads (ncu, c5: the global-load
+// prologue of k_blf_j3 held 38% of the warp samples and left the SM's other
+// CTA alone on the MUFU).  Needs W % 4 == 0 (whole 16-byte chunks per row).
+// Gradients and arithmetic are identical to k_blf_j3.
+template <int R, int TH>
+struct J3Raw {
+    using Gm = J3Geom<R, TH>;
+    static constexpr int RROWS = Gm::ROWS + 1;
+    static constexpr int XOFF = (R + 3) & ~3;                      // tile column 0 at raw column XOFF
+    static constexpr int CH = (XOFF + Gm::TW + R + 1 + 3) / 4;     // 16-byte chunks per row
+    static constexpr int RP = 4 * CH;                              // raw pitch (floats)
+    static constexpr int NCH = 4 * RROWS * CH;                     // chunks per tile (all planes)
+    static constexpr int PER_THREAD = (NCH + Gm::NT - 1) / Gm::NT;
+    static constexpr int PER_ROW = (PER_THREAD + 2 * R) / (2 * R + 1);  // per window row
+    static constexpr size_t raw_off() { return (Gm::smem_bytes() + 15) & ~(size_t)15; }
+    static constexpr size_t smem_bytes() { return raw_off() + (size_t)4 * RROWS * RP * sizeof(float); }
+    static_assert(XOFF >= R + 0 && RP >= XOFF - R + Gm::COLS + 1, "raw staging covers the window");
+};
+
+__device__ __forceinline__ void j3_cp_async16(float* dst, const float* src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+struct J3Tile {
+    int b, axis, tx0, ty0;
+};
+
+template <int R, int TH>
+__device__ __forceinline__ J3Tile j3_tile(const BlfParams& p, int t, int ntx, int nty)
+{
+    J3Tile k;
+    const int bx = t % ntx, r = t / ntx;
+    const int by = r % nty, z = r / nty;
+    k.b = z >> 1;
+    k.axis = z & 1;
+    k.tx0 = bx * J3Geom<R, TH>::TW;
+    k.ty0 = p.y0 + by * TH;
+    return k;
+}
+
+// cp.async chunks [m0, m1) (per thread: chunk threadIdx.x + NT m) of tile k
+template <int R, int TH>
+__device__ __forceinline__ void j3_prefetch(const BlfParams& p, const J3Tile& k, float* raw, int m0, int m1)
+{
+    using Rw = J3Raw<R, TH>;
+    constexpr int NT = J3Geom<R, TH>::NT;
+    const int H = p.H, W = p.W;
+    const size_t plane = (size_t)H * W;
+#pragma unroll
+    for (int m = m0; m < m1; ++m) {
+        const int c = threadIdx.x + NT * m;
+        if (Rw::NCH % NT != 0 && c >= Rw::NCH) break;
+        const int row = c / Rw::CH, q = c - row * Rw::CH;  // row over planes x RROWS
+        const int pl = row / Rw::RROWS, ii = row - pl * Rw::RROWS;
+        int y = k.ty0 - R + ii;
+        int x = k.tx0 - Rw::XOFF + 4 * q;
+        if (y < 0 || y > H || x < 0 || x > W) continue;
+        if (y == H) y = 0;
+        if (x == W) x = 0;
+        const float* base = pl == 0 ? p.guide + (size_t)k.b * p.GC * plane
+                                    : p.f + ((size_t)k.b * 3 + (pl - 1)) * plane;
+        j3_cp_async16(raw + row * Rw::RP + 4 * q, base + (size_t)y * W + x);
+    }
+}
+
+// SPREAD: the next tile's copies are issued a few per window row (else all
+// before the filter loop)
+template <int R, int TH, bool SPREAD>
+__global__ void __launch_bounds__(16 * TH, 2) k_blf_j3p(const BlfParams p, int total, int ntx, int nty)
+{
+    using Gm = J3Geom<R, TH>;
+    using Rw = J3Raw<R, TH>;
+    constexpr int NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS, GP = Gm::GP, SP = Gm::SP;
+    extern __shared__ __align__(16) float smj[];
+    float* G = smj;                                                   // [ROWS][GP]
+    float2* S01 = reinterpret_cast<float2*>(smj + ROWS * GP);         // [ROWS][SP] {g0, g1}
+    float2* S2 = S01 + ROWS * SP;                                     // [ROWS][SP] {g2, 1}
+    float* raw = smj + Rw::raw_off() / sizeof(float);                 // [4][RROWS][RP]
+    const int H = p.H, W = p.W;
+    const int lane = threadIdx.x & 31;
+
+    int t = blockIdx.x;
+    if (t >= total) return;
+    j3_prefetch<R, TH>(p, j3_tile<R, TH>(p, t, ntx, nty), raw, 0, Rw::PER_THREAD);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // only t is live across the filter loop (tiles are re-derived from it)
+    for (; t < total; t += gridDim.x) {
+        const J3Tile k = j3_tile<R, TH>(p, t, ntx, nty);
+        float s, range, sg, grange;
+        j3_decode(p.lohi, k.b, p.range_coef, s, range);
+        j3_decode(p.glohi, k.b, p.range_coef, sg, grange);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();  // raw complete; every warp done with the previous tile
+        // gradients of this axis from the staged samples (k_blf_j3's prologue)
+        const int off1 = k.axis == 0 ? 1 : Rw::RP;
+        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
+            const int y = k.ty0 - R + i;
+            const bool yin = y >= 0 && y < H;
+            const float* r0 = raw + i * Rw::RP + (Rw::XOFF - R);
+            float* grow = G + i * GP;
+            float2* s01 = S01 + i * SP;
+            float2* s2 = S2 + i * SP;
+#pragma unroll
+            for (int j = lane; j < COLS; j += 32) {
+                const int x = k.tx0 - R + j;
+                const int o = j3_sw(j);
+                if (yin && x >= 0 && x < W) {
+                    grow[j] = (r0[j + off1] - r0[j]) * sg;
+                    float g[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float* rc = r0 + (c + 1) * Rw::RROWS * Rw::RP;
+                        g[c] = rc[j + off1] - rc[j];
+                    }
+                    s01[o] = make_float2(g[0], g[1]);
+                    s2[o] = make_float2(g[2], 1.0f);
+                } else {
+                    grow[j] = kJ3Sentinel;
+                    s01[o] = make_float2(0.f, 0.f);
+                    s2[o] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+        __syncthreads();  // tile staged; raw free for the next tile's copies
+        const int tn = t + (int)gridDim.x;
+        if constexpr (SPREAD) {
+            auto hook = [&](int i) {
+                if (tn < total && i * Rw::PER_ROW < Rw::PER_THREAD) {
+                    const J3Tile kn = j3_tile<R, TH>(p, tn, ntx, nty);
+                    j3_prefetch<R, TH>(p, kn, smj + Rw::raw_off() / sizeof(float), i * Rw::PER_ROW,
+                                       min((i + 1) * Rw::PER_ROW, Rw::PER_THREAD));
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                }
+            };
+            j3_filter_tile<R, TH, false, true>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, hook);
+        } else {
+            if (tn < total) {
+                j3_prefetch<R, TH>(p, j3_tile<R, TH>(p, tn, ntx, nty), raw, 0, Rw::PER_THREAD);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+            j3_filter_tile<R, TH, false, true>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, [](int) {});
+        }
+    }
+}
+
+// persistent launch when 2 CTAs fit per SM; false otherwise
+template <int R, int TH, bool SPREAD>
+static bool launch_j3p(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
+{
+    using Gm = J3Geom<R, TH>;
+    constexpr size_t smem = J3Raw<R, TH>::smem_bytes();
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        int dev = 0;
+        occ = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            cudaFuncSetAttribute(k_blf_j3p<R, TH, SPREAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_blf_j3p<R, TH, SPREAD>, Gm::NT, smem) != cudaSuccess)
+            occ = 0;
+        cudaGetLastError();
+    }
+    if (occ < 2 || (p.W & 3) != 0) return false;
+    const int ntx = (p.W + Gm::TW - 1) / Gm::TW, nty = (p.y1 - p.y0 + TH - 1) / TH;
+    const long total = (long)ntx * nty * 2 * batch;
+    if (total > INT32_MAX) return false;
+    const int grid = (int)std::min<long>(total, (long)occ * nsm);
+    k_blf_j3p<R, TH, SPREAD><<<grid, Gm::NT, smem, st>>>(p, (int)total, ntx, nty);
+    *err = cudaGetLastError();
+    return true;
+}
+
 template <int R, int TH, bool PEERS, int MINB, bool PX = false>
 static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
 {
@@ -327,8 +529,24 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
     // pair exponents at 2 CTAs per SM by default (c5: 0.786 of the MUFU peak,
     // 0.781 at 3 CTAs, 0.765 without); the peer-storing epilogue uses the
     // same arithmetic so band exchange targets match the plain band filter
+    static const int persistent = [] {
+        // 0 (default): one CTA per tile; 1: persistent, copies before the
+        // filter loop; 2: persistent, copies spread over the window rows.
+        // Measured (c5, r01 B200): 0.778 / 0.698 / 0.587 of the MUFU peak --
+        // the persistent kernels remove the global-load stalls of the
+        // prologue but add ~7% instructions and two barriers per tile, and
+        // the other CTA on the SM already keeps the MUFU busy while one
+        // CTA stages its tile
+        const char* e = std::getenv("BLFLS_J3P");
+        return e ? std::atoi(e) : 0;
+    }();
     if (p.npeers > 0) return launch_j3_t<R, TH, true, 2, true>(p, batch, st);
-    if (px == 2) return launch_j3_t<R, TH, false, 2, true>(p, batch, st);
+    if (px == 2) {
+        cudaError_t e = cudaSuccess;
+        if (persistent == 1 && launch_j3p<R, TH, false>(p, batch, st, &e)) return e;
+        if (persistent == 2 && launch_j3p<R, TH, true>(p, batch, st, &e)) return e;
+        return launch_j3_t<R, TH, false, 2, true>(p, batch, st);
+    }
     if (px == 3) return launch_j3_t<R, TH, false, 3, true>(p, batch, st);
     if (minb == 3) return launch_j3_t<R, TH, false, 3>(p, batch, st);
     return launch_j3_t<R, TH, false, 4>(p, batch, st);

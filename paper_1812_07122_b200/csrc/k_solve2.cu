@@ -287,8 +287,28 @@ bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, in
         BLFLS_V2_ROWS(BLFLS_V2_CONSIDER)
     }
 #undef BLFLS_V2_CONSIDER
-    const int V = bestV ? bestV : narrowV;
+    int V = bestV ? bestV : narrowV;
     if (V == 1 << 30) return false;
+    // experiment knob: force the vectors per CTA of the column / row passes
+    static const int forceV[2] = {[] {
+                                      const char* e = std::getenv("BLFLS_V2_ROWV");
+                                      return e ? std::atoi(e) : 0;
+                                  }(),
+                                  [] {
+                                      const char* e = std::getenv("BLFLS_V2_COLV");
+                                      return e ? std::atoi(e) : 0;
+                                  }()};
+    if (const int fv = forceV[which == 1 ? 1 : 0]) {
+        bool have = false;
+#define BLFLS_V2_HAVE(N, VV, TV, PM) have = have || (N == n && VV == fv && PM == pmax);
+        if (which == 1) {
+            BLFLS_V2_COLS(BLFLS_V2_HAVE)
+        } else {
+            BLFLS_V2_ROWS(BLFLS_V2_HAVE)
+        }
+#undef BLFLS_V2_HAVE
+        if (have) V = fv;
+    }
 #define BLFLS_V2_GO(N, VV, TV, PM)                                  \
     if (n == N && V == VV && pmax == PM) {                          \
         launch2<Fft2<N, VV, TV, PM>>(which, p, tw, planes, st);     \
