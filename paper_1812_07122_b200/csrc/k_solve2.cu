@@ -18,6 +18,7 @@
 // the stage entry points' forward-only / inverse-only column modes) runs the
 // kernels of k_solve.cu.
 #include "blfls_internal.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 #include "fft2.cuh"
@@ -138,6 +139,80 @@ __global__ void __launch_bounds__(G::THREADS, G::THREADS <= 512 ? 65536 / (64 * 
     }
 }
 
+// Pipelined column pass: persistent CTAs stride over the column strips
+// (plane-major) with two shared buffers; the next strip is copied in by
+// 16-byte cp.async while the current one is transformed, so the global loads
+// never stall the transform (k2_col's stage 0 reads global memory directly
+// and every CTA alternates load / transform / store phases).  Same
+// arithmetic as k2_col (stage 0 runs from shared memory), bit-identical
+// spectra.  Strips past wc read the spectrum's pad columns (spitch is a
+// multiple of 16 >= roundup(wc, V)); their results are not stored.
+template <class G>
+constexpr int col_pipe_minb()
+{
+    return (int)((227u * 1024u) / (2 * G::smem_bytes() + 1024)) > 0
+               ? (int)((227u * 1024u) / (2 * G::smem_bytes() + 1024))
+               : 1;
+}
+
+template <class G>
+__global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
+    k2_col_pipe(const SolveParams p, const float2* __restrict__ tw, int nsp, int total)
+{
+    extern __shared__ __align__(16) float2 buf2[];
+    constexpr int N = G::N, V = G::V, BUF = G::PADN * G::V;
+    static_assert(V % 2 == 0, "16-byte chunks of two columns");
+    const int v = threadIdx.x % V, t = threadIdx.x / V;
+    const size_t sp = p.spitch;
+    auto issue = [&](int s, float2* dst) {
+        const int plane = s / nsp, c0 = (s - plane * nsp) * V;
+        const float2* src = p.spec + (size_t)plane * N * sp + c0;
+        for (int c = threadIdx.x; c < N * V / 2; c += G::THREADS) {
+            const int u = c / (V / 2), h = c - u * (V / 2);
+            const unsigned d = (unsigned)__cvta_generic_to_shared(dst + G::ca(2 * h, u));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + (size_t)u * sp + 2 * h)
+                         : "memory");
+        }
+    };
+    int s = blockIdx.x;
+    if (s >= total) return;
+    issue(s, buf2);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int k = 0; s < total; s += gridDim.x, ++k) {
+        float2* buf = buf2 + (k & 1) * BUF;
+        const int sn = s + gridDim.x;
+        if (sn < total) issue(sn, buf2 + ((k + 1) & 1) * BUF);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // strip s landed
+        const int plane = s / nsp;
+        const int vc = (s - plane * nsp) * V + v;
+        const bool live = vc < p.wc;
+        float2* spec = p.spec + (size_t)plane * N * sp + (live ? vc : 0);
+        auto lds = [&](int u) { return buf[G::ca(v, u)]; };
+        auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
+        s2_smem_stages<G, true, false, 0, G::NST>(buf, v, t, tw);
+        const float gx = live ? __ldg(&p.gain_x[vc]) : 0.f;
+        const float L = p.lambda, ihw = p.inv_hw;
+        auto lds_scaled = [&](int u) {
+            const float sc = ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f));
+            return cscale(buf[G::ca(v, u)], sc);
+        };
+        auto stg = [&](int u, float2 z) {
+            if (live) spec[(size_t)u * sp] = z;
+        };
+        if constexpr (G::NST == 1) {
+            s2_stage<G, true, 0, true>(t, tw, lds_scaled, stg);
+        } else {
+            s2_stage<G, true, 0, true>(t, tw, lds_scaled, sts);
+            __syncthreads();
+            s2_smem_stages<G, true, true, 1, G::NST - 1>(buf, v, t, tw);
+            s2_stage<G, true, G::NST - 1, false>(t, tw, lds, stg);
+        }
+        __syncthreads();  // buf free for the copies of strip s + 2 gridDim.x
+    }
+}
+
 // grid (ceil(H / V), planes)
 template <class G>
 __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, const float2* __restrict__ tw)
@@ -230,6 +305,26 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
 {
     constexpr size_t smem = G::smem_bytes();
     if (which == 1) {
+        static const bool pipe = [] {
+            const char* e = std::getenv("BLFLS_COL_PIPE");  // 1: pipelined column pass
+            return e != nullptr && std::atoi(e) != 0;
+        }();
+        if constexpr (G::V % 2 == 0) {
+            if (pipe) {
+                const int nsp = (p.wc + G::V - 1) / G::V;
+                const int total = nsp * planes;
+                int occ = 0, dev = 0, nsm = 148;
+                set_smem2(k2_col_pipe<G>, 2 * smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_col_pipe<G>, G::THREADS, 2 * smem);
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                if (occ > 0) {
+                    const int grid = std::min(total, occ * nsm);
+                    k2_col_pipe<G><<<grid, G::THREADS, 2 * smem, st>>>(p, tw, nsp, total);
+                    return;
+                }
+            }
+        }
         dim3 grid((p.wc + G::V - 1) / G::V, planes);
         set_smem2(k2_col<G>, smem);
         k2_col<G><<<grid, G::THREADS, smem, st>>>(p, tw);

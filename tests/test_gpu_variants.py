@@ -5,6 +5,9 @@ read once per process, so each side runs in its own subprocess).
 - BLFLS_J3P=1 / 2: the persistent cp.async-prefetching shared-gray-guide
   filter (k_blf_j3p, copies before / spread over the filter loop) against
   the default one-CTA-per-tile k_blf_j3.
+- BLFLS_COL_PIPE=1: the pipelined column pass (k2_col_pipe: persistent,
+  double-buffered cp.async strips) against k2_col, through full BLF-LS runs
+  at every column length with a high-radix geometry.
 """
 from __future__ import annotations
 
@@ -44,9 +47,31 @@ SHAPES = [(1, 40, 64, 7), (2, 50, 132, 7), (2, 16, 16, 5), (1, 70, 300, 5), (5, 
           (1, 64, 64, 15), (1, 37, 68, 3), (3, 37, 129, 7), (1, 33, 47, 15)]
 
 
-def _run(tmp_path, name, env):
+_SOLVE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1812_07122_b200 as P
+from oracle import oracle as O
+out = {{}}
+for (b, c, h, w) in {shapes!r}:
+    img = np.stack([np.stack([O.gen_plane(700 + 10 * i + k, h, w, n_sites=12) for k in range(c)])
+                    for i in range(b)])
+    if b == 1:
+        img = img[0]
+    u = P.blf_ls(img, lam=1000.0, sigma_s=3.0, sigma_r=0.1, iters=2, radius=3)
+    out[f"u_{{b}}_{{c}}_{{h}}_{{w}}"] = np.asarray(u)
+np.savez({path!r}, **out)
+"""
+
+# column lengths of the high-radix column geometries (k_solve2.cu), odd and
+# even half-spectrum widths, several planes
+SOLVE_SHAPES = [(1, 1, 512, 64), (2, 3, 512, 70), (1, 3, 1024, 96), (1, 1, 1080, 48), (1, 3, 2048, 40),
+                (3, 1, 2048, 32), (1, 1, 4096, 18)]
+
+
+def _run(tmp_path, name, env, script=_SCRIPT, shapes=SHAPES):
     path = str(tmp_path / f"{name}.npz")
-    code = _SCRIPT.format(root=str(ROOT), shapes=SHAPES, path=path)
+    code = script.format(root=str(ROOT), shapes=shapes, path=path)
     e = dict(os.environ)
     e.update(env)
     subprocess.run([sys.executable, "-c", code], check=True, env=e, cwd=str(ROOT), timeout=600)
@@ -57,6 +82,14 @@ def _run(tmp_path, name, env):
 def test_shared_guide_persistent_matches_per_tile(tmp_path, variant):
     a = _run(tmp_path, "persistent", {"BLFLS_J3P": variant})
     b = _run(tmp_path, "per_tile", {"BLFLS_J3P": "0"})
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_pipelined_column_pass_matches_k2_col(tmp_path):
+    a = _run(tmp_path, "pipe", {"BLFLS_COL_PIPE": "1"}, _SOLVE_SCRIPT, SOLVE_SHAPES)
+    b = _run(tmp_path, "plain", {"BLFLS_COL_PIPE": "0"}, _SOLVE_SCRIPT, SOLVE_SHAPES)
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
