@@ -420,7 +420,7 @@ def run_ours(args, cfg):
                "timing": "host wall clock from the first submit to blfls_sync after K steps",
                "path": "paper_1812_07122_b200.blf_ls(pinned host tensors, wait=False) -> "
                        "blfls_run(HOST_PTRS|ASYNC|CHECK_FINITE): H2D, compute, D2H on separate "
-                       "streams, two staging slots"}
+                       "streams, two staging slots; batches of >= 128 MB streamed in up to 8 image chunks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1000,6 +1000,32 @@ blfls_status ensure_host_slots(blfls_plan_t p)
 
 }  // namespace
 
+namespace {
+
+// Images per chunk of an ASYNC host-pointer call: a large host batch is
+// streamed through the two staging slots in chunks (images are independent,
+// so the results are the same bits), so chunk k + 1's H2D and chunk k - 1's
+// D2H overlap chunk k's compute instead of the whole batch's copies
+// bracketing the whole batch's compute.  Chunks of >= 64 MB of input, at most
+// 8 per call; BLFLS_HOST_CHUNKS=n overrides the count (1: off).
+int host_chunk_images(blfls_plan_t p, int batch)
+{
+    static const int env = [] {
+        const char* e = std::getenv("BLFLS_HOST_CHUNKS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (batch < 2) return batch;
+    const size_t per_image = sizeof(float) * p->plane * (p->prm.channels + p->prm.guide_channels);
+    int n = env > 0 ? env : (int)std::min<size_t>(8, (size_t)batch * per_image / (64u << 20));
+    n = std::max(1, std::min(n, batch));
+    return (batch + n - 1) / n;
+}
+
+blfls_status run_impl(blfls_plan_t p, const float* img, const float* guide, int batch, int iters, float* out,
+                      void* stream, unsigned flags);
+
+}  // namespace
+
 blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int batch, int iters,
                        float* out, void* stream, unsigned flags)
 {
@@ -1010,6 +1036,28 @@ blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int
     if ((p->prm.guide_channels == 0) != (guide == nullptr))
         return fail(BLFLS_EINVAL, "smooth: guidance image shape does not match input");
     if ((r = set_device(p))) return r;
+    if ((flags & BLFLS_HOST_PTRS) && (flags & BLFLS_ASYNC) && !(flags & BLFLS_TIME_STAGES)) {
+        const int per = host_chunk_images(p, batch);
+        if (per < batch) {
+            const size_t ci = (size_t)p->prm.channels * p->plane, cg = (size_t)p->prm.guide_channels * p->plane;
+            for (int b0 = 0; b0 < batch; b0 += per) {
+                const int nb = std::min(per, batch - b0);
+                if ((r = run_impl(p, img + b0 * ci, guide ? guide + b0 * cg : nullptr, nb, iters, out + b0 * ci,
+                                  stream, flags)))
+                    return r;
+            }
+            return BLFLS_OK;
+        }
+    }
+    return run_impl(p, img, guide, batch, iters, out, stream, flags);
+}
+
+namespace {
+
+blfls_status run_impl(blfls_plan_t p, const float* img, const float* guide, int batch, int iters, float* out,
+                      void* stream, unsigned flags)
+{
+    blfls_status r;
     cudaStream_t us = (cudaStream_t)stream;
     const size_t n = (size_t)batch * p->prm.channels * p->plane;
     const size_t ng = guide ? (size_t)batch * p->prm.guide_channels * p->plane : 0;
@@ -1078,6 +1126,8 @@ blfls_status blfls_run(blfls_plan_t p, const float* img, const float* guide, int
     CK(cudaEventSynchronize(sl->d2h));
     return BLFLS_OK;
 }
+
+}  // namespace
 
 blfls_status blfls_sync(blfls_plan_t p)
 {

@@ -372,6 +372,35 @@ def test_async_host_pipeline(gpu, oracle):
     plan.sync()  # the deferred error is reported once
 
 
+@pytest.mark.parametrize("chunks", ["3", "4", "8"])
+def test_async_host_batch_chunks(gpu, oracle, chunks):
+    """A large ASYNC host batch is streamed through the staging slots in
+    chunks of images (BLFLS_HOST_CHUNKS, read once per process: here the
+    auto rule keeps small batches whole, so the chunked runs go through a
+    subprocess); every image equals the one-call result bit for bit."""
+    import subprocess
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {str(Path(__file__).resolve().parent.parent)!r})
+import paper_1812_07122_b200 as P
+from oracle import oracle as O
+b, h, w = 7, 40, 48
+imgs = np.stack([np.stack([O.gen_plane(60 + 3 * i + c, h, w, n_sites=12) for c in range(3)])
+                 for i in range(b)]).astype(np.float32)
+guide = np.stack([O.gen_plane(90 + i, h, w, n_sites=12)[None] for i in range(b)]).astype(np.float32)
+kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+ref = P.blf_ls(imgs, guide, **kw)
+out = np.empty_like(imgs)
+P.blf_ls(imgs, guide, out=out, wait=False, **kw)
+P.sync_plans()
+assert np.array_equal(out, ref), float(np.abs(out - ref).max())
+print("ok")
+"""
+    env = dict(os.environ, BLFLS_HOST_CHUNKS=chunks)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("c,h,w,r,pad,guided", [
     (1, 45, 37, 3, 3, False),    # 51 x 43: prime 43 (direct DFT stage), odd padded width
     (3, 30, 34, 3, 16, False),   # the reference default pad: 62 x 66 (31, 11)
