@@ -73,12 +73,14 @@ def load_traffic(name):
 def blf_kernel_name(cfg):
     """The brute-force BLF kernel the library dispatches for this config
     (k_blf.cu launch_grad_blf: packed shared-guide kernel for a gray guide over
-    RGB, packed self-guided kernel at r = 7 / 15, the unpacked kernel otherwise)."""
+    RGB, packed self-guided kernel with pair exponents and the FMA-pipe exp2
+    offload at r = 5 / 7 / 15 (k_blf_p2.cu launch_p2), the unpacked kernel
+    otherwise)."""
     if cfg.guide and cfg.channels == 3 and cfg.radius in (3, 5, 7, 15):
-        return "k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums)"
-    if not cfg.guide and cfg.radius in (7, 15):
-        return "k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums" + \
-            (", FMA-pipe exp2 on every 7th tap)" if cfg.radius == 15 else ")")
+        return "k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, pair exponents)"
+    if not cfg.guide and cfg.radius in (5, 7, 15):
+        return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, pair exponents, "
+                f"FMA-pipe exp2 on every {10 if cfg.radius == 5 else 7}th tap)")
     return "k_grad_blf (fused gradient + brute-force BLF)"
 
 
