@@ -265,8 +265,9 @@ def test_baseline_config_full_parity(gpu, oracle, name):
 
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_baseline_config_properties(gpu, oracle, name):
-    """Full-size c4 / c5: size-independent properties (the oracle takes
-    minutes there; BLFLS_FULL_PARITY=1 adds the full comparison)."""
+    """Full-size c4 / c5: size-independent properties, then the oracle
+    comparison of image 0 (about 30 s of host time on the GPU box;
+    BLFLS_FULL_PARITY=0 skips it)."""
     import torch
     cfg = gpu.CONFIGS[name]
     images = cfg.batch if name != "c5" else 8
@@ -296,7 +297,7 @@ def test_baseline_config_properties(gpu, oracle, name):
     if img.shape[0] > 1:
         one = _run_cfg(gpu, cfg, img[1:2].contiguous(), None if guide is None else guide[1:2].contiguous())
         assert (one[0] - out[1]).abs().max().item() == 0.0
-    if os.environ.get("BLFLS_FULL_PARITY") == "1":
+    if os.environ.get("BLFLS_FULL_PARITY", "1") != "0":
         ref = _oracle_cfg(oracle, cfg, img, guide)
         assert maxabs(out[0].cpu().numpy(), ref) <= TOL_OUT
 
