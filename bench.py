@@ -80,7 +80,7 @@ def blf_kernel_name(cfg):
         return "k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, pair exponents)"
     if not cfg.guide and cfg.radius in (5, 7, 15):
         return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, pair exponents, "
-                f"FMA-pipe exp2 on every {10 if cfg.radius == 5 else 7}th tap)")
+                f"FMA-pipe exp2 on every { {5: 10, 15: 8}.get(cfg.radius, 7) }th tap)")
     return "k_grad_blf (fused gradient + brute-force BLF)"
 
 

@@ -340,6 +340,17 @@ static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t
     return launch_p2_t<R, 16, MODE, POLY, false, 4, PX>(p, nplanes, st);
 }
 
+// default FMA-pipe exp2 period of the pair-exponent kernel per radius (r01
+// B200 sweeps, BLFLS_P2_POLY: r = 5 every 10th tap (c3), r = 7 every 7th
+// (c2: 0.942 vs 0.939 at 8, 0.902 at 6), r = 15 every 8th (c4: 1.040 vs
+// 1.030 at 7)); the peer-storing band epilogue uses the same period so its
+// targets equal the plain band filter's bit for bit
+template <int R>
+constexpr int kP2DefaultPoly()
+{
+    return R == 5 ? 10 : (R == 15 ? 8 : 7);
+}
+
 template <int R, int MODE>
 static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
 {
@@ -356,10 +367,10 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
     // pair exponents (PX) free enough issue slots for the offload at r = 7 too
     // (r = 5: every 10th; with 32-row tiles it ties the unpacked kernel at
     // c3 and beats it at c1)
-    const int poly = poly_env >= 0 ? poly_env : (px ? (R == 5 ? 10 : 7) : (R >= 12 ? 7 : 0));
+    const int poly = poly_env >= 0 ? poly_env : (px ? kP2DefaultPoly<R>() : (R >= 12 ? 7 : 0));
     // peer-storing epilogue (fused band exchange) with the default offload, so
     // its targets equal the plain band filter's bit for bit
-    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, (R == 5 ? 10 : 7), true, 3, true>(p, nplanes, st);
+    if (p.npeers > 0) return launch_p2_t<R, 16, MODE, kP2DefaultPoly<R>(), true, 3, true>(p, nplanes, st);
     if (px) {
         switch (poly) {
             case 5: return launch_p2_sized<R, MODE, 5, true>(p, nplanes, st);
