@@ -87,7 +87,11 @@ struct J3Geom {
 // and its epilogue: targets of output rows [ty0, ty0 + TH) x columns
 // [tx0, tx0 + 64).  row_hook(i) runs at the start of window row i (the
 // persistent kernel issues its next-tile copies there).
-template <int R, int TH, bool PEERS, bool PX, class Hook>
+// XF (factorised exponent, PX only): -(a - b)^2 = -a^2 + 2ab - b^2; exp2(-b^2)
+// is folded into the staged sources of column t (G holds b), exp2(-a^2)
+// multiplies numerator and normaliser of output s alike and cancels, so one
+// FFMA2 per output pair and tap forms both exponents: e = {2a_q, 2a_q+1} b + cs
+template <int R, int TH, bool PEERS, bool PX, bool XF, class Hook>
 __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* __restrict__ G,
                                                const float2* __restrict__ S01, const float2* __restrict__ S2,
                                                int b, int axis, int tx0, int ty0, float range, Hook&& row_hook)
@@ -107,8 +111,9 @@ __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* 
     }
     if constexpr (PX) {
         unsigned long long gsp[2], m1;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[0]) : "f"(gs[0]), "f"(gs[1]));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[1]) : "f"(gs[2]), "f"(gs[3]));
+        const float xs = XF ? 2.0f : 1.0f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[0]) : "f"(xs * gs[0]), "f"(xs * gs[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[1]) : "f"(xs * gs[2]), "f"(xs * gs[3]));
         asm("mov.b64 %0, {%1, %1};" : "=l"(m1) : "f"(-1.0f));
 #pragma unroll 1
         for (int dy = -R; dy <= R; ++dy) {
@@ -148,11 +153,15 @@ __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* 
                         if (!ok0 && !ok1) continue;
                         unsigned long long gtt, d, nd, ce, e;
                         asm("mov.b64 %0, {%1, %1};" : "=l"(gtt) : "f"(gt[u]));
-                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[h]));
-                        const float2 dd = j3_unpack(d);
-                        asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
                         asm("mov.b64 %0, {%1, %2};" : "=l"(ce) : "f"(p.cep[dx0 + R].x), "f"(p.cep[dx0 + R].y));
-                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                        if constexpr (XF) {
+                            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[h]), "l"(ce));
+                        } else {
+                            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[h]));
+                            const float2 dd = j3_unpack(d);
+                            asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
+                            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                        }
                         const float2 ee = j3_unpack(e);
                         if (ok0) {
                             const float w = j3_ex2(ee.x);
@@ -256,7 +265,7 @@ __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* 
 // into the full-height buffers of all p.npeers ranks (NVLink peer pointers)
 // PX: guide difference and exponent of two adjacent outputs as one FFMA2
 // each (column-spatial pair table p.cep, row factor on per-row partial sums)
-template <int R, int TH, bool PEERS, int MINB, bool PX = false>
+template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false>
 __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
 {
     using Gm = J3Geom<R, TH>;
@@ -296,17 +305,19 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
                 const int o = j3_sw(j);
                 if (yin && x >= 0 && x < W) {
                     const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
-                    grow[j] = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
+                    const float b = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
+                    grow[j] = b;
                     float g[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const float* fc = fimg + (size_t)c * plane;
                         g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
                     }
-                    s01[o] = make_float2(g[0], g[1]);
-                    s2[o] = make_float2(g[2], 1.0f);
+                    const float bw = XF ? j3_ex2(-b * b) : 1.0f;  // exp2(-b^2) of column t
+                    s01[o] = make_float2(g[0] * bw, g[1] * bw);
+                    s2[o] = make_float2(g[2] * bw, bw);
                 } else {
-                    grow[j] = kJ3Sentinel;
+                    grow[j] = XF ? 0.0f : kJ3Sentinel;  // XF: b = 0, zero sources: weight 0
                     s01[o] = make_float2(0.f, 0.f);
                     s2[o] = make_float2(0.f, 0.f);
                 }
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     }
     __syncthreads();
 
-    j3_filter_tile<R, TH, PEERS, PX>(p, G, S01, S2, b, axis, tx0, ty0, range, [](int) {});
+    j3_filter_tile<R, TH, PEERS, PX, XF>(p, G, S01, S2, b, axis, tx0, ty0, range, [](int) {});
 }
 
 // Persistent variant: gridDim.x CTAs stride over the tiles (same order as
@@ -461,13 +472,13 @@ __global__ void __launch_bounds__(16 * TH, 2) k_blf_j3p(const BlfParams p, int t
                     asm volatile("cp.async.commit_group;" ::: "memory");
                 }
             };
-            j3_filter_tile<R, TH, false, true>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, hook);
+            j3_filter_tile<R, TH, false, true, false>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, hook);
         } else {
             if (tn < total) {
                 j3_prefetch<R, TH>(p, j3_tile<R, TH>(p, tn, ntx, nty), raw, 0, Rw::PER_THREAD);
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            j3_filter_tile<R, TH, false, true>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, [](int) {});
+            j3_filter_tile<R, TH, false, true, false>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, [](int) {});
         }
     }
 }
@@ -500,16 +511,16 @@ static bool launch_j3p(const BlfParams& p, int batch, cudaStream_t st, cudaError
     return true;
 }
 
-template <int R, int TH, bool PEERS, int MINB, bool PX = false>
+template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false>
 static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J3Geom<R, TH>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB, PX>,
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB, PX, XF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * batch);
-    k_blf_j3<R, TH, PEERS, MINB, PX><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_j3<R, TH, PEERS, MINB, PX, XF><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -526,9 +537,10 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
         const char* e = std::getenv("BLFLS_J3X");  // 0: per-tap exponents (A/B)
         return e ? std::atoi(e) : 2;
     }();
-    // pair exponents at 2 CTAs per SM by default (c5: 0.786 of the MUFU peak,
-    // 0.781 at 3 CTAs, 0.765 without); the peer-storing epilogue uses the
-    // same arithmetic so band exchange targets match the plain band filter
+    // difference form (when XF does not apply): pair exponents at 2 CTAs per
+    // SM (c5: 0.786 of the MUFU peak, 0.781 at 3 CTAs, 0.765 without); the
+    // peer-storing epilogue uses the same arithmetic so band exchange targets
+    // match the plain band filter
     static const int persistent = [] {
         // 0 (default): one CTA per tile; 1: persistent, copies before the
         // filter loop; 2: persistent, copies spread over the window rows.
@@ -540,6 +552,21 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
         const char* e = std::getenv("BLFLS_J3P");
         return e ? std::atoi(e) : 0;
     }();
+    // factorised exponents (XF) whenever exp2(2ab) cannot overflow: |a|, |b| <=
+    // range_coef (gradients of an image spanning [lo, hi] are at most hi - lo),
+    // so the largest argument is 2 coef^2 (c5, sigma_r = 0.1: 36) and
+    // exp2(-b^2) >= 2^-30 keeps the staged sources normal.  XF needs fewer
+    // registers, so it runs at 4 CTAs per SM (64 registers): c5 0.778 -> 0.818
+    // of the MUFU peak (r01 B200; XF at 2 CTAs per SM: 0.748, at 3: 0.802).
+    // BLFLS_J3_XF=0 keeps the difference form.  The peer-storing band
+    // epilogue uses the same arithmetic as the plain band filter.
+    static const int xf = [] {
+        const char* e = std::getenv("BLFLS_J3_XF");
+        return e ? std::atoi(e) : 1;
+    }();
+    const bool use_xf = xf != 0 && px == 2 && 2.0f * p.range_coef * p.range_coef <= 60.0f;
+    if (p.npeers > 0 && use_xf) return launch_j3_t<R, TH, true, 4, true, true>(p, batch, st);
+    if (use_xf) return launch_j3_t<R, TH, false, 4, true, true>(p, batch, st);
     if (p.npeers > 0) return launch_j3_t<R, TH, true, 2, true>(p, batch, st);
     if (px == 2) {
         cudaError_t e = cudaSuccess;

@@ -66,14 +66,17 @@ def test_self_guided_vs_oracle(gpu, oracle, c, h, w, r, ss, sr, lam, iters):
     assert maxabs(out, ref) <= TOL_OUT
 
 
-@pytest.mark.parametrize("c,gc,r", [(3, 1, 7), (3, 3, 5), (1, 1, 6), (3, 1, 11)])
-def test_joint_vs_oracle(gpu, oracle, c, gc, r):
+@pytest.mark.parametrize("c,gc,r,sr", [(3, 1, 7, 0.1), (3, 3, 5, 0.1), (1, 1, 6, 0.1), (3, 1, 11, 0.1),
+                                        (3, 1, 7, 0.05), (3, 1, 5, 0.2), (3, 1, 3, 0.03)])
+def test_joint_vs_oracle(gpu, oracle, c, gc, r, sr):
+    """Gray guide over RGB runs the factorised-exponent kernel for sigma_r >=
+    ~0.07 and the difference form below (k_blf_j3.cu launch_j3)."""
     h, w = 40, 64
     img = _img(oracle, c, h, w, 31)
     guide = _img(oracle, gc, h, w, 77)
     ref = oracle.blf_ls(img.astype(np.float64), guide.astype(np.float64), lam=1000.0, sigma_s=7.0,
-                        sigma_r=0.1, iters=3, radius=r)
-    out = gpu.blf_ls(img, guide, lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=3, radius=r)
+                        sigma_r=sr, iters=3, radius=r)
+    out = gpu.blf_ls(img, guide, lam=1000.0, sigma_s=7.0, sigma_r=sr, iters=3, radius=r)
     assert maxabs(out, ref) <= TOL_OUT
 
 

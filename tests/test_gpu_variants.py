@@ -4,7 +4,10 @@ read once per process, so each side runs in its own subprocess).
 
 - BLFLS_J3P=1 / 2: the persistent cp.async-prefetching shared-gray-guide
   filter (k_blf_j3p, copies before / spread over the filter loop) against
-  the default one-CTA-per-tile k_blf_j3.
+  the one-CTA-per-tile k_blf_j3 (both in the difference form,
+  BLFLS_J3_XF=0).
+- the factorised-exponent shared-guide kernel (default where it applies)
+  against the difference form: equal to fp32 round-off (not bit-identical).
 - BLFLS_COL_PIPE=1: the pipelined column pass (k2_col_pipe: persistent,
   double-buffered cp.async strips) against k2_col, through full BLF-LS runs
   at every column length with a high-radix geometry.
@@ -80,8 +83,8 @@ def _run(tmp_path, name, env, script=_SCRIPT, shapes=SHAPES):
 
 @pytest.mark.parametrize("variant", ["1", "2"])
 def test_shared_guide_persistent_matches_per_tile(tmp_path, variant):
-    a = _run(tmp_path, "persistent", {"BLFLS_J3P": variant})
-    b = _run(tmp_path, "per_tile", {"BLFLS_J3P": "0"})
+    a = _run(tmp_path, "persistent", {"BLFLS_J3P": variant, "BLFLS_J3_XF": "0"})
+    b = _run(tmp_path, "per_tile", {"BLFLS_J3P": "0", "BLFLS_J3_XF": "0"})
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
@@ -93,3 +96,13 @@ def test_pipelined_column_pass_matches_k2_col(tmp_path):
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_shared_guide_factorised_exponent_close_to_difference_form(tmp_path):
+    a = _run(tmp_path, "xf", {"BLFLS_J3_XF": "1"})
+    b = _run(tmp_path, "diff", {"BLFLS_J3_XF": "0"})
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        # targets in raw gradient units of [0,1]-range images: the factorised
+        # exponent rounds 2ab (|2ab| <= 36 at sigma_r = 0.1) instead of (a - b)^2
+        assert np.max(np.abs(a[k].astype(np.float64) - b[k])) <= 2e-5, k
