@@ -71,14 +71,14 @@ __device__ __forceinline__ void p2_decode(const uint32_t* lohi, int b, float coe
 
 }  // namespace
 
-template <int R, int TH, int MODE>
+template <int R, int TH, int MODE, bool XF = false>
 struct P2Geom {
     static constexpr int P = 4, TW = 64, NT = 16 * TH;
     static constexpr int ROWS = TH + 2 * R;
     static constexpr int COLS = TW + 2 * R;
     static constexpr int VN = P + 2 * R;
     static constexpr int VN4 = (VN + 3) & ~3;
-    static constexpr int GP = MODE == 1 ? ((COLS + 3) & ~3) + 4 : 0;  // planar guide (MODE 1)
+    static constexpr int GP = (MODE == 1 || XF) ? ((COLS + 3) & ~3) + 4 : 0;  // planar guide (MODE 1, XF)
     static constexpr int SP = (COLS + 3 + 15) & ~15;                  // {v, 1} pitch (float2)
     static constexpr size_t smem_bytes()
     {
@@ -91,10 +91,15 @@ struct P2Geom {
 // at one source column as one FFMA2 each (the weight's column-spatial term
 // from the cep pair table; the row term applied to per-row partial sums), so
 // a tap costs 1 + 0.5 + 0.5 instructions next to its MUFU.EX2
-template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX = false>
+// XF (with PX): factorised exponent, as k_blf_j3.cu: -(a - b)^2 = -a^2 + 2ab -
+// b^2, exp2(-b^2) folded into the staged source {v B, B} of column t (the
+// guide b then lives in the planar G array for both modes), exp2(-a^2)
+// cancels between numerator and normaliser: one FFMA2 {2a_q, 2a_q+1} b + cs
+// per output pair and tap
+template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX = false, bool XF = false>
 __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
 {
-    using Gm = P2Geom<R, TH, MODE>;
+    using Gm = P2Geom<R, TH, MODE, XF>;
     constexpr int P = Gm::P, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
     constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
     extern __shared__ __align__(16) float smp[];
@@ -133,12 +138,20 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
                 if (yin && x >= 0 && x < W) {
                     const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
                     const float v = __ldg(f1 + x1) - __ldg(f0 + x);
-                    if (MODE == 0) {
+                    if constexpr (XF) {
+                        const float bb = MODE == 0 ? v * s : (__ldg(g1 + x1) - __ldg(g0 + x)) * sg;
+                        const float bw = p2_ex2(-bb * bb);  // exp2(-b^2) of column t
+                        G[i * GP + j] = bb;
+                        srow[p2_sw(j)] = make_float2((MODE == 0 ? v * s : v) * bw, bw);
+                    } else if (MODE == 0) {
                         srow[p2_sw(j)] = make_float2(v * s, 1.0f);  // source = guide (scaled)
                     } else {
                         G[i * GP + j] = (__ldg(g1 + x1) - __ldg(g0 + x)) * sg;
                         srow[p2_sw(j)] = make_float2(v, 1.0f);
                     }
+                } else if constexpr (XF) {
+                    srow[p2_sw(j)] = make_float2(0.f, 0.f);  // weight 0, finite exponent
+                    G[i * GP + j] = 0.f;
                 } else {
                     srow[p2_sw(j)] = make_float2(MODE == 0 ? kP2Sentinel : 0.f, 0.f);
                     if (MODE == 1) G[i * GP + j] = kP2Sentinel;
@@ -154,13 +167,15 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
     unsigned long long acc[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-        gs[q] = MODE == 0 ? SV[(ty + R) * SP + p2_sw(tx * P + q + R)].x : G[(ty + R) * GP + tx * P + q + R];
+        gs[q] = (MODE == 0 && !XF) ? SV[(ty + R) * SP + p2_sw(tx * P + q + R)].x
+                                   : G[(ty + R) * GP + tx * P + q + R];
         acc[q] = 0ull;
     }
     if constexpr (PX) {
         unsigned long long gsp[2];
-        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[0]) : "f"(gs[0]), "f"(gs[1]));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[1]) : "f"(gs[2]), "f"(gs[3]));
+        const float xs = XF ? 2.0f : 1.0f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[0]) : "f"(xs * gs[0]), "f"(xs * gs[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[1]) : "f"(xs * gs[2]), "f"(xs * gs[3]));
         unsigned long long m1;
         asm("mov.b64 %0, {%1, %1};" : "=l"(m1) : "f"(-1.0f));
 #pragma unroll 1
@@ -179,12 +194,12 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
                     const float4 a = *reinterpret_cast<const float4*>(sv + p2_sw(tx * P + j4 + 2 * h));
                     asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h]) : "f"(a.x), "f"(a.y));
                     asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h + 1]) : "f"(a.z), "f"(a.w));
-                    if (MODE == 0) {
+                    if (MODE == 0 && !XF) {
                         gt[2 * h] = a.x;
                         gt[2 * h + 1] = a.z;
                     }
                 }
-                if (MODE == 1) {
+                if (MODE == 1 || XF) {
                     const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
                     gt[0] = g4.x;
                     gt[1] = g4.y;
@@ -202,11 +217,15 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
                         if (!ok0 && !ok1) continue;
                         unsigned long long gtt, d, nd, ce, e;
                         asm("mov.b64 %0, {%1, %1};" : "=l"(gtt) : "f"(gt[u]));
-                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[h]));
-                        const float2 dd = p2_unpack(d);
-                        asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
                         asm("mov.b64 %0, {%1, %2};" : "=l"(ce) : "f"(p.cep[dx0 + R].x), "f"(p.cep[dx0 + R].y));
-                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                        if constexpr (XF) {
+                            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[h]), "l"(ce));
+                        } else {
+                            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[h]));
+                            const float2 dd = p2_unpack(d);
+                            asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
+                            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                        }
                         const float2 ee = p2_unpack(e);
                         if (ok0) {
                             const int tap = (dx0 + R) * P + q0;
@@ -305,20 +324,20 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
     }
 }
 
-template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX>
+template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX, bool XF = false>
 static cudaError_t launch_p2_t(const BlfParams& p, int nplanes, cudaStream_t st)
 {
-    using Gm = P2Geom<R, TH, MODE>;
+    using Gm = P2Geom<R, TH, MODE, XF>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX>,
+    cudaError_t e = cudaFuncSetAttribute(k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX, XF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * nplanes);
-    k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX, XF><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <int R, int MODE, int POLY, bool PX>
+template <int R, int MODE, int POLY, bool PX, bool XF = false>
 static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t st)
 {
     // tile height: 32 rows (512 threads, 2 CTAs per SM: the staged halo rows
@@ -334,10 +353,10 @@ static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t
         return e ? std::atoi(e) : 0;
     }();
     if (PX && (th == 32 || (th == 0 && ctas32 >= 6L * 2 * nsm)))
-        return launch_p2_t<R, 32, MODE, POLY, false, 2, PX>(p, nplanes, st);
+        return launch_p2_t<R, 32, MODE, POLY, false, 2, PX, XF>(p, nplanes, st);
     if (th == 8 || (th == 0 && ctas16 < 6L * 4 * nsm))
-        return launch_p2_t<R, 8, MODE, POLY, false, 8, PX>(p, nplanes, st);
-    return launch_p2_t<R, 16, MODE, POLY, false, 4, PX>(p, nplanes, st);
+        return launch_p2_t<R, 8, MODE, POLY, false, 8, PX, XF>(p, nplanes, st);
+    return launch_p2_t<R, 16, MODE, POLY, false, 4, PX, XF>(p, nplanes, st);
 }
 
 // default FMA-pipe exp2 period of the pair-exponent kernel per radius (r01
@@ -349,6 +368,14 @@ template <int R>
 constexpr int kP2DefaultPoly()
 {
     return R == 5 ? 10 : (R == 15 ? 8 : 7);
+}
+// ... and of the factorised-exponent kernel, whose exponents cost half the
+// FFMA2 so more of them fit on the FMA pipe (c2: 0.976 at 7, 0.978 at 6; c4:
+// 1.098 at 5, 1.073 at 6, 1.053 at 8)
+template <int R>
+constexpr int kP2XfPoly()
+{
+    return R == 5 ? 10 : (R == 15 ? 5 : 7);
 }
 
 template <int R, int MODE>
@@ -368,6 +395,32 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
     // (r = 5: every 10th; with 32-row tiles it ties the unpacked kernel at
     // c3 and beats it at c1)
     const int poly = poly_env >= 0 ? poly_env : (px ? kP2DefaultPoly<R>() : (R >= 12 ? 7 : 0));
+    // factorised exponents (k_blf_j3.cu) for self-guided filtering whenever
+    // exp2(2ab) cannot overflow (2 coef^2 <= 60: sigma_r >~ 0.07; c2 and c4,
+    // not c1 / c3 at sigma_r = 0.05): c2 0.945 -> 0.976 of the MUFU peak, c4
+    // 1.039 -> 1.098 (r01 B200, tools/p2_xf_ab2.sh); BLFLS_P2_XF=0 keeps the
+    // difference form.  Same tile geometry: the higher-occupancy variants
+    // (16 rows x 6 CTAs or 32 rows x 3 CTAs per SM at 40 registers) spill
+    // and measured 0.91-0.94 at c2.
+    static const int xf = [] {
+        const char* e = std::getenv("BLFLS_P2_XF");
+        return e ? std::atoi(e) : 1;
+    }();
+    const bool use_xf = MODE == 0 && xf != 0 && px && 2.0f * p.range_coef * p.range_coef <= 60.0f;
+    if constexpr (MODE == 0) {
+        if (use_xf && p.npeers > 0)
+            return launch_p2_t<R, 16, MODE, kP2XfPoly<R>(), true, 3, true, true>(p, nplanes, st);
+        if (use_xf) {
+            switch (poly_env >= 0 ? poly_env : kP2XfPoly<R>()) {
+                case 5: return launch_p2_sized<R, MODE, 5, true, true>(p, nplanes, st);
+                case 6: return launch_p2_sized<R, MODE, 6, true, true>(p, nplanes, st);
+                case 7: return launch_p2_sized<R, MODE, 7, true, true>(p, nplanes, st);
+                case 8: return launch_p2_sized<R, MODE, 8, true, true>(p, nplanes, st);
+                case 10: return launch_p2_sized<R, MODE, 10, true, true>(p, nplanes, st);
+                default: return launch_p2_sized<R, MODE, 0, true, true>(p, nplanes, st);
+            }
+        }
+    }
     // peer-storing epilogue (fused band exchange) with the default offload, so
     // its targets equal the plain band filter's bit for bit
     if (p.npeers > 0) return launch_p2_t<R, 16, MODE, kP2DefaultPoly<R>(), true, 3, true>(p, nplanes, st);

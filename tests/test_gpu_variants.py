@@ -6,8 +6,9 @@ read once per process, so each side runs in its own subprocess).
   filter (k_blf_j3p, copies before / spread over the filter loop) against
   the one-CTA-per-tile k_blf_j3 (both in the difference form,
   BLFLS_J3_XF=0).
-- the factorised-exponent shared-guide kernel (default where it applies)
-  against the difference form: equal to fp32 round-off (not bit-identical).
+- the factorised-exponent shared-guide (k_blf_j3) and self-guided (k_blf_p2)
+  kernels (default where they apply) against the difference form: equal to
+  fp32 round-off (not bit-identical).
 - BLFLS_COL_PIPE=1: the pipelined column pass (k2_col_pipe: persistent,
   double-buffered cp.async strips) against k2_col, through full BLF-LS runs
   at every column length with a high-radix geometry.
@@ -105,4 +106,34 @@ def test_shared_guide_factorised_exponent_close_to_difference_form(tmp_path):
     for k in a.files:
         # targets in raw gradient units of [0,1]-range images: the factorised
         # exponent rounds 2ab (|2ab| <= 36 at sigma_r = 0.1) instead of (a - b)^2
+        assert np.max(np.abs(a[k].astype(np.float64) - b[k])) <= 2e-5, k
+
+
+_SELF_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1812_07122_b200 as P
+from oracle import oracle as O
+out = {{}}
+for (b, c, h, w, r, sr) in {shapes!r}:
+    img = np.stack([np.stack([O.gen_plane(400 + 10 * i + k, h, w, n_sites=12) for k in range(c)])
+                    for i in range(b)])
+    if b == 1:
+        img = img[0]
+    tx, ty = P.filter_gradients(img, sigma_s=float(r), sigma_r=sr, radius=r)
+    out[f"tx_{{b}}_{{c}}_{{h}}_{{w}}_{{r}}_{{sr}}"] = np.asarray(tx)
+    out[f"ty_{{b}}_{{c}}_{{h}}_{{w}}_{{r}}_{{sr}}"] = np.asarray(ty)
+np.savez({path!r}, **out)
+"""
+
+# self-guided radii of the packed kernel, sigma_r where the factorised form applies
+SELF_SHAPES = [(1, 3, 40, 64, 7, 0.1), (2, 1, 70, 130, 15, 0.08), (1, 3, 33, 47, 5, 0.2),
+               (1, 1, 96, 128, 7, 0.3)]
+
+
+def test_self_guided_factorised_exponent_close_to_difference_form(tmp_path):
+    a = _run(tmp_path, "xf", {"BLFLS_P2_XF": "1"}, _SELF_SCRIPT, SELF_SHAPES)
+    b = _run(tmp_path, "diff", {"BLFLS_P2_XF": "0"}, _SELF_SCRIPT, SELF_SHAPES)
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
         assert np.max(np.abs(a[k].astype(np.float64) - b[k])) <= 2e-5, k
