@@ -46,7 +46,10 @@ def build(ref: bool | None = None) -> None:
         ref = REF_SRC.is_dir()
     if ref:
         targets.append("ref")
-    subprocess.run(["make", "-s", "-C", str(HERE), f"-j{os.cpu_count() or 4}", *targets], check=True)
+    cmd = ["make", "-s", "-C", str(HERE)]
+    if subprocess.run([*cmd, f"-j{os.cpu_count() or 4}", *targets]).returncode != 0:
+        # a parallel make can lose a compiler to memory pressure; finish serially
+        subprocess.run([*cmd, "-j1", *targets], check=True)
 
 
 def _load(path: Path) -> C.CDLL:
