@@ -306,16 +306,17 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
     constexpr size_t smem = G::smem_bytes();
     if (which == 1) {
         // BLFLS_COL_PIPE: 1 pipelined column pass, 0 plain; unset = pipelined
-        // for power-of-two columns whose spectra stay L2-resident (c2 column
-        // 62 -> 56 us per step; c3's 1080 and the HBM-streaming c5 measured
-        // slower, profiles/r01_solve_knobs_c23.txt)
+        // for power-of-two columns up to 1024 whose spectra stay L2-resident
+        // (c2 column 62 -> 57 us per step; c3's 1080, the HBM-streaming c5 and
+        // L2-resident 2048-point groups of c5 measured slower,
+        // profiles/r01_solve_knobs_c23.txt)
         static const int pipe_env = [] {
             const char* e = std::getenv("BLFLS_COL_PIPE");
             return e != nullptr ? std::atoi(e) : -1;
         }();
         const size_t spec_bytes = (size_t)planes * G::N * p.spitch * sizeof(float2);
         const bool pipe = pipe_env >= 0 ? pipe_env != 0
-                                        : ((G::N & (G::N - 1)) == 0 && spec_bytes <= ((size_t)48 << 20));
+                                        : ((G::N & (G::N - 1)) == 0 && G::N <= 1024 && spec_bytes <= ((size_t)48 << 20));
         if constexpr (G::V % 2 == 0) {
             if (pipe) {
                 const int nsp = (p.wc + G::V - 1) / G::V;
