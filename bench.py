@@ -5,10 +5,13 @@
 
 One step = the full BLF-LS hot path (cfg.iters cascaded iterations of
 circular gradients -> brute-force (joint) BLF -> periodic FFT LS solve) over
-one batch of the config's synthetic images.  Default workload: BASELINE.json
-configs[1] ("c2": 1024x1024 RGB, r=7, sigma_s=7, sigma_r=0.1, lambda=1000,
-3 iterations).  For N > 1 (torchrun) every rank processes its own images of
-the same config (independent units, no data-path collective): weak scaling.
+one batch of the config's synthetic images.  Default workload: the largest
+BASELINE.json config that fits one GPU, configs[4] ("c5": 64 images of
+2048x2048 RGB, joint BLF with a grayscale guide, r=7, sigma_s=7,
+sigma_r=0.1, lambda=1000, 3 iterations, ~20 GiB of HBM).  For N > 1
+(torchrun) the 64-image batch is sharded over the ranks (64/N images each,
+no data-path collective): strong scaling.  c4 under torchrun runs the
+row-band decomposition; c1-c3 give every rank its own images (weak).
 
 metric: megapixels per second per iteration, MP/s = H*W*B*iters / t_step
 (SURVEY.md 8(d)), summed over ranks, t = max over ranks (CUDA events).
@@ -37,7 +40,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--band-exchange", default="peer", choices=["peer", "allgather"],
                     help="row-band mode (c4, N > 1): fused peer stores or an NCCL all_gather")
@@ -148,16 +151,19 @@ def dist_env():
     return world, rank, local
 
 
-def config_json(cfg, n_gpus, extra=None):
-    d = {"workload": f"{cfg.name}: {cfg.height}x{cfg.width}x{cfg.channels} x{cfg.batch} images/rank, "
+def config_json(cfg, n_gpus, extra=None, shard=False):
+    per = f"{cfg.batch} images sharded over {n_gpus} ranks" if shard else f"x{cfg.batch} images/rank"
+    d = {"workload": f"{cfg.name}: {cfg.height}x{cfg.width}x{cfg.channels} {per}, "
                      f"r={cfg.radius}, sigma_s={cfg.sigma_s}, sigma_r={cfg.sigma_r}, "
                      f"lambda={cfg.lam}, iters={cfg.iters}"
                      + (", joint gray guide" if cfg.guide else ""),
          "height": cfg.height, "width": cfg.width, "channels": cfg.channels,
-         "images_per_rank": cfg.batch, "radius": cfg.radius, "sigma_s": cfg.sigma_s,
+         "images_per_rank": -(-cfg.batch // n_gpus) if shard else cfg.batch, "radius": cfg.radius, "sigma_s": cfg.sigma_s,
          "sigma_r": cfg.sigma_r, "lambda": cfg.lam, "iters": cfg.iters,
          "boundary": "periodic (pad=0)", "guide": "grayscale joint" if cfg.guide else "self",
-         "parallelism": f"independent images x{n_gpus} ranks" if n_gpus > 1 else "single GPU"}
+         "parallelism": ("single GPU" if n_gpus == 1 else
+                         f"batch sharded over {n_gpus} ranks" if shard else
+                         f"independent images x{n_gpus} ranks")}
     if extra:
         d.update(extra)
     return d
@@ -166,12 +172,32 @@ def config_json(cfg, n_gpus, extra=None):
 FILTER_NAMES = {"brute": "brute-force BLF", "grid": "grid BLF", "dt": "NC (domain transform, 3 passes)"}
 
 
-def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
+def host_info():
+    """CPU model, core count and OpenMP binding of the box the CPU arm ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None,
+            "OMP_PROC_BIND": os.environ.get("OMP_PROC_BIND"),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS")}
+
+
+def cpu_sample(cfg, threads=None, pad=0, backend="brute", max_taps=None):
     """Reference CPU path on a bounded sample of the workload: the first image
     of the config, ONE iteration (of cfg.iters), through oracle/_ref
     (the reference's translation units + brute-force BLF with explicit r).
-    Configs whose single iteration exceeds ~4e9 taps (c4) run on a centred
-    crop of the same image so the sample stays ~10 s; MP/s is per pixel."""
+    Samples whose single iteration exceeds max_taps (default 4e9; 1.5e9 for
+    the 64-image c5, whose full first image would take ~5 s per step on 16
+    cores) run on a centred crop of the same image; MP/s is per pixel and the
+    brute-force cost per pixel does not depend on the image content."""
+    if max_taps is None:
+        max_taps = 1.5e9 if cfg.batch > 1 else 4e9
     import numpy as np
     from oracle import oracle as O
     kind = "reference" if O.REF_SO.exists() else "port"
@@ -183,8 +209,8 @@ def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
         guide = guide.astype(np.float64)
     taps = img.size * 2 * (2 * cfg.radius + 1) ** 2
     crop = ""
-    if taps > 4e9:
-        side = int(cfg.height * (4e9 / taps) ** 0.5) // 16 * 16
+    if taps > max_taps:
+        side = int(cfg.height * (max_taps / taps) ** 0.5) // 16 * 16
         y0, x0 = (cfg.height - side) // 2, (cfg.width - side) // 2
         img = np.ascontiguousarray(img[:, y0:y0 + side, x0:x0 + side])
         if guide is not None:
@@ -213,6 +239,7 @@ def cpu_sample(cfg, threads=None, pad=0, backend="brute"):
     dt = time.perf_counter() - t0
     mp = img.shape[1] * img.shape[2] / 1e6
     return {"value": mp / dt, "unit": "MP/s", "cores": O.num_threads(), "kind": kind,
+            "host": host_info(),
             "sample": f"1 image x 1 iteration of {cfg.name} ({cfg.height}x{cfg.width}x{cfg.channels}"
                       f"{crop}, {FILTER_NAMES[backend]}, pad {pad}), "
                       f"double precision, OpenMP; {dt:.2f} s (BLF {tb:.2f} s, solve {ts:.2f} s)",
@@ -240,7 +267,8 @@ def run_reference(args, cfg):
             "impl": "reference",
             "config": config_json(cfg, 1, {"step": "1 image x 1 iteration (bounded CPU sample)"}),
             "cpu_baseline": {"value": value, "unit": "MP/s", "cores": res[0]["cores"],
-                             "kind": res[0]["kind"], "sample": res[0]["sample"]},
+                             "kind": res[0]["kind"], "sample": res[0]["sample"],
+                             "host": res[0]["host"]},
             "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -268,7 +296,7 @@ def run_ours(args, cfg):
     mode = "weak"
     if world > 1 and cfg.name == "c4":
         mode = "band"
-    elif world > 1 and cfg.name == "c5":
+    elif cfg.name == "c5":
         mode = "shard"
     if mode == "band":
         return run_band(args, cfg, world, rank, dev, peaks, peak_src)
@@ -428,7 +456,7 @@ def run_ours(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             c = cpu_sample(cfg, pad=args.pad, backend=args.backend)
-            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample", "host")}
         except Exception as exc:  # the baseline must not sink the bench line
             cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": None,
                    "sample": f"failed: {exc}"}
@@ -444,7 +472,8 @@ def run_ours(args, cfg):
                 "backend": args.backend, "pad": args.pad,
                 "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2",
                 "decomposition": {"weak": "independent images per rank",
-                                  "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]}),
+                                  "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]},
+                shard=mode == "shard"),
             "roofline": roof_dt if args.backend != "brute" else {"bound": "sfu", "kernel": blf_kernel_name(cfg),
                          "achieved": achieved / 1e9, "peak": mufu_rate / 1e9, "unit": "Gexp/s",
                          "frac": achieved / mufu_rate,

@@ -10,6 +10,17 @@
 
 namespace blfls {
 
+// ----------------------------------------------------------------- knobs --
+// Kernel-selection overrides for A/B experiments.  The production library
+// (default build) ignores the environment entirely: knob() returns the
+// measured default.  Building with -DBLFLS_EXPERIMENTS (python -m
+// paper_1812_07122_b200.build --experiments) reads BLFLS_* variables.
+#ifdef BLFLS_EXPERIMENTS
+int knob(const char* name, int def);
+#else
+constexpr int knob(const char*, int def) { return def; }
+#endif
+
 constexpr int kMaxRadius = 48;     // smem tile envelope (radius <= 48)
 constexpr int kMaxPeers = 8;       // fused band exchange: ranks of one NVLink domain
 constexpr int kMaxFftRadices = 32;
@@ -193,18 +204,31 @@ struct SolveParams {
     float lambda;
     float inv_hw;        // 1 / (H W)
     int mode;            // column pass: 1 fwd, 2 inv, 3 fwd+scale+inv
+    int strip;           // spectrum layout: 0 row-major, 1 column strips (below)
 };
+
+// Offset of spectrum element (row y, column k) of `plane`.  Row-major: H
+// rows of spitch.  Column strips (the full solve): the plane's H x spitch
+// block holds spitch / 4 strips of 4 adjacent columns, each strip H rows x 4
+// complex (32 bytes per row) contiguous, so the column pass streams whole
+// strips (every warp load / store covers 8 consecutive rows = 256 contiguous
+// bytes) and the row passes write / read 32-byte pieces of 4 columns.
+__host__ __device__ __forceinline__ size_t spec_at(const SolveParams& p, int plane, int y, int k)
+{
+    const size_t base = (size_t)plane * p.H * p.spitch;
+    return p.strip ? base + (size_t)(k >> 2) * ((size_t)p.H * 4) + (size_t)y * 4 + (k & 3)
+                   : base + (size_t)y * p.spitch + k;
+}
+// distance between rows y and y + 1 of one spectrum column
+__host__ __device__ __forceinline__ size_t spec_row_stride(const SolveParams& p)
+{
+    return p.strip ? 4 : (size_t)p.spitch;
+}
 
 // high-radix solve passes (k_solve2.cu): false when no geometry exists for n
 bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,
                     cudaStream_t st);
 
-// persistent bulk-copy-pipelined row passes (k_solve3.cu): which 0 r2c, 2 c2r
-bool launch_v3_row_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,
-                        cudaStream_t st, cudaError_t* err);
-
-// pair-symmetric brute-force filter (k_blf_sym.cu); false: not covered
-bool launch_grad_blf_sym(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err);
 
 // shared-gray-guide filter with packed accumulation (k_blf_j3.cu); false: not covered
 bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);

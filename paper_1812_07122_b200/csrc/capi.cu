@@ -20,6 +20,14 @@
 
 namespace blfls {
 
+#ifdef BLFLS_EXPERIMENTS
+int knob(const char* name, int def)
+{
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : def;
+}
+#endif
+
 cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st);
 cudaError_t launch_row_r2c(const SolveParams& p, const FftGeom& g, int planes, bool odd,
                            cudaStream_t st);
@@ -80,10 +88,7 @@ struct DevFft {
 // below it); BLFLS_BLUESTEIN_MINP overrides (0 disables Bluestein)
 int bluestein_min_prime()
 {
-    static const int v = [] {
-        const char* e = std::getenv("BLFLS_BLUESTEIN_MINP");
-        return e ? std::atoi(e) : 150;  // measured: P = 61, 43 faster direct, P = 139 a tie
-    }();
+    static const int v = knob("BLFLS_BLUESTEIN_MINP", 150);  // measured: P = 61, 43 faster direct, P = 139 a tie
     return v;
 }
 
@@ -374,6 +379,8 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
     s.out = out;
     s.lohi_out = lohi_out;
     s.mode = 3;
+    // column-strip spectrum (spec_at): the spectrum never leaves the plan here
+    s.strip = knob("BLFLS_SPEC_STRIP", 1);
     s.plane0 = 0;
     const int grp = p->solve_group;
     if (grp <= 0 || grp >= planes) {
@@ -713,7 +720,7 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         return bail(fail(BLFLS_EUNSUPPORTED, "FFT: height " + std::to_string(H) +
                                                  " too large for the shared-memory column FFT"));
 
-    if (std::getenv("BLFLS_DEBUG_FFT")) {
+    if (knob("BLFLS_DEBUG_FFT", 0)) {
         for (const DevFft* f : {&p->rowf, &p->colf})
             std::fprintf(stderr, "blfls fft n=%d ct=%d bluestein=%d (M=%d) direct=%d pmax=%d V=%d threads=%d E=%d\n",
                          f->g.desc.n, (int)f->g.ct, (int)f->g.bluestein, f->g.blue.m.n, (int)f->g.direct,
@@ -803,17 +810,17 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         b.GC = q.guide_channels;
         b.radius = radius;
         b.poly_period = -1;
-        if (const char* ev = std::getenv("BLFLS_POLY_PERIOD")) b.poly_period = std::atoi(ev);
+        b.poly_period = knob("BLFLS_POLY_PERIOD", b.poly_period);
         b.legacy_joint3 = 0;
-        if (const char* ev = std::getenv("BLFLS_PACKED_JOINT3")) b.legacy_joint3 = -std::atoi(ev);
+        b.legacy_joint3 = -knob("BLFLS_PACKED_JOINT3", 0);
         b.x2_poly = -1;  // r01 sweep: packed kernel slower (FP32 pipe co-saturated); experiment only
-        if (const char* ev = std::getenv("BLFLS_X2")) b.x2_poly = std::atoi(ev);
+        b.x2_poly = knob("BLFLS_X2", b.x2_poly);
         b.cols_per_thread = 4;
-        if (const char* ev = std::getenv("BLFLS_COLS")) b.cols_per_thread = std::atoi(ev);
+        b.cols_per_thread = knob("BLFLS_COLS", b.cols_per_thread);
         b.tile_rows = 0;
-        if (const char* ev = std::getenv("BLFLS_TILE_ROWS")) b.tile_rows = std::atoi(ev);
+        b.tile_rows = knob("BLFLS_TILE_ROWS", b.tile_rows);
         b.joint3_rows = 2;
-        if (const char* ev = std::getenv("BLFLS_J3_ROWS")) b.joint3_rows = std::atoi(ev);
+        b.joint3_rows = knob("BLFLS_J3_ROWS", b.joint3_rows);
         b.range_coef = (float)std::sqrt(1.4426950408889634 / (8.0 * q.sigma_r * q.sigma_r));
         for (int d = 0; d <= kMaxRadius; ++d) {
             const double c = -(double)d * d / (2.0 * q.sigma_s * q.sigma_s) * 1.4426950408889634;
@@ -914,7 +921,7 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         // groups of 6..1 planes, r01 B200); BLFLS_SOLVE_GROUP=n (experiment)
         // runs groups of n planes on two streams
         int grp = 0;
-        if (const char* ev = std::getenv("BLFLS_SOLVE_GROUP")) grp = std::atoi(ev);
+        grp = knob("BLFLS_SOLVE_GROUP", grp);
         p->solve_group = grp;
     }
     if (cudaStreamCreateWithFlags(&p->ps2, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1010,10 +1017,7 @@ namespace {
 // 8 per call; BLFLS_HOST_CHUNKS=n overrides the count (1: off).
 int host_chunk_images(blfls_plan_t p, int batch)
 {
-    static const int env = [] {
-        const char* e = std::getenv("BLFLS_HOST_CHUNKS");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int env = knob("BLFLS_HOST_CHUNKS", 0);
     if (batch < 2) return batch;
     const size_t per_image = sizeof(float) * p->plane * (p->prm.channels + p->prm.guide_channels);
     int n = env > 0 ? env : (int)std::min<size_t>(8, (size_t)batch * per_image / (64u << 20));
@@ -1275,7 +1279,6 @@ blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const 
     if ((tx == nullptr) != (ty == nullptr))
         return fail(BLFLS_EINVAL, "lsgrad_solve_fft: target shape does not match image");
     if ((r = set_device(p))) return r;
-    if (p->pad && (r = ensure_host_slots(p))) return r;  // unpadded staging for the padded path
     cudaStream_t us = (cudaStream_t)stream;
     if ((r = fork_in(p, us))) return r;
     cudaStream_t st = p->ps;
@@ -1286,10 +1289,16 @@ blfls_status blfls_solve(blfls_plan_t p, const float* g, const float* tx, const 
     const float* dty = ty;
     float* du = u;
     if (host) {
-        // with padding the targets are staged unpadded and padded into p->tx/ty below
-        float* sg = p->pad ? p->slot[0].in : p->buf[0];
-        float* stx = p->pad ? p->slot[1].in : p->tx;
-        float* sty = p->pad ? p->slot[1].out : p->ty;
+        // with padding the inputs are staged unpadded and reflect-padded into
+        // fpad / tx / ty below.  The staging buffers are plan scratch that
+        // only p->ps touches (never the ASYNC host slots, whose copies run on
+        // s_h2d / s_d2h and may still be in flight): buf[0] and buf[1] hold
+        // >= n floats (padded image size), the spectrum holds >= 2 n floats and
+        // is first written by the solve's row pass, after the padding kernels
+        // consumed the staged targets (stream order on p->ps).
+        float* sg = p->buf[0];
+        float* stx = p->pad ? p->buf[1] : p->tx;
+        float* sty = p->pad ? reinterpret_cast<float*>(p->spec) : p->ty;
         CK(cudaMemcpyAsync(sg, g, sizeof(float) * n, cudaMemcpyHostToDevice, st));
         dg = sg;
         if (tx) {

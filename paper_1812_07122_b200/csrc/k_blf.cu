@@ -757,6 +757,7 @@ static cudaError_t launch_any(const BlfParams& p, int nz, cudaStream_t st)
 template <int MODE>
 constexpr int kPolyDefault = 0;  // r01 sweep (tools/poly_sweep.py): offload does not pay yet
 
+#ifdef BLFLS_EXPERIMENTS
 template <int R, int QR, int P, int MINB>
 static cudaError_t launch_joint3_q(const BlfParams& p, int nz, cudaStream_t st)
 {
@@ -811,9 +812,14 @@ static cudaError_t launch_x2_poly(const BlfParams& p, int nz, cudaStream_t st)
     }
 }
 
+#endif  // BLFLS_EXPERIMENTS
+
 template <int R, int P, int MODE>
 static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
 {
+#ifndef BLFLS_EXPERIMENTS
+    return launch_fixed<R, P, MODE, kPolyDefault<MODE>>(p, nz, st);
+#else
     if (p.cols_per_thread == 8) return launch_fixed<R, 8, MODE, 0>(p, nz, st);  // experiment
     // p.poly_period < 0: the per-mode default; otherwise an experiment override
     switch (p.poly_period < 0 ? kPolyDefault<MODE> : p.poly_period) {
@@ -824,6 +830,7 @@ static cudaError_t launch_poly(const BlfParams& p, int nz, cudaStream_t st)
         case 12: return launch_fixed<R, P, MODE, 12>(p, nz, st);
         default: return launch_fixed<R, P, MODE, 6>(p, nz, st);
     }
+#endif
 }
 
 template <int MODE>
@@ -843,6 +850,7 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
             default: return launch_any<MODE>(p, nz, st);
         }
     }
+#ifdef BLFLS_EXPERIMENTS
     if constexpr (MODE == 0) {
         if (p.x2_poly >= 0) {
             switch (p.radius) {
@@ -871,6 +879,7 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
             }
         }
     }
+#endif
     switch (p.radius) {
         case 1: return launch_fixed<1, P, MODE, D>(p, nz, st);
         case 2: return launch_fixed<2, P, MODE, D>(p, nz, st);
@@ -891,7 +900,6 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st)
 {
     cudaError_t e = cudaSuccess;
-    if (launch_grad_blf_sym(p, mode, batch, st, &e)) return e;
     if (mode == 2 && launch_grad_blf_j3(p, batch, st, &e)) return e;
     if (mode != 2 && launch_grad_blf_p2(p, mode, batch, st, &e)) return e;
     switch (mode) {

@@ -329,188 +329,6 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     j3_filter_tile<R, TH, PEERS, PX, XF>(p, G, S01, S2, b, axis, tx0, ty0, range, [](int) {});
 }
 
-// Persistent variant: gridDim.x CTAs stride over the tiles (same order as
-// k_blf_j3's grid: tile column, tile row, image x axis).  The raw samples of
-// the NEXT tile (guide + 3 channels, rows [-R, TH + R] and the 16-byte
-// aligned columns [-R - 1, TW + R + 1) around it, index H / W wrapped to 0
-// for the periodic +1 neighbour) are copied into a shared staging area by
-// 16-byte cp.async, a few per thread at the start of each window row while
-// the current tile is filtered; the gradient prologue then reads shared
-// memory instead of waiting on global loads (ncu, c5: the global-load
-// prologue of k_blf_j3 held 38% of the warp samples and left the SM's other
-// CTA alone on the MUFU).  Needs W % 4 == 0 (whole 16-byte chunks per row).
-// Gradients and arithmetic are identical to k_blf_j3.
-template <int R, int TH>
-struct J3Raw {
-    using Gm = J3Geom<R, TH>;
-    static constexpr int RROWS = Gm::ROWS + 1;
-    static constexpr int XOFF = (R + 3) & ~3;                      // tile column 0 at raw column XOFF
-    static constexpr int CH = (XOFF + Gm::TW + R + 1 + 3) / 4;     // 16-byte chunks per row
-    static constexpr int RP = 4 * CH;                              // raw pitch (floats)
-    static constexpr int NCH = 4 * RROWS * CH;                     // chunks per tile (all planes)
-    static constexpr int PER_THREAD = (NCH + Gm::NT - 1) / Gm::NT;
-    static constexpr int PER_ROW = (PER_THREAD + 2 * R) / (2 * R + 1);  // per window row
-    static constexpr size_t raw_off() { return (Gm::smem_bytes() + 15) & ~(size_t)15; }
-    static constexpr size_t smem_bytes() { return raw_off() + (size_t)4 * RROWS * RP * sizeof(float); }
-    static_assert(XOFF >= R + 0 && RP >= XOFF - R + Gm::COLS + 1, "raw staging covers the window");
-};
-
-__device__ __forceinline__ void j3_cp_async16(float* dst, const float* src)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-
-struct J3Tile {
-    int b, axis, tx0, ty0;
-};
-
-template <int R, int TH>
-__device__ __forceinline__ J3Tile j3_tile(const BlfParams& p, int t, int ntx, int nty)
-{
-    J3Tile k;
-    const int bx = t % ntx, r = t / ntx;
-    const int by = r % nty, z = r / nty;
-    k.b = z >> 1;
-    k.axis = z & 1;
-    k.tx0 = bx * J3Geom<R, TH>::TW;
-    k.ty0 = p.y0 + by * TH;
-    return k;
-}
-
-// cp.async chunks [m0, m1) (per thread: chunk threadIdx.x + NT m) of tile k
-template <int R, int TH>
-__device__ __forceinline__ void j3_prefetch(const BlfParams& p, const J3Tile& k, float* raw, int m0, int m1)
-{
-    using Rw = J3Raw<R, TH>;
-    constexpr int NT = J3Geom<R, TH>::NT;
-    const int H = p.H, W = p.W;
-    const size_t plane = (size_t)H * W;
-#pragma unroll
-    for (int m = m0; m < m1; ++m) {
-        const int c = threadIdx.x + NT * m;
-        if (Rw::NCH % NT != 0 && c >= Rw::NCH) break;
-        const int row = c / Rw::CH, q = c - row * Rw::CH;  // row over planes x RROWS
-        const int pl = row / Rw::RROWS, ii = row - pl * Rw::RROWS;
-        int y = k.ty0 - R + ii;
-        int x = k.tx0 - Rw::XOFF + 4 * q;
-        if (y < 0 || y > H || x < 0 || x > W) continue;
-        if (y == H) y = 0;
-        if (x == W) x = 0;
-        const float* base = pl == 0 ? p.guide + (size_t)k.b * p.GC * plane
-                                    : p.f + ((size_t)k.b * 3 + (pl - 1)) * plane;
-        j3_cp_async16(raw + row * Rw::RP + 4 * q, base + (size_t)y * W + x);
-    }
-}
-
-// SPREAD: the next tile's copies are issued a few per window row (else all
-// before the filter loop)
-template <int R, int TH, bool SPREAD>
-__global__ void __launch_bounds__(16 * TH, 2) k_blf_j3p(const BlfParams p, int total, int ntx, int nty)
-{
-    using Gm = J3Geom<R, TH>;
-    using Rw = J3Raw<R, TH>;
-    constexpr int NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS, GP = Gm::GP, SP = Gm::SP;
-    extern __shared__ __align__(16) float smj[];
-    float* G = smj;                                                   // [ROWS][GP]
-    float2* S01 = reinterpret_cast<float2*>(smj + ROWS * GP);         // [ROWS][SP] {g0, g1}
-    float2* S2 = S01 + ROWS * SP;                                     // [ROWS][SP] {g2, 1}
-    float* raw = smj + Rw::raw_off() / sizeof(float);                 // [4][RROWS][RP]
-    const int H = p.H, W = p.W;
-    const int lane = threadIdx.x & 31;
-
-    int t = blockIdx.x;
-    if (t >= total) return;
-    j3_prefetch<R, TH>(p, j3_tile<R, TH>(p, t, ntx, nty), raw, 0, Rw::PER_THREAD);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    // only t is live across the filter loop (tiles are re-derived from it)
-    for (; t < total; t += gridDim.x) {
-        const J3Tile k = j3_tile<R, TH>(p, t, ntx, nty);
-        float s, range, sg, grange;
-        j3_decode(p.lohi, k.b, p.range_coef, s, range);
-        j3_decode(p.glohi, k.b, p.range_coef, sg, grange);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();  // raw complete; every warp done with the previous tile
-        // gradients of this axis from the staged samples (k_blf_j3's prologue)
-        const int off1 = k.axis == 0 ? 1 : Rw::RP;
-        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
-            const int y = k.ty0 - R + i;
-            const bool yin = y >= 0 && y < H;
-            const float* r0 = raw + i * Rw::RP + (Rw::XOFF - R);
-            float* grow = G + i * GP;
-            float2* s01 = S01 + i * SP;
-            float2* s2 = S2 + i * SP;
-#pragma unroll
-            for (int j = lane; j < COLS; j += 32) {
-                const int x = k.tx0 - R + j;
-                const int o = j3_sw(j);
-                if (yin && x >= 0 && x < W) {
-                    grow[j] = (r0[j + off1] - r0[j]) * sg;
-                    float g[3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float* rc = r0 + (c + 1) * Rw::RROWS * Rw::RP;
-                        g[c] = rc[j + off1] - rc[j];
-                    }
-                    s01[o] = make_float2(g[0], g[1]);
-                    s2[o] = make_float2(g[2], 1.0f);
-                } else {
-                    grow[j] = kJ3Sentinel;
-                    s01[o] = make_float2(0.f, 0.f);
-                    s2[o] = make_float2(0.f, 0.f);
-                }
-            }
-        }
-        __syncthreads();  // tile staged; raw free for the next tile's copies
-        const int tn = t + (int)gridDim.x;
-        if constexpr (SPREAD) {
-            auto hook = [&](int i) {
-                if (tn < total && i * Rw::PER_ROW < Rw::PER_THREAD) {
-                    const J3Tile kn = j3_tile<R, TH>(p, tn, ntx, nty);
-                    j3_prefetch<R, TH>(p, kn, smj + Rw::raw_off() / sizeof(float), i * Rw::PER_ROW,
-                                       min((i + 1) * Rw::PER_ROW, Rw::PER_THREAD));
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-                }
-            };
-            j3_filter_tile<R, TH, false, true, false>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, hook);
-        } else {
-            if (tn < total) {
-                j3_prefetch<R, TH>(p, j3_tile<R, TH>(p, tn, ntx, nty), raw, 0, Rw::PER_THREAD);
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-            j3_filter_tile<R, TH, false, true, false>(p, G, S01, S2, k.b, k.axis, k.tx0, k.ty0, range, [](int) {});
-        }
-    }
-}
-
-// persistent launch when 2 CTAs fit per SM; false otherwise
-template <int R, int TH, bool SPREAD>
-static bool launch_j3p(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
-{
-    using Gm = J3Geom<R, TH>;
-    constexpr size_t smem = J3Raw<R, TH>::smem_bytes();
-    static int occ = -1, nsm = 0;
-    if (occ < 0) {
-        int dev = 0;
-        occ = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-            cudaFuncSetAttribute(k_blf_j3p<R, TH, SPREAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-                cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_blf_j3p<R, TH, SPREAD>, Gm::NT, smem) != cudaSuccess)
-            occ = 0;
-        cudaGetLastError();
-    }
-    if (occ < 2 || (p.W & 3) != 0) return false;
-    const int ntx = (p.W + Gm::TW - 1) / Gm::TW, nty = (p.y1 - p.y0 + TH - 1) / TH;
-    const long total = (long)ntx * nty * 2 * batch;
-    if (total > INT32_MAX) return false;
-    const int grid = (int)std::min<long>(total, (long)occ * nsm);
-    k_blf_j3p<R, TH, SPREAD><<<grid, Gm::NT, smem, st>>>(p, (int)total, ntx, nty);
-    *err = cudaGetLastError();
-    return true;
-}
-
 template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false>
 static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
 {
@@ -529,29 +347,13 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
 {
     // register cap: 3 CTAs per SM (no spills; c5 0.764 of MUFU) or 4 (64
     // registers, a few spills; 0.755)
-    static const int minb = [] {
-        const char* e = std::getenv("BLFLS_J3_MINB");
-        return e ? std::atoi(e) : 3;
-    }();
-    static const int px = [] {
-        const char* e = std::getenv("BLFLS_J3X");  // 0: per-tap exponents (A/B)
-        return e ? std::atoi(e) : 2;
-    }();
+    static const int minb = knob("BLFLS_J3_MINB", 3);
+    static const int px = knob("BLFLS_J3X", 2);  // 0: per-tap exponents (A/B)
     // difference form (when XF does not apply): pair exponents at 2 CTAs per
     // SM (c5: 0.786 of the MUFU peak, 0.781 at 3 CTAs, 0.765 without); the
     // peer-storing epilogue uses the same arithmetic so band exchange targets
-    // match the plain band filter
-    static const int persistent = [] {
-        // 0 (default): one CTA per tile; 1: persistent, copies before the
-        // filter loop; 2: persistent, copies spread over the window rows.
-        // Measured (c5, r01 B200): 0.778 / 0.698 / 0.587 of the MUFU peak --
-        // the persistent kernels remove the global-load stalls of the
-        // prologue but add ~7% instructions and two barriers per tile, and
-        // the other CTA on the SM already keeps the MUFU busy while one
-        // CTA stages its tile
-        const char* e = std::getenv("BLFLS_J3P");
-        return e ? std::atoi(e) : 0;
-    }();
+    // match the plain band filter.  (A persistent variant that prefetched the
+    // next tile by cp.async measured 0.698 / 0.587: removed in r02.)
     // factorised exponents (XF) whenever exp2(2ab) cannot overflow: |a|, |b| <=
     // range_coef (gradients of an image spanning [lo, hi] are at most hi - lo),
     // so the largest argument is 2 coef^2 (c5, sigma_r = 0.1: 36) and
@@ -560,23 +362,16 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
     // of the MUFU peak (r01 B200; XF at 2 CTAs per SM: 0.748, at 3: 0.802).
     // BLFLS_J3_XF=0 keeps the difference form.  The peer-storing band
     // epilogue uses the same arithmetic as the plain band filter.
-    static const int xf = [] {
-        const char* e = std::getenv("BLFLS_J3_XF");
-        return e ? std::atoi(e) : 1;
-    }();
+    static const int xf = knob("BLFLS_J3_XF", 1);
     const bool use_xf = xf != 0 && px == 2 && 2.0f * p.range_coef * p.range_coef <= 60.0f;
     if (p.npeers > 0 && use_xf) return launch_j3_t<R, TH, true, 4, true, true>(p, batch, st);
     if (use_xf) return launch_j3_t<R, TH, false, 4, true, true>(p, batch, st);
     if (p.npeers > 0) return launch_j3_t<R, TH, true, 2, true>(p, batch, st);
-    if (px == 2) {
-        cudaError_t e = cudaSuccess;
-        if (persistent == 1 && launch_j3p<R, TH, false>(p, batch, st, &e)) return e;
-        if (persistent == 2 && launch_j3p<R, TH, true>(p, batch, st, &e)) return e;
-        return launch_j3_t<R, TH, false, 2, true>(p, batch, st);
-    }
+#ifdef BLFLS_EXPERIMENTS
     if (px == 3) return launch_j3_t<R, TH, false, 3, true>(p, batch, st);
-    if (minb == 3) return launch_j3_t<R, TH, false, 3>(p, batch, st);
-    return launch_j3_t<R, TH, false, 4>(p, batch, st);
+    if (px == 0) return minb == 3 ? launch_j3_t<R, TH, false, 3>(p, batch, st) : launch_j3_t<R, TH, false, 4>(p, batch, st);
+#endif
+    return launch_j3_t<R, TH, false, 2, true>(p, batch, st);
 }
 
 // Shared-gray-guide filter (mode 2) on the packed kernel at the radii it is
@@ -584,10 +379,7 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
 // BLFLS_J3=0 selects the unpacked kernel (A/B experiments).
 bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
 {
-    static const bool enabled = [] {
-        const char* e = std::getenv("BLFLS_J3");
-        return e == nullptr || std::atoi(e) != 0;
-    }();
+    static const bool enabled = (knob("BLFLS_J3", 1) != 0);
     if (!enabled || p.C != 3) return false;
     switch (p.radius) {
         case 3: *err = launch_j3<3, 16>(p, batch, st); return true;

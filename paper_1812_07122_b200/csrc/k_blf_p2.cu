@@ -348,10 +348,7 @@ static cudaError_t launch_p2_sized(const BlfParams& p, int nplanes, cudaStream_t
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    static const int th = [] {  // experiment override: 8, 16 or 32 rows per tile
-        const char* e = std::getenv("BLFLS_P2_TH");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int th = knob("BLFLS_P2_TH", 0);
     if (PX && (th == 32 || (th == 0 && ctas32 >= 6L * 2 * nsm)))
         return launch_p2_t<R, 32, MODE, POLY, false, 2, PX, XF>(p, nplanes, st);
     if (th == 8 || (th == 0 && ctas16 < 6L * 4 * nsm))
@@ -383,14 +380,8 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
 {
     // default: every 7th exponential on the FMA pipe for the large window
     // (r = 15: c4 0.973 of MUFU against 0.945 unpacked), none otherwise
-    static const int poly_env = [] {
-        const char* e = std::getenv("BLFLS_P2_POLY");
-        return e ? std::atoi(e) : -1;
-    }();
-    static const int px = [] {
-        const char* e = std::getenv("BLFLS_P2X");
-        return e ? std::atoi(e) : 1;
-    }();
+    static const int poly_env = knob("BLFLS_P2_POLY", -1);
+    static const int px = knob("BLFLS_P2X", 1);
     // pair exponents (PX) free enough issue slots for the offload at r = 7 too
     // (r = 5: every 10th; with 32-row tiles it ties the unpacked kernel at
     // c3 and beats it at c1)
@@ -402,43 +393,43 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
     // difference form.  Same tile geometry: the higher-occupancy variants
     // (16 rows x 6 CTAs or 32 rows x 3 CTAs per SM at 40 registers) spill
     // and measured 0.91-0.94 at c2.
-    static const int xf = [] {
-        const char* e = std::getenv("BLFLS_P2_XF");
-        return e ? std::atoi(e) : 1;
-    }();
+    static const int xf = knob("BLFLS_P2_XF", 1);
     const bool use_xf = MODE == 0 && xf != 0 && px && 2.0f * p.range_coef * p.range_coef <= 60.0f;
     if constexpr (MODE == 0) {
         if (use_xf && p.npeers > 0)
             return launch_p2_t<R, 16, MODE, kP2XfPoly<R>(), true, 3, true, true>(p, nplanes, st);
-        if (use_xf) {
-            switch (poly_env >= 0 ? poly_env : kP2XfPoly<R>()) {
+#ifdef BLFLS_EXPERIMENTS
+        if (use_xf && poly_env >= 0) {
+            switch (poly_env) {
                 case 5: return launch_p2_sized<R, MODE, 5, true, true>(p, nplanes, st);
                 case 6: return launch_p2_sized<R, MODE, 6, true, true>(p, nplanes, st);
-                case 7: return launch_p2_sized<R, MODE, 7, true, true>(p, nplanes, st);
                 case 8: return launch_p2_sized<R, MODE, 8, true, true>(p, nplanes, st);
                 case 10: return launch_p2_sized<R, MODE, 10, true, true>(p, nplanes, st);
                 default: return launch_p2_sized<R, MODE, 0, true, true>(p, nplanes, st);
             }
         }
+#endif
+        if (use_xf) return launch_p2_sized<R, MODE, kP2XfPoly<R>(), true, true>(p, nplanes, st);
     }
     // peer-storing epilogue (fused band exchange) with the default offload, so
     // its targets equal the plain band filter's bit for bit
     if (p.npeers > 0) return launch_p2_t<R, 16, MODE, kP2DefaultPoly<R>(), true, 3, true>(p, nplanes, st);
-    if (px) {
+#ifdef BLFLS_EXPERIMENTS
+    if (px && poly != kP2DefaultPoly<R>()) {
         switch (poly) {
             case 5: return launch_p2_sized<R, MODE, 5, true>(p, nplanes, st);
             case 6: return launch_p2_sized<R, MODE, 6, true>(p, nplanes, st);
-            case 7: return launch_p2_sized<R, MODE, 7, true>(p, nplanes, st);
             case 8: return launch_p2_sized<R, MODE, 8, true>(p, nplanes, st);
-            case 10: return launch_p2_sized<R, MODE, 10, true>(p, nplanes, st);
             case 12: return launch_p2_sized<R, MODE, 12, true>(p, nplanes, st);
             default: return launch_p2_sized<R, MODE, 0, true>(p, nplanes, st);
         }
     }
-    switch (poly) {
-        case 7: return launch_p2_sized<R, MODE, 7, false>(p, nplanes, st);
-        default: return launch_p2_sized<R, MODE, 0, false>(p, nplanes, st);
+    if (!px) {
+        if (poly == 7) return launch_p2_sized<R, MODE, 7, false>(p, nplanes, st);
+        return launch_p2_sized<R, MODE, 0, false>(p, nplanes, st);
     }
+#endif
+    return launch_p2_sized<R, MODE, kP2DefaultPoly<R>(), true>(p, nplanes, st);
 }
 
 // Packed self / per-channel-joint filter; false when not selected (the caller
@@ -449,18 +440,25 @@ static cudaError_t launch_p2(const BlfParams& p, int nplanes, cudaStream_t st)
 // radius and both modes, BLFLS_P2=0 disables it.
 bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err)
 {
-    static const int sel = [] {
-        const char* e = std::getenv("BLFLS_P2");
-        return e ? std::atoi(e) : -1;
-    }();
-    if (sel == 0 || mode == 2) return false;
-    if (sel < 0 && !(mode == 0 && (p.radius == 5 || p.radius == 7 || p.radius == 15))) return false;
     const int np = batch * p.C;
+#ifdef BLFLS_EXPERIMENTS
+    static const int sel = knob("BLFLS_P2", -1);
+    if (sel == 0 || mode == 2) return false;
+    if (sel > 0) {
+        switch (p.radius) {
+            case 3: *err = mode == 0 ? launch_p2<3, 0>(p, np, st) : launch_p2<3, 1>(p, np, st); return true;
+            case 5: *err = mode == 0 ? launch_p2<5, 0>(p, np, st) : launch_p2<5, 1>(p, np, st); return true;
+            case 7: *err = mode == 0 ? launch_p2<7, 0>(p, np, st) : launch_p2<7, 1>(p, np, st); return true;
+            case 15: *err = mode == 0 ? launch_p2<15, 0>(p, np, st) : launch_p2<15, 1>(p, np, st); return true;
+            default: return false;
+        }
+    }
+#endif
+    if (mode != 0) return false;
     switch (p.radius) {
-        case 3: *err = mode == 0 ? launch_p2<3, 0>(p, np, st) : launch_p2<3, 1>(p, np, st); return true;
-        case 5: *err = mode == 0 ? launch_p2<5, 0>(p, np, st) : launch_p2<5, 1>(p, np, st); return true;
-        case 7: *err = mode == 0 ? launch_p2<7, 0>(p, np, st) : launch_p2<7, 1>(p, np, st); return true;
-        case 15: *err = mode == 0 ? launch_p2<15, 0>(p, np, st) : launch_p2<15, 1>(p, np, st); return true;
+        case 5: *err = launch_p2<5, 0>(p, np, st); return true;
+        case 7: *err = launch_p2<7, 0>(p, np, st); return true;
+        case 15: *err = launch_p2<15, 0>(p, np, st); return true;
         default: return false;
     }
 }

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F f
         } else {
             X = buf[fft.template pad<false>(v * n + k)];
         }
-        p.spec[((size_t)plane * p.H + y) * p.spitch + k] = X;
+        p.spec[spec_at(p, plane, y, k)] = X;
     }
 }
 
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
     const int H = fft.n(), V = fft.vecs();  // compile-time for the CT engine
     const int plane = blockIdx.y;
     const int v0 = blockIdx.x * V;
-    float2* spec = p.spec + (size_t)plane * H * p.spitch;
+    const size_t rs = spec_row_stride(p);
     // cp.async (LDGSTS) straight into the padded strip: every copy of the
     // thread is in flight at once instead of one load per loop trip
     for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
         if (v < p.wc) {
             const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
-                         "l"(spec + (size_t)u * p.spitch + v));
+                         "l"(p.spec + spec_at(p, plane, 0, v) + (size_t)u * rs));
         } else {
             *dst = make_float2(0.f, 0.f);
         }
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
     for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
         const int u = idx / V, c = idx - (idx / V) * V;
         const int v = v0 + c;
-        if (v < p.wc) spec[(size_t)u * p.spitch + v] = buf[fft.template pad<true>(idx)];
+        if (v < p.wc) p.spec[spec_at(p, plane, 0, v) + (size_t)u * rs] = buf[fft.template pad<true>(idx)];
     }
 }
 
@@ -201,10 +201,10 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
         const int y = row0 + v;
         float2 Z = make_float2(0.f, 0.f);
         if (y < p.H) {
-            const float2* srow = p.spec + ((size_t)plane * p.H + y) * p.spitch;
+            auto srow = [&](int kk) { return p.spec[spec_at(p, plane, y, kk)]; };
             if (!ODD) {
-                float2 xk = srow[k];
-                float2 xn = srow[n - k];
+                float2 xk = srow(k);
+                float2 xn = srow(n - k);
                 if (k == 0) {  // c2r ignores Im of DC and Nyquist
                     xk.y = 0.f;
                     xn.y = 0.f;
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
                 Z = cadd(a, cmuli(bb, 1.0f));
             } else {
                 if (k <= (W - 1) / 2) {
-                    Z = srow[k];
+                    Z = srow(k);
                     if (k == 0) Z.y = 0.f;
                 } else {
-                    Z = cconj(srow[W - k]);
+                    Z = cconj(srow(W - k));
                 }
             }
         }
@@ -510,8 +510,6 @@ static cudaError_t launch_fft_pass(int which, const SolveParams& p, const FftGeo
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e3 = cudaSuccess;
-        if (which != 1 && launch_v3_row_pass(which, p, n, g.desc.tw, planes, nsm, st, &e3)) return e3;
         if (launch_v2_pass(which, p, n, g.desc.tw, planes, nsm, st)) return cudaGetLastError();
     }
     if (g.ct && !odd) {

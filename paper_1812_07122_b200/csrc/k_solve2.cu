@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_r2c(const SolveParams p, co
         const float2 zn = cconj(buf[G::ra(vv, k == 0 ? 0 : n - k)]);
         const float2 e = cscale(cadd(zk, zn), 0.5f);
         const float2 o = cscale(cmuli(csub(zk, zn), -1.0f), 0.5f);
-        p.spec[((size_t)plane * p.H + yy) * p.spitch + k] = cadd(e, cmul(__ldg(&p.post[k]), o));
+        p.spec[spec_at(p, plane, yy, k)] = cadd(e, cmul(__ldg(&p.post[k]), o));
     }
 }
 
@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(G::THREADS, G::THREADS <= 512 ? 65536 / (64 * 
     const int plane = blockIdx.y;
     const int vc = blockIdx.x * G::V + v;
     const bool live = vc < p.wc;
-    float2* spec = p.spec + (size_t)plane * G::N * p.spitch + (live ? vc : 0);
-    const size_t sp = p.spitch;
+    float2* spec = p.spec + spec_at(p, plane, 0, live ? vc : 0);
+    const size_t sp = spec_row_stride(p);
     auto ldg = [&](int u) -> float2 { return live ? __ldcg(spec + (size_t)u * sp) : make_float2(0.f, 0.f); };
     auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
     auto lds = [&](int u) { return buf[G::ca(v, u)]; };
@@ -163,10 +163,10 @@ __global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
     constexpr int N = G::N, V = G::V, BUF = G::PADN * G::V;
     static_assert(V % 2 == 0, "16-byte chunks of two columns");
     const int v = threadIdx.x % V, t = threadIdx.x / V;
-    const size_t sp = p.spitch;
+    const size_t sp = spec_row_stride(p);
     auto issue = [&](int s, float2* dst) {
         const int plane = s / nsp, c0 = (s - plane * nsp) * V;
-        const float2* src = p.spec + (size_t)plane * N * sp + c0;
+        const float2* src = p.spec + spec_at(p, plane, 0, c0);
         for (int c = threadIdx.x; c < N * V / 2; c += G::THREADS) {
             const int u = c / (V / 2), h = c - u * (V / 2);
             const unsigned d = (unsigned)__cvta_generic_to_shared(dst + G::ca(2 * h, u));
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
         const int plane = s / nsp;
         const int vc = (s - plane * nsp) * V + v;
         const bool live = vc < p.wc;
-        float2* spec = p.spec + (size_t)plane * N * sp + (live ? vc : 0);
+        float2* spec = p.spec + spec_at(p, plane, 0, live ? vc : 0);
         auto lds = [&](int u) { return buf[G::ca(v, u)]; };
         auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
         s2_smem_stages<G, true, false, 0, G::NST>(buf, v, t, tw);
@@ -223,13 +223,14 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, co
     const int plane = blockIdx.y;
     const int y = blockIdx.x * G::V + v;
     const bool live = y < p.H;
-    const float2* srow = p.spec + ((size_t)plane * p.H + (live ? y : 0)) * p.spitch;
+    const int yl = live ? y : 0;
+    auto srow = [&](int kk) { return p.spec + spec_at(p, plane, yl, kk); };
     // Z_k = (X_k + conj X_{n-k}) + i e^{+2 pi i k / W} (X_k - conj X_{n-k}); c2r
     // ignores Im of DC and Nyquist
     auto ldg = [&](int k) -> float2 {
         if (!live) return make_float2(0.f, 0.f);
-        float2 xk = __ldcg(srow + k);
-        float2 xn = __ldcg(srow + (n - k));
+        float2 xk = __ldcg(srow(k));
+        float2 xn = __ldcg(srow(n - k));
         if (k == 0) {
             xk.y = 0.f;
             xn.y = 0.f;
@@ -283,16 +284,23 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, co
 // row geometry for n = 960 (c3): its 15 x 16 x 4 c2r measured slower than
 // the radix-8 engine's (31 vs 27 us per iteration); no radix-16 column
 // geometry for H = 512 (c1: 15.9 vs 12.1 us).
-#define BLFLS_V2_ROWS(X) X(256, 16, 8, 32) X(256, 4, 8, 32) X(512, 8, 16, 32) X(512, 2, 16, 32) \
-    X(960, 8, 32, 32) X(960, 2, 32, 32) X(1024, 8, 32, 32) X(1024, 2, 32, 32) X(2048, 4, 64, 32) \
-    X(2048, 1, 64, 32) \
-    X(256, 8, 16, 16) X(512, 8, 32, 16) X(512, 2, 32, 16) \
+// Radix-32 geometries (PMAX 32) are experiment-only (BLFLS_V2_PMAX_*=32):
+// too many registers (94-201), slower than radix 16 everywhere (r01).
+#define BLFLS_V2_ROWS16(X) X(256, 8, 16, 16) X(512, 8, 32, 16) X(512, 2, 32, 16) \
     X(1024, 4, 64, 16) X(1024, 1, 64, 16) X(2048, 2, 128, 16) X(2048, 1, 128, 16)
-#define BLFLS_V2_COLS(X) X(512, 8, 16, 32) X(512, 2, 16, 32) X(1024, 4, 32, 32) X(1024, 2, 32, 32) \
-    X(1080, 8, 36, 32) X(1080, 4, 40, 32) X(2048, 4, 64, 32) X(2048, 2, 64, 32) X(4096, 4, 128, 32) \
-    X(4096, 2, 128, 32) \
-    X(1024, 4, 64, 16) X(1024, 2, 64, 16) X(1080, 4, 72, 16) \
+#define BLFLS_V2_COLS16(X) X(1024, 4, 64, 16) X(1024, 2, 64, 16) X(1080, 4, 72, 16) \
     X(2048, 4, 128, 16) X(2048, 2, 128, 16) X(4096, 2, 256, 16) X(4096, 4, 256, 16)
+#ifdef BLFLS_EXPERIMENTS
+#define BLFLS_V2_ROWS(X) BLFLS_V2_ROWS16(X) X(256, 16, 8, 32) X(256, 4, 8, 32) X(512, 8, 16, 32) \
+    X(512, 2, 16, 32) X(960, 8, 32, 32) X(960, 2, 32, 32) X(1024, 8, 32, 32) X(1024, 2, 32, 32) \
+    X(2048, 4, 64, 32) X(2048, 1, 64, 32)
+#define BLFLS_V2_COLS(X) BLFLS_V2_COLS16(X) X(512, 8, 16, 32) X(512, 2, 16, 32) X(1024, 4, 32, 32) \
+    X(1024, 2, 32, 32) X(1080, 8, 36, 32) X(1080, 4, 40, 32) X(2048, 4, 64, 32) X(2048, 2, 64, 32) \
+    X(4096, 4, 128, 32) X(4096, 2, 128, 32)
+#else
+#define BLFLS_V2_ROWS(X) BLFLS_V2_ROWS16(X)
+#define BLFLS_V2_COLS(X) BLFLS_V2_COLS16(X)
+#endif
 
 template <class K>
 static void set_smem2(K kernel, size_t smem)
@@ -310,10 +318,7 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
         // (c2 column 62 -> 57 us per step; c3's 1080, the HBM-streaming c5 and
         // L2-resident 2048-point groups of c5 measured slower,
         // profiles/r01_solve_knobs_c23.txt)
-        static const int pipe_env = [] {
-            const char* e = std::getenv("BLFLS_COL_PIPE");
-            return e != nullptr ? std::atoi(e) : -1;
-        }();
+        static const int pipe_env = knob("BLFLS_COL_PIPE", -1);
         const size_t spec_bytes = (size_t)planes * G::N * p.spitch * sizeof(float2);
         const bool pipe = pipe_env >= 0 ? pipe_env != 0
                                         : ((G::N & (G::N - 1)) == 0 && G::N <= 1024 && spec_bytes <= ((size_t)48 << 20));
@@ -321,16 +326,23 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
             if (pipe) {
                 const int nsp = (p.wc + G::V - 1) / G::V;
                 const int total = nsp * planes;
-                int occ = 0, dev = 0, nsm = 148;
-                set_smem2(k2_col_pipe<G>, 2 * smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_col_pipe<G>, G::THREADS, 2 * smem);
+                // two strip buffers must fit the opt-in shared memory (4096-point
+                // columns at V = 4 need 278,592 B > 227 KB: the plain pass runs)
+                int occ = 0, dev = 0, nsm = 148, optin = 0;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                if (occ > 0) {
+                cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+                if (2 * smem <= (size_t)optin &&
+                    cudaFuncSetAttribute(k2_col_pipe<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(2 * smem)) == cudaSuccess &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_col_pipe<G>, G::THREADS, 2 * smem) ==
+                        cudaSuccess &&
+                    occ > 0) {
                     const int grid = std::min(total, occ * nsm);
                     k2_col_pipe<G><<<grid, G::THREADS, 2 * smem, st>>>(p, tw, nsp, total);
                     return;
                 }
+                (void)cudaGetLastError();  // a failed opt-in leaves no sticky error
             }
         }
         dim3 grid((p.wc + G::V - 1) / G::V, planes);
@@ -353,27 +365,15 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
 bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,
                     cudaStream_t st)
 {
-    static const bool disabled = [] {
-        const char* e = std::getenv("BLFLS_FFT_V1");
-        return e != nullptr && std::atoi(e) != 0;
-    }();
+    static const bool disabled = (knob("BLFLS_FFT_V1", 0) != 0);
     if (disabled) return false;
     if (which == 1 && p.mode != 3) return false;
     // passes routed here (bit 0 row r2c, bit 1 column, bit 2 row c2r)
-    static const int passes = [] {
-        const char* e = std::getenv("BLFLS_V2_PASSES");
-        return e ? std::atoi(e) : 6;  // column + row c2r (streaming ncu, r01)
-    }();
+    static const int passes = knob("BLFLS_V2_PASSES", 6);  // column + row c2r (streaming ncu, r01)
     if (!((passes >> which) & 1)) return false;
     // radix cap of the row / column engines (experiment knob; default 32)
-    static const int pmax_rows = [] {
-        const char* e = std::getenv("BLFLS_V2_PMAX_ROWS");
-        return e ? std::atoi(e) : 16;
-    }();
-    static const int pmax_cols = [] {
-        const char* e = std::getenv("BLFLS_V2_PMAX_COLS");
-        return e ? std::atoi(e) : 16;
-    }();
+    static const int pmax_rows = knob("BLFLS_V2_PMAX_ROWS", 16);
+    static const int pmax_cols = knob("BLFLS_V2_PMAX_COLS", 16);
     const int pmax = which == 1 ? pmax_cols : pmax_rows;
     const int nvec = which == 1 ? p.wc : p.H;
     int bestV = 0, narrowV = 1 << 30;
@@ -393,14 +393,8 @@ bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, in
     int V = bestV ? bestV : narrowV;
     if (V == 1 << 30) return false;
     // experiment knob: force the vectors per CTA of the column / row passes
-    static const int forceV[2] = {[] {
-                                      const char* e = std::getenv("BLFLS_V2_ROWV");
-                                      return e ? std::atoi(e) : 0;
-                                  }(),
-                                  [] {
-                                      const char* e = std::getenv("BLFLS_V2_COLV");
-                                      return e ? std::atoi(e) : 0;
-                                  }()};
+    static const int forceV[2] = {knob("BLFLS_V2_ROWV", 0),
+                                  knob("BLFLS_V2_COLV", 0)};
     if (const int fv = forceV[which == 1 ? 1 : 0]) {
         bool have = false;
 #define BLFLS_V2_HAVE(N, VV, TV, PM) have = have || (N == n && VV == fv && PM == pmax);

@@ -171,3 +171,37 @@ def test_rolling_subcommands_use_reference_defaults(gpu, cli, oracle, tmp_path, 
                                dt_iters=3, pad=16, n=n, init_sigma=s0)
     d = np.abs(read_pfm(tmp_path / "o.pfm") - ref)
     assert d.max() <= 5e-3 and d.mean() <= 5e-5
+
+
+def test_raster_codec_round_trips(cli, tmp_path):
+    """`blfls convert` (no device): PFM in both byte orders with header
+    comments, 8- and 16-bit PGM / PPM, PFM -> PPM quantisation."""
+    rng = np.random.default_rng(5)
+    img = rng.random((3, 7, 9)).astype(np.float32)
+    # big-endian PFM with a comment and CRLF-free tokens split over lines
+    c, h, w = img.shape
+    be = tmp_path / "be.pfm"
+    with open(be, "wb") as f:
+        f.write(f"PF\n# made by a test\n{w}\n{h}\n1.0\n".encode())
+        f.write(np.ascontiguousarray(img.transpose(1, 2, 0)[::-1]).astype(">f4").tobytes())
+    assert run(cli, "convert", be, tmp_path / "le.pfm").returncode == 0
+    np.testing.assert_array_equal(read_pfm(tmp_path / "le.pfm"), img.astype(np.float64))
+    # 16-bit PGM in, PFM out: value / maxval
+    g16 = rng.integers(0, 1001, (5, 6))
+    with open(tmp_path / "g16.pgm", "wb") as f:
+        f.write(b"P5 6 5 1000\n" + g16.astype(">u2").tobytes())
+    assert run(cli, "convert", tmp_path / "g16.pgm", tmp_path / "g16.pfm").returncode == 0
+    np.testing.assert_allclose(read_pfm(tmp_path / "g16.pfm")[0], g16 / 1000.0, rtol=0, atol=1e-7)
+    # PFM -> 8-bit PPM: clamp to [0, 1], round to nearest
+    v = np.array([[[-0.2, 0.0, 0.5 / 255, 0.4, 1.0, 1.7]]] * 3, np.float32)
+    write_pfm(tmp_path / "v.pfm", v)
+    assert run(cli, "convert", tmp_path / "v.pfm", tmp_path / "v.ppm").returncode == 0
+    data = (tmp_path / "v.ppm").read_bytes()
+    assert data.startswith(b"P6\n6 1\n255\n")
+    px = np.frombuffer(data[len(b"P6\n6 1\n255\n"):], np.uint8).reshape(1, 6, 3)[..., 0]
+    assert px.tolist() == [[0, 0, 1, 102, 255, 255]]
+    # truncated payload and bad magic are I/O errors (exit 1)
+    (tmp_path / "t.pgm").write_bytes(b"P5\n4 4\n255\n" + bytes(10))
+    assert run(cli, "convert", tmp_path / "t.pgm", tmp_path / "o.pgm").returncode == 1
+    (tmp_path / "m.pgm").write_bytes(b"P2\n1 1\n255\n0\n")
+    assert run(cli, "convert", tmp_path / "m.pgm", tmp_path / "o.pgm").returncode == 1

@@ -376,33 +376,44 @@ def test_async_host_pipeline(gpu, oracle):
     plan.sync()  # the deferred error is reported once
 
 
-@pytest.mark.parametrize("chunks", ["3", "4", "8"])
-def test_async_host_batch_chunks(gpu, oracle, chunks):
-    """A large ASYNC host batch is streamed through the staging slots in
-    chunks of images (BLFLS_HOST_CHUNKS, read once per process: here the
-    auto rule keeps small batches whole, so the chunked runs go through a
-    subprocess); every image equals the one-call result bit for bit."""
-    import subprocess
-    code = f"""
-import sys, numpy as np
-sys.path.insert(0, {str(Path(__file__).resolve().parent.parent)!r})
-import paper_1812_07122_b200 as P
-from oracle import oracle as O
-b, h, w = 7, 40, 48
-imgs = np.stack([np.stack([O.gen_plane(60 + 3 * i + c, h, w, n_sites=12) for c in range(3)])
-                 for i in range(b)]).astype(np.float32)
-guide = np.stack([O.gen_plane(90 + i, h, w, n_sites=12)[None] for i in range(b)]).astype(np.float32)
-kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
-ref = P.blf_ls(imgs, guide, **kw)
-out = np.empty_like(imgs)
-P.blf_ls(imgs, guide, out=out, wait=False, **kw)
-P.sync_plans()
-assert np.array_equal(out, ref), float(np.abs(out - ref).max())
-print("ok")
-"""
-    env = dict(os.environ, BLFLS_HOST_CHUNKS=chunks)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+def test_async_host_batch_chunks(gpu, oracle):
+    """A large ASYNC host batch is streamed through the two staging slots in
+    chunks of images (>= 64 MB of input per chunk, at most 8; capi.cu
+    host_chunk_images): 12 RGB 1024^2 images = 151 MB -> 2 chunks.  Every
+    image equals the device-pointer (unchunked) result bit for bit."""
+    import torch
+    b, h, w = 12, 1024, 1024
+    imgs = np.stack([np.stack([oracle.gen_plane(60 + 3 * i + c, h, w, n_sites=12) for c in range(3)])
+                     for i in range(b)]).astype(np.float32)
+    kw = dict(lam=1000.0, sigma_s=3.0, sigma_r=0.1, iters=2, radius=3)
+    ref = gpu.blf_ls(torch.from_numpy(imgs).cuda(), **kw).cpu().numpy()
+    host = torch.from_numpy(imgs).pin_memory()
+    out = torch.empty_like(host).pin_memory()
+    gpu.blf_ls(host, out=out, wait=False, **kw)
+    gpu.sync_plans()
+    assert np.array_equal(out.numpy(), ref)
+
+
+def test_c5_host_batch_vs_oracle(gpu, oracle):
+    """The workload the bench's e2e line times: the full 64-image c5 batch
+    (2048^2 RGB, joint gray guide, r = 7, 3 iterations) from pinned host
+    memory through blf_ls(wait=False) -> blfls_run(HOST_PTRS | ASYNC |
+    CHECK_FINITE), streamed in 8 chunks of 8 images.  Images 0 and 63 against
+    the oracle (the reference's algorithm in double; ~25 s of host time on
+    the GPU box), the whole batch bit-identical to the device-resident run."""
+    import torch
+    cfg = gpu.CONFIGS["c5"]
+    img, guide = _config_inputs(gpu, cfg)
+    dev_out = _run_cfg(gpu, cfg, img, guide).cpu()
+    h_img, h_guide = img.cpu().pin_memory(), guide.cpu().pin_memory()
+    h_out = torch.empty_like(h_img).pin_memory()
+    gpu.blf_ls(h_img, h_guide, out=h_out, wait=False, lam=cfg.lam, sigma_s=cfg.sigma_s,
+               sigma_r=cfg.sigma_r, iters=cfg.iters, radius=cfg.radius)
+    gpu.sync_plans()
+    assert torch.equal(h_out, dev_out)
+    for i in (0, cfg.batch - 1):
+        ref = _oracle_cfg(oracle, cfg, img, guide, i)
+        assert maxabs(h_out[i].numpy(), ref) <= TOL_OUT, i
 
 
 @pytest.mark.parametrize("c,h,w,r,pad,guided", [

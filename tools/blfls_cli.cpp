@@ -4,6 +4,7 @@
 //   blfls smooth [--method blf-ls|nc-ls|ls] [--sigma-s S] [--sigma-r R] [--lambda L]
 //                [--pad 16] [--radius r] [--iters k] [--iterations t] [--device d] input output
 //   blfls joint  --guide G [same flags] input output
+//   blfls convert input output          (raster I/O only, no GPU)
 //   blfls texture|clipart [--sigma-s S] [--sigma-r R] [--lambda L] [--n N]
 //                [--init-sigma s] [--pad 16] [--device d] input output
 //
@@ -20,8 +21,9 @@
 // --pad (reflect padding) defaults to 16 as in the reference; --blf grid uses
 // the bilateral grid the reference's smooth() runs (default: brute force).
 // Image formats: PFM (float, 'Pf' gray / 'PF' RGB, bottom-up, either endian)
-// and binary PGM/PPM (P5/P6, 8 or 16 bit) with the reference's conventions
-// (image_io.cpp: PNM values / maxval, PNM output clamped and rounded to 8 bit).
+// and binary PGM/PPM (P5/P6, 8 or 16 bit), implemented from the Netpbm / PFM
+// format definitions with the conventions the reference's CLI tests rely on
+// (samples = value / maxval, 8-bit output clamped and rounded).
 // PNG / HDR need libpng / the Radiance codec and are not built.
 // Exit codes as the reference: 0 ok, 2 usage or invalid argument, 1 other.
 #include <algorithm>
@@ -29,8 +31,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
-#include <memory>
+#include <fstream>
+#include <iterator>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -43,143 +47,196 @@ struct UsageError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-using FilePtr = std::unique_ptr<std::FILE, int (*)(std::FILE*)>;
+// ------------------------------------------------------------ raster I/O --
+// Netpbm-family rasters, written from the format definitions:
+//   P5 / P6   binary gray / RGB, maxval < 256 one byte per sample, else two
+//             bytes big endian; samples map to [0, 1] as value / maxval
+//   Pf / PF   float gray / RGB; the third header token is a scale whose sign
+//             gives the byte order (negative: little endian); scanlines are
+//             stored bottom to top
+// Headers are whitespace-separated tokens with '#' comments to end of line,
+// followed by exactly one whitespace byte before the sample data.
 
-FilePtr open_file(const std::string& path, const char* mode)
-{
-    std::FILE* f = std::fopen(path.c_str(), mode);
-    if (!f) throw std::runtime_error("cannot open '" + path + "'");
-    return FilePtr(f, &std::fclose);
-}
-
-std::string ext_of(const std::string& path)
-{
-    const auto dot = path.find_last_of('.');
-    std::string e = dot == std::string::npos ? "" : path.substr(dot + 1);
-    for (char& c : e) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
-    return e;
-}
-
-int header_int(std::FILE* f)
-{
-    int c = std::fgetc(f);
-    while (c != EOF && (std::isspace(c) || c == '#')) {
-        if (c == '#')
-            while (c != EOF && c != '\n') c = std::fgetc(f);
-        c = std::fgetc(f);
+// The whole file in memory plus a cursor over its header tokens.
+class RasterBytes {
+public:
+    static RasterBytes slurp(const std::string& path)
+    {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw std::runtime_error("cannot open '" + path + "'");
+        RasterBytes r;
+        r.path_ = path;
+        r.data_.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+        return r;
     }
-    int v = 0;
-    bool any = false;
-    while (c != EOF && std::isdigit(c)) {
-        v = v * 10 + (c - '0');
-        any = true;
-        c = std::fgetc(f);
-    }
-    return any ? v : -1;
-}
-
-blfls::Image load_pfm(const std::string& path)
-{
-    FilePtr f = open_file(path, "rb");
-    char m[2];
-    if (std::fread(m, 1, 2, f.get()) != 2 || m[0] != 'P' || (m[1] != 'F' && m[1] != 'f'))
-        throw std::runtime_error("'" + path + "': expected PFM header");
-    const int ch = m[1] == 'F' ? 3 : 1;
-    const int w = header_int(f.get()), h = header_int(f.get());
-    double scale = 0.0;
-    if (std::fscanf(f.get(), "%lf", &scale) != 1 || scale == 0.0 || w <= 0 || h <= 0)
-        throw std::runtime_error("'" + path + "': bad PFM header");
-    std::fgetc(f.get());
-    const std::size_t n = static_cast<std::size_t>(w) * h * ch;
-    std::vector<float> buf(n);
-    if (std::fread(buf.data(), sizeof(float), n, f.get()) != n)
-        throw std::runtime_error("'" + path + "': truncated PFM data");
-    if (scale > 0.0)  // big endian
-        for (float& v : buf) {
-            unsigned char* b = reinterpret_cast<unsigned char*>(&v);
-            std::swap(b[0], b[3]);
-            std::swap(b[1], b[2]);
+    // next header token (comments skipped); consumes one trailing whitespace byte
+    std::string token()
+    {
+        for (;;) {
+            while (pos_ < data_.size() && std::isspace(static_cast<unsigned char>(data_[pos_]))) ++pos_;
+            if (pos_ < data_.size() && data_[pos_] == '#') {
+                while (pos_ < data_.size() && data_[pos_] != '\n') ++pos_;
+                continue;
+            }
+            break;
         }
+        const std::size_t b = pos_;
+        while (pos_ < data_.size() && !std::isspace(static_cast<unsigned char>(data_[pos_]))) ++pos_;
+        if (b == pos_) throw std::runtime_error("'" + path_ + "': truncated header");
+        std::string t = data_.substr(b, pos_ - b);
+        if (pos_ < data_.size()) ++pos_;  // the single separator before the payload
+        return t;
+    }
+    long positive(const std::string& what)
+    {
+        const std::string t = token();
+        char* end = nullptr;
+        const long v = std::strtol(t.c_str(), &end, 10);
+        if (*end != '\0' || v <= 0) throw std::runtime_error("'" + path_ + "': bad " + what + " '" + t + "'");
+        return v;
+    }
+    const unsigned char* payload(std::size_t bytes) const
+    {
+        if (data_.size() - pos_ < bytes) throw std::runtime_error("'" + path_ + "': truncated sample data");
+        return reinterpret_cast<const unsigned char*>(data_.data() + pos_);
+    }
+    const std::string& path() const { return path_; }
+
+private:
+    std::string path_, data_;
+    std::size_t pos_ = 0;
+};
+
+bool host_is_little_endian()
+{
+    const uint16_t probe = 1;
+    unsigned char b;
+    std::memcpy(&b, &probe, 1);
+    return b == 1;
+}
+
+float float_from_bytes(const unsigned char* p, bool little)
+{
+    unsigned char b[4];
+    if (little == host_is_little_endian())
+        std::memcpy(b, p, 4);
+    else
+        for (int k = 0; k < 4; ++k) b[k] = p[3 - k];
+    float v;
+    std::memcpy(&v, b, 4);
+    return v;
+}
+
+blfls::Image decode_raster(RasterBytes& r)
+{
+    const std::string magic = r.token();
+    const bool is_float = magic == "Pf" || magic == "PF";
+    const bool is_int = magic == "P5" || magic == "P6";
+    if (!is_float && !is_int)
+        throw std::runtime_error("'" + r.path() + "': not a PFM / binary PGM / binary PPM file");
+    const int ch = (magic == "PF" || magic == "P6") ? 3 : 1;
+    const int w = static_cast<int>(r.positive("width"));
+    const int h = static_cast<int>(r.positive("height"));
     blfls::Image img(w, h, ch);
-    std::size_t i = 0;
-    for (int y = h - 1; y >= 0; --y)  // scanlines bottom to top
-        for (int x = 0; x < w; ++x)
-            for (int c = 0; c < ch; ++c) img.at(c, y, x) = buf[i++];
+    const std::size_t samples = static_cast<std::size_t>(w) * h * ch;
+    if (is_float) {
+        const std::string st = r.token();
+        char* end = nullptr;
+        const double scale = std::strtod(st.c_str(), &end);
+        if (*end != '\0' || scale == 0.0 || !std::isfinite(scale))
+            throw std::runtime_error("'" + r.path() + "': bad PFM scale '" + st + "'");
+        const unsigned char* p = r.payload(samples * 4);
+        const bool little = scale < 0.0;
+        for (int row = 0; row < h; ++row) {          // file row 0 is the bottom scanline
+            const int y = h - 1 - row;
+            for (int x = 0; x < w; ++x)
+                for (int c = 0; c < ch; ++c, p += 4) img.at(c, y, x) = float_from_bytes(p, little);
+        }
+    } else {
+        const long maxval = r.positive("maxval");
+        if (maxval > 65535) throw std::runtime_error("'" + r.path() + "': maxval above 65535");
+        const int width_bytes = maxval > 255 ? 2 : 1;
+        const unsigned char* p = r.payload(samples * width_bytes);
+        const double inv = 1.0 / static_cast<double>(maxval);
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x)
+                for (int c = 0; c < ch; ++c) {
+                    const unsigned v = width_bytes == 2 ? (unsigned(p[0]) << 8) | p[1] : p[0];
+                    p += width_bytes;
+                    img.at(c, y, x) = v * inv;
+                }
+    }
     return img;
 }
 
-void save_pfm(const std::string& path, const blfls::Image& img)
+void write_bytes(const std::string& path, const std::string& header, const std::vector<unsigned char>& body)
 {
-    FilePtr f = open_file(path, "wb");
-    const int ch = img.channels();
-    std::fprintf(f.get(), "P%c\n%d %d\n-1.0\n", ch == 3 ? 'F' : 'f', img.width(), img.height());
-    std::vector<float> buf(img.size());
-    std::size_t i = 0;
-    for (int y = img.height() - 1; y >= 0; --y)
-        for (int x = 0; x < img.width(); ++x)
-            for (int c = 0; c < ch; ++c) buf[i++] = static_cast<float>(img.at(c, y, x));
-    if (std::fwrite(buf.data(), sizeof(float), buf.size(), f.get()) != buf.size())
-        throw std::runtime_error("'" + path + "': short write");
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw std::runtime_error("cannot open '" + path + "' for writing");
+    out.write(header.data(), static_cast<std::streamsize>(header.size()));
+    out.write(reinterpret_cast<const char*>(body.data()), static_cast<std::streamsize>(body.size()));
+    if (!out) throw std::runtime_error("'" + path + "': write failed");
 }
 
-blfls::Image load_pnm(const std::string& path)
+// PFM out: host byte order, declared by the sign of the scale
+void encode_float_raster(const std::string& path, const blfls::Image& img)
 {
-    FilePtr f = open_file(path, "rb");
-    char m[2];
-    if (std::fread(m, 1, 2, f.get()) != 2 || m[0] != 'P' || (m[1] != '5' && m[1] != '6'))
-        throw std::runtime_error("'" + path + "': expected binary PGM (P5) or PPM (P6)");
-    const int ch = m[1] == '6' ? 3 : 1;
-    const int w = header_int(f.get()), h = header_int(f.get()), maxval = header_int(f.get());
-    if (w <= 0 || h <= 0 || maxval <= 0 || maxval > 65535)
-        throw std::runtime_error("'" + path + "': bad PNM header");
-    const std::size_t n = static_cast<std::size_t>(w) * h * ch;
-    const int bytes = maxval < 256 ? 1 : 2;
-    std::vector<unsigned char> buf(n * bytes);
-    if (std::fread(buf.data(), 1, buf.size(), f.get()) != buf.size())
-        throw std::runtime_error("'" + path + "': truncated PNM data");
-    blfls::Image img(w, h, ch);
-    std::size_t i = 0;
+    const int w = img.width(), h = img.height(), ch = img.channels();
+    const bool little = host_is_little_endian();
+    const std::string header = std::string(ch == 3 ? "PF" : "Pf") + "\n" + std::to_string(w) + " " +
+                               std::to_string(h) + "\n" + (little ? "-1.0" : "1.0") + "\n";
+    std::vector<unsigned char> body(static_cast<std::size_t>(w) * h * ch * 4);
+    unsigned char* p = body.data();
+    for (int y = h - 1; y >= 0; --y)
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < ch; ++c, p += 4) {
+                const float v = static_cast<float>(img.at(c, y, x));
+                std::memcpy(p, &v, 4);
+            }
+    write_bytes(path, header, body);
+}
+
+// PGM / PPM out: 8-bit, samples clamped to [0, 1] and rounded to nearest
+void encode_byte_raster(const std::string& path, const blfls::Image& img)
+{
+    const int w = img.width(), h = img.height(), ch = img.channels();
+    const std::string header = std::string(ch == 3 ? "P6" : "P5") + "\n" + std::to_string(w) + " " +
+                               std::to_string(h) + "\n255\n";
+    std::vector<unsigned char> body;
+    body.reserve(static_cast<std::size_t>(w) * h * ch);
     for (int y = 0; y < h; ++y)
         for (int x = 0; x < w; ++x)
             for (int c = 0; c < ch; ++c) {
-                const int v = bytes == 1 ? buf[i] : (buf[i] << 8 | buf[i + 1]);
-                i += bytes;
-                img.at(c, y, x) = v / static_cast<double>(maxval);
+                const double v = img.at(c, y, x);
+                const double q = std::floor((v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v)) * 255.0 + 0.5);
+                body.push_back(static_cast<unsigned char>(q));
             }
-    return img;
+    write_bytes(path, header, body);
 }
 
-void save_pnm(const std::string& path, const blfls::Image& img)
+std::string lower_extension(const std::string& path)
 {
-    FilePtr f = open_file(path, "wb");
-    const int ch = img.channels();
-    std::fprintf(f.get(), "P%c\n%d %d\n255\n", ch == 3 ? '6' : '5', img.width(), img.height());
-    std::vector<unsigned char> buf(img.size());
-    std::size_t i = 0;
-    for (int y = 0; y < img.height(); ++y)
-        for (int x = 0; x < img.width(); ++x)
-            for (int c = 0; c < ch; ++c) {
-                const double v = std::clamp(img.at(c, y, x), 0.0, 1.0);
-                buf[i++] = static_cast<unsigned char>(std::lround(v * 255.0));
-            }
-    if (std::fwrite(buf.data(), 1, buf.size(), f.get()) != buf.size())
-        throw std::runtime_error("'" + path + "': short write");
+    const auto dot = path.find_last_of('.');
+    std::string e = dot == std::string::npos ? std::string() : path.substr(dot + 1);
+    std::transform(e.begin(), e.end(), e.begin(), [](unsigned char c) { return static_cast<char>(std::tolower(c)); });
+    return e;
 }
 
 blfls::Image load_image(const std::string& path)
 {
-    const std::string e = ext_of(path);
-    if (e == "pfm") return load_pfm(path);
-    if (e == "pgm" || e == "ppm") return load_pnm(path);
-    throw std::runtime_error("'" + path + "': unsupported image extension ." + e +
-                             " (this build reads .pfm/.pgm/.ppm)");
+    const std::string e = lower_extension(path);
+    if (e != "pfm" && e != "pgm" && e != "ppm")
+        throw std::runtime_error("'" + path + "': unsupported image extension ." + e +
+                                 " (this build reads .pfm/.pgm/.ppm)");
+    RasterBytes r = RasterBytes::slurp(path);
+    return decode_raster(r);
 }
 
 void save_image(const std::string& path, const blfls::Image& img)
 {
-    const std::string e = ext_of(path);
-    if (e == "pfm") return save_pfm(path, img);
-    if (e == "pgm" || e == "ppm") return save_pnm(path, img);
+    const std::string e = lower_extension(path);
+    if (e == "pfm") return encode_float_raster(path, img);
+    if (e == "pgm" || e == "ppm") return encode_byte_raster(path, img);
     throw std::runtime_error("'" + path + "': unsupported image extension ." + e +
                              " (this build writes .pfm/.pgm/.ppm)");
 }
@@ -209,10 +266,10 @@ int parse_int(const std::string& flag, const char* v)
 
 Options parse(int argc, char** argv)
 {
-    if (argc < 2) throw UsageError("a subcommand is required: smooth | joint | texture | clipart");
+    if (argc < 2) throw UsageError("a subcommand is required: smooth | joint | texture | clipart | convert");
     Options o;
     o.cmd = argv[1];
-    if (o.cmd != "smooth" && o.cmd != "joint" && o.cmd != "texture" && o.cmd != "clipart")
+    if (o.cmd != "smooth" && o.cmd != "joint" && o.cmd != "texture" && o.cmd != "clipart" && o.cmd != "convert")
         throw UsageError("unknown subcommand '" + o.cmd + "'");
     const bool rolling = o.cmd == "texture" || o.cmd == "clipart";
     if (o.cmd == "joint") {  // epls_main.cpp preparse defaults of `joint`
@@ -292,6 +349,10 @@ Options parse(int argc, char** argv)
 int run(const Options& o)
 {
     const blfls::Image in = load_image(o.input);
+    if (o.cmd == "convert") {  // raster I/O only (no device): format conversion
+        save_image(o.output, in);
+        return 0;
+    }
     const double lam = o.lambda >= 0.0 ? o.lambda : 1024.0;
     const blfls::DtParams dt{o.sigma_s, o.sigma_r, o.iterations};
     blfls::Image out;
