@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define BLFLS_ABI_VERSION 2
+#define BLFLS_ABI_VERSION 3
 
 typedef enum blfls_status {
     BLFLS_OK = 0,
@@ -197,6 +197,48 @@ blfls_status blfls_blf_brute(const float* src, int cs, const float* guide, int c
 blfls_status blfls_gaussian_blur(const float* in, int channels, int height, int width,
                                  double sigma, float* out, int device, void* stream,
                                  unsigned flags);
+
+/* ------------------------------------------------------------ multi-GPU --
+ * One process driving several devices (the C++ host's multi-GPU path; the
+ * Python host uses one process per GPU over torch.distributed instead,
+ * paper_1812_07122_b200/multigpu.py).  Two decompositions of epls::smooth
+ * cascades:
+ *
+ *  BLFLS_MULTI_BATCH  the batch is split into contiguous shards, one per
+ *                     device entry; each entry has its own plan, stream and
+ *                     host thread and runs blfls_run(HOST_PTRS | ASYNC) on its
+ *                     shard (no data-path exchange: images are independent,
+ *                     pipelines.cpp:57-94 per image).
+ *  BLFLS_MULTI_BAND   ONE image (max_batch 1) in row bands: per iteration every
+ *                     entry filters its band and stores the band's targets
+ *                     into the full-height target buffers of every entry
+ *                     (NVLink peer stores from the filter kernel,
+ *                     blfls_filter_gradients_rows_peers), then every entry
+ *                     runs the full FFT solve redundantly, so each holds the
+ *                     whole next iterate; ordering by cross-device events.
+ *
+ * A device may appear more than once (several entries on one GPU share it).
+ * Distinct devices need peer access in band mode (BLFLS_EUNSUPPORTED
+ * otherwise; there is no silent fallback).  Results are bit-identical to
+ * blfls_run on one device.  img / guide / out are HOST pointers (flags may add
+ * BLFLS_CHECK_FINITE); the call returns when `out` is complete. */
+#define BLFLS_MULTI_BATCH 0
+#define BLFLS_MULTI_BAND 1
+
+typedef struct blfls_multi_s* blfls_multi_t;
+
+/* params->max_batch = the largest batch per call (1 in band mode);
+ * params->device is ignored: `devices` (n entries, 1..8) lists the GPUs. */
+blfls_status blfls_multi_create(const blfls_params* params, const int* devices, int ndevices,
+                                int mode, blfls_multi_t* multi);
+blfls_status blfls_multi_run(blfls_multi_t multi, const float* img, const float* guide, int batch,
+                             int iters, float* out, unsigned flags);
+blfls_status blfls_multi_destroy(blfls_multi_t multi);
+
+/* Page-locked host buffers (cudaHostAlloc) for HOST_PTRS calls, so host code
+ * needs no CUDA runtime of its own (the C++ host's blfls::Plan staging). */
+blfls_status blfls_host_alloc(size_t bytes, void** ptr);
+blfls_status blfls_host_free(void* ptr);
 
 /* Counters of the last blfls_run on this plan (for the bench's roofline). */
 typedef struct blfls_stats {

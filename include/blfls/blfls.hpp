@@ -11,6 +11,14 @@
 //   blfls::flash_no_flash(a, f, s)  ~ epls::flash_no_flash (applications.cpp:58-64)
 //   blfls::blf_ls(...)              the north-star cascade (iters smooth() calls)
 //   blfls::lsgrad_solve_fft(...)    ~ epls::lsgrad_solve_fft (solver.cpp:88-124)
+//   blfls::Plan                     a reusable plan (twiddles, spectral tables,
+//                                   workspace, CUDA graphs, pinned staging):
+//                                   the reference calls smooth() repeatedly with
+//                                   one spec (pipelines.cpp:111-115); so do the
+//                                   free functions here, through a per-thread
+//                                   cache of Plans keyed on the spec
+//   blfls::MultiPlan                several GPUs from one process (batch shards
+//                                   or row bands, blfls_multi_*)
 //
 // Errors throw like the reference: std::invalid_argument for shape,
 // parameter and non-finite input; std::runtime_error for CUDA failures;
@@ -18,11 +26,14 @@
 // link against paper_1812_07122_b200/_lib/libblfls.so.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <list>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "blfls/blfls.h"
@@ -114,27 +125,231 @@ struct PlanDeleter {
 };
 using PlanPtr = std::unique_ptr<blfls_plan_s, PlanDeleter>;
 
-inline PlanPtr make_plan(int h, int w, int c, int gc, int radius, double ss, double sr, double lam,
-                         int batch, int device, int pad = 0, int backend = BLFLS_BACKEND_BRUTE,
-                         int dt_iterations = 0)
+inline blfls_params make_params(int h, int w, int c, int gc, int radius, double ss, double sr, double lam,
+                                int batch, int device, int pad = 0, int backend = BLFLS_BACKEND_BRUTE,
+                                int dt_iterations = 0)
 {
-    blfls_params p{h, w, c, gc, radius, ss, sr, lam, batch, device, pad, backend, dt_iterations};
+    return blfls_params{h, w, c, gc, radius, ss, sr, lam, batch, device, pad, backend, dt_iterations};
+}
+
+inline PlanPtr make_plan(const blfls_params& p)
+{
     blfls_plan_t raw = nullptr;
     check(blfls_plan_create(&p, &raw));
     return PlanPtr(raw);
 }
 
+// f(begin, end) over [0, n) on up to hardware_concurrency threads (chunks of
+// >= 1 Mi elements; small ranges run inline): the double <-> float
+// conversions of the Image interface
+template <class F>
+inline void parallel_for(std::size_t n, F&& f)
+{
+    constexpr std::size_t grain = std::size_t(1) << 20;
+    std::size_t nt = std::max(1u, std::thread::hardware_concurrency());
+    nt = std::min(nt, n / grain);
+    if (nt <= 1) {
+        f(std::size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(nt);
+    const std::size_t per = (n + nt - 1) / nt;
+    for (std::size_t t = 0; t < nt; ++t) {
+        const std::size_t b = t * per, e = std::min(n, b + per);
+        if (b < e) th.emplace_back([&f, b, e] { f(b, e); });
+    }
+    for (auto& t : th) t.join();
+}
+
+inline void to_float(const double* src, float* dst, std::size_t n)
+{
+    parallel_for(n, [&](std::size_t b, std::size_t e) {
+        for (std::size_t i = b; i < e; ++i) dst[i] = static_cast<float>(src[i]);
+    });
+}
+
+inline void to_double(const float* src, double* dst, std::size_t n)
+{
+    parallel_for(n, [&](std::size_t b, std::size_t e) {
+        for (std::size_t i = b; i < e; ++i) dst[i] = src[i];
+    });
+}
+
 inline std::vector<float> to_f32(const Image& img)
 {
     std::vector<float> v(img.size());
-    for (std::size_t i = 0; i < v.size(); ++i) v[i] = static_cast<float>(img.data()[i]);
+    to_float(img.data().data(), v.data(), v.size());
     return v;
+}
+
+// page-locked float buffer (blfls_host_alloc), grown on demand
+class PinnedFloats {
+public:
+    PinnedFloats() = default;
+    PinnedFloats(const PinnedFloats&) = delete;
+    PinnedFloats& operator=(const PinnedFloats&) = delete;
+    ~PinnedFloats() { blfls_host_free(p_); }
+    float* reserve(std::size_t n)
+    {
+        if (n > n_) {
+            blfls_host_free(p_);
+            p_ = nullptr;
+            n_ = 0;
+            void* q = nullptr;
+            check(blfls_host_alloc(n * sizeof(float), &q));
+            p_ = static_cast<float*>(q);
+            n_ = n;
+        }
+        return p_;
+    }
+
+private:
+    float* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+}  // namespace detail
+
+/// A reusable BLF-LS plan: created once per (shape, parameters, device),
+/// then run on any number of batches <= max_batch.  Not thread-safe (one per
+/// host thread), like the C ABI's plans.
+class Plan {
+public:
+    explicit Plan(const blfls_params& prm) : prm_(prm), plan_(detail::make_plan(prm)) {}
+    Plan(int height, int width, int channels, int guide_channels, int radius, double sigma_s,
+         double sigma_r, double lambda, int max_batch = 1, int device = 0, int pad = 0,
+         int backend = BLFLS_BACKEND_BRUTE, int dt_iterations = 0)
+        : Plan(detail::make_params(height, width, channels, guide_channels, radius, sigma_s, sigma_r,
+                                   lambda, max_batch, device, pad, backend, dt_iterations))
+    {
+    }
+    const blfls_params& params() const { return prm_; }
+    blfls_plan_t handle() const { return plan_.get(); }
+    std::size_t image_floats() const { return (std::size_t)prm_.height * prm_.width * prm_.channels; }
+    std::size_t guide_floats() const { return (std::size_t)prm_.height * prm_.width * prm_.guide_channels; }
+
+    /// float host buffers, batch x C x H x W (pinned memory is fastest);
+    /// returns when `out` is written
+    void run(const float* img, const float* guide, int batch, int iters, float* out,
+             bool check_finite = true)
+    {
+        detail::check(blfls_run(plan_.get(), img, guide, batch, iters, out, nullptr,
+                                BLFLS_HOST_PTRS | BLFLS_SYNC | (check_finite ? BLFLS_CHECK_FINITE : 0u)));
+    }
+    /// queued H2D / compute / D2H on the plan's streams; consecutive calls
+    /// overlap.  Buffers must stay valid and `out` is readable after sync()
+    /// (which throws std::invalid_argument for deferred non-finite input).
+    void run_async(const float* img, const float* guide, int batch, int iters, float* out,
+                   bool check_finite = true)
+    {
+        detail::check(blfls_run(plan_.get(), img, guide, batch, iters, out, nullptr,
+                                BLFLS_HOST_PTRS | BLFLS_ASYNC | (check_finite ? BLFLS_CHECK_FINITE : 0u)));
+    }
+    void sync() { detail::check(blfls_sync(plan_.get())); }
+
+    /// the Image interface: double <-> float through pinned staging reused
+    /// across calls (multi-threaded conversion for large images)
+    Image run(const Image& img, const Image* guide, int iters)
+    {
+        if (img.width() != prm_.width || img.height() != prm_.height || img.channels() != prm_.channels)
+            throw std::invalid_argument("Plan::run: image shape does not match the plan");
+        if ((guide != nullptr) != (prm_.guide_channels != 0) ||
+            (guide && (guide->width() != img.width() || guide->height() != img.height() ||
+                       guide->channels() != prm_.guide_channels)))
+            throw std::invalid_argument("smooth: guidance image shape does not match input");
+        float* in = in_.reserve(img.size());
+        float* out = out_.reserve(img.size());
+        detail::to_float(img.data().data(), in, img.size());
+        float* gd = nullptr;
+        if (guide) {
+            gd = gd_.reserve(guide->size());
+            detail::to_float(guide->data().data(), gd, guide->size());
+        }
+        run(in, gd, 1, iters, out);
+        Image res(img.width(), img.height(), img.channels());
+        detail::to_double(out, res.data().data(), img.size());
+        return res;
+    }
+
+    /// lsgrad_solve_fft (solver.cpp:88-124) with this plan's lambda / pad
+    Image solve(const Image& g, const Image& tx, const Image& ty)
+    {
+        if (!g.same_shape(tx) || !g.same_shape(ty))
+            throw std::invalid_argument("lsgrad_solve_fft: target shape does not match image");
+        const std::size_t n = g.size();
+        float* a = in_.reserve(3 * n);
+        float* out = out_.reserve(n);
+        detail::to_float(g.data().data(), a, n);
+        detail::to_float(tx.data().data(), a + n, n);
+        detail::to_float(ty.data().data(), a + 2 * n, n);
+        detail::check(blfls_solve(plan_.get(), a, a + n, a + 2 * n, 1, out, nullptr,
+                                  BLFLS_HOST_PTRS | BLFLS_CHECK_FINITE | BLFLS_SYNC));
+        Image res(g.width(), g.height(), g.channels());
+        detail::to_double(out, res.data().data(), n);
+        return res;
+    }
+
+private:
+    blfls_params prm_;
+    detail::PlanPtr plan_;
+    detail::PinnedFloats in_, gd_, out_;
+};
+
+/// Several GPUs from one process (blfls_multi_*): BLFLS_MULTI_BATCH shards a
+/// batch over the device list, BLFLS_MULTI_BAND splits one image into row
+/// bands with NVLink peer stores of the targets.  A device may repeat.
+class MultiPlan {
+public:
+    MultiPlan(const blfls_params& prm, const std::vector<int>& devices, int mode = BLFLS_MULTI_BATCH)
+        : prm_(prm)
+    {
+        blfls_multi_t m = nullptr;
+        detail::check(blfls_multi_create(&prm, devices.data(), (int)devices.size(), mode, &m));
+        m_.reset(m);
+    }
+    const blfls_params& params() const { return prm_; }
+    void run(const float* img, const float* guide, int batch, int iters, float* out, bool check_finite = true)
+    {
+        detail::check(blfls_multi_run(m_.get(), img, guide, batch, iters, out,
+                                      BLFLS_HOST_PTRS | (check_finite ? BLFLS_CHECK_FINITE : 0u)));
+    }
+
+private:
+    struct Deleter {
+        void operator()(blfls_multi_s* m) const { blfls_multi_destroy(m); }
+    };
+    blfls_params prm_;
+    std::unique_ptr<blfls_multi_s, Deleter> m_;
+};
+
+namespace detail {
+
+// per-thread cache of Plans keyed on every plan parameter (LRU, 8 entries)
+inline Plan& cached_plan(const blfls_params& p)
+{
+    thread_local std::list<Plan> cache;
+    for (auto it = cache.begin(); it != cache.end(); ++it) {
+        const blfls_params& q = it->params();
+        if (q.height == p.height && q.width == p.width && q.channels == p.channels &&
+            q.guide_channels == p.guide_channels && q.radius == p.radius && q.sigma_s == p.sigma_s &&
+            q.sigma_r == p.sigma_r && q.lambda == p.lambda && q.max_batch == p.max_batch &&
+            q.device == p.device && q.pad == p.pad && q.backend == p.backend &&
+            q.dt_iterations == p.dt_iterations) {
+            cache.splice(cache.begin(), cache, it);
+            return cache.front();
+        }
+    }
+    if (cache.size() >= 8) cache.pop_back();
+    cache.emplace_front(p);
+    return cache.front();
 }
 
 }  // namespace detail
 
 /// `iters` cascaded smooth() calls with the brute-force (joint) BLF, guide
 /// held fixed.  guide: nullptr, 1 channel, or img.channels() channels.
+/// Repeated calls with the same shape and parameters reuse one cached Plan.
 inline Image blf_ls(const Image& img, const Image* guide, double lambda, double sigma_s,
                     double sigma_r, int iters = 1, int radius = -1, int device = 0, int pad = 0,
                     int backend = BLFLS_BACKEND_BRUTE, int dt_iterations = 0)
@@ -142,16 +357,11 @@ inline Image blf_ls(const Image& img, const Image* guide, double lambda, double 
     if (guide && (guide->width() != img.width() || guide->height() != img.height() ||
                   (guide->channels() != 1 && guide->channels() != img.channels())))
         throw std::invalid_argument("smooth: guidance image shape does not match input");
-    auto plan = detail::make_plan(img.height(), img.width(), img.channels(),
-                                  guide ? guide->channels() : 0, radius, sigma_s, sigma_r, lambda,
-                                  1, device, pad, backend, dt_iterations);
-    std::vector<float> in = detail::to_f32(img), out(img.size()), gd;
-    if (guide) gd = detail::to_f32(*guide);
-    detail::check(blfls_run(plan.get(), in.data(), guide ? gd.data() : nullptr, 1, iters,
-                            out.data(), nullptr, BLFLS_HOST_PTRS | BLFLS_CHECK_FINITE | BLFLS_SYNC));
-    Image res(img.width(), img.height(), img.channels());
-    for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
-    return res;
+    Plan& plan = detail::cached_plan(detail::make_params(img.height(), img.width(), img.channels(),
+                                                         guide ? guide->channels() : 0, radius, sigma_s,
+                                                         sigma_r, lambda, 1, device, pad, backend,
+                                                         dt_iterations));
+    return plan.run(img, guide, iters);
 }
 
 /// `iters` cascaded smooth() calls of kind NC_LS (nc_filter, domain_transform.cpp:138-156).
@@ -182,7 +392,7 @@ inline Image gaussian_blur(const Image& img, double sigma, int device = 0)
     detail::check(blfls_gaussian_blur(in.data(), img.channels(), img.height(), img.width(), sigma,
                                       out.data(), device, nullptr, BLFLS_HOST_PTRS | BLFLS_SYNC));
     Image res(img.width(), img.height(), img.channels());
-    for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
+    detail::to_double(out.data(), res.data().data(), out.size());
     return res;
 }
 
@@ -198,7 +408,7 @@ inline Image blf_brute(const Image& src, const Image& guide, const RangeSpatialP
                                   src.width(), 1, radius, p.sigma_s, p.sigma_r, out.data(), device,
                                   nullptr, BLFLS_HOST_PTRS | BLFLS_CHECK_FINITE | BLFLS_SYNC));
     Image res(src.width(), src.height(), src.channels());
-    for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
+    detail::to_double(out.data(), res.data().data(), out.size());
     return res;
 }
 
@@ -234,15 +444,9 @@ inline Image lsgrad_solve_fft(const Image& g, const Image& tx, const Image& ty, 
     if (!g.same_shape(tx) || !g.same_shape(ty))
         throw std::invalid_argument("lsgrad_solve_fft: target shape does not match image");
     if (pad < 0) throw std::invalid_argument("solver: pad must be >= 0");
-    auto plan = detail::make_plan(g.height(), g.width(), g.channels(), 0, 1, 1.0, 1.0, lambda, 1,
-                                  device, pad);
-    std::vector<float> a = detail::to_f32(g), b = detail::to_f32(tx), c = detail::to_f32(ty),
-                       out(g.size());
-    detail::check(blfls_solve(plan.get(), a.data(), b.data(), c.data(), 1, out.data(), nullptr,
-                              BLFLS_HOST_PTRS | BLFLS_CHECK_FINITE | BLFLS_SYNC));
-    Image res(g.width(), g.height(), g.channels());
-    for (std::size_t i = 0; i < out.size(); ++i) res.data()[i] = out[i];
-    return res;
+    Plan& plan = detail::cached_plan(
+        detail::make_params(g.height(), g.width(), g.channels(), 0, 1, 1.0, 1.0, lambda, 1, device, pad));
+    return plan.solve(g, tx, ty);
 }
 
 }  // namespace blfls

@@ -6,10 +6,12 @@ is visible, every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libblfls.so"
+# BLFLS_LIBRARY: an A/B experiments build (build.py --experiments -> _lib_exp/)
+LIB_PATH = Path(os.environ.get("BLFLS_LIBRARY") or Path(__file__).resolve().parent / "_lib" / "libblfls.so")
 
 BLFLS_OK = 0
 BLFLS_EINVAL = 1
@@ -35,8 +37,12 @@ EXPORTS = (
     "blfls_filter_gradients_rows", "blfls_solve", "blfls_rfft2", "blfls_irfft2",
     "blfls_generate", "blfls_last_stats", "blfls_stage_times", "blfls_debug_ranges", "blfls_mufu_peak", "blfls_last_error",
     "blfls_version", "blfls_abi_version", "blfls_gaussian_blur", "blfls_blf_brute",
-    "blfls_forward_gradients", "blfls_filter_gradients_rows_peers",
+    "blfls_forward_gradients", "blfls_filter_gradients_rows_peers", "blfls_multi_create",
+    "blfls_multi_run", "blfls_multi_destroy", "blfls_host_alloc", "blfls_host_free",
 )
+
+MULTI_BATCH = 0
+MULTI_BAND = 1
 
 
 class BlflsError(RuntimeError):
@@ -111,6 +117,11 @@ def lib() -> C.CDLL:
             L.blfls_forward_gradients.argtypes = [fp, ip, ip, ip, fp, fp, ip, vp, C.c_uint]
             L.blfls_blf_brute.argtypes = [fp, ip, fp, ip, ip, ip, ip, ip, C.c_double, C.c_double, fp,
                                           ip, vp, C.c_uint]
+            L.blfls_multi_create.argtypes = [C.POINTER(Params), C.POINTER(C.c_int), ip, ip, C.POINTER(vp)]
+            L.blfls_multi_run.argtypes = [vp, fp, fp, ip, ip, fp, C.c_uint]
+            L.blfls_multi_destroy.argtypes = [vp]
+            L.blfls_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+            L.blfls_host_free.argtypes = [vp]
             L.blfls_last_error.restype = C.c_char_p
             L.blfls_version.restype = C.c_char_p
             for name in EXPORTS:
@@ -175,6 +186,31 @@ class Plan:
         s = Stats()
         check(lib().blfls_last_stats(self.handle, C.byref(s)))
         return s
+
+
+class MultiPlan:
+    """blfls_multi_* (one process, several device entries; a device may
+    repeat): MULTI_BATCH shards the batch, MULTI_BAND splits one image into
+    row bands with NVLink peer stores.  Host float32 buffers."""
+
+    def __init__(self, params: Params, devices, mode=MULTI_BATCH):
+        self.params = params
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        check(lib().blfls_multi_create(C.byref(params), devs, len(devices), int(mode), C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.blfls_multi_destroy(h)
+            self.handle = None
+
+    def run(self, img, guide, batch, iters, out, check_finite=True):
+        """img / guide / out: C-contiguous float32 numpy arrays (host)."""
+        ptr = lambda a: None if a is None else a.ctypes.data
+        check(lib().blfls_multi_run(self.handle, ptr(img), ptr(guide), int(batch), int(iters), ptr(out),
+                                    HOST_PTRS | (CHECK_FINITE if check_finite else 0)))
 
 
 def mufu_peak(device: int = 0):

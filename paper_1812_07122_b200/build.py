@@ -58,15 +58,45 @@ def build_cli(verbose: bool = False) -> Path:
     return CLI
 
 
-def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
-    OUT_DIR.mkdir(exist_ok=True)
+BENCH_SRC = ROOT / "tools" / "blfls_bench.cpp"
+BENCH = OUT_DIR / "blfls_bench"
+CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+
+
+def build_bench(verbose: bool = False) -> Path:
+    """The C++ host end-to-end benchmark (tools/blfls_bench.cpp) over libblfls.so."""
+    if BENCH.exists() and BENCH.stat().st_mtime > max(BENCH_SRC.stat().st_mtime, LIB.stat().st_mtime,
+                                                       (INCLUDE / "blfls" / "blfls.hpp").stat().st_mtime):
+        return BENCH
+    cmd = ["g++", "-std=c++17", "-O2", "-pthread", f"-I{INCLUDE}", f"-I{CUDA_HOME / 'include'}", str(BENCH_SRC),
+           "-o", str(BENCH), f"-L{OUT_DIR}", "-lblfls", f"-L{CUDA_HOME / 'lib64'}", "-lcudart",
+           f"-Wl,-rpath,$ORIGIN", f"-Wl,-rpath,{CUDA_HOME / 'lib64'}"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed:\n{r.stdout}\n{r.stderr}")
+    return BENCH
+
+
+EXP_DIR = PKG / "_lib_exp"
+
+
+def build(verbose: bool = False, ptxas_info: bool = False, experiments: bool = False) -> Path:
+    """experiments=True: an A/B build with -DBLFLS_EXPERIMENTS into _lib_exp/
+    (kernel-selection knobs read from BLFLS_* environment variables; load it
+    with BLFLS_LIBRARY=<path>).  The production library never reads them."""
+    out_dir = EXP_DIR if experiments else OUT_DIR
+    lib_path = out_dir / "libblfls.so"
+    out_dir.mkdir(exist_ok=True)
     objs = []
     jobs = []
     for src in _sources():
-        obj = OUT_DIR / (src.stem + ".o")
+        obj = out_dir / (src.stem + ".o")
         objs.append(obj)
         if _needs(obj, src) or ptxas_info:
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [NVCC, *ARCH, *FLAGS, *(["-DBLFLS_EXPERIMENTS"] if experiments else []), "-c", str(src),
+                   "-o", str(obj)]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -83,13 +113,15 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
         for err in ex.map(run, jobs):
             if ptxas_info and err:
                 sys.stderr.write(err)
-    if jobs or not LIB.exists():
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static"]
+    if jobs or not lib_path.exists():
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(lib_path), *map(str, objs), "-cudart", "static"]
         run(cmd)
+    if experiments:
+        return lib_path
     build_cli(verbose)
+    build_bench(verbose)
     return LIB
 
 
 if __name__ == "__main__":
-    build(verbose=True, ptxas_info="-v" in sys.argv)
-    print(LIB)
+    print(build(verbose=True, ptxas_info="-v" in sys.argv, experiments="--experiments" in sys.argv))

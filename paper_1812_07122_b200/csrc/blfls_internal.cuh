@@ -1,6 +1,7 @@
 // blfls_internal.cuh -- shared definitions of the sm_100a BLF-LS library.
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -20,6 +21,9 @@ int knob(const char* name, int def);
 #else
 constexpr int knob(const char*, int def) { return def; }
 #endif
+
+// sets the calling thread's blfls_last_error() message and returns st
+blfls_status report(blfls_status st, const std::string& msg);
 
 constexpr int kMaxRadius = 48;     // smem tile envelope (radius <= 48)
 constexpr int kMaxPeers = 8;       // fused band exchange: ranks of one NVLink domain
@@ -209,20 +213,27 @@ struct SolveParams {
 
 // Offset of spectrum element (row y, column k) of `plane`.  Row-major: H
 // rows of spitch.  Column strips (the full solve): the plane's H x spitch
-// block holds spitch / 4 strips of 4 adjacent columns, each strip H rows x 4
-// complex (32 bytes per row) contiguous, so the column pass streams whole
-// strips (every warp load / store covers 8 consecutive rows = 256 contiguous
-// bytes) and the row passes write / read 32-byte pieces of 4 columns.
+// block holds spitch / 16 strips of 16 adjacent columns, each strip H rows x
+// 16 complex (one 128-byte line per row) contiguous.  The row passes still
+// read / write whole 128-byte lines (a warp's 32 consecutive columns = 2
+// lines, as row-major), while a column-pass CTA's V-column slice of a strip
+// is a 128-byte-pitch walk through one contiguous H x 128 B block that the
+// strip's other CTAs (adjacent blockIdx.x, co-resident) read alongside,
+// instead of one 32-byte sector per 8 KB row (row-major at W = 2048).
+// (4-column strips, 32 B per row: column pass 9.26 -> 7.30 ms per c5 step,
+// but the row c2r 4.66 -> 7.68 ms: its warps then touched 8 strips each.)
+constexpr int kSpecStrip = 16;
 __host__ __device__ __forceinline__ size_t spec_at(const SolveParams& p, int plane, int y, int k)
 {
     const size_t base = (size_t)plane * p.H * p.spitch;
-    return p.strip ? base + (size_t)(k >> 2) * ((size_t)p.H * 4) + (size_t)y * 4 + (k & 3)
+    return p.strip ? base + (size_t)(k / kSpecStrip) * ((size_t)p.H * kSpecStrip) + (size_t)y * kSpecStrip +
+                         (k % kSpecStrip)
                    : base + (size_t)y * p.spitch + k;
 }
 // distance between rows y and y + 1 of one spectrum column
 __host__ __device__ __forceinline__ size_t spec_row_stride(const SolveParams& p)
 {
-    return p.strip ? 4 : (size_t)p.spitch;
+    return p.strip ? kSpecStrip : (size_t)p.spitch;
 }
 
 // high-radix solve passes (k_solve2.cu): false when no geometry exists for n

@@ -640,6 +640,10 @@ void free_plan(blfls_plan_t p)
 
 }  // namespace
 
+namespace blfls {
+blfls_status report(blfls_status st, const std::string& msg) { return fail(st, msg); }
+}  // namespace blfls
+
 extern "C" {
 
 const char* blfls_last_error(void) { return g_err.c_str(); }

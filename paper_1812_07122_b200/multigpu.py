@@ -188,7 +188,8 @@ def gpu_band_ops(height, width, channels, guide_channels, *, lam, sigma_s, sigma
                  device, fused=False, group=None):
     """(filter_rows, solve) bound to the C ABI on CUDA `device` for band_blf_ls;
     fused=True returns (GpuBandPeers, solve) for the fused peer-store exchange
-    (falls back to the all-gather pair when symmetric memory is unavailable)."""
+    and raises when symmetric memory is unavailable (use fused=False for the
+    NCCL all-gather exchange)."""
     import torch
 
     from . import _capi
@@ -216,8 +217,7 @@ def gpu_band_ops(height, width, channels, guide_channels, *, lam, sigma_s, sigma
         return u
 
     if fused:
-        try:
-            return GpuBandPeers(plan, channels, height, width, device, group), solve
-        except Exception:  # no symmetric memory / NVLink P2P here: keep the collective
-            pass
+        # no silent fallback: a failed symmetric-memory rendezvous raises; the
+        # caller picks the all-gather exchange explicitly (fused=False)
+        return GpuBandPeers(plan, channels, height, width, device, group), solve
     return filter_rows, solve

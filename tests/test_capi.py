@@ -45,7 +45,7 @@ def test_python_binding_lists_all_exports():
 def test_abi_version_and_strings(lib):
     lib.blfls_abi_version.restype = ctypes.c_int
     lib.blfls_version.restype = ctypes.c_char_p
-    assert lib.blfls_abi_version() == 2
+    assert lib.blfls_abi_version() == 3
     assert b"sm_100a" in lib.blfls_version()
 
 
@@ -94,3 +94,21 @@ def test_no_cpu_fallback_in_product():
         text = f.read_text()
         for bad in ("from oracle", "import oracle", "liboracle", "libepls_ref", "orc_"):
             assert bad not in text, (f, bad)
+
+
+def test_multi_create_validation_without_gpu():
+    """blfls_multi_create validates before touching a device."""
+    from paper_1812_07122_b200 import _capi
+    L = _capi.lib()
+    h = ctypes.c_void_p()
+    ok = _capi.Params(64, 64, 1, 0, 3, 1.0, 0.1, 1.0, 2, 0, 0, 0, 0)
+    devs = (ctypes.c_int * 2)(0, 0)
+    assert L.blfls_multi_create(ctypes.byref(ok), devs, 0, 0, ctypes.byref(h)) == _capi.BLFLS_EINVAL
+    assert L.blfls_multi_create(ctypes.byref(ok), devs, 9, 0, ctypes.byref(h)) == _capi.BLFLS_EINVAL
+    assert L.blfls_multi_create(ctypes.byref(ok), devs, 2, 7, ctypes.byref(h)) == _capi.BLFLS_EINVAL
+    # band mode: one image only, brute force, pad 0
+    assert L.blfls_multi_create(ctypes.byref(ok), devs, 2, _capi.MULTI_BAND, ctypes.byref(h)) == _capi.BLFLS_EINVAL
+    padded = _capi.Params(64, 64, 1, 0, 3, 1.0, 0.1, 1.0, 1, 0, 16, 0, 0)
+    assert L.blfls_multi_create(ctypes.byref(padded), devs, 2, _capi.MULTI_BAND,
+                                ctypes.byref(h)) == _capi.BLFLS_EUNSUPPORTED
+    assert L.blfls_multi_run(None, None, None, 1, 1, None, 1) == _capi.BLFLS_EINVAL

@@ -635,3 +635,46 @@ def test_band_peer_stores_match_band_filter(gpu, oracle, nbands, npeers, guided)
         _capi.check(_capi.lib().blfls_filter_gradients_rows_peers(
             plan.handle, img.data_ptr(), None if guide is None else guide.data_ptr(), 0, h, txp,
             typ, 9, stream, _capi.DEVICE_PTRS))
+
+
+# ------------------------------------------------ single-process multi-GPU --
+
+def test_multi_batch_entry_bit_identical(gpu, oracle):
+    """blfls_multi_run(BATCH) over the device list {0, 0} (two plans, two
+    host threads on one GPU) equals one blfls_run bit for bit, for even and
+    odd batches (shards of 2+2 and 2+1)."""
+    from paper_1812_07122_b200 import _capi
+    b, c, h, w = 4, 3, 40, 72
+    imgs = np.stack([_img(oracle, c, h, w, 700 + i) for i in range(b)]).astype(np.float32)
+    guides = np.stack([_img(oracle, 1, h, w, 800 + i) for i in range(b)]).astype(np.float32)
+    kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=3, radius=7)
+    ref = gpu.blf_ls(imgs, guides, **kw)
+    prm = _capi.Params(h, w, c, 1, 7, 7.0, 0.1, 1000.0, b, 0, 0, 0, 0)
+    m = _capi.MultiPlan(prm, [0, 0], _capi.MULTI_BATCH)
+    out = np.full_like(imgs, -1.0)
+    m.run(imgs, guides, b, 3, out)
+    assert np.array_equal(out, ref)
+    out3 = np.full_like(imgs[:3], -1.0)
+    m.run(np.ascontiguousarray(imgs[:3]), np.ascontiguousarray(guides[:3]), 3, 3, out3)
+    assert np.array_equal(out3, ref[:3])
+    bad = imgs.copy()
+    bad[2, 1, 3, 4] = np.nan
+    with pytest.raises(gpu.InvalidArgument):
+        m.run(bad, guides, b, 3, out)
+
+
+@pytest.mark.parametrize("nbands", [2, 3])
+def test_multi_band_entry_bit_identical(gpu, oracle, nbands):
+    """blfls_multi_run(BAND) with nbands entries on GPU 0: every entry filters
+    its row band and stores the targets into every entry's buffers from the
+    filter kernel; the redundant solves then equal one blfls_run bit for bit."""
+    from paper_1812_07122_b200 import _capi
+    c, h, w = 1, 96, 128
+    img = _img(oracle, c, h, w, 21).astype(np.float32)
+    kw = dict(lam=2000.0, sigma_s=12.0, sigma_r=0.08, radius=15)
+    ref = gpu.blf_ls(img, iters=2, **kw)
+    prm = _capi.Params(h, w, c, 0, 15, 12.0, 0.08, 2000.0, 1, 0, 0, 0, 0)
+    m = _capi.MultiPlan(prm, [0] * nbands, _capi.MULTI_BAND)
+    out = np.full_like(img, -1.0)
+    m.run(img, None, 1, 2, out)
+    assert np.array_equal(out, ref)
