@@ -243,6 +243,8 @@ bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, in
 
 // shared-gray-guide filter with packed accumulation (k_blf_j3.cu); false: not covered
 bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
+// eight outputs per thread, factorised exponents (k_blf_j8.cu); false: not covered
+bool launch_grad_blf_j8(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
 
 // self / per-channel-joint filter with packed accumulation (k_blf_p2.cu); false: not covered
 bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err);
