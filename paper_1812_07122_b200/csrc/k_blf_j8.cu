@@ -32,6 +32,8 @@
 
 namespace blfls {
 
+#ifdef BLFLS_EXPERIMENTS  // measured slower than k_blf_j3 (see launch_grad_blf_j8)
+
 namespace {
 
 __device__ __forceinline__ float j8_ex2(float x)
@@ -54,6 +56,35 @@ __device__ __forceinline__ unsigned long long j8_fmul2(float a, unsigned long lo
     asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(aa), "l"(b));
     return d;
+}
+// exp2 of both lanes of an f32x2 pair on the FMA pipe: round-to-nearest
+// split x = j + f (|f| <= 1/2) by the 1.5 * 2^23 shifter, degree-5 minimax
+// polynomial for 2^f (rel. err 2.3e-7, the coefficients of k_blf.cu
+// poly_ex2), 2^j by an exponent-field add.  The factorised exponents are
+// within [-2 coef^2 + cs_min, 2 coef^2] subset of [-125, 60], no clamping.
+__device__ __forceinline__ float2 j8_poly_ex2x2(unsigned long long x)
+{
+    unsigned long long t, jj, f, pp, magic, c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(magic) : "f"(12582912.0f));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(x), "l"(magic));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(jj) : "l"(t), "l"(magic));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(jj));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(pp) : "f"(0.001327647129073739f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.009675541892647743f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.05550713092088699f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.24022120237350464f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.6931469440460205f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(1.0000001192092896f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    float2 tv, pv;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(tv.x), "=f"(tv.y) : "l"(t));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(pv.x), "=f"(pv.y) : "l"(pp));
+    return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                       __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
 }
 __device__ __forceinline__ unsigned long long j8_pack(float x, float y)
 {
@@ -107,69 +138,69 @@ struct J8Geom {
     }
 };
 
-template <int R, int TH, int MINB>
-__global__ void __launch_bounds__(8 * TH, MINB) k_blf_j8(const BlfParams p)
+// Stages one tile: this axis' circular gradients (image.cpp:72-95) of guide
+// and channels into G / S01 / S2, a warp per tile row and a lane per column,
+// by `nworkers` threads (worker = 0 .. nworkers - 1, whole warps).
+// Out-of-image cells hold b = 0 and zero sources (weight 0: the clipped
+// window, bilateral.cpp:56-57).
+template <int R, int TH>
+__device__ __forceinline__ void j8_stage(const BlfParams& p, float* G, float2* S01, float2* S2, int b, int axis,
+                                         int tx0, int ty0, int worker, int nworkers)
 {
     using Gm = J8Geom<R, TH>;
-    constexpr int P = Gm::P, TPR = Gm::TPR, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
-    constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
-    extern __shared__ __align__(16) float smj8[];
-    float* G = smj8;                                                  // [ROWS][GP] scaled guide b
-    float2* S01 = reinterpret_cast<float2*>(smj8 + ROWS * GP);        // [ROWS][SP] {g0 B, g1 B}
-    float2* S2 = S01 + ROWS * SP;                                     // [ROWS][SP] {g2 B, B}
-
+    constexpr int ROWS = Gm::ROWS, COLS = Gm::COLS, GP = Gm::GP, SP = Gm::SP;
     const int H = p.H, W = p.W;
-    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
-    const int tx0 = blockIdx.x * TW;
-    const int ty0 = p.y0 + blockIdx.y * TH;
     const size_t plane = (size_t)H * W;
-    float s, range, sg, grange;
-    j8_decode(p.lohi, b, p.range_coef, s, range);
+    float sg, grange;
     j8_decode(p.glohi, b, p.range_coef, sg, grange);
     const float* fimg = p.f + (size_t)b * 3 * plane;
     const float* gimg = p.guide + (size_t)b * p.GC * plane;
-
-    // ---- prologue: this axis' circular gradients of guide and channels
-    // (image.cpp:72-95), warp per tile row, lane per column; out-of-image
-    // cells hold b = 0 and zero sources (weight 0: the clipped window,
-    // bilateral.cpp:56-57)
-    {
-        const int lane = threadIdx.x & 31;
-        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
-            const int y = ty0 - R + i;
-            const bool yin = y >= 0 && y < H;
-            const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
-            const size_t r0 = (size_t)(yin ? y : 0) * W, r1 = (size_t)(yin ? yn : 0) * W;
-            float* grow = G + i * GP;
-            float2* s01 = S01 + i * SP;
-            float2* s2 = S2 + i * SP;
-            for (int j = lane; j < COLS; j += 32) {
-                const int x = tx0 - R + j;
-                const int o = j8_ssw(j);
-                if (yin && x >= 0 && x < W) {
-                    const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
-                    const float bb = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
-                    grow[j8_gsw(j)] = bb;
-                    float g[3];
+    const int lane = worker & 31;
+    for (int i = worker >> 5; i < ROWS; i += nworkers >> 5) {
+        const int y = ty0 - R + i;
+        const bool yin = y >= 0 && y < H;
+        const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+        const size_t r0 = (size_t)(yin ? y : 0) * W, r1 = (size_t)(yin ? yn : 0) * W;
+        float* grow = G + i * GP;
+        float2* s01 = S01 + i * SP;
+        float2* s2 = S2 + i * SP;
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float* fc = fimg + (size_t)c * plane;
-                        g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
-                    }
-                    const float bw = j8_ex2(-bb * bb);  // exp2(-b^2) of column t
-                    s01[o] = make_float2(g[0] * bw, g[1] * bw);
-                    s2[o] = make_float2(g[2] * bw, bw);
-                } else {
-                    grow[j8_gsw(j)] = 0.0f;
-                    s01[o] = make_float2(0.f, 0.f);
-                    s2[o] = make_float2(0.f, 0.f);
+        for (int j = lane; j < COLS; j += 32) {
+            const int x = tx0 - R + j;
+            const int o = j8_ssw(j);
+            if (yin && x >= 0 && x < W) {
+                const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                const float bb = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
+                grow[j8_gsw(j)] = bb;
+                float g[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float* fc = fimg + (size_t)c * plane;
+                    g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
                 }
+                const float bw = j8_ex2(-bb * bb);  // exp2(-b^2) of column t
+                s01[o] = make_float2(g[0] * bw, g[1] * bw);
+                s2[o] = make_float2(g[2] * bw, bw);
+            } else {
+                grow[j8_gsw(j)] = 0.0f;
+                s01[o] = make_float2(0.f, 0.f);
+                s2[o] = make_float2(0.f, 0.f);
             }
         }
     }
-    __syncthreads();
+}
 
-    const int tx = threadIdx.x % TPR, ty = threadIdx.x / TPR;
+// Filters one staged tile and stores its targets: thread tid in [0, NT)
+// owns outputs (ty0 + tid / 8, tx0 + 8 (tid % 8) .. + 7).
+// POLYK > 0: every POLYK-th exponent pair runs on the FMA pipe (j8_poly_ex2x2)
+template <int R, int TH, int POLYK = 0>
+__device__ __forceinline__ void j8_filter(const BlfParams& p, const float* G, const float2* S01, const float2* S2,
+                                          int b, int axis, int tx0, int ty0, int tid)
+{
+    using Gm = J8Geom<R, TH>;
+    constexpr int P = Gm::P, TPR = Gm::TPR, VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
+    const int H = p.H, W = p.W;
+    const int tx = tid % TPR, ty = tid / TPR;
     const int ox = tx0 + tx * P, oy = ty0 + ty;
     unsigned long long acc01[P], acc2z[P], gsp[P / 2];
     {
@@ -220,24 +251,33 @@ __global__ void __launch_bounds__(8 * TH, MINB) k_blf_j8(const BlfParams p)
                     asm("mov.b64 %0, {%1, %1};" : "=l"(gtt) : "f"(gt[u]));
                     asm("mov.b64 %0, {%1, %2};" : "=l"(ce) : "f"(p.cep[dx0 + R].x), "f"(p.cep[dx0 + R].y));
                     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[h]), "l"(ce));
-                    const float2 ee = j8_unpack(e);
+                    const bool poly = POLYK > 0 && ok0 && ok1 && (j * (P / 2) + h) % (POLYK > 0 ? POLYK : 1) ==
+                                                                 (POLYK > 0 ? POLYK - 1 : 0);
+                    float2 ww;
+                    if (poly) {
+                        ww = j8_poly_ex2x2(e);
+                    } else {
+                        const float2 ee = j8_unpack(e);
+                        ww.x = ok0 ? j8_ex2(ee.x) : 0.f;
+                        ww.y = ok1 ? j8_ex2(ee.y) : 0.f;
+                    }
                     if (ok0) {
-                        const float w = j8_ex2(ee.x);
-                        acc01[q0] = j8_ffma2(w, v01[u], acc01[q0]);
-                        acc2z[q0] = j8_ffma2(w, v2z[u], acc2z[q0]);
+                        acc01[q0] = j8_ffma2(ww.x, v01[u], acc01[q0]);
+                        acc2z[q0] = j8_ffma2(ww.x, v2z[u], acc2z[q0]);
                     }
                     if (ok1) {
-                        const float w = j8_ex2(ee.y);
-                        acc01[q0 + 1] = j8_ffma2(w, v01[u], acc01[q0 + 1]);
-                        acc2z[q0 + 1] = j8_ffma2(w, v2z[u], acc2z[q0 + 1]);
+                        acc01[q0 + 1] = j8_ffma2(ww.y, v01[u], acc01[q0 + 1]);
+                        acc2z[q0 + 1] = j8_ffma2(ww.y, v2z[u], acc2z[q0 + 1]);
                     }
                 }
             }
         }
     }
 
-    // ---- epilogue: T = num / z per channel (the z >= centre weight > 0)
+    // ---- epilogue: T = num / z per channel (z >= the centre weight > 0)
     if (oy < p.y1) {
+        float s, range;
+        j8_decode(p.lohi, b, p.range_coef, s, range);
         const float oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
         float* dst = axis == 0 ? p.tx : p.ty;
         const size_t pl = (size_t)p.out_rows * W;
@@ -265,30 +305,146 @@ __global__ void __launch_bounds__(8 * TH, MINB) k_blf_j8(const BlfParams p)
             }
         }
     }
-    (void)COLS;
 }
 
-template <int R, int TH, int MINB>
+// One CTA per tile: every thread stages, then filters.
+template <int R, int TH, int MINB, int POLYK>
+__global__ void __launch_bounds__(8 * TH, MINB) k_blf_j8(const BlfParams p)
+{
+    using Gm = J8Geom<R, TH>;
+    extern __shared__ __align__(16) float smj8[];
+    float* G = smj8;                                                        // [ROWS][GP] scaled guide b
+    float2* S01 = reinterpret_cast<float2*>(smj8 + Gm::ROWS * Gm::GP);      // [ROWS][SP] {g0 B, g1 B}
+    float2* S2 = S01 + Gm::ROWS * Gm::SP;                                   // [ROWS][SP] {g2 B, B}
+    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
+    const int tx0 = blockIdx.x * Gm::TW, ty0 = p.y0 + blockIdx.y * TH;
+    j8_stage<R, TH>(p, G, S01, S2, b, axis, tx0, ty0, threadIdx.x, Gm::NT);
+    __syncthreads();
+    j8_filter<R, TH, POLYK>(p, G, S01, S2, b, axis, tx0, ty0, threadIdx.x);
+}
+
+// Persistent, warp-specialised: NT filter threads (warps 0 .. NT/32 - 1) and
+// NT staging threads (the other half) per CTA, two staged-tile buffers.  The
+// stagers fill buffer k & 1 with tile k (global loads, gradients, exp2(-b^2))
+// while the filter warps work on tile k - 1, so the filter warps never wait
+// on global memory (in k_blf_j8 / k_blf_j3 the staging loads are the top
+// warp stall, and all CTAs of an SM can be staging at once).  Handshake by
+// named barriers (bar.arrive / bar.sync over all 2 NT threads): FULL[s] (1,
+// 2) stagers -> filter, EMPTY[s] (3, 4) filter -> stagers.  Tiles in the
+// order of k_blf_j8's grid (tile column, tile row, image x axis).
+template <int R, int TH>
+__global__ void __launch_bounds__(16 * TH, 2) k_blf_j8p(const BlfParams p, int ntx, int nty, int total)
+{
+    using Gm = J8Geom<R, TH>;
+    constexpr int NT = Gm::NT;
+    constexpr int BUF = Gm::ROWS * Gm::GP + 2 * 2 * Gm::ROWS * Gm::SP;  // floats per buffer
+    extern __shared__ __align__(16) float smj8[];
+    const int ntiles = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto decode = [&](int t, int& b, int& axis, int& tx0, int& ty0) {
+        const int cx = t % ntx, r = t / ntx, cy = r % nty, z = r / nty;
+        b = z >> 1;
+        axis = z & 1;
+        tx0 = cx * Gm::TW;
+        ty0 = p.y0 + cy * TH;
+    };
+    auto bufs = [&](int s, float*& G, float2*& S01, float2*& S2) {
+        G = smj8 + s * BUF;
+        S01 = reinterpret_cast<float2*>(G + Gm::ROWS * Gm::GP);
+        S2 = S01 + Gm::ROWS * Gm::SP;
+    };
+    if ((int)threadIdx.x >= NT) {
+        // stagers
+        const int w = threadIdx.x - NT;
+        for (int k = 0; k < ntiles; ++k) {
+            const int s = k & 1;
+            if (k >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + s), "r"(2 * NT) : "memory");
+            int b, axis, tx0, ty0;
+            decode(blockIdx.x + k * gridDim.x, b, axis, tx0, ty0);
+            float* G;
+            float2 *S01, *S2;
+            bufs(s, G, S01, S2);
+            j8_stage<R, TH>(p, G, S01, S2, b, axis, tx0, ty0, w, NT);
+            asm volatile("bar.arrive %0, %1;" ::"r"(1 + s), "r"(2 * NT) : "memory");
+        }
+    } else {
+        // filter warps
+        for (int k = 0; k < ntiles; ++k) {
+            const int s = k & 1;
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "r"(2 * NT) : "memory");
+            int b, axis, tx0, ty0;
+            decode(blockIdx.x + k * gridDim.x, b, axis, tx0, ty0);
+            float* G;
+            float2 *S01, *S2;
+            bufs(s, G, S01, S2);
+            j8_filter<R, TH>(p, G, S01, S2, b, axis, tx0, ty0, threadIdx.x);
+            // the stagers wait for this buffer only before tile k + 2
+            if (k + 2 < ntiles) asm volatile("bar.arrive %0, %1;" ::"r"(3 + s), "r"(2 * NT) : "memory");
+        }
+    }
+}
+
+template <int R, int TH, int MINB, int POLYK = 0>
 static cudaError_t launch_j8_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J8Geom<R, TH>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_j8<R, TH, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j8<R, TH, MINB, POLYK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * batch);
-    k_blf_j8<R, TH, MINB><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_j8<R, TH, MINB, POLYK><<<grid, Gm::NT, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int R, int TH>
+static cudaError_t launch_j8p_t(const BlfParams& p, int batch, int ctas_per_sm, cudaStream_t st)
+{
+    using Gm = J8Geom<R, TH>;
+    constexpr size_t smem = 2 * Gm::smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j8p<R, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int ntx = (p.W + Gm::TW - 1) / Gm::TW, nty = (p.y1 - p.y0 + TH - 1) / TH;
+    const long total = (long)ntx * nty * 2 * batch;
+    if (total > INT32_MAX) return cudaErrorInvalidValue;
+    const int grid = (int)std::min<long>(total, (long)ctas_per_sm * nsm);
+    k_blf_j8p<R, TH><<<grid, 2 * Gm::NT, smem, st>>>(p, ntx, nty, (int)total);
     return cudaGetLastError();
 }
 
 // Shared-gray-guide filter with 8 outputs per thread: factorised exponents
 // only (2 range_coef^2 <= 60) and no peer-storing epilogue; false otherwise
-// (the caller runs k_blf_j3).
+// (the caller runs k_blf_j3).  Experiments build only: on c5 (r02 B200,
+// tools/ab_j8.sh) it measured 0.765 of the MUFU rate against k_blf_j3's
+// 0.820 -- the LDS traffic halves (L1 48% vs 80% of peak) but 128 registers
+// and 50 KB per 4-warp CTA leave 16 warps per SM, and the tile staging
+// (global-load latency, 17% of the stall samples) is no longer hidden;
+// 24 / 32-row tiles 0.81 / 0.80, every 4th..12th exponent pair on the FMA
+// pipe 0.715..0.76, the persistent warp-specialised variant (stager warps
+// fill the next tile while filter warps work) 0.65 at 8 filter warps per SM.
 bool launch_grad_blf_j8(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
 {
-    static const int enabled = knob("BLFLS_J8", 1);
+    static const int enabled = knob("BLFLS_J8", 0);
     static const int th = knob("BLFLS_J8_TH", 16);
+    static const int persistent = knob("BLFLS_J8P", 0);
+    static const int polyk = knob("BLFLS_J8_POLY", 0);
     if (!enabled || p.C != 3 || p.npeers > 0 || !(2.0f * p.range_coef * p.range_coef <= 60.0f)) return false;
+#ifdef BLFLS_EXPERIMENTS
+    if (persistent && p.radius == 7) {
+        *err = launch_j8p_t<7, 16>(p, batch, 2, st);
+        return true;
+    }
+    if (p.radius == 7 && polyk) {
+        switch (polyk) {
+            case 4: *err = th == 24 ? launch_j8_t<7, 24, 3, 4>(p, batch, st) : launch_j8_t<7, 16, 4, 4>(p, batch, st); return true;
+            case 6: *err = th == 24 ? launch_j8_t<7, 24, 3, 6>(p, batch, st) : launch_j8_t<7, 16, 4, 6>(p, batch, st); return true;
+            case 8: *err = th == 24 ? launch_j8_t<7, 24, 3, 8>(p, batch, st) : launch_j8_t<7, 16, 4, 8>(p, batch, st); return true;
+            default: *err = th == 24 ? launch_j8_t<7, 24, 3, 12>(p, batch, st) : launch_j8_t<7, 16, 4, 12>(p, batch, st); return true;
+        }
+    }
+#endif
     switch (p.radius) {
         case 7:
 #ifdef BLFLS_EXPERIMENTS
@@ -302,6 +458,12 @@ bool launch_grad_blf_j8(const BlfParams& p, int batch, cudaStream_t st, cudaErro
         default: return false;
     }
     (void)th;
+    (void)persistent;
+    (void)polyk;
 }
+
+#else
+bool launch_grad_blf_j8(const BlfParams&, int, cudaStream_t, cudaError_t*) { return false; }
+#endif  // BLFLS_EXPERIMENTS
 
 }  // namespace blfls
