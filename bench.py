@@ -75,15 +75,23 @@ def load_traffic(name):
 
 def blf_kernel_name(cfg):
     """The brute-force BLF kernel the library dispatches for this config
-    (k_blf.cu launch_grad_blf: packed shared-guide kernel for a gray guide over
-    RGB, packed self-guided kernel with pair exponents and the FMA-pipe exp2
-    offload at r = 5 / 7 / 15 (k_blf_p2.cu launch_p2), the unpacked kernel
-    otherwise)."""
+    (k_blf.cu launch_grad_blf): the factorised-exponent form whenever
+    2 range_coef^2 <= 60 (range_coef = sqrt(log2 e / (8 sigma_r^2)), i.e.
+    sigma_r >= 0.0775), else the difference form; k_blf_j3 for a gray guide
+    over RGB (r = 3, 5, 7, 15), k_blf_p2 for self-guided r = 5, 7, 15 with
+    the FMA-pipe exp2 offload period of k_blf_p2.cu kP2XfPoly / kP2DefaultPoly,
+    k_grad_blf otherwise."""
+    import math
+    coef2 = math.log2(math.e) / (8.0 * cfg.sigma_r ** 2)
+    xf = 2.0 * coef2 <= 60.0
+    form = "factorised exponents" if xf else "difference-form pair exponents"
     if cfg.guide and cfg.channels == 3 and cfg.radius in (3, 5, 7, 15):
-        return "k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, pair exponents)"
+        return (f"k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, {form}"
+                + (", 4 CTAs/SM)" if xf else ", 2 CTAs/SM)"))
     if not cfg.guide and cfg.radius in (5, 7, 15):
-        return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, pair exponents, "
-                f"FMA-pipe exp2 on every { {5: 10, 15: 8}.get(cfg.radius, 7) }th tap)")
+        period = ({5: 10, 7: 7, 15: 5} if xf else {5: 10, 7: 7, 15: 8})[cfg.radius]
+        return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, "
+                f"{form}, FMA-pipe exp2 on every {period}th tap)")
     return "k_grad_blf (fused gradient + brute-force BLF)"
 
 

@@ -95,8 +95,9 @@ def build(verbose: bool = False, ptxas_info: bool = False, experiments: bool = F
         obj = out_dir / (src.stem + ".o")
         objs.append(obj)
         if _needs(obj, src) or ptxas_info:
-            cmd = [NVCC, *ARCH, *FLAGS, *(["-DBLFLS_EXPERIMENTS"] if experiments else []), "-c", str(src),
-                   "-o", str(obj)]
+            extra = os.environ.get("BLFLS_EXP_DEFINES", "").split() if experiments else []
+            cmd = [NVCC, *ARCH, *FLAGS, *(["-DBLFLS_EXPERIMENTS"] if experiments else []), *extra, "-c",
+                   str(src), "-o", str(obj)]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)

@@ -208,33 +208,8 @@ struct SolveParams {
     float lambda;
     float inv_hw;        // 1 / (H W)
     int mode;            // column pass: 1 fwd, 2 inv, 3 fwd+scale+inv
-    int strip;           // spectrum layout: 0 row-major, 1 column strips (below)
 };
 
-// Offset of spectrum element (row y, column k) of `plane`.  Row-major: H
-// rows of spitch.  Column strips (the full solve): the plane's H x spitch
-// block holds spitch / 16 strips of 16 adjacent columns, each strip H rows x
-// 16 complex (one 128-byte line per row) contiguous.  The row passes still
-// read / write whole 128-byte lines (a warp's 32 consecutive columns = 2
-// lines, as row-major), while a column-pass CTA's V-column slice of a strip
-// is a 128-byte-pitch walk through one contiguous H x 128 B block that the
-// strip's other CTAs (adjacent blockIdx.x, co-resident) read alongside,
-// instead of one 32-byte sector per 8 KB row (row-major at W = 2048).
-// (4-column strips, 32 B per row: column pass 9.26 -> 7.30 ms per c5 step,
-// but the row c2r 4.66 -> 7.68 ms: its warps then touched 8 strips each.)
-constexpr int kSpecStrip = 16;
-__host__ __device__ __forceinline__ size_t spec_at(const SolveParams& p, int plane, int y, int k)
-{
-    const size_t base = (size_t)plane * p.H * p.spitch;
-    return p.strip ? base + (size_t)(k / kSpecStrip) * ((size_t)p.H * kSpecStrip) + (size_t)y * kSpecStrip +
-                         (k % kSpecStrip)
-                   : base + (size_t)y * p.spitch + k;
-}
-// distance between rows y and y + 1 of one spectrum column
-__host__ __device__ __forceinline__ size_t spec_row_stride(const SolveParams& p)
-{
-    return p.strip ? kSpecStrip : (size_t)p.spitch;
-}
 
 // high-radix solve passes (k_solve2.cu): false when no geometry exists for n
 bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, int planes, int nsm,

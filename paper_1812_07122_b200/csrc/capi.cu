@@ -379,11 +379,6 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
     s.out = out;
     s.lohi_out = lohi_out;
     s.mode = 3;
-    // column-strip spectrum (spec_at) -- measured slower overall at c5 (r02:
-    // 4-column strips col 9.26 -> 7.30 ms/step but row c2r 4.66 -> 7.68 and
-    // r2c 8.99 -> 9.61; 16-column strips col 8.82, c2r 7.02, r2c 9.53: the
-    // row passes lose DRAM page locality), so row-major stays the default
-    s.strip = knob("BLFLS_SPEC_STRIP", 0);
     s.plane0 = 0;
     const int grp = p->solve_group;
     if (grp <= 0 || grp >= planes) {

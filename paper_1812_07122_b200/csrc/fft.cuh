@@ -462,14 +462,23 @@ constexpr bool ct_supported(int n)
 // per 8 (rows) / V pad elements per 8*V (columns) spreads them over all banks.
 template <int V>
 constexpr int ct_log2(int v) { return v <= 1 ? 0 : 1 + ct_log2<V>(v / 2); }
-template <int V, bool COLS>
+// Rows of a power-of-two length take one pad slot per 16 complex instead:
+// with 8-byte elements a half-warp's 16 consecutive reads (every stage's
+// inputs and the row epilogues) then stay inside one 128-byte bank line --
+// per 8 they straddle a pad slot and conflict 2-way -- while the stride-8
+// first-stage writes still spread over all banks (c5 row r2c 9.25 -> 8.75
+// ms per step, c4 178 -> 168 us; c3's 960-point rows measured slower, so
+// mixed-radix lengths keep the per-8 pad).
+template <int N>
+constexpr int ct_row_pad_block() { return (N & (N - 1)) == 0 ? 16 : 8; }
+template <int V, bool COLS, int PB = 8>
 __device__ __forceinline__ int ct_pad(int flat)
 {
     if (COLS) {
         constexpr int L = ct_log2<V>(V);
         return flat + ((flat >> (3 + L)) << L);
     }
-    return flat + (flat >> 3);
+    return flat + flat / PB;
 }
 
 template <int N, int V, int TV, bool COLS, bool INV, int P, int S>
@@ -479,17 +488,18 @@ __device__ __forceinline__ void ct_stage(float2* buf, int v, int t, const float2
     constexpr int NB = (NBP + TV - 1) / TV;
     constexpr bool PRED = NB * TV != NBP;
     constexpr float sg = INV ? 1.0f : -1.0f;
-    auto addr = [&](int j) { return ct_pad<V, COLS>(COLS ? j * V + v : v * N + j); };
+    constexpr int PB = COLS ? 8 : ct_row_pad_block<N>();  // elements per pad slot
+    auto addr = [&](int j) { return ct_pad<V, COLS, PB>(COLS ? j * V + v : v * N + j); };
     // ct_pad adds one pad slot per 8 (rows) / per 8 V (columns) elements, so
     // indices j + m D with D a multiple of 8 map to addr(j) + m D (9/8) (x V
     // for columns): the butterfly's P inputs (D = NBP) and, when the stage
     // stride S is a multiple of 8 (or S = 1 with P | 8, outputs inside one
     // 8-block), its P outputs are a base address plus compile-time offsets.
-    constexpr bool LIN_IN = NBP % 8 == 0;
-    constexpr bool LIN_OUT = S % 8 == 0 || (S == 1 && 8 % P == 0);
+    constexpr bool LIN_IN = NBP % PB == 0;
+    constexpr bool LIN_OUT = S % PB == 0 || (S == 1 && PB % P == 0);
     constexpr int VS = COLS ? V : 1;
-    constexpr int STR_IN = LIN_IN ? NBP / 8 * 9 * VS : 0;
-    constexpr int STR_OUT = S == 1 ? VS : (LIN_OUT ? S / 8 * 9 * VS : 0);
+    constexpr int STR_IN = LIN_IN ? NBP / PB * (PB + 1) * VS : 0;
+    constexpr int STR_OUT = S == 1 ? VS : (LIN_OUT ? S / PB * (PB + 1) * VS : 0);
     float2 a[NB][P];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -553,13 +563,13 @@ struct CtFft {
     __device__ __forceinline__ int n() const { return N; }
     __device__ __forceinline__ int vecs() const { return V; }
     template <bool COLS>
-    __device__ __forceinline__ int pad(int flat) const { return ct_pad<V, COLS>(flat); }
+    __device__ __forceinline__ int pad(int flat) const { return ct_pad<V, COLS, COLS ? 8 : ct_row_pad_block<N_>()>(flat); }
     __device__ __forceinline__ int threads() const { return THREADS; }  // compile-time
     static size_t smem_bytes(bool cols)
     {
         const int last = V * N - 1;
         const int L = ct_log2<V>(V);
-        const int padded = cols ? last + ((last >> (3 + L)) << L) : last + (last >> 3);
+        const int padded = cols ? last + ((last >> (3 + L)) << L) : last + last / ct_row_pad_block<N_>();
         return (size_t)(padded + 1) * sizeof(float2);
     }
     template <bool COLS>

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F f
         } else {
             X = buf[fft.template pad<false>(v * n + k)];
         }
-        p.spec[spec_at(p, plane, y, k)] = X;
+        p.spec[((size_t)plane * p.H + y) * p.spitch + k] = X;
     }
 }
 
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
     const int H = fft.n(), V = fft.vecs();  // compile-time for the CT engine
     const int plane = blockIdx.y;
     const int v0 = blockIdx.x * V;
-    const size_t rs = spec_row_stride(p);
+    float2* spec = p.spec + (size_t)plane * H * p.spitch;
     // cp.async (LDGSTS) straight into the padded strip: every copy of the
     // thread is in flight at once instead of one load per loop trip
     for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
         if (v < p.wc) {
             const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
-                         "l"(p.spec + spec_at(p, plane, 0, v) + (size_t)u * rs));
+                         "l"(spec + (size_t)u * p.spitch + v));
         } else {
             *dst = make_float2(0.f, 0.f);
         }
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
     for (int idx = threadIdx.x; idx < V * H; idx += fft.threads()) {
         const int u = idx / V, c = idx - (idx / V) * V;
         const int v = v0 + c;
-        if (v < p.wc) p.spec[spec_at(p, plane, 0, v) + (size_t)u * rs] = buf[fft.template pad<true>(idx)];
+        if (v < p.wc) spec[(size_t)u * p.spitch + v] = buf[fft.template pad<true>(idx)];
     }
 }
 
@@ -201,10 +201,10 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
         const int y = row0 + v;
         float2 Z = make_float2(0.f, 0.f);
         if (y < p.H) {
-            auto srow = [&](int kk) { return p.spec[spec_at(p, plane, y, kk)]; };
+            const float2* srow = p.spec + ((size_t)plane * p.H + y) * p.spitch;
             if (!ODD) {
-                float2 xk = srow(k);
-                float2 xn = srow(n - k);
+                float2 xk = srow[k];
+                float2 xn = srow[n - k];
                 if (k == 0) {  // c2r ignores Im of DC and Nyquist
                     xk.y = 0.f;
                     xn.y = 0.f;
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(1024) k_row_c2r(const SolveParams p, const F f
                 Z = cadd(a, cmuli(bb, 1.0f));
             } else {
                 if (k <= (W - 1) / 2) {
-                    Z = srow(k);
+                    Z = srow[k];
                     if (k == 0) Z.y = 0.f;
                 } else {
-                    Z = cconj(srow(W - k));
+                    Z = cconj(srow[W - k]);
                 }
             }
         }

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_r2c(const SolveParams p, co
         const float2 zn = cconj(buf[G::ra(vv, k == 0 ? 0 : n - k)]);
         const float2 e = cscale(cadd(zk, zn), 0.5f);
         const float2 o = cscale(cmuli(csub(zk, zn), -1.0f), 0.5f);
-        p.spec[spec_at(p, plane, yy, k)] = cadd(e, cmul(__ldg(&p.post[k]), o));
+        p.spec[((size_t)plane * p.H + yy) * p.spitch + k] = cadd(e, cmul(__ldg(&p.post[k]), o));
     }
 }
 
@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(G::THREADS, G::THREADS <= 512 ? 65536 / (64 * 
     const int plane = blockIdx.y;
     const int vc = blockIdx.x * G::V + v;
     const bool live = vc < p.wc;
-    float2* spec = p.spec + spec_at(p, plane, 0, live ? vc : 0);
-    const size_t sp = spec_row_stride(p);
+    float2* spec = p.spec + (size_t)plane * G::N * p.spitch + (live ? vc : 0);
+    const size_t sp = p.spitch;
     auto ldg = [&](int u) -> float2 { return live ? __ldcg(spec + (size_t)u * sp) : make_float2(0.f, 0.f); };
     auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
     auto lds = [&](int u) { return buf[G::ca(v, u)]; };
@@ -163,10 +163,10 @@ __global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
     constexpr int N = G::N, V = G::V, BUF = G::PADN * G::V;
     static_assert(V % 2 == 0, "16-byte chunks of two columns");
     const int v = threadIdx.x % V, t = threadIdx.x / V;
-    const size_t sp = spec_row_stride(p);
+    const size_t sp = p.spitch;
     auto issue = [&](int s, float2* dst) {
         const int plane = s / nsp, c0 = (s - plane * nsp) * V;
-        const float2* src = p.spec + spec_at(p, plane, 0, c0);
+        const float2* src = p.spec + (size_t)plane * N * sp + c0;
         for (int c = threadIdx.x; c < N * V / 2; c += G::THREADS) {
             const int u = c / (V / 2), h = c - u * (V / 2);
             const unsigned d = (unsigned)__cvta_generic_to_shared(dst + G::ca(2 * h, u));
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
         const int plane = s / nsp;
         const int vc = (s - plane * nsp) * V + v;
         const bool live = vc < p.wc;
-        float2* spec = p.spec + spec_at(p, plane, 0, live ? vc : 0);
+        float2* spec = p.spec + (size_t)plane * N * sp + (live ? vc : 0);
         auto lds = [&](int u) { return buf[G::ca(v, u)]; };
         auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
         s2_smem_stages<G, true, false, 0, G::NST>(buf, v, t, tw);
@@ -223,14 +223,13 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, co
     const int plane = blockIdx.y;
     const int y = blockIdx.x * G::V + v;
     const bool live = y < p.H;
-    const int yl = live ? y : 0;
-    auto srow = [&](int kk) { return p.spec + spec_at(p, plane, yl, kk); };
+    const float2* srow = p.spec + ((size_t)plane * p.H + (live ? y : 0)) * p.spitch;
     // Z_k = (X_k + conj X_{n-k}) + i e^{+2 pi i k / W} (X_k - conj X_{n-k}); c2r
     // ignores Im of DC and Nyquist
     auto ldg = [&](int k) -> float2 {
         if (!live) return make_float2(0.f, 0.f);
-        float2 xk = __ldcg(srow(k));
-        float2 xn = __ldcg(srow(n - k));
+        float2 xk = __ldcg(srow + k);
+        float2 xn = __ldcg(srow + (n - k));
         if (k == 0) {
             xk.y = 0.f;
             xn.y = 0.f;
