@@ -296,10 +296,12 @@ def run_reference(args, cfg):
     value = res[0]["mp"] / t
     line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg.name == "c5" else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Voronoi + ramp + noise, BASELINE generator)",
             "impl": "reference",
-            "config": config_json(cfg, 1, {"step": "1 image x 1 iteration (bounded CPU sample)"}),
+            "config": config_json(cfg, args.gpus, {"step": "1 image x 1 iteration (bounded CPU sample)"},
+                                  shard=cfg.name == "c5"),
             "cpu_baseline": {"value": value, "unit": "MP/s", "cores": res[0]["cores"],
                              "kind": res[0]["kind"], "sample": res[0]["sample"],
                              "host": res[0]["host"]},
