@@ -246,9 +246,13 @@ __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* 
         for (int c = 0; c < 3; ++c) {
             const size_t off = ((size_t)b * 3 + c) * pl + orow + ox;
             if constexpr (PEERS) {
+                const bool vec = ox + P <= W && (off & 3) == 0;  // 16-byte peer stores
                 for (int k = 0; k < p.npeers; ++k) {
                     float* d = (axis == 0 ? p.peer_tx[k] : p.peer_ty[k]) + off;
-                    for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[c][q];
+                    if (vec)
+                        *reinterpret_cast<float4*>(d) = make_float4(t[c][0], t[c][1], t[c][2], t[c][3]);
+                    else
+                        for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[c][q];
                 }
             } else if (ox + P <= W && (off & 3) == 0) {
                 *reinterpret_cast<float4*>(dst + off) = make_float4(t[c][0], t[c][1], t[c][2], t[c][3]);

@@ -307,9 +307,15 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
         const size_t off = ((size_t)b * C + c0) * ((size_t)p.out_rows * W) +
                            (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W + ox;
         if constexpr (PEERS) {
+            // one 16-byte store per peer (NVLink writes of whole 16-byte
+            // chunks; P = 4 outputs per thread) where aligned and in range
+            const bool vec = ox + P <= W && (off & 3) == 0;
             for (int k = 0; k < p.npeers; ++k) {
                 float* d = (axis == 0 ? p.peer_tx[k] : p.peer_ty[k]) + off;
-                for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[q];
+                if (vec)
+                    *reinterpret_cast<float4*>(d) = make_float4(t[0], t[1], t[2], t[3]);
+                else
+                    for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[q];
             }
         } else {
             float* dst = (axis == 0 ? p.tx : p.ty) + off;
