@@ -276,6 +276,137 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_c2r(const SolveParams p, co
     if (p.lohi_out != nullptr) block_minmax_atomic2(lo, hi, p.lohi_out + 2 * ((p.plane0 + plane) / p.C));
 }
 
+// ---------------------------------------------------- TMA bulk-copy c2r --
+// Persistent row c2r: CTAs stride over tiles of V spectrum rows (plane-major).
+// The V padded rows of a tile are contiguous in the half spectrum (pitch
+// spitch), so ONE bulk copy (cp.async.bulk, the TMA engine: SASS UBLKCP)
+// moves them into a shared landing buffer, completing on an mbarrier; two
+// landing buffers, so tile k + 1's copy is in flight while tile k is
+// transformed.  Stage 0 then builds the half-length complex rows from shared
+// memory instead of two dependent global loads per element (k2_row_c2r's top
+// stall, 39-47% long-scoreboard at c5).  Same arithmetic and output order as
+// k2_row_c2r: bit-identical images and min/max.
+__device__ __forceinline__ void tma_mbar_init(uint64_t* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_mbar_wait(uint64_t* bar, unsigned parity)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(b), "r"(parity)
+            : "memory");
+    }
+}
+
+template <class G>
+__global__ void __launch_bounds__(G::THREADS, 2) k2_row_c2r_tma(const SolveParams p, const float2* __restrict__ tw,
+                                                            int tiles_per_plane, int total)
+{
+    extern __shared__ __align__(128) float2 smc[];
+    constexpr int n = G::N, V = G::V;
+    const int sp = p.spitch;
+    float2* buf = smc;                                                     // FFT work buffer
+    float2* land = smc + ((G::smem_bytes() / sizeof(float2) + 15) & ~(size_t)15);  // [2][V][spitch]
+    __shared__ __align__(8) uint64_t bar[2];
+    const int v = threadIdx.x / G::TV, t = threadIdx.x - v * G::TV;
+    auto tile_src = [&](int tile, int& plane, int& y0, int& rows) {
+        plane = tile / tiles_per_plane;
+        y0 = (tile - plane * tiles_per_plane) * V;
+        rows = min(V, p.H - y0);
+    };
+    auto issue = [&](int tile, int s) {
+        int plane, y0, rows;
+        tile_src(tile, plane, y0, rows);
+        tma_bulk_g2s(land + (size_t)s * V * sp, p.spec + ((size_t)plane * p.H + y0) * sp,
+                     (unsigned)(rows * sp * sizeof(float2)), &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        tma_mbar_init(&bar[0], 1);
+        tma_mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int tile = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (tile < total) issue(tile, 0);
+        if (tile + (int)gridDim.x < total) issue(tile + gridDim.x, 1);
+    }
+    for (int k = 0; tile < total; ++k, tile += gridDim.x) {
+        const int s = k & 1;
+        int plane, y0, rows;
+        tile_src(tile, plane, y0, rows);
+        const int y = y0 + v;
+        const bool live = v < rows;
+        const float2* srow = land + ((size_t)s * V + v) * sp;
+        auto ld = [&](int kk) -> float2 {
+            if (!live) return make_float2(0.f, 0.f);
+            float2 xk = srow[kk];
+            float2 xn = srow[n - kk];
+            if (kk == 0) {
+                xk.y = 0.f;
+                xn.y = 0.f;
+            }
+            const float2 xnc = cconj(xn);
+            const float2 a = cadd(xk, xnc);
+            const float2 bb = cmul(csub(xk, xnc), cconj(__ldg(&p.post[kk])));
+            return cadd(a, cmuli(bb, 1.0f));
+        };
+        auto sts = [&](int j, float2 z) { buf[G::ra(v, j)] = z; };
+        auto lds = [&](int j) { return buf[G::ra(v, j)]; };
+        float lo = INFINITY, hi = -INFINITY;
+        const int yo = y - p.opad;
+        const bool out_row = live && yo >= 0 && yo < p.oH;
+        float* orow = p.out + (size_t)plane * p.oH * p.oW + (size_t)(out_row ? yo : 0) * p.oW;
+        auto sto = [&](int j, float2 z) {
+            if (!out_row) return;
+            if (p.opad == 0) {
+                *reinterpret_cast<float2*>(orow + 2 * j) = z;
+                lo = fminf(lo, fminf(z.x, z.y));
+                hi = fmaxf(hi, fmaxf(z.x, z.y));
+            } else {
+                const int x0 = 2 * j - p.opad;
+                if (x0 >= 0 && x0 < p.oW) {
+                    orow[x0] = z.x;
+                    lo = fminf(lo, z.x);
+                    hi = fmaxf(hi, z.x);
+                }
+                if (x0 + 1 >= 0 && x0 + 1 < p.oW) {
+                    orow[x0 + 1] = z.y;
+                    lo = fminf(lo, z.y);
+                    hi = fmaxf(hi, z.y);
+                }
+            }
+        };
+        tma_mbar_wait(&bar[s], (k >> 1) & 1);
+        s2_stage<G, true, 0, false>(t, tw, ld, sts);
+        __syncthreads();  // landing[s] consumed, buffer written
+        if (threadIdx.x == 0 && tile + 2 * (int)gridDim.x < total) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(tile + 2 * gridDim.x, s);
+        }
+        s2_smem_stages<G, false, true, 1, G::NST - 1>(buf, v, t, tw);
+        s2_stage<G, true, G::NST - 1, false>(t, tw, lds, sto);
+        if (p.lohi_out != nullptr) block_minmax_atomic2(lo, hi, p.lohi_out + 2 * ((p.plane0 + plane) / p.C));
+        __syncthreads();  // buf reads of the last stage done before the next tile's stage 0
+    }
+}
+
 // ------------------------------------------------------------ launchers --
 
 // Row geometries (N = W/2, V rows, TV threads per row, PMAX) and column
@@ -352,6 +483,33 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
         set_smem2(k2_row_r2c<G>, smem);
         k2_row_r2c<G><<<grid, G::THREADS, smem, st>>>(p, tw);
     } else {
+        // the TMA-fed persistent c2r for streaming workloads (spectra beyond
+        // L2, power-of-two rows of a multi-stage geometry): BLFLS_C2R_TMA
+        static const int tma = knob("BLFLS_C2R_TMA", 1);
+        const size_t spec_bytes = (size_t)planes * p.H * p.spitch * sizeof(float2);
+        if constexpr (G::NST > 1) {
+            if (tma && spec_bytes > ((size_t)64 << 20)) {
+                const size_t land = (size_t)2 * G::V * p.spitch * sizeof(float2);
+                const size_t sm2 = ((smem + 127) & ~(size_t)127) + land;
+                int occ = 0, dev = 0, nsm = 148, optin = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+                if (sm2 <= (size_t)optin &&
+                    cudaFuncSetAttribute(k2_row_c2r_tma<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm2) == cudaSuccess &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_row_c2r_tma<G>, G::THREADS, sm2) ==
+                        cudaSuccess &&
+                    occ > 0) {
+                    const int tpp = (p.H + G::V - 1) / G::V;
+                    const long total = (long)tpp * planes;
+                    const int grid = (int)std::min<long>(total, (long)occ * nsm);
+                    k2_row_c2r_tma<G><<<grid, G::THREADS, sm2, st>>>(p, tw, tpp, (int)total);
+                    return;
+                }
+                (void)cudaGetLastError();
+            }
+        }
         dim3 grid((p.H + G::V - 1) / G::V, planes);
         set_smem2(k2_row_c2r<G>, smem);
         k2_row_c2r<G><<<grid, G::THREADS, smem, st>>>(p, tw);

@@ -111,3 +111,23 @@ def test_exponent_form_switch_vs_oracle(gpu, oracle, side, kind, pattern):
     ref = oracle.blf_ls(img32.astype(np.float64), None if guide is None else g32.astype(np.float64),
                         lam=1000.0, sigma_s=7.0, sigma_r=sr, iters=2, radius=r)
     assert maxabs(out, ref) <= TOL_OUT
+
+
+def test_tma_c2r_matches_plain_c2r(gpu, oracle):
+    """The row c2r pass streams its spectrum rows through TMA bulk copies
+    (k2_row_c2r_tma) when a launch's spectra exceed 64 MB: 10 planes of
+    2048^2 (166 MB) -> TMA pass; the same planes two at a time (33 MB) ->
+    k2_row_c2r.  Bit-identical images (and hence the fused min/max)."""
+    import torch
+    h = w = 2048
+    rng = np.random.default_rng(11)
+    g = torch.from_numpy(rng.random((10, 1, h, w), dtype=np.float32)).cuda()
+    tx = (torch.rand_like(g) - 0.5) * 0.1
+    ty = (torch.rand_like(g) - 0.5) * 0.1
+    big = gpu.lsgrad_solve_fft(g, (tx, ty), gpu.SolveParams(1000.0, 0))
+    for i in range(0, 10, 2):
+        small = gpu.lsgrad_solve_fft(g[i:i + 2].contiguous(), (tx[i:i + 2].contiguous(), ty[i:i + 2].contiguous()),
+                                     gpu.SolveParams(1000.0, 0))
+        assert torch.equal(small, big[i:i + 2]), i
+    ref = oracle.lsgrad_solve_fft(g[3].cpu().numpy(), tx[3].cpu().numpy(), ty[3].cpu().numpy(), lam=1000.0)
+    assert maxabs(big[3].cpu().numpy(), ref) <= 5e-5
