@@ -559,13 +559,14 @@ __device__ __forceinline__ void ct_stages(float2* buf, int v, int t, const float
 template <int N_, int V_, int TV_>
 struct CtFft {
     static constexpr int N = N_, V = V_, TV = TV_, THREADS = V_ * TV_;
+    static constexpr bool kCompileTime = true;
     const float2* tw;
     __device__ __forceinline__ int n() const { return N; }
     __device__ __forceinline__ int vecs() const { return V; }
     template <bool COLS>
     __device__ __forceinline__ int pad(int flat) const { return ct_pad<V, COLS, COLS ? 8 : ct_row_pad_block<N_>()>(flat); }
     __device__ __forceinline__ int threads() const { return THREADS; }  // compile-time
-    static size_t smem_bytes(bool cols)
+    __host__ __device__ static constexpr size_t smem_bytes(bool cols)
     {
         const int last = V * N - 1;
         const int L = ct_log2<V>(V);
@@ -586,6 +587,7 @@ struct CtFft {
 
 template <int E, bool GENERIC>
 struct RtFft {
+    static constexpr bool kCompileTime = false;
     FftDesc d;
     int V, log2V;
     __device__ __forceinline__ int n() const { return d.n; }

@@ -110,6 +110,135 @@ __global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F f
     }
 }
 
+// ------------------------------------------------ TMA bulk-copy row r2c --
+// Persistent row r2c (even W, W % 4 == 0, targets present) for streaming
+// solves: a tile is V rows of one plane.  Its inputs are contiguous rows --
+// f and Tx rows [y0, y0 + V), Ty rows [y0 - 1, y0 + V) (row H - 1 for the
+// circular Ty[y - 1] of row 0) -- so three or four bulk copies (the TMA
+// engine, SASS UBLKCP) land them in shared memory, completing on an mbarrier.
+// One landing buffer: the next tile's copies are issued as soon as this
+// tile's fold has read it, so they fly during the FFT and the spectrum
+// stores.  The fold reads shared memory instead of four dependent float4
+// global loads per 4 pixels (k_row_r2c's top stall, 27% long-scoreboard at
+// c5).  Same arithmetic and order as k_row_r2c: bit-identical spectra.
+__device__ __forceinline__ void r2c_mbar_init(uint64_t* bar)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void r2c_bulk(void* dst, const void* src, unsigned bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void r2c_expect(uint64_t* bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void r2c_wait(uint64_t* bar, unsigned parity)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(b), "r"(parity)
+            : "memory");
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(1024) k_row_r2c_tma(const SolveParams p, const F fft, int tiles_per_plane,
+                                                      int total)
+{
+    extern __shared__ __align__(128) float2 buf[];
+    constexpr int n = F::N, V = F::V, W = 2 * F::N;
+    // landing rows after the FFT buffer: f [V][W], tx [V][W], ty [V + 1][W]
+    float* land = reinterpret_cast<float*>(buf) + ((F::smem_bytes(false) / sizeof(float) + 31) & ~(size_t)31);
+    float* lf = land;
+    float* ltx = land + V * W;
+    float* lty = land + 2 * V * W;  // row 0 = Ty[y0 - 1]
+    __shared__ __align__(8) uint64_t bar;
+    auto tile_of = [&](int tile, int& plane, int& y0, int& rows) {
+        plane = tile / tiles_per_plane;
+        y0 = (tile - plane * tiles_per_plane) * V;
+        rows = min(V, p.H - y0);
+    };
+    auto issue = [&](int tile) {  // one thread
+        int plane, y0, rows;
+        tile_of(tile, plane, y0, rows);
+        const size_t po = (size_t)plane * p.H * W;
+        const unsigned rb = (unsigned)(rows * W * sizeof(float)), wb = (unsigned)(W * sizeof(float));
+        r2c_expect(&bar, 3 * rb + wb);
+        r2c_bulk(lf, p.f + po + (size_t)y0 * W, rb, &bar);
+        r2c_bulk(ltx, p.tx + po + (size_t)y0 * W, rb, &bar);
+        if (y0 > 0) {
+            r2c_bulk(lty, p.ty + po + (size_t)(y0 - 1) * W, rb + wb, &bar);
+        } else {
+            r2c_bulk(lty, p.ty + po + (size_t)(p.H - 1) * W, wb, &bar);
+            r2c_bulk(lty + W, p.ty + po, rb, &bar);
+        }
+    };
+    if (threadIdx.x == 0) {
+        r2c_mbar_init(&bar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int tile = blockIdx.x;
+    if (threadIdx.x == 0 && tile < total) issue(tile);
+    for (int k = 0; tile < total; ++k, tile += gridDim.x) {
+        int plane, y0, rows;
+        tile_of(tile, plane, y0, rows);
+        r2c_wait(&bar, k & 1);
+        // fold r = f + lambda (Dx^T Tx + Dy^T Ty), 4 pixels (2 complex) per thread
+        constexpr int w4 = W / 4;
+        const float L = p.lambda;
+#pragma unroll
+        for (int e = threadIdx.x; e < V * w4; e += F::THREADS) {
+            const int v = e / w4, x4 = e - v * w4;
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (v < rows) {
+                const int o = v * W + 4 * x4;
+                r = *reinterpret_cast<const float4*>(lf + o);
+                const float4 a = *reinterpret_cast<const float4*>(ltx + o);
+                const float4 b = *reinterpret_cast<const float4*>(lty + W + o);
+                const float4 c = *reinterpret_cast<const float4*>(lty + o);
+                const float am = ltx[v * W + (x4 == 0 ? W - 1 : 4 * x4 - 1)];
+                r.x = fmaf(L, (am - a.x) + (c.x - b.x), r.x);
+                r.y = fmaf(L, (a.x - a.y) + (c.y - b.y), r.y);
+                r.z = fmaf(L, (a.y - a.z) + (c.z - b.z), r.z);
+                r.w = fmaf(L, (a.z - a.w) + (c.w - b.w), r.w);
+            }
+            const int j = v * n + 2 * x4;
+            buf[fft.template pad<false>(j)] = make_float2(r.x, r.y);
+            buf[fft.template pad<false>(j + 1)] = make_float2(r.z, r.w);
+        }
+        __syncthreads();  // landing consumed: the next tile's copies may land now
+        if (threadIdx.x == 0 && tile + (int)gridDim.x < total) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(tile + gridDim.x);
+        }
+        fft.template run<false>(buf, false);
+        const int wc = p.wc;
+        for (int idx = threadIdx.x; idx < V * wc; idx += F::THREADS) {
+            const int v = idx / wc, kk = idx - (idx / wc) * wc;
+            const int y = y0 + v;
+            if (v >= rows) continue;
+            const float2 zk = buf[fft.template pad<false>(v * n + (kk == n ? 0 : kk))];
+            const float2 zn = cconj(buf[fft.template pad<false>(v * n + (kk == 0 ? 0 : n - kk))]);
+            const float2 e = cscale(cadd(zk, zn), 0.5f);
+            const float2 o = cscale(cmuli(csub(zk, zn), -1.0f), 0.5f);
+            p.spec[((size_t)plane * p.H + y) * p.spitch + kk] = cadd(e, cmul(__ldg(&p.post[kk]), o));
+        }
+        __syncthreads();  // buf reads done before the next fold writes it
+    }
+}
+
 // grid: (ceil(wc / V), planes); V adjacent columns per CTA, layout buf[u*V + c]
 template <class F>
 __global__ void __launch_bounds__(1024) k_col(const SolveParams p, const F fft)
@@ -437,6 +566,36 @@ static void launch_pass(int which, const SolveParams& p, const F& f, int V, int 
         return;
     }
     dim3 grid((p.H + V - 1) / V, planes);
+#ifdef BLFLS_EXPERIMENTS
+    if constexpr (F::kCompileTime) {
+        // the TMA-fed persistent r2c (experiments build, BLFLS_R2C_TMA=1):
+        // measured slower than k_row_r2c (r02 B200: c5 9.22 vs 8.83 ms per
+        // step, c4 175 vs 164 us) -- the 56 KB landing rows leave 3 CTAs per
+        // SM where k_row_r2c runs 6, and its global loads were not the limit
+        // (issue 70% active)
+        static const int tma = knob("BLFLS_R2C_TMA", 0);
+        const size_t in_bytes = (size_t)planes * p.H * p.W * 3 * sizeof(float);
+        if (which == 0 && !odd && tma && p.tx != nullptr && (p.W % 4) == 0 && in_bytes > ((size_t)128 << 20)) {
+            const size_t sm2 = ((smem + 127) & ~(size_t)127) + (size_t)(3 * F::V + 1) * p.W * sizeof(float);
+            int occ = 0, dev = 0, nsm = 148, optin = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            if (sm2 <= (size_t)optin &&
+                cudaFuncSetAttribute(k_row_r2c_tma<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2) ==
+                    cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_r2c_tma<F>, threads, sm2) == cudaSuccess &&
+                occ > 0) {
+                const int tpp = (p.H + V - 1) / V;
+                const long total = (long)tpp * planes;
+                const int g = (int)std::min<long>(total, (long)occ * nsm);
+                k_row_r2c_tma<F><<<g, threads, sm2, st>>>(p, f, tpp, (int)total);
+                return;
+            }
+            (void)cudaGetLastError();
+        }
+    }
+#endif
     if (which == 0) {
         if (odd) { set_smem(k_row_r2c<true, F>, smem); k_row_r2c<true, F><<<grid, threads, smem, st>>>(p, f); }
         else { set_smem(k_row_r2c<false, F>, smem); k_row_r2c<false, F><<<grid, threads, smem, st>>>(p, f); }

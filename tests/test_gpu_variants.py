@@ -113,11 +113,12 @@ def test_exponent_form_switch_vs_oracle(gpu, oracle, side, kind, pattern):
     assert maxabs(out, ref) <= TOL_OUT
 
 
-def test_tma_c2r_matches_plain_c2r(gpu, oracle):
-    """The row c2r pass streams its spectrum rows through TMA bulk copies
+def test_tma_row_c2r_matches_plain(gpu, oracle):
+    """The row c2r streams its spectrum rows through TMA bulk copies
     (k2_row_c2r_tma) when a launch's spectra exceed 64 MB: 10 planes of
-    2048^2 (166 MB) -> TMA pass; the same planes two at a time (33 MB) ->
-    k2_row_c2r.  Bit-identical images (and hence the fused min/max)."""
+    2048^2 (166 MB of spectra) -> the TMA pass; the same planes two at a
+    time (33 MB) -> k2_row_c2r.  Bit-identical images (and hence the fused
+    min/max)."""
     import torch
     h = w = 2048
     rng = np.random.default_rng(11)
