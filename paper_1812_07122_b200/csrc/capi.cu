@@ -533,8 +533,19 @@ blfls_status enq_run(blfls_plan_t p, const float* in, const float* guide, float*
         r = enq_minmax(p, guide, (size_t)p->prm.guide_channels * p->plane, batch, p->glohi, st);
         if (r) return r;
     }
-    r = enq_minmax(p, in, per_image, batch, p->lohi, st);
-    if (r) return r;
+    // The image's own (lo, hi) (normalize_to_unit, image.cpp:46-60) only
+    // enters the range kernel when the image guides itself: the solve is
+    // affine-equivariant (den(0,0) = 1, conj(otf)(0) = 0), so with a separate
+    // guide the normalise / denormalise pair cancels exactly and the
+    // brute-force kernels never read it (the grid / DT backends normalise the
+    // image like the reference and do).  Skipped for guided brute force: the
+    // iteration-1 min/max pass (c5: 3.2 GB, 0.5 ms per step) and the c2r
+    // epilogue's reductions.
+    const bool need_range = !(p->prm.backend == BLFLS_BACKEND_BRUTE && p->prm.guide_channels > 0);
+    if (need_range) {
+        r = enq_minmax(p, in, per_image, batch, p->lohi, st);
+        if (r) return r;
+    }
     const float* g_use = guide;
     if (guide && p->pad > 0) {  // pipelines.cpp:82-83: the guide is padded once
         CK(launch_reflect_pad(guide, p->gpad, p->prm.height, p->prm.width, p->pad,
@@ -547,7 +558,7 @@ blfls_status enq_run(blfls_plan_t p, const float* in, const float* guide, float*
         const bool last = k == iters - 1;
         float* nxt = last ? out : p->buf[k & 1];
         uint32_t* lo_cur = p->lohi + (size_t)(k & 1) * 2 * mb;
-        uint32_t* lo_nxt = last ? nullptr : p->lohi + (size_t)((k + 1) & 1) * 2 * mb;
+        uint32_t* lo_nxt = (last || !need_range) ? nullptr : p->lohi + (size_t)((k + 1) & 1) * 2 * mb;
         const float* f = cur;
         if (p->pad > 0) {  // pipelines.cpp:76-78: reflect-pad every smooth() input
             CK(launch_reflect_pad(cur, p->fpad, p->prm.height, p->prm.width, p->pad,
