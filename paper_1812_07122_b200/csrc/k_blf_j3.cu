@@ -46,6 +46,34 @@ __device__ __forceinline__ float2 j3_unpack(unsigned long long r)
     asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
     return v;
 }
+// exp2 of both lanes of an f32x2 pair on the FMA pipe (XF exponents lie in
+// [-2 coef^2 + cs_min, 2 coef^2], inside [-125, 60]: no clamping): split
+// x = j + f by the 1.5 * 2^23 shifter, degree-5 polynomial for 2^f (rel. err
+// 2.3e-7, the coefficients of k_blf.cu poly_ex2), 2^j by an exponent add
+__device__ __forceinline__ float2 j3_poly_ex2x2(unsigned long long x)
+{
+    unsigned long long t, jj, f, pp, magic, c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(magic) : "f"(12582912.0f));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(x), "l"(magic));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(jj) : "l"(t), "l"(magic));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(jj));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(pp) : "f"(0.001327647129073739f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.009675541892647743f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.05550713092088699f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.24022120237350464f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.6931469440460205f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(1.0000001192092896f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    float2 tv, pv;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(tv.x), "=f"(tv.y) : "l"(t));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(pv.x), "=f"(pv.y) : "l"(pp));
+    return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                       __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
+}
 // 16-byte chunk swizzle of the interleaved source rows: a thread's 4 output
 // columns make consecutive lanes read chunks 2 apart, so quarter-warps would
 // hit each 128-byte bank line twice; flipping bit 0 of the chunk index in
@@ -91,7 +119,7 @@ struct J3Geom {
 // is folded into the staged sources of column t (G holds b), exp2(-a^2)
 // multiplies numerator and normaliser of output s alike and cancels, so one
 // FFMA2 per output pair and tap forms both exponents: e = {2a_q, 2a_q+1} b + cs
-template <int R, int TH, bool PEERS, bool PX, bool XF, class Hook>
+template <int R, int TH, bool PEERS, bool PX, bool XF, int POLYK, class Hook>
 __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* __restrict__ G,
                                                const float2* __restrict__ S01, const float2* __restrict__ S2,
                                                int b, int axis, int tx0, int ty0, float range, Hook&& row_hook)
@@ -162,16 +190,24 @@ __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* 
                             asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
                             asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
                         }
-                        const float2 ee = j3_unpack(e);
+                        // POLYK > 0 (XF): every POLYK-th exponent pair on the FMA pipe
+                        constexpr int PK = POLYK > 0 ? POLYK : 1;
+                        const bool poly = XF && POLYK > 0 && ok0 && ok1 && (j * (P / 2) + h) % PK == PK - 1;
+                        float2 ww;
+                        if (poly) {
+                            ww = j3_poly_ex2x2(e);
+                        } else {
+                            const float2 ee = j3_unpack(e);
+                            ww.x = ok0 ? j3_ex2(ee.x) : 0.f;
+                            ww.y = ok1 ? j3_ex2(ee.y) : 0.f;
+                        }
                         if (ok0) {
-                            const float w = j3_ex2(ee.x);
-                            r01[q0] = j3_ffma2(w, v01[u], r01[q0]);
-                            r2z[q0] = j3_ffma2(w, v2z[u], r2z[q0]);
+                            r01[q0] = j3_ffma2(ww.x, v01[u], r01[q0]);
+                            r2z[q0] = j3_ffma2(ww.x, v2z[u], r2z[q0]);
                         }
                         if (ok1) {
-                            const float w = j3_ex2(ee.y);
-                            r01[q0 + 1] = j3_ffma2(w, v01[u], r01[q0 + 1]);
-                            r2z[q0 + 1] = j3_ffma2(w, v2z[u], r2z[q0 + 1]);
+                            r01[q0 + 1] = j3_ffma2(ww.y, v01[u], r01[q0 + 1]);
+                            r2z[q0 + 1] = j3_ffma2(ww.y, v2z[u], r2z[q0 + 1]);
                         }
                     }
                 }
@@ -269,7 +305,7 @@ __device__ __forceinline__ void j3_filter_tile(const BlfParams& p, const float* 
 // into the full-height buffers of all p.npeers ranks (NVLink peer pointers)
 // PX: guide difference and exponent of two adjacent outputs as one FFMA2
 // each (column-spatial pair table p.cep, row factor on per-row partial sums)
-template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false>
+template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false, int POLYK = 0>
 __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
 {
     using Gm = J3Geom<R, TH>;
@@ -330,19 +366,19 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_j3(const BlfParams p)
     }
     __syncthreads();
 
-    j3_filter_tile<R, TH, PEERS, PX, XF>(p, G, S01, S2, b, axis, tx0, ty0, range, [](int) {});
+    j3_filter_tile<R, TH, PEERS, PX, XF, POLYK>(p, G, S01, S2, b, axis, tx0, ty0, range, [](int) {});
 }
 
-template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false>
+template <int R, int TH, bool PEERS, int MINB, bool PX = false, bool XF = false, int POLYK = 0>
 static cudaError_t launch_j3_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J3Geom<R, TH>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB, PX, XF>,
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j3<R, TH, PEERS, MINB, PX, XF, POLYK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + TH - 1) / TH, 2 * batch);
-    k_blf_j3<R, TH, PEERS, MINB, PX, XF><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_j3<R, TH, PEERS, MINB, PX, XF, POLYK><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -369,6 +405,18 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
     static const int xf = knob("BLFLS_J3_XF", 1);
     const bool use_xf = xf != 0 && px == 2 && 2.0f * p.range_coef * p.range_coef <= 60.0f;
     if (p.npeers > 0 && use_xf) return launch_j3_t<R, TH, true, 4, true, true>(p, batch, st);
+#ifdef BLFLS_EXPERIMENTS
+    static const int polyk = knob("BLFLS_J3_POLY", 0);
+    if (use_xf && polyk) {
+        switch (polyk) {
+            case 4: return launch_j3_t<R, TH, false, 4, true, true, 4>(p, batch, st);
+            case 6: return launch_j3_t<R, TH, false, 4, true, true, 6>(p, batch, st);
+            case 8: return launch_j3_t<R, TH, false, 4, true, true, 8>(p, batch, st);
+            case 12: return launch_j3_t<R, TH, false, 4, true, true, 12>(p, batch, st);
+            default: return launch_j3_t<R, TH, false, 3, true, true, 6>(p, batch, st);  // 3 CTAs/SM
+        }
+    }
+#endif
     if (use_xf) return launch_j3_t<R, TH, false, 4, true, true>(p, batch, st);
     if (p.npeers > 0) return launch_j3_t<R, TH, true, 2, true>(p, batch, st);
 #ifdef BLFLS_EXPERIMENTS
