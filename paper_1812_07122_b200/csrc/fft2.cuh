@@ -46,6 +46,16 @@ constexpr Plan2 c2_plan(int N, int PMAX)
     return s;
 }
 
+// the same radices in reverse order (the inverse column transform of the
+// fused forward / inverse pass, s2_fwd_last_inv_first)
+constexpr Plan2 c2_reverse(Plan2 p)
+{
+    Plan2 r{};
+    r.n = p.n;
+    for (int i = 0; i < p.n; ++i) r.r[i] = p.r[p.n - 1 - i];
+    return r;
+}
+
 // first factor of an in-register composite DFT of P points
 constexpr int c2_split(int P)
 {
@@ -143,10 +153,12 @@ __device__ __forceinline__ void dft_reg(float2 (&a)[P])
 // radices <= PMAX.  Shared layout (one pad slot per 2^LG elements):
 //   rows:    element j of vector v at v * RS + j + (j >> LG)
 //   columns: element u of vector v at (u + (u >> LG)) * V + v
-template <int N_, int V_, int TV_, int PMAX_>
+template <int N_, int V_, int TV_, int PMAX_, bool REV_ = false>
 struct Fft2 {
     static constexpr int N = N_, V = V_, TV = TV_, THREADS = V_ * TV_, PMAX = PMAX_;
-    static constexpr Plan2 plan = c2_plan(N_, PMAX_);
+    static constexpr Plan2 fplan = c2_plan(N_, PMAX_);
+    static constexpr Plan2 plan = REV_ ? c2_reverse(fplan) : fplan;
+    using Rev = Fft2<N_, V_, TV_, PMAX_, !REV_>;
     static constexpr int NST = plan.n;
     static constexpr int radix(int i) { return plan.r[i]; }
     static constexpr int stride(int i)
@@ -155,7 +167,7 @@ struct Fft2 {
         for (int k = 0; k < i; ++k) s *= plan.r[k];
         return s;
     }
-    static constexpr int LG = plan.r[0] <= 16 ? 4 : 5;
+    static constexpr int LG = fplan.r[0] <= 16 ? 4 : 5;  // one layout for both radix orders
     static constexpr int PADN = N_ + (N_ >> LG) + 1;  // padded vector length
     __device__ static __forceinline__ int ra(int v, int j) { return v * PADN + j + (j >> LG); }
     __device__ static __forceinline__ int ca(int v, int u) { return (u + (u >> LG)) * V_ + v; }
@@ -221,6 +233,74 @@ __device__ __forceinline__ void s2_stage(int t, const float2* __restrict__ tw, L
                         const float2 w = tt < 8 ? wl[tt] : (tt % 8 == 0 ? wh : cmul(wh, wl[tt % 8]));
                         st(obase + S * tt, cmul(a[i][tt], w));
                     }
+                }
+            }
+        }
+    }
+}
+
+// The last stage of a forward transform on plan G fused with the first stage
+// of the inverse on the reversed plan G::Rev.  Stockham's last stage maps
+// the inputs {bb + r N/P} of butterfly bb to the outputs {bb + t N/P}, and
+// the reversed plan's first stage (same radix P, stride 1) reads exactly
+// {bb + r N/P} for the same bb: the thread keeps its butterflies in
+// registers across the two stages, applying scale(u) to element u in
+// between, instead of a shared-memory round trip and a barrier.  ld reads
+// the forward's input u (shared memory), st stores the inverse stage-0
+// output o.  The caller syncs before and after (in-place buffer).
+template <class G, class Ld, class Sc, class St>
+__device__ __forceinline__ void s2_fwd_last_inv_first(int t, const float2* __restrict__ tw, Ld&& ld, Sc&& scale,
+                                                      St&& st)
+{
+    using R = typename G::Rev;
+    constexpr int N = G::N, TV = G::TV;
+    constexpr int P = G::radix(G::NST - 1);
+    static_assert(R::radix(0) == P && R::stride(0) == 1 && G::stride(G::NST - 1) * P == N, "reversed plan");
+    constexpr int NBP = N / P;
+    constexpr int NB = (NBP + TV - 1) / TV;
+    constexpr bool PRED = NB * TV != NBP;
+    float2 a[NB][P];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int bb = t + i * TV;
+        if (!PRED || bb < NBP) {
+#pragma unroll
+            for (int r = 0; r < P; ++r) a[i][r] = ld(bb + r * NBP);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int bb = t + i * TV;
+        if (!PRED || bb < NBP) {
+            dft_reg<P, false>(a[i]);  // forward: y[bb + t N/P] = a[i][t]
+#pragma unroll
+            for (int r = 0; r < P; ++r) a[i][r] = cscale(a[i][r], scale(bb + r * NBP));
+            dft_reg<P, true>(a[i]);  // inverse stage 0 (stride 1): q = bb, outputs P bb + t
+            const int obase = P * bb;
+            st(obase, a[i][0]);
+            float2 w1 = __ldg(&tw[bb]);
+            w1.y = -w1.y;
+            if constexpr (P <= 8) {
+                float2 wt = w1;
+#pragma unroll
+                for (int tt = 1; tt < P; ++tt) {
+                    st(obase + tt, cmul(a[i][tt], wt));
+                    if (tt + 1 < P) wt = cmul(wt, w1);
+                }
+            } else {
+                float2 wl[8];
+                wl[1] = w1;
+#pragma unroll
+                for (int b = 2; b < 8; ++b) wl[b] = cmul(wl[b - 1], w1);
+                float2 w8 = __ldg(&tw[8 * bb]);
+                w8.y = -w8.y;
+                float2 wh = w8;
+#pragma unroll
+                for (int tt = 1; tt < P; ++tt) {
+                    if (tt >= 16 && tt % 8 == 0) wh = cmul(wh, w8);
+                    const float2 w = tt < 8 ? wl[tt] : (tt % 8 == 0 ? wh : cmul(wh, wl[tt % 8]));
+                    st(obase + tt, cmul(a[i][tt], w));
                 }
             }
         }

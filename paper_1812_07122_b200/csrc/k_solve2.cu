@@ -119,23 +119,29 @@ __global__ void __launch_bounds__(G::THREADS, G::THREADS <= 512 ? 65536 / (64 * 
     auto lds = [&](int u) { return buf[G::ca(v, u)]; };
     s2_stage<G, false, 0, false>(t, tw, ldg, sts);
     __syncthreads();
-    s2_smem_stages<G, true, false, 1, G::NST>(buf, v, t, tw);
     const float gx = live ? __ldg(&p.gain_x[vc]) : 0.f;
     const float L = p.lambda, ihw = p.inv_hw;
-    auto lds_scaled = [&](int u) {
-        const float sc = ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f));
-        return cscale(buf[G::ca(v, u)], sc);
-    };
     auto stg = [&](int u, float2 z) {
         if (live) spec[(size_t)u * sp] = z;
     };
     if constexpr (G::NST == 1) {
+        s2_smem_stages<G, true, false, 1, G::NST>(buf, v, t, tw);
+        auto lds_scaled = [&](int u) {
+            const float sc = ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f));
+            return cscale(buf[G::ca(v, u)], sc);
+        };
         s2_stage<G, true, 0, false>(t, tw, lds_scaled, stg);
     } else {
-        s2_stage<G, true, 0, true>(t, tw, lds_scaled, sts);
+        // forward stages 1 .. NST-2 in shared memory, then the forward's last
+        // stage and the inverse's first (reversed radix order) in registers
+        // with 1 / (H W den) in between (fft2.cuh s2_fwd_last_inv_first)
+        using R = typename G::Rev;
+        s2_smem_stages<G, true, false, 1, G::NST - 1>(buf, v, t, tw);
+        auto scale = [&](int u) { return ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f)); };
+        s2_fwd_last_inv_first<G>(t, tw, lds, scale, sts);
         __syncthreads();
-        s2_smem_stages<G, true, true, 1, G::NST - 1>(buf, v, t, tw);
-        s2_stage<G, true, G::NST - 1, false>(t, tw, lds, stg);
+        s2_smem_stages<R, true, true, 1, R::NST - 1>(buf, v, t, tw);
+        s2_stage<R, true, R::NST - 1, false>(t, tw, lds, stg);
     }
 }
 
@@ -191,23 +197,26 @@ __global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
         float2* spec = p.spec + (size_t)plane * N * sp + (live ? vc : 0);
         auto lds = [&](int u) { return buf[G::ca(v, u)]; };
         auto sts = [&](int u, float2 z) { buf[G::ca(v, u)] = z; };
-        s2_smem_stages<G, true, false, 0, G::NST>(buf, v, t, tw);
         const float gx = live ? __ldg(&p.gain_x[vc]) : 0.f;
         const float L = p.lambda, ihw = p.inv_hw;
-        auto lds_scaled = [&](int u) {
-            const float sc = ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f));
-            return cscale(buf[G::ca(v, u)], sc);
-        };
         auto stg = [&](int u, float2 z) {
             if (live) spec[(size_t)u * sp] = z;
         };
         if constexpr (G::NST == 1) {
+            s2_smem_stages<G, true, false, 0, G::NST>(buf, v, t, tw);
+            auto lds_scaled = [&](int u) {
+                const float sc = ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f));
+                return cscale(buf[G::ca(v, u)], sc);
+            };
             s2_stage<G, true, 0, true>(t, tw, lds_scaled, stg);
         } else {
-            s2_stage<G, true, 0, true>(t, tw, lds_scaled, sts);
+            using R = typename G::Rev;
+            s2_smem_stages<G, true, false, 0, G::NST - 1>(buf, v, t, tw);
+            auto scale = [&](int u) { return ihw * __frcp_rn(fmaf(L, __ldg(&p.gain_y[u]) + gx, 1.0f)); };
+            s2_fwd_last_inv_first<G>(t, tw, lds, scale, sts);
             __syncthreads();
-            s2_smem_stages<G, true, true, 1, G::NST - 1>(buf, v, t, tw);
-            s2_stage<G, true, G::NST - 1, false>(t, tw, lds, stg);
+            s2_smem_stages<R, true, true, 1, R::NST - 1>(buf, v, t, tw);
+            s2_stage<R, true, R::NST - 1, false>(t, tw, lds, stg);
         }
         __syncthreads();  // buf free for the copies of strip s + 2 gridDim.x
     }
