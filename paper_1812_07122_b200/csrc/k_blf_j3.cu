@@ -404,7 +404,7 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
     // epilogue uses the same arithmetic as the plain band filter.
     static const int xf = knob("BLFLS_J3_XF", 1);
     const bool use_xf = xf != 0 && px == 2 && 2.0f * p.range_coef * p.range_coef <= 60.0f;
-    if (p.npeers > 0 && use_xf) return launch_j3_t<R, TH, true, 4, true, true>(p, batch, st);
+    if (p.npeers > 0 && use_xf) return launch_j3_t<R, TH, true, TH >= 32 ? 2 : 4, true, true>(p, batch, st);
 #ifdef BLFLS_EXPERIMENTS
     static const int polyk = knob("BLFLS_J3_POLY", 0);
     if (use_xf && polyk) {
@@ -417,7 +417,10 @@ static cudaError_t launch_j3(const BlfParams& p, int batch, cudaStream_t st)
         }
     }
 #endif
-    if (use_xf) return launch_j3_t<R, TH, false, 4, true, true>(p, batch, st);
+    // 4 CTAs of 16 rows (256 threads) per SM at 64 registers; 32-row tiles
+    // (2 CTAs of 512 threads, the halo staged once per 32 output rows) below
+    constexpr int XMINB = TH >= 32 ? 2 : 4;
+    if (use_xf) return launch_j3_t<R, TH, false, XMINB, true, true>(p, batch, st);
     if (p.npeers > 0) return launch_j3_t<R, TH, true, 2, true>(p, batch, st);
 #ifdef BLFLS_EXPERIMENTS
     if (px == 3) return launch_j3_t<R, TH, false, 3, true>(p, batch, st);
@@ -436,7 +439,17 @@ bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaErro
     switch (p.radius) {
         case 3: *err = launch_j3<3, 16>(p, batch, st); return true;
         case 5: *err = launch_j3<5, 16>(p, batch, st); return true;
-        case 7: *err = launch_j3<7, 16>(p, batch, st); return true;
+        case 7:
+            // 32-row tiles when the factorised form runs (2 CTAs of 512
+            // threads per SM, the 2R halo rows staged once per 32 output rows
+            // instead of 16): c5 0.817 -> 0.831 of the MUFU rate (r02 B200,
+            // tools/ab_j3th.sh); the difference form keeps 16 rows
+            if (2.0f * p.range_coef * p.range_coef <= 60.0f && knob("BLFLS_J3_TH", 32) == 32) {
+                *err = launch_j3<7, 32>(p, batch, st);
+                return true;
+            }
+            *err = launch_j3<7, 16>(p, batch, st);
+            return true;
         case 15: *err = launch_j3<15, 16>(p, batch, st); return true;
         default: return false;
     }
