@@ -354,7 +354,7 @@ def run_ours(args, cfg):
     out = torch.empty_like(img)
     radius = cfg.radius if args.backend == "brute" else 0  # the plan key blf_ls uses
     kw = dict(lam=cfg.lam, sigma_s=cfg.sigma_s, sigma_r=cfg.sigma_r, iters=cfg.iters,
-              radius=cfg.radius, check_finite=False, pad=args.pad, backend=args.backend)
+              radius=cfg.radius, check_finite=True, pad=args.pad, backend=args.backend)
     in_bytes = img.numel() * 4 + (guide.numel() * 4 if guide is not None else 0)
     flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     l2_resident = in_bytes * 4 < 100e6
@@ -517,6 +517,7 @@ def run_ours(args, cfg):
             "data": "synthetic (seeded Voronoi + ramp + noise, BASELINE generator, generated on device)",
             "config": config_json(cfg, world, {
                 "backend": args.backend, "pad": args.pad,
+                "finite_check": "every call, inside the timed region (require_finite, image.cpp:21-27)",
                 "l2": "flushed between steps (256 MB write)" if l2_resident else "inputs larger than L2",
                 "decomposition": {"weak": "independent images per rank",
                                   "shard": f"batch of {cfg.batch} sharded over {world} ranks"}[mode]},
