@@ -60,7 +60,11 @@ typedef enum blfls_status {
                                   consecutive calls overlap H2D / compute / D2H.  Inputs
                                   must stay valid and outputs are readable only after
                                   blfls_sync (which also reports deferred non-finite
-                                  input when CHECK_FINITE is set). */
+                                  input when CHECK_FINITE is set).  With device pointers
+                                  the call stays ordered on `stream`; only the
+                                  CHECK_FINITE verdict is deferred to blfls_sync (the
+                                  input is still scanned on the device in every call,
+                                  without a host round trip). */
 
 typedef struct blfls_plan_s* blfls_plan_t;
 

@@ -240,10 +240,12 @@ def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, ite
     (written into ``out`` when given: an fp32 array/tensor of the image's shape
     in the same memory space, e.g. pinned host memory).
 
-    ``wait=False`` (host memory only, ``out`` required, input already fp32
+    ``wait=False`` with host memory (``out`` required, input already fp32
     contiguous) returns immediately: H2D, compute and D2H are queued on the
     plan's copy/compute streams so consecutive calls overlap; call
     ``get_plan(...).sync()`` (or ``sync_plans()``) before reading ``out``.
+    With CUDA tensors the work is ordered on the current stream as always and
+    only the non-finite check's verdict is deferred to that sync.
     """
     img = _Img(image)
     gd = None if guide is None else _Img(guide, "guide")
@@ -279,7 +281,11 @@ def blf_ls(image, guide=None, *, lam: float, sigma_s: float, sigma_r: float, ite
     if not use_graph:
         flags |= NO_GRAPH
     flags |= int(extra_flags)
-    if not wait:
+    if not wait and img.torch:
+        # device tensors: ordered on the current stream as usual; only the
+        # non-finite verdict is deferred to get_plan(...).sync() / sync_plans()
+        flags |= ASYNC
+    elif not wait:
         if img.torch or finish:
             raise InvalidArgument(_capi.BLFLS_EINVAL, "wait=False needs host memory and `out`")
         src = image.numpy() if hasattr(image, "numpy") and not isinstance(image, np.ndarray) else image

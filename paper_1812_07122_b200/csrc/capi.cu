@@ -1004,8 +1004,10 @@ blfls_status ensure_host_slots(blfls_plan_t p)
     if (p->s_h2d) return BLFLS_OK;
     CK(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
-    CK(cudaMalloc(&p->nonfinite_acc, sizeof(unsigned)));
-    CK(cudaMemset(p->nonfinite_acc, 0, sizeof(unsigned)));
+    if (!p->nonfinite_acc) {
+        CK(cudaMalloc(&p->nonfinite_acc, sizeof(unsigned)));
+        CK(cudaMemset(p->nonfinite_acc, 0, sizeof(unsigned)));
+    }
     for (auto& sl : p->slot) {
         CK(cudaMalloc(&sl.in, sizeof(float) * p->img_elems));
         CK(cudaMalloc(&sl.out, sizeof(float) * p->img_elems));
@@ -1079,10 +1081,19 @@ blfls_status run_impl(blfls_plan_t p, const float* img, const float* guide, int 
     const size_t n = (size_t)batch * p->prm.channels * p->plane;
     const size_t ng = guide ? (size_t)batch * p->prm.guide_channels * p->plane : 0;
     const bool host = flags & BLFLS_HOST_PTRS;
-    const bool async = (flags & BLFLS_ASYNC) && host;
+    const bool async_host = (flags & BLFLS_ASYNC) && host;
+    // ASYNC device calls: ordered on the caller's stream as usual, but the
+    // non-finite check is counted on the device and reported by blfls_sync
+    // (no host round trip per call)
+    const bool async_dev = (flags & BLFLS_ASYNC) && !host;
+    const bool async = async_host || async_dev;
     // ASYNC host calls are ordered by blfls_sync, not by the caller's stream:
     // joining it would chain call k+1's H2D behind call k's D2H
-    if (!async && (r = fork_in(p, us))) return r;
+    if (!async_host && (r = fork_in(p, us))) return r;
+    if (async_dev && !p->nonfinite_acc) {
+        CK(cudaMalloc(&p->nonfinite_acc, sizeof(unsigned)));
+        CK(cudaMemset(p->nonfinite_acc, 0, sizeof(unsigned)));
+    }
     cudaStream_t st = p->ps;
     const float* din = img;
     const float* dguide = guide;
@@ -1155,6 +1166,8 @@ blfls_status blfls_sync(blfls_plan_t p)
     if (p->s_h2d) {
         CK(cudaStreamSynchronize(p->s_h2d));
         CK(cudaStreamSynchronize(p->s_d2h));
+    }
+    if (p->nonfinite_acc) {
         unsigned h = 0;
         CK(cudaMemcpy(&h, p->nonfinite_acc, sizeof(unsigned), cudaMemcpyDeviceToHost));
         CK(cudaMemset(p->nonfinite_acc, 0, sizeof(unsigned)));

@@ -678,3 +678,25 @@ def test_multi_band_entry_bit_identical(gpu, oracle, nbands):
     out = np.full_like(img, -1.0)
     m.run(img, None, 1, 2, out)
     assert np.array_equal(out, ref)
+
+
+def test_async_device_calls_defer_the_finite_check(gpu, oracle):
+    """blf_ls(wait=False) on CUDA tensors: ordered on the current stream as
+    usual (same bits as the synchronous call), the non-finite verdict is
+    reported once by the plan's sync (BLFLS_ASYNC with device pointers)."""
+    import torch
+    x = torch.from_numpy(_img(oracle, 3, 40, 64, 61)).cuda()
+    g = torch.from_numpy(_img(oracle, 1, 40, 64, 62)).cuda()
+    kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, iters=2, radius=7)
+    ref = gpu.blf_ls(x, g, **kw)
+    out = torch.empty_like(x)
+    gpu.blf_ls(x, g, out=out, wait=False, **kw)
+    plan = gpu.get_plan(40, 64, 3, 1, 7, 7.0, 0.1, 1000.0, 1, 0)
+    plan.sync()
+    assert torch.equal(out, ref)
+    bad = x.clone()
+    bad[0, 5, 7] = float("inf")
+    gpu.blf_ls(bad, g, out=out, wait=False, **kw)  # returns without raising
+    with pytest.raises(gpu.InvalidArgument):
+        plan.sync()
+    plan.sync()  # reported once
