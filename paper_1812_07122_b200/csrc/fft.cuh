@@ -560,6 +560,9 @@ template <int N_, int V_, int TV_>
 struct CtFft {
     static constexpr int N = N_, V = V_, TV = TV_, THREADS = V_ * TV_;
     static constexpr bool kCompileTime = true;
+    // row r2c launch bounds: the fold phase is load-latency bound, so the
+    // CT row pass runs at 2048 resident threads per SM (32 registers)
+    static constexpr int kMaxThreads = THREADS, kRowMinBlocks = 2048 / THREADS;
     const float2* tw;
     __device__ __forceinline__ int n() const { return N; }
     __device__ __forceinline__ int vecs() const { return V; }
@@ -588,6 +591,7 @@ struct CtFft {
 template <int E, bool GENERIC>
 struct RtFft {
     static constexpr bool kCompileTime = false;
+    static constexpr int kMaxThreads = 1024, kRowMinBlocks = 1;
     FftDesc d;
     int V, log2V;
     __device__ __forceinline__ int n() const { return d.n; }

@@ -34,7 +34,7 @@ __device__ __forceinline__ float fold_value(const SolveParams& p, const float* f
 
 // grid: (ceil(H / V), planes); V rows per CTA; n = W/2 (even W) or W (odd W)
 template <bool ODD, class F>
-__global__ void __launch_bounds__(1024) k_row_r2c(const SolveParams p, const F fft)
+__global__ void __launch_bounds__(F::kMaxThreads, F::kRowMinBlocks) k_row_r2c(const SolveParams p, const F fft)
 {
     extern __shared__ __align__(16) float2 buf[];
     const int n = fft.n(), V = fft.vecs();
