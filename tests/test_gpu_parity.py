@@ -700,3 +700,39 @@ def test_async_device_calls_defer_the_finite_check(gpu, oracle):
     with pytest.raises(gpu.InvalidArgument):
         plan.sync()
     plan.sync()  # reported once
+
+
+def test_multi_band_joint_gray_guide(gpu, oracle):
+    """Row bands with the shared-gray-guide filter (k_blf_j3's peer-storing
+    epilogue, factorised exponents): two entries on GPU 0 equal one
+    blfls_run bit for bit, and the oracle within 1e-4."""
+    from paper_1812_07122_b200 import _capi
+    c, h, w = 3, 72, 128
+    img = _img(oracle, c, h, w, 41).astype(np.float32)
+    guide = _img(oracle, 1, h, w, 42).astype(np.float32)
+    kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, radius=7)
+    ref = gpu.blf_ls(img, guide, iters=3, **kw)
+    prm = _capi.Params(h, w, c, 1, 7, 7.0, 0.1, 1000.0, 1, 0, 0, 0, 0)
+    m = _capi.MultiPlan(prm, [0, 0], _capi.MULTI_BAND)
+    out = np.full_like(img, -1.0)
+    m.run(img, guide, 1, 3, out)
+    assert np.array_equal(out, ref)
+    assert maxabs(out, oracle.blf_ls(img.astype(np.float64), guide.astype(np.float64), iters=3, **kw)) <= TOL_OUT
+
+
+def test_tma_c2r_with_reflect_padding(gpu, oracle):
+    """pad 16 on a batch whose padded spectra exceed 64 MB (the TMA c2r,
+    cropping in its epilogue) equals the same images one at a time (plain
+    c2r) bit for bit, and image 0 matches the oracle."""
+    import torch
+    b, c, h, w = 8, 3, 1024, 1024
+    imgs = torch.from_numpy(np.stack([_img(oracle, c, h, w, 500 + i) for i in range(b)])).cuda()
+    kw = dict(lam=1000.0, sigma_s=3.0, sigma_r=0.1, iters=1, radius=3, pad=16)
+    big = gpu.blf_ls(imgs, **kw)
+    for i in (0, 5):
+        one = gpu.blf_ls(imgs[i:i + 1].contiguous(), **kw)
+        assert torch.equal(one, big[i:i + 1]), i
+    small = imgs[0, :, :256, :256].cpu().numpy().astype(np.float64)  # oracle on a crop (pad path)
+    ref = oracle.blf_ls(small, lam=1000.0, sigma_s=3.0, sigma_r=0.1, iters=1, radius=3, pad=16)
+    out = gpu.blf_ls(imgs[0, :, :256, :256].contiguous(), **kw).cpu().numpy()
+    assert maxabs(out, ref) <= TOL_OUT
