@@ -208,7 +208,19 @@ struct SolveParams {
     float lambda;
     float inv_hw;        // 1 / (H W)
     int mode;            // column pass: 1 fwd, 2 inv, 3 fwd+scale+inv
+    // mode 3 as a cyclic tridiagonal solve per spectrum column (k_col_tri.cu):
+    // tri[v] = (rho, rho^rpt, rho^len_last, 1 / (1 - rho^H)), tri_scale[v] =
+    // rho / (lambda W); nullptr: the column FFT pair runs
+    const float4* tri;
+    const float* tri_scale;
+    int tri_rpt;         // rows per thread the tables were built for
 };
+
+// tridiagonal column pass (k_col_tri.cu)
+int tri_rows_per_thread(int H, int wc, int planes, int nsm);
+bool tri_supported(int H, int rpt);
+void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri, std::vector<float>& scale);
+cudaError_t launch_col_tri(const SolveParams& p, int planes, cudaStream_t st);
 
 
 // high-radix solve passes (k_solve2.cu): false when no geometry exists for n

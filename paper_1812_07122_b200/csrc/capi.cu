@@ -266,6 +266,9 @@ struct blfls_plan_s {
     float* gain_x = nullptr;
     float* gain_y = nullptr;
     float2* post = nullptr;
+    float4* tri = nullptr;       // tridiagonal column pass tables (k_col_tri.cu)
+    float* tri_scale = nullptr;
+    int tri_rpt = 0;
     // workspace (max_batch images)
     size_t plane = 0, img_elems = 0;  // user (unpadded) plane H*W
     // reflect padding: the BLF and the solve run on the padded grid Hp x Wp
@@ -365,6 +368,9 @@ SolveParams solve_params(blfls_plan_t p)
     s.gain_y = p->gain_y;
     s.post = p->post;
     s.spec = p->spec;
+    s.tri = p->tri;
+    s.tri_scale = p->tri_scale;
+    s.tri_rpt = p->tri_rpt;
     return s;
 }
 
@@ -631,7 +637,7 @@ void free_plan(blfls_plan_t p)
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
-    void* ptrs[] = {p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
+    void* ptrs[] = {p->tri, p->tri_scale, p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
                     p->rowf.tw, p->colf.tw, p->rowf.chirp, p->rowf.btw, p->rowf.hf, p->rowf.hi,
                     p->colf.chirp, p->colf.btw, p->colf.hf, p->colf.hi, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
@@ -766,6 +772,20 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         cudaMemcpy(p->gain_x, gx.data(), sizeof(float) * p->wc, cudaMemcpyHostToDevice);
         cudaMemcpy(p->gain_y, gy.data(), sizeof(float) * H, cudaMemcpyHostToDevice);
         cudaMemcpy(p->post, post.data(), sizeof(float2) * p->wc, cudaMemcpyHostToDevice);
+        // the solve's column pass as a cyclic tridiagonal solve (BLFLS_COL_TRI=0
+        // in the experiments build keeps the column FFT pair)
+        const int rpt = tri_rows_per_thread(H, p->wc, q.max_batch * C, p->nsm);
+        if (knob("BLFLS_COL_TRI", 1) != 0 && tri_supported(H, rpt)) {
+            std::vector<float4> t4;
+            std::vector<float> tsc;
+            tri_tables(H, W, p->wc, q.lambda, rpt, t4, tsc);
+            if (cudaMalloc(&p->tri, sizeof(float4) * p->wc) != cudaSuccess ||
+                cudaMalloc(&p->tri_scale, sizeof(float) * p->wc) != cudaSuccess)
+                return bail(fail(BLFLS_ENOMEM, "plan: table allocation failed"));
+            cudaMemcpy(p->tri, t4.data(), sizeof(float4) * p->wc, cudaMemcpyHostToDevice);
+            cudaMemcpy(p->tri_scale, tsc.data(), sizeof(float) * p->wc, cudaMemcpyHostToDevice);
+            p->tri_rpt = rpt;
+        }
         auto fill = [](DevFft& f, int n, const std::vector<int>& rad) {
             f.g.desc.n = n;
             f.g.desc.nstages = (int)rad.size();
