@@ -124,6 +124,9 @@ struct BlfParams {
     // column: cep[i] = (cs[|i - r|], cs[|i - r - 1|]), i in [0, 2r + 1]
     // (entries outside the window hold cs[r]; k_blf_p2.cu pair exponents)
     float2 cep[2 * kMaxRadius + 2];
+    // row-factor fold of k_blf_j3r.cu: rfold[d + r] = wy(d - 1) / wy(d) for the
+    // window rows d in (-r, r], rfold[0] = 1
+    float rfold[2 * kMaxRadius + 2];
     // fused band exchange (multi-GPU row bands): npeers > 0 writes every target
     // into the full-height tx / ty of each peer (NVLink peer-mapped pointers,
     // rank order) instead of tx / ty -- the all-gather done by the epilogue
@@ -230,6 +233,8 @@ bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, in
 
 // shared-gray-guide filter with packed accumulation (k_blf_j3.cu); false: not covered
 bool launch_grad_blf_j3(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
+// two output rows per thread, row factor folded into the sums (k_blf_j3r.cu); false: not covered
+bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
 // eight outputs per thread, factorised exponents (k_blf_j8.cu); false: not covered
 bool launch_grad_blf_j8(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
 

@@ -864,6 +864,12 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
             const int a = std::min(std::abs(i - radius), radius), c = std::min(std::abs(i - radius - 1), radius);
             b.cep[i] = make_float2(b.cs[a], b.cs[c]);
         }
+        b.rfold[0] = 1.0f;
+        for (int i = 1; i < 2 * kMaxRadius + 2; ++i) {
+            const int d = i - radius;  // window row; wy(d - 1) / wy(d)
+            const double e = ((double)d * d - (double)(d - 1) * (d - 1)) / (2.0 * q.sigma_s * q.sigma_s);
+            b.rfold[i] = d <= radius ? (float)std::exp(std::min(e, 80.0)) : 1.0f;
+        }
         // shared-memory envelope of the generic kernel
         const int narr = p->mode == 0 ? 2 : (p->mode == 1 ? 4 : 8);
         const size_t smem = (size_t)narr * (16 + 2 * radius) * (((64 + 2 * radius) + 3) & ~3) * 4;

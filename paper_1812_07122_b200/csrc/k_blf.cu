@@ -900,6 +900,7 @@ static cudaError_t dispatch_mode(const BlfParams& p, int nz, cudaStream_t st)
 cudaError_t launch_grad_blf(const BlfParams& p, int mode, int batch, cudaStream_t st)
 {
     cudaError_t e = cudaSuccess;
+    if (mode == 2 && launch_grad_blf_j3r(p, batch, st, &e)) return e;
     if (mode == 2 && launch_grad_blf_j8(p, batch, st, &e)) return e;
     if (mode == 2 && launch_grad_blf_j3(p, batch, st, &e)) return e;
     if (mode != 2 && launch_grad_blf_p2(p, mode, batch, st, &e)) return e;

@@ -1,0 +1,322 @@
+// k_blf_j3r.cu -- shared-grayscale-guide brute-force BLF (the joint filter of
+// bilateral.cpp:28-77 as filter_gradients applies it to the three channels
+// with one guide, pipelines.cpp:33-53), TWO output rows x four columns per
+// thread.
+//
+// k_blf_j3 (one row x four columns per thread) is co-limited by shared-memory
+// bandwidth: every thread re-reads its 20 staged source columns for each of
+// its window rows, 100 wavefronts per 60 warp-MUFU.EX2, i.e. 83% of the
+// shared pipe at the MUFU bound (ncu: mio_throttle the top stall).  Here a
+// staged source row r serves the output rows y and y + 1 of the thread
+// (dy = r - y and r - y - 1), so the same loads feed twice the taps.
+//
+// Registers for eight outputs come from dropping the per-row partial sums:
+// the row factor wy(dy) is folded into the accumulators themselves.  Before
+// the taps of window row dy are added (with the weight exp2(2ab + cs[|dx|]),
+// no row term), the accumulators are multiplied by wy(dy - 1) / wy(dy); after
+// the last row they hold sum_dy wy(dy) / wy(R) * (row sum), and the common
+// 1 / wy(R) cancels between numerator and normaliser.  Same factorised
+// exponent as k_blf_j3<XF>: exp2(-b^2) is folded into the staged sources,
+// exp2(-a^2) cancels.
+//
+// 32 x 64 output tiles, 256 threads (16 x 16), 73.6 KB of staged sources, 85
+// registers: 3 CTAs = 24 warps per SM.
+#include <algorithm>
+#include <cstdint>
+
+#include "blfls_internal.cuh"
+
+namespace blfls {
+
+namespace {
+
+__device__ __forceinline__ float r_ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// d.xy = {a, a} * b.xy + c.xy
+__device__ __forceinline__ unsigned long long r_ffma2(float a, unsigned long long b, unsigned long long c)
+{
+    unsigned long long aa, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long r_fmul2(float a, unsigned long long b)
+{
+    unsigned long long aa, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(aa), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float2 r_unpack(unsigned long long r)
+{
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+// 16-byte chunk swizzle of the interleaved source rows (k_blf_j3.cu j3_sw)
+__device__ __forceinline__ int r_sw(int col)
+{
+    const int k = col >> 1;
+    return ((k ^ ((k >> 3) & 1)) << 1) | (col & 1);
+}
+__device__ __forceinline__ void r_decode(const uint32_t* lohi, int b, float coef, float& s, float& range)
+{
+    const float lo = ordered_to_float(lohi[2 * b]);
+    const float hi = ordered_to_float(lohi[2 * b + 1]);
+    range = hi - lo;
+    s = range > 0.f ? coef / range : coef;
+}
+
+template <int R>
+struct J3rGeom {
+    static constexpr int P = 4, TW = 64, TH = 32, NT = 256;
+    static constexpr int ROWS = TH + 2 * R;
+    static constexpr int COLS = TW + 2 * R;
+    static constexpr int VN = P + 2 * R;          // window columns per thread
+    static constexpr int VN4 = (VN + 3) & ~3;     // rounded to column quads
+    static constexpr int GP = (TW - P + VN4 + 3) & ~3;  // pitch: the last thread's last quad
+    static constexpr int SP = GP;
+    static constexpr size_t smem_bytes()
+    {
+        return (size_t)ROWS * GP * sizeof(float) + (size_t)2 * ROWS * SP * sizeof(float2);
+    }
+};
+
+// the taps of one staged source row for the output rows in MASK (bit k: row k)
+template <int R, int MASK>
+__device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restrict__ grow,
+                                        const float2* __restrict__ s01, const float2* __restrict__ s2, int tx,
+                                        const unsigned long long (&gsp)[2][2], unsigned long long (&a01)[2][4],
+                                        unsigned long long (&a2z)[2][4])
+{
+    using Gm = J3rGeom<R>;
+    constexpr int P = Gm::P, VN = Gm::VN, VN4 = Gm::VN4;
+#pragma unroll
+    for (int j4 = 0; j4 < VN4; j4 += 4) {
+        const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+        const float gt[4] = {g4.x, g4.y, g4.z, g4.w};
+        unsigned long long v01[4], v2z[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int pc = r_sw(tx * P + j4 + 2 * h);
+            const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
+            const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
+            asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h + 1]) : "f"(c.z), "f"(c.w));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j4 + u;
+            if (j >= VN) break;
+            unsigned long long gtt;
+            asm("mov.b64 %0, {%1, %1};" : "=l"(gtt) : "f"(gt[u]));
+#pragma unroll
+            for (int h = 0; h < P / 2; ++h) {
+                const int q0 = 2 * h, dx0 = j - q0 - R;
+                const bool ok0 = dx0 >= -R && dx0 <= R, ok1 = dx0 - 1 >= -R && dx0 - 1 <= R;
+                if (!ok0 && !ok1) continue;
+                unsigned long long ce;
+                asm("mov.b64 %0, {%1, %2};" : "=l"(ce) : "f"(p.cep[dx0 + R].x), "f"(p.cep[dx0 + R].y));
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!((MASK >> k) & 1)) continue;
+                    unsigned long long e;
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[k][h]), "l"(ce));
+                    const float2 ee = r_unpack(e);
+                    if (ok0) {
+                        const float w = r_ex2(ee.x);
+                        a01[k][q0] = r_ffma2(w, v01[u], a01[k][q0]);
+                        a2z[k][q0] = r_ffma2(w, v2z[u], a2z[k][q0]);
+                    }
+                    if (ok1) {
+                        const float w = r_ex2(ee.y);
+                        a01[k][q0 + 1] = r_ffma2(w, v01[u], a01[k][q0 + 1]);
+                        a2z[k][q0 + 1] = r_ffma2(w, v2z[u], a2z[k][q0 + 1]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// blockIdx.z = image * 2 + axis; PEERS: fused band exchange (k_blf_j3.cu)
+template <int R, bool PEERS>
+__global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
+{
+    using Gm = J3rGeom<R>;
+    constexpr int P = Gm::P, TW = Gm::TW, TH = Gm::TH, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
+    constexpr int GP = Gm::GP, SP = Gm::SP;
+    extern __shared__ __align__(16) float smr[];
+    float* G = smr;                                               // [ROWS][GP]  b (scaled guide gradient)
+    float2* S01 = reinterpret_cast<float2*>(smr + ROWS * GP);     // [ROWS][SP] {g0 B, g1 B}
+    float2* S2 = S01 + ROWS * SP;                                 // [ROWS][SP] {g2 B, B}, B = exp2(-b^2)
+
+    const int H = p.H, W = p.W;
+    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
+    const int tx0 = blockIdx.x * TW;
+    const int ty0 = p.y0 + blockIdx.y * TH;
+    const size_t plane = (size_t)H * W;
+    float s, range, sg, grange;
+    r_decode(p.lohi, b, p.range_coef, s, range);
+    r_decode(p.glohi, b, p.range_coef, sg, grange);
+    const float* fimg = p.f + (size_t)b * 3 * plane;
+    const float* gimg = p.guide + (size_t)b * p.GC * plane;
+
+    // ---- staging: this axis' circular gradients of guide and channels, warp
+    // per tile row, lane per column; cells outside the image: b = 0, zero
+    // sources (weight exp2(cs) on a zero source and a zero normaliser term)
+    {
+        const int lane = threadIdx.x & 31;
+        for (int i = threadIdx.x >> 5; i < ROWS; i += NT / 32) {
+            const int y = ty0 - R + i;
+            const bool yin = y >= 0 && y < H;
+            const int yn = axis == 0 ? y : (y + 1 == H ? 0 : y + 1);
+            const size_t r0 = (size_t)(yin ? y : 0) * W, r1 = (size_t)(yin ? yn : 0) * W;
+            float* grow = G + i * GP;
+            float2* s01 = S01 + i * SP;
+            float2* s2 = S2 + i * SP;
+#pragma unroll
+            for (int j = lane; j < COLS; j += 32) {
+                const int x = tx0 - R + j;
+                const int o = r_sw(j);
+                if (yin && x >= 0 && x < W) {
+                    const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
+                    const float bb = (__ldg(gimg + r1 + x1) - __ldg(gimg + r0 + x)) * sg;
+                    grow[j] = bb;
+                    float g[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float* fc = fimg + (size_t)c * plane;
+                        g[c] = __ldg(fc + r1 + x1) - __ldg(fc + r0 + x);
+                    }
+                    const float bw = r_ex2(-bb * bb);
+                    s01[o] = make_float2(g[0] * bw, g[1] * bw);
+                    s2[o] = make_float2(g[2] * bw, bw);
+                } else {
+                    grow[j] = 0.0f;
+                    s01[o] = make_float2(0.f, 0.f);
+                    s2[o] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x & 15, typ = threadIdx.x >> 4;
+    unsigned long long gsp[2][2], a01[2][4], a2z[2][4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float* ga = G + (2 * typ + k + R) * GP + tx * P + R;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[k][0]) : "f"(2.0f * ga[0]), "f"(2.0f * ga[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[k][1]) : "f"(2.0f * ga[2]), "f"(2.0f * ga[3]));
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            a01[k][q] = 0ull;
+            a2z[k][q] = 0ull;
+        }
+    }
+    // staged row 2 typ + i holds source row (output row 0) - R + i
+    const float* grow = G + (2 * typ) * GP + tx * P;
+    const float2* s01 = S01 + (2 * typ) * SP;
+    const float2* s2 = S2 + (2 * typ) * SP;
+    j3r_row<R, 1>(p, grow, s01, s2, tx, gsp, a01, a2z);
+#pragma unroll 1
+    for (int i = 1; i <= 2 * R; ++i) {
+        grow += GP;
+        s01 += SP;
+        s2 += SP;
+        const float f0 = p.rfold[i], f1 = p.rfold[i - 1];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            a01[0][q] = r_fmul2(f0, a01[0][q]);
+            a2z[0][q] = r_fmul2(f0, a2z[0][q]);
+            a01[1][q] = r_fmul2(f1, a01[1][q]);
+            a2z[1][q] = r_fmul2(f1, a2z[1][q]);
+        }
+        j3r_row<R, 3>(p, grow, s01, s2, tx, gsp, a01, a2z);
+    }
+    {
+        const float f1 = p.rfold[2 * R];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            a01[1][q] = r_fmul2(f1, a01[1][q]);
+            a2z[1][q] = r_fmul2(f1, a2z[1][q]);
+        }
+        j3r_row<R, 2>(p, grow + GP, s01 + SP, s2 + SP, tx, gsp, a01, a2z);
+    }
+
+    const int ox = tx0 + tx * P;
+    const float oscale = (p.normalized_out && range > 0.f) ? 1.f / range : 1.f;
+    float* dst = axis == 0 ? p.tx : p.ty;
+    const size_t pl = (size_t)p.out_rows * W;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int oy = ty0 + 2 * typ + k;
+        if (oy >= p.y1) continue;
+        const size_t orow = (size_t)(oy - (p.out_rows == H ? 0 : p.y0)) * W;
+        float t[3][P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const float2 n01 = r_unpack(a01[k][q]);
+            const float2 n2z = r_unpack(a2z[k][q]);
+            const float inv = oscale / n2z.y;
+            t[0][q] = n01.x * inv;
+            t[1][q] = n01.y * inv;
+            t[2][q] = n2z.x * inv;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const size_t off = ((size_t)b * 3 + c) * pl + orow + ox;
+            if constexpr (PEERS) {
+                const bool vec = ox + P <= W && (off & 3) == 0;  // 16-byte peer stores
+                for (int n = 0; n < p.npeers; ++n) {
+                    float* d = (axis == 0 ? p.peer_tx[n] : p.peer_ty[n]) + off;
+                    if (vec)
+                        *reinterpret_cast<float4*>(d) = make_float4(t[c][0], t[c][1], t[c][2], t[c][3]);
+                    else
+                        for (int q = 0; q < P && ox + q < W; ++q) d[q] = t[c][q];
+                }
+            } else if (ox + P <= W && (off & 3) == 0) {
+                *reinterpret_cast<float4*>(dst + off) = make_float4(t[c][0], t[c][1], t[c][2], t[c][3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (ox + q < W) dst[off + q] = t[c][q];
+            }
+        }
+    }
+}
+
+template <int R, bool PEERS>
+static cudaError_t launch_j3r_t(const BlfParams& p, int batch, cudaStream_t st)
+{
+    using Gm = J3rGeom<R>;
+    constexpr size_t smem = Gm::smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k_blf_j3r<R, PEERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + Gm::TH - 1) / Gm::TH, 2 * batch);
+    k_blf_j3r<R, PEERS><<<grid, Gm::NT, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// Two-row shared-gray-guide filter where it applies: three channels, r = 7,
+// factorised exponents cannot overflow (2 coef^2 <= 60, k_blf_j3.cu) and the
+// folded row factors stay in range (1 / wy(R) <= 2^57).  false: not covered.
+bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
+{
+    if (knob("BLFLS_J3R", 1) == 0) return false;
+    if (p.C != 3 || p.radius != 7) return false;
+    if (2.0f * p.range_coef * p.range_coef > 60.0f || -p.cs[p.radius] > 57.0f) return false;
+    *err = p.npeers > 0 ? launch_j3r_t<7, true>(p, batch, st) : launch_j3r_t<7, false>(p, batch, st);
+    return true;
+}
+
+}  // namespace blfls
