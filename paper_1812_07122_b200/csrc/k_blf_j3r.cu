@@ -57,6 +57,34 @@ __device__ __forceinline__ float2 r_unpack(unsigned long long r)
     asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
     return v;
 }
+// exp2 of both lanes of an f32x2 pair on the FMA pipe (factorised exponents lie
+// in [-2 coef^2 + cs_min, 2 coef^2], inside [-125, 60]: no clamping): split
+// x = j + f by the 1.5 * 2^23 shifter, degree-5 polynomial for 2^f (rel. err
+// 2.3e-7, the coefficients of k_blf.cu poly_ex2), 2^j by an exponent add
+__device__ __forceinline__ float2 r_poly_ex2x2(unsigned long long x)
+{
+    unsigned long long t, jj, f, pp, magic, c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(magic) : "f"(12582912.0f));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(x), "l"(magic));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(jj) : "l"(t), "l"(magic));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(jj));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(pp) : "f"(0.001327647129073739f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.009675541892647743f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.05550713092088699f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.24022120237350464f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(0.6931469440460205f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(1.0000001192092896f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c));
+    float2 tv, pv;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(tv.x), "=f"(tv.y) : "l"(t));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(pv.x), "=f"(pv.y) : "l"(pp));
+    return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                       __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
+}
 // 16-byte chunk swizzle of the interleaved source rows (k_blf_j3.cu j3_sw)
 __device__ __forceinline__ int r_sw(int col)
 {
@@ -91,7 +119,7 @@ struct J3rGeom {
 };
 
 // the taps of one staged source row for the output rows in MASK (bit k: row k)
-template <int R, int MASK>
+template <int R, int MASK, int FAKE = 0, int POLYK = 0>
 __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restrict__ grow,
                                         const float2* __restrict__ s01, const float2* __restrict__ s2, int tx,
                                         const unsigned long long (&gsp)[2][2], unsigned long long (&a01)[2][4],
@@ -107,8 +135,9 @@ __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restr
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int pc = r_sw(tx * P + j4 + 2 * h);
-            const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
-            const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
+            // FAKE (experiments): no source loads -- the MUFU / FFMA2 mix without the LDS traffic
+            const float4 a = FAKE ? make_float4(g4.x, g4.y, g4.z, g4.w) : *reinterpret_cast<const float4*>(s01 + pc);
+            const float4 c = FAKE ? make_float4(g4.w, g4.z, g4.y, g4.x) : *reinterpret_cast<const float4*>(s2 + pc);
             asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
             asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
             asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
@@ -132,16 +161,24 @@ __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restr
                     if (!((MASK >> k) & 1)) continue;
                     unsigned long long e;
                     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[k][h]), "l"(ce));
-                    const float2 ee = r_unpack(e);
+                    // POLYK > 0: every POLYK-th exponent pair of the row on the FMA pipe
+                    constexpr int PK = POLYK > 0 ? POLYK : 1;
+                    const bool poly = POLYK > 0 && ok0 && ok1 && ((j * (P / 2) + h) * 2 + k) % PK == PK - 1;
+                    float2 ww;
+                    if (poly) {
+                        ww = r_poly_ex2x2(e);
+                    } else {
+                        const float2 ee = r_unpack(e);
+                        ww.x = ok0 ? r_ex2(ee.x) : 0.f;
+                        ww.y = ok1 ? r_ex2(ee.y) : 0.f;
+                    }
                     if (ok0) {
-                        const float w = r_ex2(ee.x);
-                        a01[k][q0] = r_ffma2(w, v01[u], a01[k][q0]);
-                        a2z[k][q0] = r_ffma2(w, v2z[u], a2z[k][q0]);
+                        a01[k][q0] = r_ffma2(ww.x, v01[u], a01[k][q0]);
+                        a2z[k][q0] = r_ffma2(ww.x, v2z[u], a2z[k][q0]);
                     }
                     if (ok1) {
-                        const float w = r_ex2(ee.y);
-                        a01[k][q0 + 1] = r_ffma2(w, v01[u], a01[k][q0 + 1]);
-                        a2z[k][q0 + 1] = r_ffma2(w, v2z[u], a2z[k][q0 + 1]);
+                        a01[k][q0 + 1] = r_ffma2(ww.y, v01[u], a01[k][q0 + 1]);
+                        a2z[k][q0 + 1] = r_ffma2(ww.y, v2z[u], a2z[k][q0 + 1]);
                     }
                 }
             }
@@ -152,7 +189,7 @@ __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restr
 }  // namespace
 
 // blockIdx.z = image * 2 + axis; PEERS: fused band exchange (k_blf_j3.cu)
-template <int R, bool PEERS>
+template <int R, bool PEERS, int FAKE = 0, int POLYK = 0>
 __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
 {
     using Gm = J3rGeom<R>;
@@ -181,46 +218,55 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
         // aligned column quads: one task = 4 staged cells of one row from 16-byte
         // loads (8-9 load instructions per 4 cells instead of 8 per cell, ~4
         // dependent rounds per thread instead of ~17)
-        constexpr int QPR = COLS / 4;
-        for (int t = threadIdx.x; t < ROWS * QPR; t += NT) {
+        constexpr int QPR = COLS / 4, NTASK = ROWS * QPR;
+        struct Quad {
+            float4 v0[4], v1[4];  // guide, c0, c1, c2: the cells and (axis 1) their +1 row / (axis 0, .x) the cell after
+            bool in;
+        };
+        auto qload = [&](int t, Quad& q) {
             const int i = t / QPR, c = t - i * QPR;
             const int y = ty0 - R + i, x = tx0 - Gm::OX + 4 * c;
-            float4 bq = make_float4(0.f, 0.f, 0.f, 0.f), sa = bq, sb = bq, sc = bq, sd = bq;
-            if (y >= 0 && y < H && x >= 0 && x < W) {
-                const size_t r0 = (size_t)y * W + x;
-                float4 v0[4], v1[4];  // guide, c0, c1, c2: this cell and its +1 neighbour
-                float e[4];
-                if (axis == 0) {
-                    const size_t rn = (size_t)y * W + (x + 4 == W ? 0 : x + 4);
-                    v0[0] = __ldg(reinterpret_cast<const float4*>(gimg + r0));
-                    e[0] = __ldg(gimg + rn);
+            q.in = y >= 0 && y < H && x >= 0 && x < W;
+            if (!q.in) return;
+            const int r0 = y * W + x;  // offsets within a plane fit 32 bits
+            if (axis == 0) {
+                const int rn = y * W + (x + 4 == W ? 0 : x + 4);
+                q.v0[0] = __ldg(reinterpret_cast<const float4*>(gimg + r0));
+                q.v1[0].x = __ldg(gimg + rn);
 #pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        v0[ch + 1] = __ldg(reinterpret_cast<const float4*>(fimg + ch * plane + r0));
-                        e[ch + 1] = __ldg(fimg + ch * plane + rn);
-                    }
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) v1[ch] = make_float4(v0[ch].y, v0[ch].z, v0[ch].w, e[ch]);
-                } else {
-                    const size_t r1 = (size_t)(y + 1 == H ? 0 : y + 1) * W + x;
-                    v0[0] = __ldg(reinterpret_cast<const float4*>(gimg + r0));
-                    v1[0] = __ldg(reinterpret_cast<const float4*>(gimg + r1));
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        v0[ch + 1] = __ldg(reinterpret_cast<const float4*>(fimg + ch * plane + r0));
-                        v1[ch + 1] = __ldg(reinterpret_cast<const float4*>(fimg + ch * plane + r1));
-                    }
+                for (int ch = 0; ch < 3; ++ch) {
+                    q.v0[ch + 1] = __ldg(reinterpret_cast<const float4*>(fimg + ch * plane + r0));
+                    q.v1[ch + 1].x = __ldg(fimg + ch * plane + rn);
                 }
-                bq = make_float4((v1[0].x - v0[0].x) * sg, (v1[0].y - v0[0].y) * sg, (v1[0].z - v0[0].z) * sg,
-                                 (v1[0].w - v0[0].w) * sg);
+            } else {
+                const int r1 = (y + 1 == H ? 0 : y + 1) * W + x;
+                q.v0[0] = __ldg(reinterpret_cast<const float4*>(gimg + r0));
+                q.v1[0] = __ldg(reinterpret_cast<const float4*>(gimg + r1));
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    q.v0[ch + 1] = __ldg(reinterpret_cast<const float4*>(fimg + ch * plane + r0));
+                    q.v1[ch + 1] = __ldg(reinterpret_cast<const float4*>(fimg + ch * plane + r1));
+                }
+            }
+        };
+        auto qstore = [&](int t, const Quad& q) {
+            const int i = t / QPR, c = t - i * QPR;
+            float4 bq = make_float4(0.f, 0.f, 0.f, 0.f), sa = bq, sb = bq, sc = bq, sd = bq;
+            if (q.in) {
+                float4 d[4];  // gradients of guide, c0, c1, c2
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const float4 a = q.v0[ch];
+                    const float4 n = axis == 0 ? make_float4(a.y, a.z, a.w, q.v1[ch].x) : q.v1[ch];
+                    d[ch] = make_float4(n.x - a.x, n.y - a.y, n.z - a.z, n.w - a.w);
+                }
+                bq = make_float4(d[0].x * sg, d[0].y * sg, d[0].z * sg, d[0].w * sg);
                 const float w0 = r_ex2(-bq.x * bq.x), w1 = r_ex2(-bq.y * bq.y);
                 const float w2 = r_ex2(-bq.z * bq.z), w3 = r_ex2(-bq.w * bq.w);
-                sa = make_float4((v1[1].x - v0[1].x) * w0, (v1[2].x - v0[2].x) * w0, (v1[1].y - v0[1].y) * w1,
-                                 (v1[2].y - v0[2].y) * w1);
-                sb = make_float4((v1[1].z - v0[1].z) * w2, (v1[2].z - v0[2].z) * w2, (v1[1].w - v0[1].w) * w3,
-                                 (v1[2].w - v0[2].w) * w3);
-                sc = make_float4((v1[3].x - v0[3].x) * w0, w0, (v1[3].y - v0[3].y) * w1, w1);
-                sd = make_float4((v1[3].z - v0[3].z) * w2, w2, (v1[3].w - v0[3].w) * w3, w3);
+                sa = make_float4(d[1].x * w0, d[2].x * w0, d[1].y * w1, d[2].y * w1);
+                sb = make_float4(d[1].z * w2, d[2].z * w2, d[1].w * w3, d[2].w * w3);
+                sc = make_float4(d[3].x * w0, w0, d[3].y * w1, w1);
+                sd = make_float4(d[3].z * w2, w2, d[3].w * w3, w3);
             }
             // chunks 2c, 2c + 1 of the interleaved rows (r_sw: swapped in odd groups of 8 chunks)
             const int k0 = (2 * c) ^ ((c >> 2) & 1), k1 = k0 ^ 1;
@@ -229,6 +275,13 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
             *reinterpret_cast<float4*>(S01 + i * SP + 2 * k1) = sb;
             *reinterpret_cast<float4*>(S2 + i * SP + 2 * k0) = sc;
             *reinterpret_cast<float4*>(S2 + i * SP + 2 * k1) = sd;
+        };
+        // (two tasks in flight per thread need > 80 registers: the spills cost
+        // more than the second round of loads hides, 0.862 vs 0.872 of MUFU)
+        for (int t = threadIdx.x; t < NTASK; t += NT) {
+            Quad q;
+            qload(t, q);
+            qstore(t, q);
         }
     } else {
         // any width: warp per tile row, lane per column
@@ -284,7 +337,7 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
     const float* grow = G + (2 * typ) * GP + tx * P;
     const float2* s01 = S01 + (2 * typ) * SP;
     const float2* s2 = S2 + (2 * typ) * SP;
-    j3r_row<R, 1>(p, grow, s01, s2, tx, gsp, a01, a2z);
+    j3r_row<R, 1, FAKE, POLYK>(p, grow, s01, s2, tx, gsp, a01, a2z);
 #pragma unroll 1
     for (int i = 1; i <= 2 * R; ++i) {
         grow += GP;
@@ -298,7 +351,7 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
             a01[1][q] = r_fmul2(f1, a01[1][q]);
             a2z[1][q] = r_fmul2(f1, a2z[1][q]);
         }
-        j3r_row<R, 3>(p, grow, s01, s2, tx, gsp, a01, a2z);
+        j3r_row<R, 3, FAKE, POLYK>(p, grow, s01, s2, tx, gsp, a01, a2z);
     }
     {
         const float f1 = p.rfold[2 * R];
@@ -307,7 +360,7 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
             a01[1][q] = r_fmul2(f1, a01[1][q]);
             a2z[1][q] = r_fmul2(f1, a2z[1][q]);
         }
-        j3r_row<R, 2>(p, grow + GP, s01 + SP, s2 + SP, tx, gsp, a01, a2z);
+        j3r_row<R, 2, FAKE, POLYK>(p, grow + GP, s01 + SP, s2 + SP, tx, gsp, a01, a2z);
     }
 
     const int ox = tx0 + tx * P;
@@ -352,15 +405,16 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
     }
 }
 
-template <int R, bool PEERS>
+template <int R, bool PEERS, int FAKE = 0, int POLYK = 0>
 static cudaError_t launch_j3r_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J3rGeom<R>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_j3r<R, PEERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_blf_j3r<R, PEERS, FAKE, POLYK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + Gm::TH - 1) / Gm::TH, 2 * batch);
-    k_blf_j3r<R, PEERS><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_j3r<R, PEERS, FAKE, POLYK><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -372,7 +426,27 @@ bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaErr
     if (knob("BLFLS_J3R", 1) == 0) return false;
     if (p.C != 3 || p.radius != 7) return false;
     if (2.0f * p.range_coef * p.range_coef > 60.0f || -p.cs[p.radius] > 57.0f) return false;
-    *err = p.npeers > 0 ? launch_j3r_t<7, true>(p, batch, st) : launch_j3r_t<7, false>(p, batch, st);
+    // every 12th exponent pair of a window row runs on the FMA pipe (f32x2
+    // polynomial exp2): the FMA pipe is ~60% busy at the MUFU bound, so the
+    // freed MUFU slots pay (c5 r02: 0.870 -> 0.891 of the MUFU rate; periods
+    // 24 / 16 / 10 / 8 / 6: 0.887 / 0.887 / 0.889 / 0.887 / 0.872).  The
+    // peer-storing band epilogue uses the same arithmetic.
+#ifdef BLFLS_EXPERIMENTS
+    if (knob("BLFLS_J3R_FAKE", 0)) {  // wrong results: pipe-interference experiment only
+        *err = launch_j3r_t<7, false, 1>(p, batch, st);
+        return true;
+    }
+    switch (p.npeers > 0 ? 12 : knob("BLFLS_J3R_POLY", 12)) {
+        case 0: *err = launch_j3r_t<7, false, 0, 0>(p, batch, st); return true;
+        case 6: *err = launch_j3r_t<7, false, 0, 6>(p, batch, st); return true;
+        case 8: *err = launch_j3r_t<7, false, 0, 8>(p, batch, st); return true;
+        case 10: *err = launch_j3r_t<7, false, 0, 10>(p, batch, st); return true;
+        case 16: *err = launch_j3r_t<7, false, 0, 16>(p, batch, st); return true;
+        case 24: *err = launch_j3r_t<7, false, 0, 24>(p, batch, st); return true;
+        default: break;
+    }
+#endif
+    *err = p.npeers > 0 ? launch_j3r_t<7, true, 0, 12>(p, batch, st) : launch_j3r_t<7, false, 0, 12>(p, batch, st);
     return true;
 }
 
