@@ -212,10 +212,8 @@ struct SolveParams {
     float inv_hw;        // 1 / (H W)
     int mode;            // column pass: 1 fwd, 2 inv, 3 fwd+scale+inv
     // mode 3 as a cyclic tridiagonal solve per spectrum column (k_col_tri.cu):
-    // tri[v] = (rho, rho^rpt, rho^len_last, 1 / (1 - rho^H)), tri_scale[v] =
-    // rho / (lambda W); nullptr: the column FFT pair runs
+    // two float4 per column (tri_tables); nullptr: the column FFT pair runs
     const float4* tri;
-    const float* tri_scale;
     int tri_rpt;         // rows per thread the tables were built for
 };
 

@@ -267,7 +267,6 @@ struct blfls_plan_s {
     float* gain_y = nullptr;
     float2* post = nullptr;
     float4* tri = nullptr;       // tridiagonal column pass tables (k_col_tri.cu)
-    float* tri_scale = nullptr;
     int tri_rpt = 0;
     // workspace (max_batch images)
     size_t plane = 0, img_elems = 0;  // user (unpadded) plane H*W
@@ -369,7 +368,6 @@ SolveParams solve_params(blfls_plan_t p)
     s.post = p->post;
     s.spec = p->spec;
     s.tri = p->tri;
-    s.tri_scale = p->tri_scale;
     s.tri_rpt = p->tri_rpt;
     return s;
 }
@@ -637,7 +635,7 @@ void free_plan(blfls_plan_t p)
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
-    void* ptrs[] = {p->tri, p->tri_scale, p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
+    void* ptrs[] = {p->tri, p->gain_x, p->gain_y, p->post, p->buf[0], p->buf[1], p->tx, p->ty, p->spec,
                     p->in_dev, p->guide_dev, p->out_dev, p->lohi, p->glohi, p->nonfinite,
                     p->rowf.tw, p->colf.tw, p->rowf.chirp, p->rowf.btw, p->rowf.hf, p->rowf.hi,
                     p->colf.chirp, p->colf.btw, p->colf.hf, p->colf.hi, p->fpad, p->gpad, p->grid.wgrid, p->grid.vgrid,
@@ -779,11 +777,9 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
             std::vector<float4> t4;
             std::vector<float> tsc;
             tri_tables(H, W, p->wc, q.lambda, rpt, t4, tsc);
-            if (cudaMalloc(&p->tri, sizeof(float4) * p->wc) != cudaSuccess ||
-                cudaMalloc(&p->tri_scale, sizeof(float) * p->wc) != cudaSuccess)
+            if (cudaMalloc(&p->tri, sizeof(float4) * t4.size()) != cudaSuccess)
                 return bail(fail(BLFLS_ENOMEM, "plan: table allocation failed"));
-            cudaMemcpy(p->tri, t4.data(), sizeof(float4) * p->wc, cudaMemcpyHostToDevice);
-            cudaMemcpy(p->tri_scale, tsc.data(), sizeof(float) * p->wc, cudaMemcpyHostToDevice);
+            cudaMemcpy(p->tri, t4.data(), sizeof(float4) * t4.size(), cudaMemcpyHostToDevice);
             p->tri_rpt = rpt;
         }
         auto fill = [](DevFft& f, int n, const std::vector<int>& rad) {

@@ -63,49 +63,72 @@ struct TriVec<2> {
 // q / K reads its K consecutive segments conflict-free
 __device__ __forceinline__ int tri_pos(int q, int K) { return (q % K) * 32 + q / K; }
 
+// One recursion step x' = m x + t in the state type ST.  float: the multiplier
+// as a hi + lo pair (two FMAs); double (the low-frequency columns, below): one
+// DFMA with m = hi + lo.
+template <class ST>
+struct TriMul;
+template <>
+struct TriMul<float> {
+    float hi, lo;
+    __device__ __forceinline__ TriMul(float h, float l) : hi(h), lo(l) {}
+    __device__ __forceinline__ float step(float S, float t) const { return fmaf(lo, S, fmaf(hi, S, t)); }
+    __device__ __forceinline__ float value() const { return hi; }
+};
+template <>
+struct TriMul<double> {
+    double m;
+    __device__ __forceinline__ TriMul(float h, float l) : m((double)h + (double)l) {}
+    __device__ __forceinline__ double step(double S, double t) const { return fma(m, S, t); }
+    __device__ __forceinline__ double value() const { return m; }
+};
+
 // One warp per real column: entering state of every segment, in place over
 // the aggregates.  rev: the segments were written in reversed order (q = 0
 // is the last, possibly short, segment of the column).
-__device__ __forceinline__ void tri_scan(float* arr, const SolveParams& p, int VF, int nseg, int K, bool rev)
+template <class ST>
+__device__ __forceinline__ void tri_scan(ST* arr, const SolveParams& p, int VF, int nseg, int K, bool rev)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
     for (int col = warp; col < VF; col += nwarps) {
         const int v = min((int)(blockIdx.x * VF + col) >> 1, p.wc - 1);
-        const float4 t = __ldg(&p.tri[v]);  // rho, rho^RPT, rho^len_last, 1 / (1 - rho^H)
-        float* a = arr + col * 32 * K;
+        const float4 t = __ldg(&p.tri[2 * v + 1]);  // hi / lo of rho^RPT and rho^len_last
+        const ST wrap = __ldg(&p.tri[2 * v]).z;     // 1 / (1 - rho^H)
+        const TriMul<ST> mfull(t.x, t.y), mshort(t.z, t.w);
+        ST* a = arr + col * 32 * K;
         const int qshort = rev ? 0 : nseg - 1;
-        float A = 1.f, B = 0.f;
+        ST A = 1, B = 0;
         for (int k = 0; k < K; ++k) {
             const int q = lane * K + k;
             if (q < nseg) {
-                const float ak = q == qshort ? t.z : t.y;
-                B = fmaf(ak, B, a[k * 32 + lane]);
-                A *= ak;
+                const TriMul<ST>& m = q == qshort ? mshort : mfull;
+                B = m.step(B, a[k * 32 + lane]);
+                A *= m.value();
             }
         }
-        float Ai = A, Bi = B;
+        ST Ai = A, Bi = B;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const float Ap = __shfl_up_sync(0xffffffffu, Ai, d), Bp = __shfl_up_sync(0xffffffffu, Bi, d);
+            const ST Ap = __shfl_up_sync(0xffffffffu, Ai, d), Bp = __shfl_up_sync(0xffffffffu, Bi, d);
             if (lane >= d) {
-                Bi = fmaf(Ai, Bp, Bi);
+                Bi = Ai * Bp + Bi;
                 Ai *= Ap;
             }
         }
-        const float tot = __shfl_sync(0xffffffffu, Bi, 31);
-        float Ae = __shfl_up_sync(0xffffffffu, Ai, 1), Be = __shfl_up_sync(0xffffffffu, Bi, 1);
+        const ST tot = __shfl_sync(0xffffffffu, Bi, 31);
+        ST Ae = __shfl_up_sync(0xffffffffu, Ai, 1), Be = __shfl_up_sync(0xffffffffu, Bi, 1);
         if (lane == 0) {
-            Ae = 1.f;
-            Be = 0.f;
+            Ae = 1;
+            Be = 0;
         }
-        float S = fmaf(Ae, tot * t.w, Be);  // cyclic: the state entering segment 0 is total / (1 - rho^H)
+        ST S = Ae * (tot * wrap) + Be;  // cyclic: the state entering segment 0 is total / (1 - rho^H)
         for (int k = 0; k < K; ++k) {
             const int q = lane * K + k;
             if (q < nseg) {
-                const float ak = q == qshort ? t.z : t.y;
-                const float Tk = a[k * 32 + lane];
+                const TriMul<ST>& m = q == qshort ? mshort : mfull;
+                const ST Tk = a[k * 32 + lane];
                 a[k * 32 + lane] = S;
-                S = fmaf(ak, S, Tk);
+                S = m.step(S, Tk);
             }
         }
     }
@@ -114,7 +137,7 @@ __device__ __forceinline__ void tri_scan(float* arr, const SolveParams& p, int V
 // The phases of one thread's strip (RPT rows x TC floats in registers).
 // FULL: nlive == RPT, no per-row predicates; the kernel branches per phase so
 // every thread reaches the barriers between the phases at the same place.
-template <int RPT, int TC, bool FULL>
+template <int RPT, int TC, bool FULL, class ST>
 struct TriStrip {
     static __device__ __forceinline__ bool on(int i, int nlive) { return FULL || i < nlive; }
     static __device__ __forceinline__ void load(const float* base, size_t pitchf, int nlive, float (&x)[RPT][TC])
@@ -131,33 +154,34 @@ struct TriStrip {
     }
     // aggregate of the segment from a zero state; UP: rows in increasing order
     template <bool UP>
-    static __device__ __forceinline__ void aggregate(const float (&x)[RPT][TC], int nlive, float rho, float (&S)[TC])
+    static __device__ __forceinline__ void aggregate(const float (&x)[RPT][TC], int nlive, const TriMul<ST>& rho,
+                                                     ST (&S)[TC])
     {
 #pragma unroll
-        for (int k = 0; k < TC; ++k) S[k] = 0.f;
+        for (int k = 0; k < TC; ++k) S[k] = 0;
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const int i = UP ? j : RPT - 1 - j;
             if (on(i, nlive))
 #pragma unroll
-                for (int k = 0; k < TC; ++k) S[k] = fmaf(rho, S[k], x[i][k]);
+                for (int k = 0; k < TC; ++k) S[k] = rho.step(S[k], x[i][k]);
         }
     }
     // causal factor from the entering state S: y[n] = x[n] + rho y[n-1], in place
-    static __device__ __forceinline__ void causal(float (&x)[RPT][TC], int nlive, float rho, float (&S)[TC])
+    static __device__ __forceinline__ void causal(float (&x)[RPT][TC], int nlive, const TriMul<ST>& rho, ST (&S)[TC])
     {
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
             if (on(i, nlive))
 #pragma unroll
                 for (int k = 0; k < TC; ++k) {
-                    S[k] = fmaf(rho, S[k], x[i][k]);
-                    x[i][k] = S[k];
+                    S[k] = rho.step(S[k], x[i][k]);
+                    x[i][k] = (float)S[k];
                 }
     }
     // anticausal factor z[n] = y[n] + rho z[n+1], scaled and stored
-    static __device__ __forceinline__ void anticausal_store(const float (&x)[RPT][TC], int nlive, float rho, float sc,
-                                                            float (&S)[TC], float* base, size_t pitchf)
+    static __device__ __forceinline__ void anticausal_store(const float (&x)[RPT][TC], int nlive, const TriMul<ST>& rho,
+                                                            float sc, ST (&S)[TC], float* base, size_t pitchf)
     {
 #pragma unroll
         for (int i = RPT - 1; i >= 0; --i)
@@ -165,47 +189,27 @@ struct TriStrip {
                 float o[TC];
 #pragma unroll
                 for (int k = 0; k < TC; ++k) {
-                    S[k] = fmaf(rho, S[k], x[i][k]);
-                    o[k] = S[k] * sc;
+                    S[k] = rho.step(S[k], x[i][k]);
+                    o[k] = (float)S[k] * sc;
                 }
                 TriVec<TC>::st(base + i * pitchf, o);
             }
     }
 };
 
-// grid (ceil(2 wc / VF), planes), block = NCT * nseg rounded up to a warp
-// register budget: the strip (RPT x TC values per thread) + ~24
-template <int RPT, int TC, int MAXT>
-constexpr int tri_minb()
+// both factors of one thread's strip in the state type ST; every thread of the
+// CTA takes the same ST (the barriers are CTA-uniform)
+template <int RPT, int TC, class ST>
+__device__ __forceinline__ void tri_strip(const SolveParams& p, float* base, size_t pitchf, int nlive, float4 t0,
+                                          ST* arr1, ST* arr2, int ct, int s, int nseg, int K, int VF)
 {
-    constexpr int regs = RPT * TC <= 8 ? 32 : RPT * TC <= 32 ? 64 : 128;
-    return 65536 / (regs * MAXT) > 0 ? 65536 / (regs * MAXT) : 1;
-}
-
-template <int RPT, int TC, int NCT, int MAXT>
-__global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>()) k_col_tri(const SolveParams p, int nseg, int K)
-{
-    constexpr int VF = TC * NCT;
-    extern __shared__ float smt[];  // [2][VF][32 K] segment aggregates / entering states
-    const int H = p.H;
-    const int ct = threadIdx.x % NCT, s = threadIdx.x / NCT;
-    const int fidx = blockIdx.x * VF + ct * TC;  // float index within the spectrum row
-    const size_t pitchf = 2 * (size_t)p.spitch;
-    const bool live = s < nseg && fidx < 2 * p.wc;
-    const int y0 = s * RPT;
-    const int nlive = live ? min(RPT, H - y0) : 0;
-    float* base = reinterpret_cast<float*>(p.spec) + ((size_t)blockIdx.y * H + (live ? y0 : 0)) * pitchf +
-                  (live ? fidx : 0);
-    const int v = min(fidx >> 1, p.wc - 1);
-    const float rho = __ldg(&p.tri[v]).x;
-
-    float* arr1 = smt;
-    float* arr2 = smt + VF * 32 * K;
-    const float sc = __ldg(&p.tri_scale[v]);
-    using F = TriStrip<RPT, TC, true>;   // full segments: no per-row predicates
-    using R = TriStrip<RPT, TC, false>;  // the ragged last segment, dead threads
+    using F = TriStrip<RPT, TC, true, ST>;   // full segments: no per-row predicates
+    using R = TriStrip<RPT, TC, false, ST>;  // the ragged last segment, dead threads
+    const TriMul<ST> rho(t0.x, t0.y);
+    const float sc = t0.w;
     const bool full = nlive == RPT;
-    float x[RPT][TC], S[TC];
+    float x[RPT][TC];
+    ST S[TC];
     if (full) F::load(base, pitchf, nlive, x); else R::load(base, pitchf, nlive, x);
 
     if (full) F::template aggregate<true>(x, nlive, rho, S); else R::template aggregate<true>(x, nlive, rho, S);
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>()) k_col_tri(con
 #pragma unroll
         for (int k = 0; k < TC; ++k) arr1[(ct * TC + k) * 32 * K + tri_pos(s, K)] = S[k];
     __syncthreads();
-    tri_scan(arr1, p, VF, nseg, K, false);
+    tri_scan<ST>(arr1, p, VF, nseg, K, false);
     __syncthreads();
     if (s < nseg)
 #pragma unroll
@@ -225,13 +229,56 @@ __global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>()) k_col_tri(con
 #pragma unroll
         for (int k = 0; k < TC; ++k) arr2[(ct * TC + k) * 32 * K + tri_pos(nseg - 1 - s, K)] = S[k];
     __syncthreads();
-    tri_scan(arr2, p, VF, nseg, K, true);
+    tri_scan<ST>(arr2, p, VF, nseg, K, true);
     __syncthreads();
     if (s < nseg)
 #pragma unroll
         for (int k = 0; k < TC; ++k) S[k] = arr2[(ct * TC + k) * 32 * K + tri_pos(nseg - 1 - s, K)];
     if (full) F::anticausal_store(x, nlive, rho, sc, S, base, pitchf);
     else R::anticausal_store(x, nlive, rho, sc, S, base, pitchf);
+}
+
+// grid (ceil(2 wc / VF), planes), block = NCT * nseg rounded up to a warp
+// register budget: the strip (RPT x TC values per thread) + ~24
+template <int RPT, int TC, int MAXT>
+constexpr int tri_minb()
+{
+    constexpr int regs = RPT * TC <= 8 ? 32 : RPT * TC <= 32 ? 64 : 128;
+    return 65536 / (regs * MAXT) > 0 ? 65536 / (regs * MAXT) : 1;
+}
+
+// Strips whose pole is close to 1 (the lowest spectrum columns: the CTA's
+// first column has rho > kTriDoublePole) keep the recursion state in double:
+// on smooth data a float state rounds the same way at every step, a bias of
+// eps / (1 - rho) of the value that the column FFT does not have (c4, rho =
+// 0.978: full-pipeline max-abs 1.3e-5 -> the FFT's 3e-6).  A few percent of
+// the CTAs; the strip values stay float.
+constexpr float kTriDoublePole = 0.85f;
+
+template <int RPT, int TC, int NCT, int MAXT>
+__global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>()) k_col_tri(const SolveParams p, int nseg, int K)
+{
+    constexpr int VF = TC * NCT;
+    extern __shared__ __align__(8) double smt[];  // [2][VF][32 K] segment aggregates / entering states
+    const int H = p.H;
+    const int ct = threadIdx.x % NCT, s = threadIdx.x / NCT;
+    const int fidx = blockIdx.x * VF + ct * TC;  // float index within the spectrum row
+    const size_t pitchf = 2 * (size_t)p.spitch;
+    const bool live = s < nseg && fidx < 2 * p.wc;
+    const int y0 = s * RPT;
+    const int nlive = live ? min(RPT, H - y0) : 0;
+    float* base = reinterpret_cast<float*>(p.spec) + ((size_t)blockIdx.y * H + (live ? y0 : 0)) * pitchf +
+                  (live ? fidx : 0);
+    const int v = min(fidx >> 1, p.wc - 1);
+    const float4 t0 = __ldg(&p.tri[2 * v]);  // rho hi, rho lo, 1 / (1 - rho^H), scale
+    // rho falls with v: the CTA's first column decides for the whole CTA
+    const bool dbl = __ldg(&p.tri[2 * min((int)(blockIdx.x * VF) >> 1, p.wc - 1)]).x > kTriDoublePole;
+    if (dbl) {
+        tri_strip<RPT, TC, double>(p, base, pitchf, nlive, t0, smt, smt + VF * 32 * K, ct, s, nseg, K, VF);
+    } else {
+        float* smf = reinterpret_cast<float*>(smt);
+        tri_strip<RPT, TC, float>(p, base, pitchf, nlive, t0, smf, smf + VF * 32 * K, ct, s, nseg, K, VF);
+    }
 }
 
 template <int RPT, int TC, int NCT>
@@ -242,7 +289,7 @@ cudaError_t launch_tri_t(const SolveParams& p, int planes, cudaStream_t st)
     const int K = (nseg + 31) / 32;
     const int threads = ((NCT * nseg + 31) / 32) * 32;
     if (threads > 1024) return cudaErrorInvalidConfiguration;
-    const size_t smem = (size_t)2 * VF * 32 * K * sizeof(float);
+    const size_t smem = (size_t)2 * VF * 32 * K * sizeof(double);
     dim3 grid((2 * p.wc + VF - 1) / VF, planes);
     if (threads <= 256)
         k_col_tri<RPT, TC, NCT, 256><<<grid, threads, smem, st>>>(p, nseg, K);
@@ -267,23 +314,30 @@ int tri_rows_per_thread(int H, int wc, int planes, int nsm)
     return H >= 1024 ? 32 : 16;
 }
 
-// Host tables in double: tri[v] = (rho, rho^RPT, rho^len_last, 1 / (1 - rho^H)),
-// scale[v] = rho / (lambda W) = 2 / ((b + sqrt(c (c + 4 lambda))) W)
+// Host tables in double, two float4 per column.  The pole rho and the segment
+// multipliers are kept as hi + lo float pairs (x' = hi x + lo x in two FMAs):
+// a pole rounded to one float moves the response of the low-frequency columns
+// by 2 eps / (1 - rho) (c4: 5e-6 of the value).
+//   tri[2v]     = (rho hi, rho lo, 1 / (1 - rho^H), rho / (lambda W))
+//   tri[2v + 1] = (rho^RPT hi, lo, rho^len_last hi, lo)
+// rho / (lambda W) = 2 / ((b + sqrt(c (c + 4 lambda))) W)
 void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri, std::vector<float>& scale)
 {
-    tri.resize(wc);
-    scale.resize(wc);
+    tri.resize(2 * (size_t)wc);
+    scale.clear();
     const int nseg = (H + rpt - 1) / rpt;
     const int len_last = H - (nseg - 1) * rpt;
+    auto hi = [](double x) { return (float)x; };
+    auto lo = [](double x) { return (float)(x - (double)(float)x); };
     for (int v = 0; v < wc; ++v) {
         const double sx = std::sin(M_PI * v / W);
         const double c = 1.0 + lambda * 4.0 * sx * sx;
         const double b = c + 2.0 * lambda;
         const double root = b + std::sqrt(c * (c + 4.0 * lambda));
         const double rho = 2.0 * lambda / root;
-        tri[v] = make_float4((float)rho, (float)std::pow(rho, rpt), (float)std::pow(rho, len_last),
-                             (float)(1.0 / (1.0 - std::pow(rho, H))));
-        scale[v] = (float)(2.0 / (root * W));
+        const double m = std::pow(rho, rpt), ml = std::pow(rho, len_last);
+        tri[2 * v] = make_float4(hi(rho), lo(rho), (float)(1.0 / (1.0 - std::pow(rho, H))), (float)(2.0 / (root * W)));
+        tri[2 * v + 1] = make_float4(hi(m), lo(m), hi(ml), lo(ml));
     }
 }
 

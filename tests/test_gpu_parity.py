@@ -193,8 +193,8 @@ def test_guidance_equal_input_matches_self(gpu, oracle):
     # exact in the reference (one code path); here the self-guided and the guided
     # filter are different kernels whose targets differ in the last bits, and the
     # solve sees them scaled by lambda = 1024 (|f + lambda div T| ~ 100): measured
-    # 1.7e-6 (6.0e-7 with the column FFT pair of r01, tools/tri_accuracy.py)
-    assert maxabs(a, b) <= 3e-6
+    # 9.5e-7 (6.0e-7 with the column FFT pair of r01, tools/tri_accuracy.py)
+    assert maxabs(a, b) <= 2e-6
 
 
 def test_fidelity_monotone_in_lambda(gpu, oracle):
