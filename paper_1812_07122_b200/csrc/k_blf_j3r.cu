@@ -119,7 +119,7 @@ struct J3rGeom {
 };
 
 // the taps of one staged source row for the output rows in MASK (bit k: row k)
-template <int R, int MASK, int FAKE = 0, int POLYK = 0>
+template <int R, int MASK, int POLYK>
 __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restrict__ grow,
                                         const float2* __restrict__ s01, const float2* __restrict__ s2, int tx,
                                         const unsigned long long (&gsp)[2][2], unsigned long long (&a01)[2][4],
@@ -135,9 +135,8 @@ __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restr
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int pc = r_sw(tx * P + j4 + 2 * h);
-            // FAKE (experiments): no source loads -- the MUFU / FFMA2 mix without the LDS traffic
-            const float4 a = FAKE ? make_float4(g4.x, g4.y, g4.z, g4.w) : *reinterpret_cast<const float4*>(s01 + pc);
-            const float4 c = FAKE ? make_float4(g4.w, g4.z, g4.y, g4.x) : *reinterpret_cast<const float4*>(s2 + pc);
+            const float4 a = *reinterpret_cast<const float4*>(s01 + pc);
+            const float4 c = *reinterpret_cast<const float4*>(s2 + pc);
             asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h]) : "f"(a.x), "f"(a.y));
             asm("mov.b64 %0, {%1, %2};" : "=l"(v01[2 * h + 1]) : "f"(a.z), "f"(a.w));
             asm("mov.b64 %0, {%1, %2};" : "=l"(v2z[2 * h]) : "f"(c.x), "f"(c.y));
@@ -189,7 +188,7 @@ __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restr
 }  // namespace
 
 // blockIdx.z = image * 2 + axis; PEERS: fused band exchange (k_blf_j3.cu)
-template <int R, bool PEERS, int FAKE = 0, int POLYK = 0>
+template <int R, bool PEERS, int POLYK>
 __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
 {
     using Gm = J3rGeom<R>;
@@ -337,7 +336,7 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
     const float* grow = G + (2 * typ) * GP + tx * P;
     const float2* s01 = S01 + (2 * typ) * SP;
     const float2* s2 = S2 + (2 * typ) * SP;
-    j3r_row<R, 1, FAKE, POLYK>(p, grow, s01, s2, tx, gsp, a01, a2z);
+    j3r_row<R, 1, POLYK>(p, grow, s01, s2, tx, gsp, a01, a2z);
 #pragma unroll 1
     for (int i = 1; i <= 2 * R; ++i) {
         grow += GP;
@@ -351,7 +350,7 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
             a01[1][q] = r_fmul2(f1, a01[1][q]);
             a2z[1][q] = r_fmul2(f1, a2z[1][q]);
         }
-        j3r_row<R, 3, FAKE, POLYK>(p, grow, s01, s2, tx, gsp, a01, a2z);
+        j3r_row<R, 3, POLYK>(p, grow, s01, s2, tx, gsp, a01, a2z);
     }
     {
         const float f1 = p.rfold[2 * R];
@@ -360,7 +359,7 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
             a01[1][q] = r_fmul2(f1, a01[1][q]);
             a2z[1][q] = r_fmul2(f1, a2z[1][q]);
         }
-        j3r_row<R, 2, FAKE, POLYK>(p, grow + GP, s01 + SP, s2 + SP, tx, gsp, a01, a2z);
+        j3r_row<R, 2, POLYK>(p, grow + GP, s01 + SP, s2 + SP, tx, gsp, a01, a2z);
     }
 
     const int ox = tx0 + tx * P;
@@ -405,16 +404,16 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
     }
 }
 
-template <int R, bool PEERS, int FAKE = 0, int POLYK = 0>
+template <int R, bool PEERS, int POLYK>
 static cudaError_t launch_j3r_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J3rGeom<R>;
     constexpr size_t smem = Gm::smem_bytes();
     cudaError_t e =
-        cudaFuncSetAttribute(k_blf_j3r<R, PEERS, FAKE, POLYK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blf_j3r<R, PEERS, POLYK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + Gm::TH - 1) / Gm::TH, 2 * batch);
-    k_blf_j3r<R, PEERS, FAKE, POLYK><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_j3r<R, PEERS, POLYK><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -431,22 +430,22 @@ bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaErr
     // freed MUFU slots pay (c5 r02: 0.870 -> 0.891 of the MUFU rate; periods
     // 24 / 16 / 10 / 8 / 6: 0.887 / 0.887 / 0.889 / 0.887 / 0.872).  The
     // peer-storing band epilogue uses the same arithmetic.
+    // Measured and removed (profiles/r02_ab_summary.md): the same loop without
+    // its source loads reaches 0.925 (the LDS traffic costs ~5 points through
+    // the shared MIO queue); an L2 prefetch of a later tile's raw rows 0.891;
+    // two staging tasks in flight per thread (spills at 80 registers) 0.862.
 #ifdef BLFLS_EXPERIMENTS
-    if (knob("BLFLS_J3R_FAKE", 0)) {  // wrong results: pipe-interference experiment only
-        *err = launch_j3r_t<7, false, 1>(p, batch, st);
-        return true;
-    }
     switch (p.npeers > 0 ? 12 : knob("BLFLS_J3R_POLY", 12)) {
-        case 0: *err = launch_j3r_t<7, false, 0, 0>(p, batch, st); return true;
-        case 6: *err = launch_j3r_t<7, false, 0, 6>(p, batch, st); return true;
-        case 8: *err = launch_j3r_t<7, false, 0, 8>(p, batch, st); return true;
-        case 10: *err = launch_j3r_t<7, false, 0, 10>(p, batch, st); return true;
-        case 16: *err = launch_j3r_t<7, false, 0, 16>(p, batch, st); return true;
-        case 24: *err = launch_j3r_t<7, false, 0, 24>(p, batch, st); return true;
+        case 0: *err = launch_j3r_t<7, false, 0>(p, batch, st); return true;
+        case 6: *err = launch_j3r_t<7, false, 6>(p, batch, st); return true;
+        case 8: *err = launch_j3r_t<7, false, 8>(p, batch, st); return true;
+        case 10: *err = launch_j3r_t<7, false, 10>(p, batch, st); return true;
+        case 16: *err = launch_j3r_t<7, false, 16>(p, batch, st); return true;
+        case 24: *err = launch_j3r_t<7, false, 24>(p, batch, st); return true;
         default: break;
     }
 #endif
-    *err = p.npeers > 0 ? launch_j3r_t<7, true, 0, 12>(p, batch, st) : launch_j3r_t<7, false, 0, 12>(p, batch, st);
+    *err = p.npeers > 0 ? launch_j3r_t<7, true, 12>(p, batch, st) : launch_j3r_t<7, false, 12>(p, batch, st);
     return true;
 }
 
