@@ -77,14 +77,19 @@ def blf_kernel_name(cfg):
     """The brute-force BLF kernel the library dispatches for this config
     (k_blf.cu launch_grad_blf): the factorised-exponent form whenever
     2 range_coef^2 <= 60 (range_coef = sqrt(log2 e / (8 sigma_r^2)), i.e.
-    sigma_r >= 0.0775), else the difference form; k_blf_j3 for a gray guide
-    over RGB (r = 3, 5, 7, 15), k_blf_p2 for self-guided r = 5, 7, 15 with
+    sigma_r >= 0.0775), else the difference form; for a gray guide over RGB
+    k_blf_j3r at r = 7 with factorised exponents (c5), k_blf_j3 at r = 3, 5,
+    15 or the difference form; k_blf_p2 for self-guided r = 5, 7, 15 with
     the FMA-pipe exp2 offload period of k_blf_p2.cu kP2XfPoly / kP2DefaultPoly,
     k_grad_blf otherwise."""
     import math
     coef2 = math.log2(math.e) / (8.0 * cfg.sigma_r ** 2)
     xf = 2.0 * coef2 <= 60.0
     form = "factorised exponents" if xf else "difference-form pair exponents"
+    if cfg.guide and cfg.channels == 3 and cfg.radius == 7 and xf:
+        return ("k_blf_j3r (fused gradient + shared-gray-guide brute-force BLF, two output rows x four columns "
+                "per thread, FFMA2-packed sums, factorised exponents, row factor folded into the sums, FMA-pipe "
+                "exp2 on every 12th exponent pair, 32 x 64 tiles staged by aligned column quads, 3 CTAs/SM)")
     if cfg.guide and cfg.channels == 3 and cfg.radius in (3, 5, 7, 15):
         tiles = ", 32-row tiles, 2 CTAs/SM)" if xf and cfg.radius == 7 else (", 4 CTAs/SM)" if xf else ", 2 CTAs/SM)")
         return (f"k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, {form}" + tiles)

@@ -221,7 +221,7 @@ struct SolveParams {
 int tri_rows_per_thread(int H, int wc, int planes, int nsm);
 bool tri_supported(int H, int rpt);
 void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri, std::vector<float>& scale);
-cudaError_t launch_col_tri(const SolveParams& p, int planes, cudaStream_t st);
+cudaError_t launch_col_tri(const SolveParams& p, int planes, int nsm, cudaStream_t st);
 
 
 // high-radix solve passes (k_solve2.cu): false when no geometry exists for n

@@ -63,72 +63,84 @@ struct TriVec<2> {
 // q / K reads its K consecutive segments conflict-free
 __device__ __forceinline__ int tri_pos(int q, int K) { return (q % K) * 32 + q / K; }
 
-// One recursion step x' = m x + t in the state type ST.  float: the multiplier
-// as a hi + lo pair (two FMAs); double (the low-frequency columns, below): one
-// DFMA with m = hi + lo.
-template <class ST>
-struct TriMul;
-template <>
-struct TriMul<float> {
-    float hi, lo;
-    __device__ __forceinline__ TriMul(float h, float l) : hi(h), lo(l) {}
-    __device__ __forceinline__ float step(float S, float t) const { return fmaf(lo, S, fmaf(hi, S, t)); }
-    __device__ __forceinline__ float value() const { return hi; }
+// One recursion step S' = m S + t.  TriPlain: the state is one float.  TriComp
+// (the low-frequency strips, below): the state is an unevaluated float pair
+// h + l and the multiplier a hi + lo pair.  The rounding error of
+// y = fl(m.hi h + t) is recovered as fl(m.hi h - y) + t -- that FMA result has
+// the magnitude of t, (1 - rho) of the state's, so its own rounding is a few
+// percent of the error it measures -- and carried in l, so the recursion does
+// not accumulate the systematic rounding of a float state.  5 FP32 operations
+// per step instead of 1; an exact two-sum version (11) measured no better, a
+// double state 8x slower per CTA.
+struct TriPlain {
+    float h;
+    __device__ __forceinline__ void zero() { h = 0.f; }
+    __device__ __forceinline__ void set(float v) { h = v; }
+    __device__ __forceinline__ float value() const { return h; }
+    __device__ __forceinline__ void step(float mh, float, float t) { h = fmaf(mh, h, t); }
 };
-template <>
-struct TriMul<double> {
-    double m;
-    __device__ __forceinline__ TriMul(float h, float l) : m((double)h + (double)l) {}
-    __device__ __forceinline__ double step(double S, double t) const { return fma(m, S, t); }
-    __device__ __forceinline__ double value() const { return m; }
+struct TriComp {
+    float h, l;
+    __device__ __forceinline__ void zero() { h = l = 0.f; }
+    __device__ __forceinline__ void set(float v)
+    {
+        h = v;
+        l = 0.f;
+    }
+    __device__ __forceinline__ float value() const { return h + l; }
+    __device__ __forceinline__ void step(float mh, float ml, float t)
+    {
+        const float y = fmaf(mh, h, t);
+        const float r = fmaf(ml, h, __fadd_rn(fmaf(mh, h, -y), t));
+        l = fmaf(mh, l, r);
+        h = y;
+    }
 };
 
 // One warp per real column: entering state of every segment, in place over
 // the aggregates.  rev: the segments were written in reversed order (q = 0
 // is the last, possibly short, segment of the column).
-template <class ST>
-__device__ __forceinline__ void tri_scan(ST* arr, const SolveParams& p, int VF, int nseg, int K, bool rev)
+__device__ __forceinline__ void tri_scan(float* arr, const SolveParams& p, int VF, int nseg, int K, bool rev)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
     for (int col = warp; col < VF; col += nwarps) {
         const int v = min((int)(blockIdx.x * VF + col) >> 1, p.wc - 1);
         const float4 t = __ldg(&p.tri[2 * v + 1]);  // hi / lo of rho^RPT and rho^len_last
-        const ST wrap = __ldg(&p.tri[2 * v]).z;     // 1 / (1 - rho^H)
-        const TriMul<ST> mfull(t.x, t.y), mshort(t.z, t.w);
-        ST* a = arr + col * 32 * K;
+        const float wrap = __ldg(&p.tri[2 * v]).z;  // 1 / (1 - rho^H)
+        float* a = arr + col * 32 * K;
         const int qshort = rev ? 0 : nseg - 1;
-        ST A = 1, B = 0;
+        float A = 1.f, B = 0.f;
         for (int k = 0; k < K; ++k) {
             const int q = lane * K + k;
             if (q < nseg) {
-                const TriMul<ST>& m = q == qshort ? mshort : mfull;
-                B = m.step(B, a[k * 32 + lane]);
-                A *= m.value();
+                const float ak = q == qshort ? t.z : t.x, al = q == qshort ? t.w : t.y;
+                B = fmaf(al, B, fmaf(ak, B, a[k * 32 + lane]));
+                A *= ak;
             }
         }
-        ST Ai = A, Bi = B;
+        float Ai = A, Bi = B;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const ST Ap = __shfl_up_sync(0xffffffffu, Ai, d), Bp = __shfl_up_sync(0xffffffffu, Bi, d);
+            const float Ap = __shfl_up_sync(0xffffffffu, Ai, d), Bp = __shfl_up_sync(0xffffffffu, Bi, d);
             if (lane >= d) {
-                Bi = Ai * Bp + Bi;
+                Bi = fmaf(Ai, Bp, Bi);
                 Ai *= Ap;
             }
         }
-        const ST tot = __shfl_sync(0xffffffffu, Bi, 31);
-        ST Ae = __shfl_up_sync(0xffffffffu, Ai, 1), Be = __shfl_up_sync(0xffffffffu, Bi, 1);
+        const float tot = __shfl_sync(0xffffffffu, Bi, 31);
+        float Ae = __shfl_up_sync(0xffffffffu, Ai, 1), Be = __shfl_up_sync(0xffffffffu, Bi, 1);
         if (lane == 0) {
-            Ae = 1;
-            Be = 0;
+            Ae = 1.f;
+            Be = 0.f;
         }
-        ST S = Ae * (tot * wrap) + Be;  // cyclic: the state entering segment 0 is total / (1 - rho^H)
+        float S = fmaf(Ae, tot * wrap, Be);  // cyclic: the state entering segment 0 is total / (1 - rho^H)
         for (int k = 0; k < K; ++k) {
             const int q = lane * K + k;
             if (q < nseg) {
-                const TriMul<ST>& m = q == qshort ? mshort : mfull;
-                const ST Tk = a[k * 32 + lane];
+                const float ak = q == qshort ? t.z : t.x, al = q == qshort ? t.w : t.y;
+                const float Tk = a[k * 32 + lane];
                 a[k * 32 + lane] = S;
-                S = m.step(S, Tk);
+                S = fmaf(al, S, fmaf(ak, S, Tk));
             }
         }
     }
@@ -154,33 +166,33 @@ struct TriStrip {
     }
     // aggregate of the segment from a zero state; UP: rows in increasing order
     template <bool UP>
-    static __device__ __forceinline__ void aggregate(const float (&x)[RPT][TC], int nlive, const TriMul<ST>& rho,
+    static __device__ __forceinline__ void aggregate(const float (&x)[RPT][TC], int nlive, float rh, float rl,
                                                      ST (&S)[TC])
     {
 #pragma unroll
-        for (int k = 0; k < TC; ++k) S[k] = 0;
+        for (int k = 0; k < TC; ++k) S[k].zero();
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const int i = UP ? j : RPT - 1 - j;
             if (on(i, nlive))
 #pragma unroll
-                for (int k = 0; k < TC; ++k) S[k] = rho.step(S[k], x[i][k]);
+                for (int k = 0; k < TC; ++k) S[k].step(rh, rl, x[i][k]);
         }
     }
     // causal factor from the entering state S: y[n] = x[n] + rho y[n-1], in place
-    static __device__ __forceinline__ void causal(float (&x)[RPT][TC], int nlive, const TriMul<ST>& rho, ST (&S)[TC])
+    static __device__ __forceinline__ void causal(float (&x)[RPT][TC], int nlive, float rh, float rl, ST (&S)[TC])
     {
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
             if (on(i, nlive))
 #pragma unroll
                 for (int k = 0; k < TC; ++k) {
-                    S[k] = rho.step(S[k], x[i][k]);
-                    x[i][k] = (float)S[k];
+                    S[k].step(rh, rl, x[i][k]);
+                    x[i][k] = S[k].value();
                 }
     }
     // anticausal factor z[n] = y[n] + rho z[n+1], scaled and stored
-    static __device__ __forceinline__ void anticausal_store(const float (&x)[RPT][TC], int nlive, const TriMul<ST>& rho,
+    static __device__ __forceinline__ void anticausal_store(const float (&x)[RPT][TC], int nlive, float rh, float rl,
                                                             float sc, ST (&S)[TC], float* base, size_t pitchf)
     {
 #pragma unroll
@@ -189,53 +201,52 @@ struct TriStrip {
                 float o[TC];
 #pragma unroll
                 for (int k = 0; k < TC; ++k) {
-                    S[k] = rho.step(S[k], x[i][k]);
-                    o[k] = (float)S[k] * sc;
+                    S[k].step(rh, rl, x[i][k]);
+                    o[k] = S[k].value() * sc;
                 }
                 TriVec<TC>::st(base + i * pitchf, o);
             }
     }
 };
 
-// both factors of one thread's strip in the state type ST; every thread of the
-// CTA takes the same ST (the barriers are CTA-uniform)
+// both factors of one thread's strip with the state type ST; every thread of
+// the CTA takes the same ST (the barriers are CTA-uniform)
 template <int RPT, int TC, class ST>
 __device__ __forceinline__ void tri_strip(const SolveParams& p, float* base, size_t pitchf, int nlive, float4 t0,
-                                          ST* arr1, ST* arr2, int ct, int s, int nseg, int K, int VF)
+                                          float* arr1, float* arr2, int ct, int s, int nseg, int K, int VF)
 {
     using F = TriStrip<RPT, TC, true, ST>;   // full segments: no per-row predicates
     using R = TriStrip<RPT, TC, false, ST>;  // the ragged last segment, dead threads
-    const TriMul<ST> rho(t0.x, t0.y);
-    const float sc = t0.w;
-    const bool full = nlive == RPT;
+    const float rh = t0.x, rl = t0.y, sc = t0.w;
+    // one path per warp: a warp that holds the ragged segment (or dead
+    // threads) runs the predicated phases for all its threads
+    const bool full = __all_sync(0xffffffffu, nlive == RPT);
     float x[RPT][TC];
     ST S[TC];
     if (full) F::load(base, pitchf, nlive, x); else R::load(base, pitchf, nlive, x);
 
-    if (full) F::template aggregate<true>(x, nlive, rho, S); else R::template aggregate<true>(x, nlive, rho, S);
+    if (full) F::template aggregate<true>(x, nlive, rh, rl, S); else R::template aggregate<true>(x, nlive, rh, rl, S);
     if (s < nseg)
 #pragma unroll
-        for (int k = 0; k < TC; ++k) arr1[(ct * TC + k) * 32 * K + tri_pos(s, K)] = S[k];
+        for (int k = 0; k < TC; ++k) arr1[(ct * TC + k) * 32 * K + tri_pos(s, K)] = S[k].value();
     __syncthreads();
-    tri_scan<ST>(arr1, p, VF, nseg, K, false);
+    tri_scan(arr1, p, VF, nseg, K, false);
     __syncthreads();
-    if (s < nseg)
 #pragma unroll
-        for (int k = 0; k < TC; ++k) S[k] = arr1[(ct * TC + k) * 32 * K + tri_pos(s, K)];
-    if (full) F::causal(x, nlive, rho, S); else R::causal(x, nlive, rho, S);
+    for (int k = 0; k < TC; ++k) S[k].set(s < nseg ? arr1[(ct * TC + k) * 32 * K + tri_pos(s, K)] : 0.f);
+    if (full) F::causal(x, nlive, rh, rl, S); else R::causal(x, nlive, rh, rl, S);
 
-    if (full) F::template aggregate<false>(x, nlive, rho, S); else R::template aggregate<false>(x, nlive, rho, S);
+    if (full) F::template aggregate<false>(x, nlive, rh, rl, S); else R::template aggregate<false>(x, nlive, rh, rl, S);
     if (s < nseg)
 #pragma unroll
-        for (int k = 0; k < TC; ++k) arr2[(ct * TC + k) * 32 * K + tri_pos(nseg - 1 - s, K)] = S[k];
+        for (int k = 0; k < TC; ++k) arr2[(ct * TC + k) * 32 * K + tri_pos(nseg - 1 - s, K)] = S[k].value();
     __syncthreads();
-    tri_scan<ST>(arr2, p, VF, nseg, K, true);
+    tri_scan(arr2, p, VF, nseg, K, true);
     __syncthreads();
-    if (s < nseg)
 #pragma unroll
-        for (int k = 0; k < TC; ++k) S[k] = arr2[(ct * TC + k) * 32 * K + tri_pos(nseg - 1 - s, K)];
-    if (full) F::anticausal_store(x, nlive, rho, sc, S, base, pitchf);
-    else R::anticausal_store(x, nlive, rho, sc, S, base, pitchf);
+    for (int k = 0; k < TC; ++k) S[k].set(s < nseg ? arr2[(ct * TC + k) * 32 * K + tri_pos(nseg - 1 - s, K)] : 0.f);
+    if (full) F::anticausal_store(x, nlive, rh, rl, sc, S, base, pitchf);
+    else R::anticausal_store(x, nlive, rh, rl, sc, S, base, pitchf);
 }
 
 // grid (ceil(2 wc / VF), planes), block = NCT * nseg rounded up to a warp
@@ -248,18 +259,18 @@ constexpr int tri_minb()
 }
 
 // Strips whose pole is close to 1 (the lowest spectrum columns: the CTA's
-// first column has rho > kTriDoublePole) keep the recursion state in double:
-// on smooth data a float state rounds the same way at every step, a bias of
-// eps / (1 - rho) of the value that the column FFT does not have (c4, rho =
-// 0.978: full-pipeline max-abs 1.3e-5 -> the FFT's 3e-6).  A few percent of
-// the CTAs; the strip values stay float.
-constexpr float kTriDoublePole = 0.85f;
+// first column has rho > kTriCompPole) run the compensated recursion: a float
+// state rounds with a bias of eps / (1 - rho) of the value that the column
+// FFT does not have (c4, rho = 0.978: full-pipeline max-abs 1.3e-5 against
+// the FFT's 3.2e-6; compensated: 2.5e-6).  A few percent of the CTAs.
+constexpr float kTriCompPole = 0.85f;
 
 template <int RPT, int TC, int NCT, int MAXT>
-__global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>()) k_col_tri(const SolveParams p, int nseg, int K)
+__global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>())
+    k_col_tri(const SolveParams p, int nseg, int K, float pole)
 {
     constexpr int VF = TC * NCT;
-    extern __shared__ __align__(8) double smt[];  // [2][VF][32 K] segment aggregates / entering states
+    extern __shared__ float smt[];  // [2][VF][32 K] segment aggregates / entering states
     const int H = p.H;
     const int ct = threadIdx.x % NCT, s = threadIdx.x / NCT;
     const int fidx = blockIdx.x * VF + ct * TC;  // float index within the spectrum row
@@ -272,13 +283,13 @@ __global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>()) k_col_tri(con
     const int v = min(fidx >> 1, p.wc - 1);
     const float4 t0 = __ldg(&p.tri[2 * v]);  // rho hi, rho lo, 1 / (1 - rho^H), scale
     // rho falls with v: the CTA's first column decides for the whole CTA
-    const bool dbl = __ldg(&p.tri[2 * min((int)(blockIdx.x * VF) >> 1, p.wc - 1)]).x > kTriDoublePole;
-    if (dbl) {
-        tri_strip<RPT, TC, double>(p, base, pitchf, nlive, t0, smt, smt + VF * 32 * K, ct, s, nseg, K, VF);
-    } else {
-        float* smf = reinterpret_cast<float*>(smt);
-        tri_strip<RPT, TC, float>(p, base, pitchf, nlive, t0, smf, smf + VF * 32 * K, ct, s, nseg, K, VF);
-    }
+    const bool comp = __ldg(&p.tri[2 * min((int)(blockIdx.x * VF) >> 1, p.wc - 1)]).x > pole;
+    float* arr1 = smt;
+    float* arr2 = smt + VF * 32 * K;
+    if (comp)
+        tri_strip<RPT, TC, TriComp>(p, base, pitchf, nlive, t0, arr1, arr2, ct, s, nseg, K, VF);
+    else
+        tri_strip<RPT, TC, TriPlain>(p, base, pitchf, nlive, t0, arr1, arr2, ct, s, nseg, K, VF);
 }
 
 template <int RPT, int TC, int NCT>
@@ -289,29 +300,33 @@ cudaError_t launch_tri_t(const SolveParams& p, int planes, cudaStream_t st)
     const int K = (nseg + 31) / 32;
     const int threads = ((NCT * nseg + 31) / 32) * 32;
     if (threads > 1024) return cudaErrorInvalidConfiguration;
-    const size_t smem = (size_t)2 * VF * 32 * K * sizeof(double);
+    const size_t smem = (size_t)2 * VF * 32 * K * sizeof(float);
     dim3 grid((2 * p.wc + VF - 1) / VF, planes);
+    const float pole = 0.01f * knob("BLFLS_TRI_COMP", (int)(100 * kTriCompPole));  // experiments: 200 = never
     if (threads <= 256)
-        k_col_tri<RPT, TC, NCT, 256><<<grid, threads, smem, st>>>(p, nseg, K);
+        k_col_tri<RPT, TC, NCT, 256><<<grid, threads, smem, st>>>(p, nseg, K, pole);
     else if (threads <= 512)
-        k_col_tri<RPT, TC, NCT, 512><<<grid, threads, smem, st>>>(p, nseg, K);
+        k_col_tri<RPT, TC, NCT, 512><<<grid, threads, smem, st>>>(p, nseg, K, pole);
     else
-        k_col_tri<RPT, TC, NCT, 1024><<<grid, threads, smem, st>>>(p, nseg, K);
+        k_col_tri<RPT, TC, NCT, 1024><<<grid, threads, smem, st>>>(p, nseg, K, pole);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-// rows per thread of the tridiagonal column pass: 32 (one strip = 4 thread
-// columns x H / 32 segments; measured fastest on every BASELINE size,
-// profiles/r02_tri_ab.txt); 16 for short columns so a strip still fills
-// four warps
+// rows per thread of the tridiagonal column pass: 32 (64 strip values per
+// thread, 128 registers, 512 resident threads per SM) when the launch fills
+// the GPU several times over (c4, c5: streaming from HBM, 128 KB of loads in
+// flight per SM), else 16 (twice the threads at 64 registers: c1-c3 are one
+// or two waves, latency-bound).  Measured with the bench's stage timers,
+// cold L2 (profiles/r02_tri_ab.txt).
 int tri_rows_per_thread(int H, int wc, int planes, int nsm)
 {
     const int forced = knob("BLFLS_TRI_RPT", 0);
     if (forced == 8 || forced == 16 || forced == 32) return forced;
-    (void)wc, (void)planes, (void)nsm;
-    return H >= 1024 ? 32 : 16;
+    const long strips = (long)planes * ((2 * wc + 7) / 8);
+    const long threads32 = strips * 4 * ((H + 31) / 32);
+    return threads32 >= 5L * 256 * nsm && H >= 1024 ? 32 : 16;
 }
 
 // Host tables in double, two float4 per column.  The pole rho and the segment
@@ -343,17 +358,20 @@ void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4
 
 bool tri_supported(int H, int rpt) { return 4 * ((H + rpt - 1) / rpt) <= 1024 && H >= 2; }
 
-cudaError_t launch_col_tri(const SolveParams& p, int planes, cudaStream_t st)
+cudaError_t launch_col_tri(const SolveParams& p, int planes, int nsm, cudaStream_t st)
 {
-    // thread shape: TC floats per thread x NCT thread columns (VF = TC NCT
-    // floats = VF / 2 spectrum columns per CTA).  Default: one complex value
-    // per thread and row (8-byte loads), 4 columns = one 32-byte sector per
-    // row and CTA; at RPT = 32 that is 64 data registers, 2 CTAs of 256
-    // threads per SM with 128 KB of loads in flight (c5: 1.47 ms per
-    // iteration, 4.45 TB/s; the scalar 8-column shape 1.66 ms).
-#ifdef BLFLS_EXPERIMENTS
-    const int shape = knob("BLFLS_TRI_SHAPE", 1);
+    // thread shape: TC floats per thread x NCT thread columns (VF = TC NCT = 8
+    // floats = one 32-byte sector per spectrum row and CTA).  Default: one
+    // complex value per thread and row (8-byte loads, 4 thread columns); at
+    // RPT = 32 that is 64 data registers, 2 CTAs of 256 threads per SM (c5:
+    // 1.47 ms per iteration, 4.45 TB/s; the scalar 8-column shape 1.66 ms).
+    // Launches far below one wave (c1) take the scalar shape: twice the
+    // threads per strip (c1 column pass 17.7 -> 9.9 us per step).
     const int nseg = (p.H + p.tri_rpt - 1) / p.tri_rpt;
+    const long threads = (long)planes * ((2 * p.wc + 7) / 8) * 4 * nseg;
+    const bool scalar = threads < 256L * nsm && 8 * nseg <= 1024;
+#ifdef BLFLS_EXPERIMENTS
+    const int shape = knob("BLFLS_TRI_SHAPE", scalar ? 0 : 1);
 #define BLFLS_TRI_GO(R)                                                                    \
     if (p.tri_rpt == R) {                                                                  \
         if (shape == 0 && 8 * nseg <= 1024) return launch_tri_t<R, 1, 8>(p, planes, st);   \
@@ -367,7 +385,7 @@ cudaError_t launch_col_tri(const SolveParams& p, int planes, cudaStream_t st)
 #undef BLFLS_TRI_GO
 #else
     if (p.tri_rpt == 32) return launch_tri_t<32, 2, 4>(p, planes, st);
-    if (p.tri_rpt == 16) return launch_tri_t<16, 2, 4>(p, planes, st);
+    if (p.tri_rpt == 16) return scalar ? launch_tri_t<16, 1, 8>(p, planes, st) : launch_tri_t<16, 2, 4>(p, planes, st);
 #endif
     return cudaErrorInvalidConfiguration;
 }

@@ -707,7 +707,12 @@ cudaError_t launch_row_r2c(const SolveParams& p, const FftGeom& g, int planes, b
 cudaError_t launch_col(const SolveParams& p, const FftGeom& g, int planes, cudaStream_t st)
 {
     // forward + 1 / den + inverse of a column = a cyclic tridiagonal solve
-    if (p.mode == 3 && p.tri != nullptr) return launch_col_tri(p, planes, st);
+    if (p.mode == 3 && p.tri != nullptr) {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        return launch_col_tri(p, planes, nsm, st);
+    }
     return launch_fft_pass(1, p, g, planes, false, st);
 }
 

@@ -102,6 +102,11 @@ __global__ void __launch_bounds__(G::THREADS) k2_row_r2c(const SolveParams p, co
     }
 }
 
+// The column FFT pair (forward, 1 / den, inverse) of r01 / early r02.  The
+// production solve runs the column pass as a cyclic tridiagonal solve
+// (k_col_tri.cu, launch_col in k_solve.cu); these kernels remain in the
+// experiments build for A/B runs (BLFLS_COL_TRI=0).
+#ifdef BLFLS_EXPERIMENTS
 // grid (ceil(wc / V), planes): V adjacent spectrum columns, forward FFT,
 // 1 / (H W (1 + lambda (4 sin^2(pi u/H) + 4 sin^2(pi v/W)))), inverse FFT
 template <class G>
@@ -221,6 +226,8 @@ __global__ void __launch_bounds__(G::THREADS, col_pipe_minb<G>())
         __syncthreads();  // buf free for the copies of strip s + 2 gridDim.x
     }
 }
+
+#endif  // BLFLS_EXPERIMENTS
 
 // grid (ceil(H / V), planes)
 template <class G>
@@ -452,6 +459,7 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
 {
     constexpr size_t smem = G::smem_bytes();
     if (which == 1) {
+#ifdef BLFLS_EXPERIMENTS
         // BLFLS_COL_PIPE: 1 pipelined column pass, 0 plain; unset = pipelined
         // for power-of-two columns up to 1024 whose spectra stay L2-resident
         // (c2 column 62 -> 57 us per step; c3's 1080, the HBM-streaming c5 and
@@ -487,6 +495,7 @@ static void launch2(int which, const SolveParams& p, const float2* tw, int plane
         dim3 grid((p.wc + G::V - 1) / G::V, planes);
         set_smem2(k2_col<G>, smem);
         k2_col<G><<<grid, G::THREADS, smem, st>>>(p, tw);
+#endif
     } else if (which == 0) {
         dim3 grid((p.H + G::V - 1) / G::V, planes);
         set_smem2(k2_row_r2c<G>, smem);
@@ -534,6 +543,9 @@ bool launch_v2_pass(int which, const SolveParams& p, int n, const float2* tw, in
     static const bool disabled = (knob("BLFLS_FFT_V1", 0) != 0);
     if (disabled) return false;
     if (which == 1 && p.mode != 3) return false;
+#ifndef BLFLS_EXPERIMENTS
+    if (which == 1) return false;  // mode 3 is k_col_tri; modes 1 / 2 run k_col (k_solve.cu)
+#endif
     // passes routed here (bit 0 row r2c, bit 1 column, bit 2 row c2r)
     static const int passes = knob("BLFLS_V2_PASSES", 6);  // column + row c2r (streaming ncu, r01)
     if (!((passes >> which) & 1)) return false;

@@ -3,12 +3,9 @@ production library ignores BLFLS_* variables; only a -DBLFLS_EXPERIMENTS
 build reads them).  Every variant the default library selects at run time
 is reached through inputs that make the library choose it:
 
-- the column pass: k2_col_pipe (persistent, double-buffered cp.async
-  strips) for power-of-two columns up to 1024 points whose spectra total
-  <= 48 MB, the plain k2_col above that.  The same images solved in a small
-  batch (pipelined; 774 strips > resident CTAs, so the CTAs' buffer
-  alternation runs) and inside a larger batch (plain) must give the same
-  bits (k_solve2.cu launch2).
+- the column pass (k_col_tri.cu since r02; r01 switched between a pipelined
+  and a plain column FFT on the spectrum size): the same images solved in a
+  small batch and inside a larger batch must give the same bits.
 - the exponent forms of the packed filters: factorised (XF) when
   2 range_coef^2 <= 60, i.e. sigma_r >= 0.07753, the difference form below
   (k_blf_j3.cu launch_j3, k_blf_p2.cu launch_p2).  Both sides of the switch
@@ -41,8 +38,9 @@ def test_switch_constant():
 
 
 def test_pipelined_and_plain_column_pass_agree(gpu, oracle):
-    """1024-point columns: 2 RGB images = 6 planes x 4.3 MB of spectrum ->
-    k2_col_pipe; the same 2 images among 4 = 12 planes, 52 MB -> k2_col."""
+    """1024-point columns: 2 RGB images alone and among 4 (r01: 6 planes x 4.3 MB
+    of spectrum ran the pipelined column FFT, 12 planes the plain one; the
+    tridiagonal column pass of r02 is one kernel, still batch-invariant)."""
     h = w = 1024
     imgs = np.stack([np.stack([oracle.gen_plane(600 + 10 * i + c, h, w, n_sites=12) for c in range(3)])
                      for i in range(4)]).astype(np.float32)
