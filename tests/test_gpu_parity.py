@@ -80,6 +80,51 @@ def test_joint_vs_oracle(gpu, oracle, c, gc, r, sr):
     assert maxabs(out, ref) <= TOL_OUT
 
 
+@pytest.mark.parametrize("h,w,batch", [(33, 64, 1), (47, 130, 2), (64, 66, 1), (70, 199, 1), (31, 8, 1)])
+def test_two_row_shared_guide_kernel_shapes(gpu, oracle, h, w, batch):
+    """k_blf_j3r (gray guide over RGB, r = 7, sigma_r >= 0.0775): odd heights (the
+    second row of a thread's pair falls outside), widths that are not a multiple
+    of the 64-column tile, of 4 (the scalar staging path) or smaller than the
+    window, batches; targets against the oracle's filter_gradients and the full
+    pipeline against blf_ls."""
+    img = np.stack([_img(oracle, 3, h, w, 300 + 7 * i) for i in range(batch)])
+    guide = np.stack([_img(oracle, 1, h, w, 400 + 7 * i) for i in range(batch)])
+    kw = dict(sigma_s=7.0, sigma_r=0.1, radius=7)
+    tx, ty = gpu.filter_gradients(img, guide, **kw)
+    for i in range(batch):
+        # pipelines.cpp:33-53: image and guide to [0, 1], gradients remapped to [0, 1],
+        # the guide's gradient on the same axis as range image
+        gn, _, _ = oracle.normalize_to_unit(img[i].astype(np.float64))
+        qn, _, _ = oracle.normalize_to_unit(guide[i].astype(np.float64))
+        for t, gr, qr in zip((tx, ty), oracle.forward_gradients(gn), oracle.forward_gradients(qn)):
+            ref = np.stack([2.0 * oracle.blf_brute_r((gr[c:c + 1] + 1) / 2, (qr + 1) / 2, **kw)[0] - 1.0
+                            for c in range(3)])
+            assert maxabs(np.asarray(t).reshape(batch, 3, h, w)[i], ref) <= TOL_TARGET
+    out = gpu.blf_ls(img, guide, lam=1000.0, iters=2, **kw)
+    for i in range(batch):
+        ref = oracle.blf_ls(img[i].astype(np.float64), guide[i].astype(np.float64), lam=1000.0, iters=2, **kw)
+        assert maxabs(np.asarray(out)[i], ref) <= TOL_OUT
+
+
+def test_two_row_kernel_unaligned_device_pointers(gpu, oracle):
+    """Device tensors whose data pointers are not 16-byte aligned take the scalar
+    staging of k_blf_j3r; same targets as the aligned call (bit-identical: the
+    staged values do not depend on how they were loaded)."""
+    import torch
+    h, w = 40, 128
+    img = torch.from_numpy(_img(oracle, 3, h, w, 501).astype(np.float32)).cuda()
+    guide = torch.from_numpy(_img(oracle, 1, h, w, 502).astype(np.float32)).cuda()
+    kw = dict(sigma_s=7.0, sigma_r=0.1, radius=7)
+    ax, ay = gpu.filter_gradients(img, guide, **kw)
+    buf_i = torch.empty(img.numel() + 1, device="cuda")
+    buf_g = torch.empty(guide.numel() + 1, device="cuda")
+    img_u = buf_i[1:].view_as(img).copy_(img)
+    guide_u = buf_g[1:].view_as(guide).copy_(guide)
+    assert img_u.data_ptr() % 16 != 0 and guide_u.data_ptr() % 16 != 0
+    ux, uy = gpu.filter_gradients(img_u, guide_u, **kw)
+    assert torch.equal(ax, ux) and torch.equal(ay, uy)
+
+
 def test_batch_matches_single(gpu, oracle):
     imgs = np.stack([_img(oracle, 3, 32, 48, 100 + i) for i in range(4)])
     guides = np.stack([_img(oracle, 1, 32, 48, 200 + i) for i in range(4)])
