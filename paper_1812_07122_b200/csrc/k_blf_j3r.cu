@@ -187,8 +187,12 @@ __device__ __forceinline__ void j3r_row(const BlfParams& p, const float* __restr
 
 }  // namespace
 
-// blockIdx.z = image * 2 + axis; PEERS: fused band exchange (k_blf_j3.cu)
-template <int R, bool PEERS, int POLYK>
+// blockIdx.y = tile row * 2 + axis, blockIdx.z = image: the two axis CTAs of a
+// tile row are neighbours in launch order, so they run at the same time on
+// different SMs and the second one's staging loads find the raw rows in L2
+// (ROWMAJ = false: blockIdx.z = image * 2 + axis, the r01 order, experiments).
+// PEERS: fused band exchange (k_blf_j3.cu)
+template <int R, bool PEERS, int POLYK, bool ROWMAJ = true>
 __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
 {
     using Gm = J3rGeom<R>;
@@ -201,9 +205,10 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
     float2* S2 = S01 + ROWS * SP;                                 // [ROWS][SP] {g2 B, B}, B = exp2(-b^2)
 
     const int H = p.H, W = p.W;
-    const int b = blockIdx.z >> 1, axis = blockIdx.z & 1;
+    const int b = ROWMAJ ? blockIdx.z : blockIdx.z >> 1;
+    const int axis = ROWMAJ ? blockIdx.y & 1 : blockIdx.z & 1;
     const int tx0 = blockIdx.x * TW;
-    const int ty0 = p.y0 + blockIdx.y * TH;
+    const int ty0 = p.y0 + (ROWMAJ ? blockIdx.y >> 1 : blockIdx.y) * TH;
     const size_t plane = (size_t)H * W;
     float s, range, sg, grange;
     r_decode(p.lohi, b, p.range_coef, s, range);
@@ -404,16 +409,17 @@ __global__ void __launch_bounds__(256, 3) k_blf_j3r(const BlfParams p)
     }
 }
 
-template <int R, bool PEERS, int POLYK>
+template <int R, bool PEERS, int POLYK, bool ROWMAJ = true>
 static cudaError_t launch_j3r_t(const BlfParams& p, int batch, cudaStream_t st)
 {
     using Gm = J3rGeom<R>;
     constexpr size_t smem = Gm::smem_bytes();
     cudaError_t e =
-        cudaFuncSetAttribute(k_blf_j3r<R, PEERS, POLYK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blf_j3r<R, PEERS, POLYK, ROWMAJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((p.W + Gm::TW - 1) / Gm::TW, (p.y1 - p.y0 + Gm::TH - 1) / Gm::TH, 2 * batch);
-    k_blf_j3r<R, PEERS, POLYK><<<grid, Gm::NT, smem, st>>>(p);
+    const int gy = (p.y1 - p.y0 + Gm::TH - 1) / Gm::TH;
+    dim3 grid((p.W + Gm::TW - 1) / Gm::TW, ROWMAJ ? 2 * gy : gy, ROWMAJ ? batch : 2 * batch);
+    k_blf_j3r<R, PEERS, POLYK, ROWMAJ><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -435,6 +441,10 @@ bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaErr
     // the shared MIO queue); an L2 prefetch of a later tile's raw rows 0.891;
     // two staging tasks in flight per thread (spills at 80 registers) 0.862.
 #ifdef BLFLS_EXPERIMENTS
+    if (p.npeers == 0 && knob("BLFLS_J3R_ROWMAJ", 1) == 0) {
+        *err = launch_j3r_t<7, false, 12, false>(p, batch, st);
+        return true;
+    }
     switch (p.npeers > 0 ? 12 : knob("BLFLS_J3R_POLY", 12)) {
         case 0: *err = launch_j3r_t<7, false, 0>(p, batch, st); return true;
         case 6: *err = launch_j3r_t<7, false, 6>(p, batch, st); return true;
