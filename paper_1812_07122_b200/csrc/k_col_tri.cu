@@ -34,6 +34,10 @@
 
 #include "blfls_internal.cuh"
 
+#ifndef BLFLS_TRI_REGS64
+#define BLFLS_TRI_REGS64 128  // register budget of the 64-value strips (experiments: -DBLFLS_TRI_REGS64=80)
+#endif
+
 namespace blfls {
 
 namespace {
@@ -254,7 +258,7 @@ __device__ __forceinline__ void tri_strip(const SolveParams& p, float* base, siz
 template <int RPT, int TC, int MAXT>
 constexpr int tri_minb()
 {
-    constexpr int regs = RPT * TC <= 8 ? 32 : RPT * TC <= 32 ? 64 : 128;
+    constexpr int regs = RPT * TC <= 8 ? 32 : RPT * TC <= 32 ? 64 : (BLFLS_TRI_REGS64);
     return 65536 / (regs * MAXT) > 0 ? 65536 / (regs * MAXT) : 1;
 }
 
