@@ -770,18 +770,20 @@ def test_async_device_calls_defer_the_finite_check(gpu, oracle):
     plan.sync()  # reported once
 
 
-def test_multi_band_joint_gray_guide(gpu, oracle):
-    """Row bands with the shared-gray-guide filter (k_blf_j3's peer-storing
-    epilogue, factorised exponents): two entries on GPU 0 equal one
-    blfls_run bit for bit, and the oracle within 1e-4."""
+@pytest.mark.parametrize("h,ndev", [(72, 2), (71, 3)])
+def test_multi_band_joint_gray_guide(gpu, oracle, h, ndev):
+    """Row bands with the shared-gray-guide filter (k_blf_j3r's peer-storing
+    epilogue; bands that start on even and on odd rows, so a thread's row pair
+    straddles differently than in the single launch): the entries on GPU 0
+    equal one blfls_run bit for bit, and the oracle within 1e-4."""
     from paper_1812_07122_b200 import _capi
-    c, h, w = 3, 72, 128
+    c, w = 3, 128
     img = _img(oracle, c, h, w, 41).astype(np.float32)
     guide = _img(oracle, 1, h, w, 42).astype(np.float32)
     kw = dict(lam=1000.0, sigma_s=7.0, sigma_r=0.1, radius=7)
     ref = gpu.blf_ls(img, guide, iters=3, **kw)
     prm = _capi.Params(h, w, c, 1, 7, 7.0, 0.1, 1000.0, 1, 0, 0, 0, 0)
-    m = _capi.MultiPlan(prm, [0, 0], _capi.MULTI_BAND)
+    m = _capi.MultiPlan(prm, [0] * ndev, _capi.MULTI_BAND)
     out = np.full_like(img, -1.0)
     m.run(img, guide, 1, 3, out)
     assert np.array_equal(out, ref)
