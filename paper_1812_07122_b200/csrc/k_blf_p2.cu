@@ -75,11 +75,18 @@ template <int R, int TH, int MODE, bool XF = false>
 struct P2Geom {
     static constexpr int P = 4, TW = 64, NT = 16 * TH;
     static constexpr int ROWS = TH + 2 * R;
-    static constexpr int COLS = TW + 2 * R;
     static constexpr int VN = P + 2 * R;
-    static constexpr int VN4 = (VN + 3) & ~3;
-    static constexpr int GP = (MODE == 1 || XF) ? ((COLS + 3) & ~3) + 4 : 0;  // planar guide (MODE 1, XF)
-    static constexpr int SP = (COLS + 3 + 15) & ~15;                  // {v, 1} pitch (float2)
+    // QUAD (factorised form, radii whose window starts one column after an
+    // aligned quad): the staged tile starts OX columns left of the outputs, a
+    // multiple of 4, so 16-byte image loads map to 16-byte shared stores
+    // (k_blf_j3r.cu); r = 5 would read 20 instead of 16 columns per window row
+    static constexpr bool QUAD = XF && (R == 7 || R == 15);
+    static constexpr int OX = QUAD ? ((R + 3) & ~3) : R;
+    static constexpr int J0 = OX - R;                    // first window column of thread column 0
+    static constexpr int VN4 = (J0 + VN + 3) & ~3;
+    static constexpr int COLS = QUAD ? TW - P + VN4 : TW + 2 * R;
+    static constexpr int GP = QUAD ? COLS : ((MODE == 1 || XF) ? ((COLS + 3) & ~3) + 4 : 0);  // planar guide (MODE 1, XF)
+    static constexpr int SP = QUAD ? COLS : (COLS + 3 + 15) & ~15;    // {v, 1} pitch (float2)
     static constexpr size_t smem_bytes()
     {
         return (size_t)ROWS * GP * sizeof(float) + (size_t)ROWS * SP * sizeof(float2);
@@ -119,6 +126,54 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
     const float* fimg = p.f + ((size_t)b * C + c0) * plane;
     const float* gimg = MODE == 0 ? fimg : p.guide + ((size_t)b * p.GC + (p.GC == 1 ? 0 : c0)) * plane;
 
+    // staging
+    bool quads = false;
+    if constexpr (Gm::QUAD)
+        quads = (W & 3) == 0 &&
+                ((reinterpret_cast<uintptr_t>(fimg) | reinterpret_cast<uintptr_t>(gimg)) & 15) == 0;
+    if (quads) {
+        // aligned column quads (k_blf_j3r.cu): one task = 4 staged cells of one
+        // row from 16-byte loads
+        constexpr int QPR = COLS / 4;
+        for (int t = threadIdx.x; t < ROWS * QPR; t += NT) {
+            const int i = t / QPR, c = t - i * QPR;
+            const int y = ty0 - R + i, x = tx0 - Gm::OX + 4 * c;
+            float4 bq = make_float4(0.f, 0.f, 0.f, 0.f), sa = bq, sb = bq;
+            if (y >= 0 && y < H && x >= 0 && x < W) {
+                const int r0 = y * W + x;
+                float4 a = __ldg(reinterpret_cast<const float4*>(fimg + r0)), n, ga = a, gn;
+                if (axis == 0) {
+                    const int rn = y * W + (x + 4 == W ? 0 : x + 4);
+                    n = make_float4(a.y, a.z, a.w, __ldg(fimg + rn));
+                    if (MODE == 1) {
+                        ga = __ldg(reinterpret_cast<const float4*>(gimg + r0));
+                        gn = make_float4(ga.y, ga.z, ga.w, __ldg(gimg + rn));
+                    }
+                } else {
+                    const int r1 = (y + 1 == H ? 0 : y + 1) * W + x;
+                    n = __ldg(reinterpret_cast<const float4*>(fimg + r1));
+                    if (MODE == 1) {
+                        ga = __ldg(reinterpret_cast<const float4*>(gimg + r0));
+                        gn = __ldg(reinterpret_cast<const float4*>(gimg + r1));
+                    }
+                }
+                const float4 v = make_float4(n.x - a.x, n.y - a.y, n.z - a.z, n.w - a.w);
+                if (MODE == 0)
+                    bq = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+                else
+                    bq = make_float4((gn.x - ga.x) * sg, (gn.y - ga.y) * sg, (gn.z - ga.z) * sg, (gn.w - ga.w) * sg);
+                const float w0 = p2_ex2(-bq.x * bq.x), w1 = p2_ex2(-bq.y * bq.y);
+                const float w2 = p2_ex2(-bq.z * bq.z), w3 = p2_ex2(-bq.w * bq.w);
+                const float4 u = MODE == 0 ? bq : v;  // MODE 0: the source is the scaled gradient
+                sa = make_float4(u.x * w0, w0, u.y * w1, w1);
+                sb = make_float4(u.z * w2, w2, u.w * w3, w3);
+            }
+            const int k0 = (2 * c) ^ ((c >> 2) & 1), k1 = k0 ^ 1;  // p2_sw of chunks 2c, 2c + 1
+            *reinterpret_cast<float4*>(G + i * GP + 4 * c) = bq;
+            *reinterpret_cast<float4*>(SV + i * SP + 2 * k0) = sa;
+            *reinterpret_cast<float4*>(SV + i * SP + 2 * k1) = sb;
+        }
+    } else
     // staging: warp per tile row, lane per column (no per-element division;
     // the row's base pointer and wrap row are computed once)
     {
@@ -134,7 +189,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
             float2* srow = SV + i * SP;
 #pragma unroll
             for (int j = lane; j < COLS; j += 32) {
-                const int x = tx0 - R + j;
+                const int x = tx0 - Gm::OX + j;
                 if (yin && x >= 0 && x < W) {
                     const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
                     const float v = __ldg(f1 + x1) - __ldg(f0 + x);
@@ -168,7 +223,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
 #pragma unroll
     for (int q = 0; q < P; ++q) {
         gs[q] = (MODE == 0 && !XF) ? SV[(ty + R) * SP + p2_sw(tx * P + q + R)].x
-                                   : G[(ty + R) * GP + tx * P + q + R];
+                                   : G[(ty + R) * GP + tx * P + q + Gm::OX];
         acc[q] = 0ull;
     }
     if constexpr (PX) {
@@ -208,8 +263,8 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int j = j4 + u;
-                    if (j >= VN) break;
+                    const int j = j4 + u - Gm::J0;  // window column
+                    if (j < 0 || j >= VN) continue;
 #pragma unroll
                     for (int h = 0; h < P / 2; ++h) {
                         const int q0 = 2 * h, dx0 = j - q0 - R;
