@@ -94,7 +94,7 @@ def blf_kernel_name(cfg):
         tiles = ", 32-row tiles, 2 CTAs/SM)" if xf and cfg.radius == 7 else (", 4 CTAs/SM)" if xf else ", 2 CTAs/SM)")
         return (f"k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, {form}" + tiles)
     if not cfg.guide and cfg.radius in (5, 7, 15):
-        period = ({5: 10, 7: 7, 15: 5} if xf else {5: 10, 7: 7, 15: 8})[cfg.radius]
+        period = ({5: 10, 7: 6, 15: 5} if xf else {5: 10, 7: 7, 15: 8})[cfg.radius]
         return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, "
                 f"{form}, FMA-pipe exp2 on every {period}th tap)")
     return "k_grad_blf (fused gradient + brute-force BLF)"

@@ -428,12 +428,13 @@ constexpr int kP2DefaultPoly()
     return R == 5 ? 10 : (R == 15 ? 8 : 7);
 }
 // ... and of the factorised-exponent kernel, whose exponents cost half the
-// FFMA2 so more of them fit on the FMA pipe (c2: 0.976 at 7, 0.978 at 6; c4:
-// 1.098 at 5, 1.073 at 6, 1.053 at 8)
+// FFMA2 so more of them fit on the FMA pipe (r02, with the quad staging: c2
+// 0.985 / 1.000 / 0.994 / 0.984 at 5 / 6 / 7 / 8; c4 1.103 / 1.084 / 1.075 at
+// 5 / 6 / 8)
 template <int R>
 constexpr int kP2XfPoly()
 {
-    return R == 5 ? 10 : (R == 15 ? 5 : 7);
+    return R == 5 ? 10 : (R == 15 ? 5 : 6);
 }
 
 template <int R, int MODE>
