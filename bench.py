@@ -479,12 +479,18 @@ def run_ours(args, cfg):
         for k in range(2):
             P.blf_ls(h_img, h_guide, out=h_outs[k % 2], wait=False, **hkw)
         plan_e.sync()
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            P.blf_ls(h_img, h_guide, out=h_outs[k % 2], wait=False, **hkw)
-        plan_e.sync()
-        e_ms = [(time.perf_counter() - t0) * 1e3 / args.steps]
-        e_step = statistics.mean(e_ms)
+        # three runs of K steps each, the median reported (all three listed): the
+        # copies run at 70-75% of the host link's one-direction rate in both
+        # directions at once, so a run now and then is transfer-bound when the
+        # host side is slow (1 run in ~8 on the pool's VMs: 135 instead of 108 ms)
+        e_ms = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            for k in range(args.steps):
+                P.blf_ls(h_img, h_guide, out=h_outs[k % 2], wait=False, **hkw)
+            plan_e.sync()
+            e_ms.append((time.perf_counter() - t0) * 1e3 / args.steps)
+        e_step = statistics.median(e_ms)
         if world > 1:
             t = torch.tensor([e_step], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -492,7 +498,9 @@ def run_ours(args, cfg):
         e2e = {"value": mp_total / (e_step * 1e-3), "unit": "MP/s",
                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out.numel() * 4,
                "ms_per_step": e_step,
-               "timing": "host wall clock from the first submit to blfls_sync after K steps",
+               "ms_per_step_runs": e_ms,
+               "timing": "host wall clock from the first submit to blfls_sync after K steps; "
+                         "median of three such runs (ms_per_step_runs lists all)",
                "path": "paper_1812_07122_b200.blf_ls(pinned host tensors, wait=False) -> "
                        "blfls_run(HOST_PTRS|ASYNC|CHECK_FINITE): H2D, compute, D2H on separate "
                        "streams, two staging slots; batches of >= 128 MB streamed in up to 8 image chunks"}
