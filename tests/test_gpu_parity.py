@@ -165,7 +165,7 @@ def test_solve_stage_vs_oracle_and_dense(gpu, oracle):
 
 
 @pytest.mark.parametrize("h,w", [(2, 8), (3, 6), (31, 10), (33, 12), (64, 6), (100, 18), (513, 8),
-                                 (1025, 8), (1080, 16), (2050, 4), (4100, 4)])
+                                 (1025, 8), (1080, 16), (2050, 4), (4100, 4), (5000, 4), (8192, 4)])
 def test_tridiagonal_column_pass(gpu, oracle, h, w):
     """The solve's column pass is a cyclic tridiagonal solve per spectrum column
     (k_col_tri.cu) instead of forward FFT / den / inverse FFT (solver.cpp:107-120):
