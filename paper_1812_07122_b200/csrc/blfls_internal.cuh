@@ -220,7 +220,7 @@ struct SolveParams {
 // tridiagonal column pass (k_col_tri.cu)
 int tri_rows_per_thread(int H, int wc, int planes, int nsm);
 bool tri_supported(int H, int rpt);
-void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri, std::vector<float>& scale);
+void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri);
 cudaError_t launch_col_tri(const SolveParams& p, int planes, int nsm, cudaStream_t st);
 
 

@@ -775,8 +775,7 @@ blfls_status blfls_plan_create(const blfls_params* prm, blfls_plan_t* out)
         const int rpt = tri_rows_per_thread(H, p->wc, q.max_batch * C, p->nsm);
         if (knob("BLFLS_COL_TRI", 1) != 0 && tri_supported(H, rpt)) {
             std::vector<float4> t4;
-            std::vector<float> tsc;
-            tri_tables(H, W, p->wc, q.lambda, rpt, t4, tsc);
+            tri_tables(H, W, p->wc, q.lambda, rpt, t4);
             if (cudaMalloc(&p->tri, sizeof(float4) * t4.size()) != cudaSuccess)
                 return bail(fail(BLFLS_ENOMEM, "plan: table allocation failed"));
             cudaMemcpy(p->tri, t4.data(), sizeof(float4) * t4.size(), cudaMemcpyHostToDevice);

@@ -340,10 +340,9 @@ int tri_rows_per_thread(int H, int wc, int planes, int nsm)
 //   tri[2v]     = (rho hi, rho lo, 1 / (1 - rho^H), rho / (lambda W))
 //   tri[2v + 1] = (rho^RPT hi, lo, rho^len_last hi, lo)
 // rho / (lambda W) = 2 / ((b + sqrt(c (c + 4 lambda))) W)
-void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri, std::vector<float>& scale)
+void tri_tables(int H, int W, int wc, double lambda, int rpt, std::vector<float4>& tri)
 {
     tri.resize(2 * (size_t)wc);
-    scale.clear();
     const int nseg = (H + rpt - 1) / rpt;
     const int len_last = H - (nseg - 1) * rpt;
     auto hi = [](double x) { return (float)x; };
