@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--pad", type=int, default=0, help="reflect padding (reference default 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the short c1-c4 lines attached to the default c5 line (other_configs)")
     return ap.parse_args()
 
 
@@ -564,9 +566,34 @@ def run_ours(args, cfg):
             "e2e_cpp": e2e_cpp,
             "cpu_baseline": cpu,
         }
+        if (world == 1 and cfg.name == "c5" and args.backend == "brute" and args.pad == 0
+                and not args.no_other_configs):
+            line["other_configs"] = other_configs()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_configs():
+    """The remaining BASELINE configs (c1-c4: parity-test cases, one image each) as
+    short device-resident lines of this same script, one child process each, after
+    the headline measurement: value, stage times and the two roofline fractions."""
+    import subprocess
+    out = {}
+    for name in ("c1", "c2", "c3", "c4"):
+        cmd = [sys.executable, str(Path(__file__).resolve()), "--config", name, "--steps", "10", "--warmup", "3",
+               "--no-e2e", "--no-cpu-baseline", "--no-other-configs"]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            out[name] = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+                         "ms_per_step": d["ms_per_step"], "steps": d["steps"], "warmup": d["warmup"],
+                         "blf_frac_of_mufu": d["roofline"]["frac"], "blf_kernel": d["roofline"]["kernel"],
+                         "solve_frac_of_hbm": d["roofline_solve"]["frac"],
+                         "stage_ms_per_step": d["stage_ms_per_step"], "l2": d["config"].get("l2")}
+        except Exception as exc:  # the headline line does not depend on these
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 def run_band(args, cfg, world, rank, dev, peaks, peak_src):
