@@ -17,6 +17,13 @@
 
 #include "blfls_internal.cuh"
 
+#ifndef BLFLS_P2_QUAD5
+// quad staging for the r = 5 self-guided tiles too: their window starts 3 columns
+// into an aligned quad, so a window row reads 20 instead of 16 staged columns,
+// and still c1 BLF 25.5 -> 24.3 us, c3 1.095 -> 1.081 ms per step (r02)
+#define BLFLS_P2_QUAD5 1
+#endif
+
 namespace blfls {
 
 namespace {
@@ -71,7 +78,7 @@ __device__ __forceinline__ void p2_decode(const uint32_t* lohi, int b, float coe
 
 }  // namespace
 
-template <int R, int TH, int MODE, bool XF = false>
+template <int R, int TH, int MODE, bool XF = false, bool PX = true>
 struct P2Geom {
     static constexpr int P = 4, TW = 64, NT = 16 * TH;
     static constexpr int ROWS = TH + 2 * R;
@@ -80,12 +87,12 @@ struct P2Geom {
     // aligned quad): the staged tile starts OX columns left of the outputs, a
     // multiple of 4, so 16-byte image loads map to 16-byte shared stores
     // (k_blf_j3r.cu); r = 5 would read 20 instead of 16 columns per window row
-    static constexpr bool QUAD = XF && (R == 7 || R == 15);
+    static constexpr bool QUAD = PX && ((XF && (R == 7 || R == 15)) || (BLFLS_P2_QUAD5 && R == 5 && MODE == 0));
     static constexpr int OX = QUAD ? ((R + 3) & ~3) : R;
     static constexpr int J0 = OX - R;                    // first window column of thread column 0
     static constexpr int VN4 = (J0 + VN + 3) & ~3;
     static constexpr int COLS = QUAD ? TW - P + VN4 : TW + 2 * R;
-    static constexpr int GP = QUAD ? COLS : ((MODE == 1 || XF) ? ((COLS + 3) & ~3) + 4 : 0);  // planar guide (MODE 1, XF)
+    static constexpr int GP = !(MODE == 1 || XF) ? 0 : (QUAD ? COLS : ((COLS + 3) & ~3) + 4);  // planar guide (MODE 1, XF)
     static constexpr int SP = QUAD ? COLS : (COLS + 3 + 15) & ~15;    // {v, 1} pitch (float2)
     static constexpr size_t smem_bytes()
     {
@@ -106,7 +113,7 @@ struct P2Geom {
 template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX = false, bool XF = false>
 __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
 {
-    using Gm = P2Geom<R, TH, MODE, XF>;
+    using Gm = P2Geom<R, TH, MODE, XF, PX>;
     constexpr int P = Gm::P, TW = Gm::TW, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
     constexpr int VN = Gm::VN, VN4 = Gm::VN4, GP = Gm::GP, SP = Gm::SP;
     extern __shared__ __align__(16) float smp[];
@@ -162,14 +169,22 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
                     bq = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
                 else
                     bq = make_float4((gn.x - ga.x) * sg, (gn.y - ga.y) * sg, (gn.z - ga.z) * sg, (gn.w - ga.w) * sg);
-                const float w0 = p2_ex2(-bq.x * bq.x), w1 = p2_ex2(-bq.y * bq.y);
-                const float w2 = p2_ex2(-bq.z * bq.z), w3 = p2_ex2(-bq.w * bq.w);
                 const float4 u = MODE == 0 ? bq : v;  // MODE 0: the source is the scaled gradient
-                sa = make_float4(u.x * w0, w0, u.y * w1, w1);
-                sb = make_float4(u.z * w2, w2, u.w * w3, w3);
+                if constexpr (XF) {
+                    const float w0 = p2_ex2(-bq.x * bq.x), w1 = p2_ex2(-bq.y * bq.y);
+                    const float w2 = p2_ex2(-bq.z * bq.z), w3 = p2_ex2(-bq.w * bq.w);
+                    sa = make_float4(u.x * w0, w0, u.y * w1, w1);
+                    sb = make_float4(u.z * w2, w2, u.w * w3, w3);
+                } else {
+                    sa = make_float4(u.x, 1.0f, u.y, 1.0f);
+                    sb = make_float4(u.z, 1.0f, u.w, 1.0f);
+                }
+            } else if constexpr (!XF) {  // difference form: a sentinel guide value gives weight 0
+                sa = sb = make_float4(MODE == 0 ? kP2Sentinel : 0.f, 0.f, MODE == 0 ? kP2Sentinel : 0.f, 0.f);
+                bq = make_float4(kP2Sentinel, kP2Sentinel, kP2Sentinel, kP2Sentinel);
             }
             const int k0 = (2 * c) ^ ((c >> 2) & 1), k1 = k0 ^ 1;  // p2_sw of chunks 2c, 2c + 1
-            *reinterpret_cast<float4*>(G + i * GP + 4 * c) = bq;
+            if constexpr (MODE == 1 || XF) *reinterpret_cast<float4*>(G + i * GP + 4 * c) = bq;
             *reinterpret_cast<float4*>(SV + i * SP + 2 * k0) = sa;
             *reinterpret_cast<float4*>(SV + i * SP + 2 * k1) = sb;
         }
@@ -222,7 +237,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
     unsigned long long acc[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-        gs[q] = (MODE == 0 && !XF) ? SV[(ty + R) * SP + p2_sw(tx * P + q + R)].x
+        gs[q] = (MODE == 0 && !XF) ? SV[(ty + R) * SP + p2_sw(tx * P + q + Gm::OX)].x
                                    : G[(ty + R) * GP + tx * P + q + Gm::OX];
         acc[q] = 0ull;
     }
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(16 * TH, MINB) k_blf_p2(const BlfParams p)
 template <int R, int TH, int MODE, int POLY, bool PEERS, int MINB, bool PX, bool XF = false>
 static cudaError_t launch_p2_t(const BlfParams& p, int nplanes, cudaStream_t st)
 {
-    using Gm = P2Geom<R, TH, MODE, XF>;
+    using Gm = P2Geom<R, TH, MODE, XF, PX>;
     constexpr size_t smem = Gm::smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k_blf_p2<R, TH, MODE, POLY, PEERS, MINB, PX, XF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
