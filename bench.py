@@ -583,8 +583,12 @@ def other_configs():
     for name in ("c1", "c2", "c3", "c4"):
         cmd = [sys.executable, str(Path(__file__).resolve()), "--config", name, "--steps", "10", "--warmup", "3",
                "--no-e2e", "--no-cpu-baseline", "--no-other-configs"]
+        # plain single-process children even when this line runs under torchrun
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT", "GROUP_RANK",
+                            "LOCAL_WORLD_SIZE", "ROLE_RANK", "ROLE_WORLD_SIZE") and not k.startswith("TORCHELASTIC")}
         try:
-            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
             d = json.loads(r.stdout.strip().splitlines()[-1])
             out[name] = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
                          "ms_per_step": d["ms_per_step"], "steps": d["steps"], "warmup": d["warmup"],
