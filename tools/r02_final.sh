@@ -10,9 +10,9 @@ python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.
 python bench.py --impl reference --steps 20 --warmup 5 > $O/final_ref.json 2> $O/final_ref.err
 python tools/parity_report.py > $O/final_parity.txt 2>&1
 # launch list of the bench command (after it ran clean above)
-python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/final_c5_short.json 2>&1 && \
+python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-other-configs > $O/final_c5_short.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02_launches_c5.csv \
-    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/final_ncu_launch.log 2>&1
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-other-configs > $O/final_ncu_launch.log 2>&1
 # --set full of the 64-image BLF launch and of the column pass (24 planes)
 python tools/prof_blf_c5.py 64 > $O/final_prof_blf.txt 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_blf_j3r -c 1 -o $O/r02_ncu_blf_c5_j3r -f \
