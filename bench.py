@@ -588,7 +588,7 @@ def other_configs():
                if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT", "GROUP_RANK",
                             "LOCAL_WORLD_SIZE", "ROLE_RANK", "ROLE_WORLD_SIZE") and not k.startswith("TORCHELASTIC")}
         try:
-            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=120, env=env)
             d = json.loads(r.stdout.strip().splitlines()[-1])
             out[name] = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
                          "ms_per_step": d["ms_per_step"], "steps": d["steps"], "warmup": d["warmup"],
