@@ -88,7 +88,7 @@ def blf_kernel_name(cfg):
     coef2 = math.log2(math.e) / (8.0 * cfg.sigma_r ** 2)
     xf = 2.0 * coef2 <= 60.0
     form = "factorised exponents" if xf else "difference-form pair exponents"
-    if cfg.guide and cfg.channels == 3 and cfg.radius == 7 and xf:
+    if cfg.guide and cfg.channels == 3 and cfg.radius in (3, 5, 7) and xf:
         return ("k_blf_j3r (fused gradient + shared-gray-guide brute-force BLF, two output rows x four columns "
                 "per thread, FFMA2-packed sums, factorised exponents, row factor folded into the sums, FMA-pipe "
                 "exp2 on every 12th exponent pair, 32 x 64 tiles staged by aligned column quads, 3 CTAs/SM)")

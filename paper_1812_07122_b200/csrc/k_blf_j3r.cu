@@ -429,7 +429,7 @@ static cudaError_t launch_j3r_t(const BlfParams& p, int batch, cudaStream_t st)
 bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err)
 {
     if (knob("BLFLS_J3R", 1) == 0) return false;
-    if (p.C != 3 || p.radius != 7) return false;
+    if (p.C != 3 || (p.radius != 7 && p.radius != 5 && p.radius != 3)) return false;
     if (2.0f * p.range_coef * p.range_coef > 60.0f || -p.cs[p.radius] > 57.0f) return false;
     // every 12th exponent pair of a window row runs on the FMA pipe (f32x2
     // polynomial exp2): the FMA pipe is ~60% busy at the MUFU bound, so the
@@ -441,11 +441,11 @@ bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaErr
     // the shared MIO queue); an L2 prefetch of a later tile's raw rows 0.891;
     // two staging tasks in flight per thread (spills at 80 registers) 0.862.
 #ifdef BLFLS_EXPERIMENTS
-    if (p.npeers == 0 && knob("BLFLS_J3R_ROWMAJ", 1) == 0) {
+    if (p.radius == 7 && p.npeers == 0 && knob("BLFLS_J3R_ROWMAJ", 1) == 0) {
         *err = launch_j3r_t<7, false, 12, false>(p, batch, st);
         return true;
     }
-    switch (p.npeers > 0 ? 12 : knob("BLFLS_J3R_POLY", 12)) {
+    switch (p.npeers > 0 || p.radius != 7 ? 12 : knob("BLFLS_J3R_POLY", 12)) {
         case 0: *err = launch_j3r_t<7, false, 0>(p, batch, st); return true;
         case 6: *err = launch_j3r_t<7, false, 6>(p, batch, st); return true;
         case 8: *err = launch_j3r_t<7, false, 8>(p, batch, st); return true;
@@ -455,6 +455,17 @@ bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaErr
         default: break;
     }
 #endif
+    // r = 5 and r = 3 windows start 3 / 1 columns into an aligned quad (r = 5 reads 20
+    // instead of 16 staged columns per row, still half of k_blf_j3's per exponential);
+    // r = 15 tiles (62 x 96 staged cells) would leave one CTA per SM: k_blf_j3
+    if (p.radius == 5) {
+        *err = p.npeers > 0 ? launch_j3r_t<5, true, 12>(p, batch, st) : launch_j3r_t<5, false, 12>(p, batch, st);
+        return true;
+    }
+    if (p.radius == 3) {
+        *err = p.npeers > 0 ? launch_j3r_t<3, true, 12>(p, batch, st) : launch_j3r_t<3, false, 12>(p, batch, st);
+        return true;
+    }
     *err = p.npeers > 0 ? launch_j3r_t<7, true, 12>(p, batch, st) : launch_j3r_t<7, false, 12>(p, batch, st);
     return true;
 }

@@ -80,16 +80,17 @@ def test_joint_vs_oracle(gpu, oracle, c, gc, r, sr):
     assert maxabs(out, ref) <= TOL_OUT
 
 
-@pytest.mark.parametrize("h,w,batch", [(33, 64, 1), (47, 130, 2), (64, 66, 1), (70, 199, 1), (31, 8, 1)])
-def test_two_row_shared_guide_kernel_shapes(gpu, oracle, h, w, batch):
-    """k_blf_j3r (gray guide over RGB, r = 7, sigma_r >= 0.0775): odd heights (the
+@pytest.mark.parametrize("h,w,batch,r", [(33, 64, 1, 7), (47, 130, 2, 7), (64, 66, 1, 7), (70, 199, 1, 7), (31, 8, 1, 7),
+                                         (41, 132, 2, 5), (38, 70, 1, 5), (35, 68, 1, 3), (20, 196, 2, 3)])
+def test_two_row_shared_guide_kernel_shapes(gpu, oracle, h, w, batch, r):
+    """k_blf_j3r (gray guide over RGB, r = 3, 5, 7, sigma_r >= 0.0775): odd heights (the
     second row of a thread's pair falls outside), widths that are not a multiple
     of the 64-column tile, of 4 (the scalar staging path) or smaller than the
     window, batches; targets against the oracle's filter_gradients and the full
     pipeline against blf_ls."""
     img = np.stack([_img(oracle, 3, h, w, 300 + 7 * i) for i in range(batch)])
     guide = np.stack([_img(oracle, 1, h, w, 400 + 7 * i) for i in range(batch)])
-    kw = dict(sigma_s=7.0, sigma_r=0.1, radius=7)
+    kw = dict(sigma_s=float(r), sigma_r=0.1, radius=r)
     tx, ty = gpu.filter_gradients(img, guide, **kw)
     for i in range(batch):
         # pipelines.cpp:33-53: image and guide to [0, 1], gradients remapped to [0, 1],
