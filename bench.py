@@ -95,6 +95,10 @@ def blf_kernel_name(cfg):
     if cfg.guide and cfg.channels == 3 and cfg.radius in (3, 5, 7, 15):
         tiles = ", 32-row tiles, 2 CTAs/SM)" if xf and cfg.radius == 7 else (", 4 CTAs/SM)" if xf else ", 2 CTAs/SM)")
         return (f"k_blf_j3 (fused gradient + shared-gray-guide brute-force BLF, FFMA2-packed sums, {form}" + tiles)
+    if not cfg.guide and cfg.radius in (7, 15) and xf and cfg.height * cfg.width * cfg.channels * cfg.batch >= 3 * (1 << 20):
+        return ("k_blf_p2r (fused gradient + self-guided brute-force BLF, two output rows x four columns per "
+                "thread, FFMA2-packed sums, factorised exponents, row factor folded into the sums, FMA-pipe exp2 "
+                "on every 4th exponent pair, 32 x 64 tiles staged by aligned column quads)")
     if not cfg.guide and cfg.radius in (5, 7, 15):
         period = ({5: 10, 7: 6, 15: 5} if xf else {5: 10, 7: 7, 15: 8})[cfg.radius]
         return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, "

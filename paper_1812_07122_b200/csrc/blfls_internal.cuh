@@ -236,6 +236,8 @@ bool launch_grad_blf_j3r(const BlfParams& p, int batch, cudaStream_t st, cudaErr
 // eight outputs per thread, factorised exponents (k_blf_j8.cu); false: not covered
 bool launch_grad_blf_j8(const BlfParams& p, int batch, cudaStream_t st, cudaError_t* err);
 
+// self-guided filter, two output rows per thread (k_blf_p2r.cu); false: not covered
+bool launch_grad_blf_p2r(const BlfParams& p, int nplanes, int nsm, cudaStream_t st, cudaError_t* err);
 // self / per-channel-joint filter with packed accumulation (k_blf_p2.cu); false: not covered
 bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st, cudaError_t* err);
 

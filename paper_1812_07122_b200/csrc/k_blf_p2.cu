@@ -532,6 +532,12 @@ bool launch_grad_blf_p2(const BlfParams& p, int mode, int batch, cudaStream_t st
     }
 #endif
     if (mode != 0) return false;
+    {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (launch_grad_blf_p2r(p, np, nsm, st, err)) return true;
+    }
     switch (p.radius) {
         case 5: *err = launch_p2<5, 0>(p, np, st); return true;
         case 7: *err = launch_p2<7, 0>(p, np, st); return true;

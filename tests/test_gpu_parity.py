@@ -126,6 +126,32 @@ def test_two_row_kernel_unaligned_device_pointers(gpu, oracle):
     assert torch.equal(ax, ux) and torch.equal(ay, uy)
 
 
+@pytest.mark.parametrize("h,w,r,sr", [(601, 1030, 7, 0.1), (577, 1092, 7, 0.08), (330, 2000, 15, 0.08)])
+def test_two_row_self_guided_kernel_shapes(gpu, oracle, h, w, r, sr):
+    """k_blf_p2r (self-guided, r = 7 / 15, sigma_r >= 0.0775) runs when the grid
+    fills the GPU, so its ragged cases need large images: odd heights, widths that
+    are not a multiple of the 64-column tile or of 4 (the scalar staging path),
+    two RGB images; targets against the oracle's brute-force filter on one plane
+    of each image, and against k_blf_p2's on all of them (a single small-batch
+    call of the same planes dispatches k_blf_p2)."""
+    img = np.stack([_img(oracle, 3, h, w, 700 + 7 * i) for i in range(2)])
+    kw = dict(sigma_s=float(r) if r == 7 else 12.0, sigma_r=sr, radius=r)
+    tx, ty = (np.asarray(t) for t in gpu.filter_gradients(img, **kw))
+    for i in range(2):
+        gn, _, _ = oracle.normalize_to_unit(img[i].astype(np.float64))
+        c = i + 1
+        for t, gr in zip((tx, ty), oracle.forward_gradients(gn)):
+            ref = 2.0 * oracle.blf_brute_r((gr[c:c + 1] + 1) / 2, (gr[c:c + 1] + 1) / 2, **kw)[0] - 1.0
+            assert maxabs(t[i, c], ref) <= TOL_TARGET
+    # one gray plane alone is a grid of < 6 waves: k_blf_p2 (per-image range: use a
+    # gray image whose range equals its own)
+    gray = img[0, :1]
+    sx, sy = (np.asarray(t) for t in gpu.filter_gradients(gray, **kw))
+    big = np.stack([np.repeat(gray, 3, axis=0)] * 2)
+    bx, by = (np.asarray(t) for t in gpu.filter_gradients(big, **kw))
+    assert maxabs(bx[1, 2], sx[0]) <= TOL_TARGET and maxabs(by[0, 1], sy[0]) <= TOL_TARGET
+
+
 def test_batch_matches_single(gpu, oracle):
     imgs = np.stack([_img(oracle, 3, 32, 48, 100 + i) for i in range(4)])
     guides = np.stack([_img(oracle, 1, 32, 48, 200 + i) for i in range(4)])

@@ -1,0 +1,11 @@
+#!/bin/bash
+# c2 / c4 self-guided BLF: two rows per thread (k_blf_p2r) and its FMA-pipe exp2 period vs k_blf_p2
+E=paper_1812_07122_b200/_lib_exp/libblfls.so
+for c in c2 c4; do
+  for v in "BLFLS_P2R=0" "BLFLS_P2R_POLY=0" "BLFLS_P2R_POLY=12" "BLFLS_P2R_POLY=8" "BLFLS_P2R_POLY=6" "BLFLS_P2R_POLY=5" "BLFLS_P2R_POLY=4" "BLFLS_P2R_POLY=3"; do
+    env BLFLS_LIBRARY=$E $v python bench.py --config $c --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/p2r.json 2>/dev/null
+    python -c "
+import json
+d=json.load(open('gpurun_out/p2r.json')); print('$c $v', round(d['value'],1), round(d['roofline']['frac'],4), round(d['stage_ms_per_step']['grad_blf'],4))"
+  done
+done
