@@ -99,6 +99,11 @@ def blf_kernel_name(cfg):
         return ("k_blf_p2r (fused gradient + self-guided brute-force BLF, two output rows x four columns per "
                 "thread, FFMA2-packed sums, factorised exponents, row factor folded into the sums, FMA-pipe exp2 "
                 "on every 4th exponent pair, 32 x 64 tiles staged by aligned column quads)")
+    if (not cfg.guide and cfg.radius == 5 and not xf
+            and cfg.height * cfg.width * cfg.channels * cfg.batch >= 3 * (1 << 20)):
+        return ("k_blf_p2r (fused gradient + self-guided brute-force BLF, two output rows x four columns per "
+                "thread, FFMA2-packed sums, difference-form pair exponents, row factor folded into the sums, "
+                "FMA-pipe exp2 on every 8th exponent pair, 32 x 64 tiles staged by aligned column quads)")
     if not cfg.guide and cfg.radius in (5, 7, 15):
         period = ({5: 10, 7: 6, 15: 5} if xf else {5: 10, 7: 7, 15: 8})[cfg.radius]
         return ("k_blf_p2 (fused gradient + self-guided brute-force BLF, FFMA2-packed sums, "

@@ -92,7 +92,9 @@ __device__ __forceinline__ void q_decode(const uint32_t* lohi, int b, float coef
     s = range > 0.f ? coef / range : coef;
 }
 
-template <int R>
+constexpr float kP2rSentinel = 1.0e15f;  // difference form: a guide value whose weight is exactly 0
+
+template <int R, bool XF = true>
 struct P2rGeom {
     static constexpr int P = 4, TW = 64, TH = 32, NT = 256;
     static constexpr int ROWS = TH + 2 * R;
@@ -101,7 +103,7 @@ struct P2rGeom {
     static constexpr int VN = P + 2 * R;
     static constexpr int VN4 = (J0 + VN + 3) & ~3;
     static constexpr int COLS = TW - P + VN4;
-    static constexpr int GP = COLS, SP = COLS;
+    static constexpr int GP = XF ? COLS : 0, SP = COLS;  // difference form: b is the source's .x
     static constexpr int MINB = R <= 7 ? 4 : 3;
     static constexpr size_t smem_bytes()
     {
@@ -110,23 +112,37 @@ struct P2rGeom {
 };
 
 // the taps of one staged source row for the output rows in MASK (bit k: row k)
-template <int R, int MASK, int POLYK>
+// XF: factorised exponent e = {2a_q, 2a_q+1} b + cs (sources {b B, B}); else the
+// difference form d = a - b, e = -d d + cs (sources {b, 1}, b read from the source)
+template <int R, int MASK, int POLYK, bool XF>
 __device__ __forceinline__ void p2r_row(const BlfParams& p, const float* __restrict__ grow,
                                         const float2* __restrict__ sv, int tx,
                                         const unsigned long long (&gsp)[2][2], unsigned long long (&acc)[2][4])
 {
-    using Gm = P2rGeom<R>;
+    using Gm = P2rGeom<R, XF>;
     constexpr int P = Gm::P, VN = Gm::VN, VN4 = Gm::VN4;
+    unsigned long long m1;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(m1) : "f"(-1.0f));
 #pragma unroll
     for (int j4 = 0; j4 < VN4; j4 += 4) {
-        const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
-        const float gt[4] = {g4.x, g4.y, g4.z, g4.w};
+        float gt[4];
+        if constexpr (XF) {
+            const float4 g4 = *reinterpret_cast<const float4*>(grow + j4);
+            gt[0] = g4.x;
+            gt[1] = g4.y;
+            gt[2] = g4.z;
+            gt[3] = g4.w;
+        }
         unsigned long long v1[4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float4 a = *reinterpret_cast<const float4*>(sv + q_sw(tx * P + j4 + 2 * h));
             asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h]) : "f"(a.x), "f"(a.y));
             asm("mov.b64 %0, {%1, %2};" : "=l"(v1[2 * h + 1]) : "f"(a.z), "f"(a.w));
+            if constexpr (!XF) {
+                gt[2 * h] = a.x;
+                gt[2 * h + 1] = a.z;
+            }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -145,11 +161,23 @@ __device__ __forceinline__ void p2r_row(const BlfParams& p, const float* __restr
                 for (int k = 0; k < 2; ++k) {
                     if (!((MASK >> k) & 1)) continue;
                     unsigned long long e;
-                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[k][h]), "l"(ce));
+                    if constexpr (XF) {
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(gtt), "l"(gsp[k][h]), "l"(ce));
+                    } else {
+                        unsigned long long d, nd;
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(gtt), "l"(m1), "l"(gsp[k][h]));
+                        const float2 dd = q_unpack(d);
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-dd.x), "f"(-dd.y));
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(nd), "l"(d), "l"(ce));
+                    }
                     constexpr int PK = POLYK > 0 ? POLYK : 1;
                     const bool poly = POLYK > 0 && ok0 && ok1 && ((j * (P / 2) + h) * 2 + k) % PK == PK - 1;
                     float2 ww;
                     if (poly) {
+                        if constexpr (!XF) {  // the polynomial's range: clamp (weights below 2^-125 are 0 to fp32 sums)
+                            const float2 ee = q_unpack(e);
+                            asm("mov.b64 %0, {%1, %2};" : "=l"(e) : "f"(fmaxf(ee.x, -125.0f)), "f"(fmaxf(ee.y, -125.0f)));
+                        }
                         ww = q_poly_ex2x2(e);
                     } else {
                         const float2 ee = q_unpack(e);
@@ -167,15 +195,15 @@ __device__ __forceinline__ void p2r_row(const BlfParams& p, const float* __restr
 }  // namespace
 
 // blockIdx.y = tile row * 2 + axis, blockIdx.z = plane (image * C + channel)
-template <int R, bool PEERS, int POLYK>
-__global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfParams p)
+template <int R, bool PEERS, int POLYK, bool XF = true>
+__global__ void __launch_bounds__(256, P2rGeom<R, XF>::MINB) k_blf_p2r(const BlfParams p)
 {
-    using Gm = P2rGeom<R>;
+    using Gm = P2rGeom<R, XF>;
     constexpr int P = Gm::P, TW = Gm::TW, TH = Gm::TH, NT = Gm::NT, ROWS = Gm::ROWS, COLS = Gm::COLS;
     constexpr int GP = Gm::GP, SP = Gm::SP;
     extern __shared__ __align__(16) float smq[];
     float* G = smq;                                              // [ROWS][GP]  b (scaled gradient)
-    float2* SV = reinterpret_cast<float2*>(smq + ROWS * GP);     // [ROWS][SP] {b B, B}, B = exp2(-b^2)
+    float2* SV = reinterpret_cast<float2*>(smq + ROWS * GP);     // [ROWS][SP] {b B, B}, B = exp2(-b^2); !XF: {b, 1}
 
     const int H = p.H, W = p.W, C = p.C;
     const int pl = blockIdx.z, axis = blockIdx.y & 1;
@@ -195,6 +223,7 @@ __global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfPara
             const int i = t / QPR, c = t - i * QPR;
             const int y = ty0 - R + i, x = tx0 - Gm::OX + 4 * c;
             float4 bq = make_float4(0.f, 0.f, 0.f, 0.f), sa = bq, sb = bq;
+            if constexpr (!XF) sa = sb = make_float4(kP2rSentinel, 0.f, kP2rSentinel, 0.f);
             if (y >= 0 && y < H && x >= 0 && x < W) {
                 const int r0 = y * W + x;
                 const float4 a = __ldg(reinterpret_cast<const float4*>(fimg + r0));
@@ -204,13 +233,18 @@ __global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfPara
                 else
                     n = __ldg(reinterpret_cast<const float4*>(fimg + (y + 1 == H ? 0 : y + 1) * W + x));
                 bq = make_float4((n.x - a.x) * s, (n.y - a.y) * s, (n.z - a.z) * s, (n.w - a.w) * s);
-                const float w0 = q_ex2(-bq.x * bq.x), w1 = q_ex2(-bq.y * bq.y);
-                const float w2 = q_ex2(-bq.z * bq.z), w3 = q_ex2(-bq.w * bq.w);
-                sa = make_float4(bq.x * w0, w0, bq.y * w1, w1);
-                sb = make_float4(bq.z * w2, w2, bq.w * w3, w3);
+                if constexpr (XF) {
+                    const float w0 = q_ex2(-bq.x * bq.x), w1 = q_ex2(-bq.y * bq.y);
+                    const float w2 = q_ex2(-bq.z * bq.z), w3 = q_ex2(-bq.w * bq.w);
+                    sa = make_float4(bq.x * w0, w0, bq.y * w1, w1);
+                    sb = make_float4(bq.z * w2, w2, bq.w * w3, w3);
+                } else {
+                    sa = make_float4(bq.x, 1.0f, bq.y, 1.0f);
+                    sb = make_float4(bq.z, 1.0f, bq.w, 1.0f);
+                }
             }
             const int k0 = (2 * c) ^ ((c >> 2) & 1), k1 = k0 ^ 1;  // q_sw of chunks 2c, 2c + 1
-            *reinterpret_cast<float4*>(G + i * GP + 4 * c) = bq;
+            if constexpr (XF) *reinterpret_cast<float4*>(G + i * GP + 4 * c) = bq;
             *reinterpret_cast<float4*>(SV + i * SP + 2 * k0) = sa;
             *reinterpret_cast<float4*>(SV + i * SP + 2 * k1) = sb;
         }
@@ -224,14 +258,14 @@ __global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfPara
             const float* f1 = fimg + (size_t)(yin ? yn : 0) * W;
             for (int j = lane; j < COLS; j += 32) {
                 const int x = tx0 - Gm::OX + j;
-                float bb = 0.f, bw = 0.f;
+                float bb = XF ? 0.f : kP2rSentinel, bw = 0.f;
                 if (yin && x >= 0 && x < W) {
                     const int x1 = axis == 0 ? (x + 1 == W ? 0 : x + 1) : x;
                     bb = (__ldg(f1 + x1) - __ldg(f0 + x)) * s;
-                    bw = q_ex2(-bb * bb);
+                    bw = XF ? q_ex2(-bb * bb) : 1.0f;
                 }
-                G[i * GP + j] = bb;
-                SV[i * SP + q_sw(j)] = make_float2(bb * bw, bw);
+                if constexpr (XF) G[i * GP + j] = bb;
+                SV[i * SP + q_sw(j)] = XF ? make_float2(bb * bw, bw) : make_float2(bb, bw);
             }
         }
     }
@@ -241,16 +275,20 @@ __global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfPara
     unsigned long long gsp[2][2], acc[2][4];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float* ga = G + (2 * typ + k + R) * GP + tx * P + Gm::OX;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[k][0]) : "f"(2.0f * ga[0]), "f"(2.0f * ga[1]));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[k][1]) : "f"(2.0f * ga[2]), "f"(2.0f * ga[3]));
+        float ga[4];
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+            ga[q] = XF ? 2.0f * G[(2 * typ + k + R) * GP + tx * P + Gm::OX + q]
+                       : SV[(2 * typ + k + R) * SP + q_sw(tx * P + Gm::OX + q)].x;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[k][0]) : "f"(ga[0]), "f"(ga[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gsp[k][1]) : "f"(ga[2]), "f"(ga[3]));
 #pragma unroll
         for (int q = 0; q < P; ++q) acc[k][q] = 0ull;
     }
     // staged row 2 typ + i holds source row (output row 0) - R + i
     const float* grow = G + (2 * typ) * GP + tx * P;
     const float2* sv = SV + (2 * typ) * SP;
-    p2r_row<R, 1, POLYK>(p, grow, sv, tx, gsp, acc);
+    p2r_row<R, 1, POLYK, XF>(p, grow, sv, tx, gsp, acc);
 #pragma unroll 1
     for (int i = 1; i <= 2 * R; ++i) {
         grow += GP;
@@ -261,13 +299,13 @@ __global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfPara
             acc[0][q] = q_fmul2(f0, acc[0][q]);
             acc[1][q] = q_fmul2(f1, acc[1][q]);
         }
-        p2r_row<R, 3, POLYK>(p, grow, sv, tx, gsp, acc);
+        p2r_row<R, 3, POLYK, XF>(p, grow, sv, tx, gsp, acc);
     }
     {
         const float f1 = p.rfold[2 * R];
 #pragma unroll
         for (int q = 0; q < P; ++q) acc[1][q] = q_fmul2(f1, acc[1][q]);
-        p2r_row<R, 2, POLYK>(p, grow + GP, sv + SP, tx, gsp, acc);
+        p2r_row<R, 2, POLYK, XF>(p, grow + GP, sv + SP, tx, gsp, acc);
     }
 
     const int ox = tx0 + tx * P;
@@ -304,36 +342,37 @@ __global__ void __launch_bounds__(256, P2rGeom<R>::MINB) k_blf_p2r(const BlfPara
     }
 }
 
-template <int R, bool PEERS, int POLYK>
+template <int R, bool PEERS, int POLYK, bool XF = true>
 static cudaError_t launch_p2r_t(const BlfParams& p, int nplanes, cudaStream_t st)
 {
-    using Gm = P2rGeom<R>;
+    using Gm = P2rGeom<R, XF>;
     constexpr size_t smem = Gm::smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_blf_p2r<R, PEERS, POLYK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_blf_p2r<R, PEERS, POLYK, XF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int gy = (p.y1 - p.y0 + Gm::TH - 1) / Gm::TH;
     dim3 grid((p.W + Gm::TW - 1) / Gm::TW, 2 * gy, nplanes);
-    k_blf_p2r<R, PEERS, POLYK><<<grid, Gm::NT, smem, st>>>(p);
+    k_blf_p2r<R, PEERS, POLYK, XF><<<grid, Gm::NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <int R, int DEF>
+template <int R, int DEF, bool XF = true>
 static cudaError_t launch_p2r(const BlfParams& p, int nplanes, cudaStream_t st)
 {
-    if (p.npeers > 0) return launch_p2r_t<R, true, DEF>(p, nplanes, st);
+    if (p.npeers > 0) return launch_p2r_t<R, true, DEF, XF>(p, nplanes, st);
 #ifdef BLFLS_EXPERIMENTS
     switch (knob("BLFLS_P2R_POLY", DEF)) {
-        case 0: return launch_p2r_t<R, false, 0>(p, nplanes, st);
-        case 3: return launch_p2r_t<R, false, 3>(p, nplanes, st);
-        case 4: return launch_p2r_t<R, false, 4>(p, nplanes, st);
-        case 5: return launch_p2r_t<R, false, 5>(p, nplanes, st);
-        case 6: return launch_p2r_t<R, false, 6>(p, nplanes, st);
-        case 8: return launch_p2r_t<R, false, 8>(p, nplanes, st);
-        case 12: return launch_p2r_t<R, false, 12>(p, nplanes, st);
+        case 0: return launch_p2r_t<R, false, 0, XF>(p, nplanes, st);
+        case 3: return launch_p2r_t<R, false, 3, XF>(p, nplanes, st);
+        case 4: return launch_p2r_t<R, false, 4, XF>(p, nplanes, st);
+        case 5: return launch_p2r_t<R, false, 5, XF>(p, nplanes, st);
+        case 6: return launch_p2r_t<R, false, 6, XF>(p, nplanes, st);
+        case 8: return launch_p2r_t<R, false, 8, XF>(p, nplanes, st);
+        case 12: return launch_p2r_t<R, false, 12, XF>(p, nplanes, st);
         default: break;
     }
 #endif
-    return launch_p2r_t<R, false, DEF>(p, nplanes, st);
+    return launch_p2r_t<R, false, DEF, XF>(p, nplanes, st);
 }
 
 // Two-row self-guided filter where it applies: r = 7 or 15, factorised
@@ -342,10 +381,18 @@ static cudaError_t launch_p2r(const BlfParams& p, int nplanes, cudaStream_t st)
 bool launch_grad_blf_p2r(const BlfParams& p, int nplanes, int nsm, cudaStream_t st, cudaError_t* err)
 {
     if (knob("BLFLS_P2R", 1) == 0) return false;
-    if (p.radius != 7 && p.radius != 15) return false;
-    if (2.0f * p.range_coef * p.range_coef > 60.0f || -p.cs[p.radius] > 57.0f) return false;
+    if (-p.cs[p.radius] > 57.0f) return false;
     const long ctas = (long)((p.W + 63) / 64) * ((p.y1 - p.y0 + 31) / 32) * 2 * nplanes;
     if (ctas < 6L * 3 * nsm) return false;
+    if (2.0f * p.range_coef * p.range_coef > 60.0f) {
+        // difference form (sigma_r < 0.0775: c3): r = 5 only; every 8th exponent pair on the
+        // FMA pipe (tools/ab_p2r_diff.sh, c3: k_blf_p2 0.901 | none 0.875, 12th 0.906, 8th
+        // 0.947, 6th 0.937, 5th 0.919, 4th 0.894, 3rd 0.832 of the MUFU rate)
+        if (p.radius != 5 || knob("BLFLS_P2R_DIFF", 1) == 0) return false;
+        *err = launch_p2r<5, 8, false>(p, nplanes, st);
+        return true;
+    }
+    if (p.radius != 7 && p.radius != 15) return false;
     // every 4th exponent pair of a window row on the FMA pipe (r02 B200, tools/ab_p2r.sh;
     // fraction of the MUFU rate, k_blf_p2 first: c2 1.001 | none 0.907, 12th 0.963, 8th
     // 1.001, 6th 1.012, 5th 1.025, 4th 1.059, 3rd 0.987; c4 1.104 | 0.970, 1.045, 1.086,
