@@ -12,7 +12,7 @@ LIB = Path(sys.argv[1]) if len(sys.argv) > 1 else \
 KEYS = ["FFMA2", "FMUL2", "FADD2", "FFMA", "MUFU.EX2", "MUFU.RCP", "LDS", "STS", "LDG", "STG", "LDGSTS",
         "DFMA", "UBLKCP", "UTMALDG", "UTMASTG", "BAR", "SHFL", "ATOMS", "RED", "HMMA", "UTCHMMA"]
 # kernels the c1-c5 workloads dispatch (launch list of the bench / smoke)
-WANT = [r"k_blf_j3rILi7ELb0ELi12E", r"k_col_triILi32ELi2ELi4ELi256E", r"k_blf_j3ILi7ELi32ELb0ELi2ELb1ELb1E", r"k_blf_p2ILi7ELi32ELi0ELi7ELb0ELi2ELb1ELb1E",
+WANT = [r"k_blf_j3rILi7ELb0ELi12E", r"k_blf_p2rILi7ELb0ELi4ELb1E", r"k_blf_p2rILi15ELb0ELi4ELb1E", r"k_blf_p2rILi5ELb0ELi8ELb0E", r"k_col_triILi32ELi2ELi4ELi256E", r"k_blf_j3ILi7ELi32ELb0ELi2ELb1ELb1E", r"k_blf_p2ILi7ELi32ELi0ELi7ELb0ELi2ELb1ELb1E",
         r"k_blf_p2ILi15ELi16ELi0ELi5ELb0ELi4ELb1ELb1E", r"k_blf_p2ILi5ELi32ELi0ELi10ELb0ELi2ELb1ELb0E",
         r"k_row_r2cILb0ENS_5CtFftILi1024ELi2ELi128E", r"k2_colINS_4Fft2ILi2048ELi4ELi128ELi16E",
         r"k2_row_c2rINS_4Fft2ILi1024ELi4ELi64ELi16E", r"k2_row_c2r_tmaINS_4Fft2ILi1024ELi4ELi64ELi16E", r"k_grid_splat_tiled", r"k_dt_window"]
