@@ -215,6 +215,10 @@ struct SolveParams {
     // two float4 per column (tri_tables); nullptr: the column FFT pair runs
     const float4* tri;
     int tri_rpt;         // rows per thread the tables were built for
+    // the tridiagonal column pass also resets the per-image (lo, hi) slots the
+    // row c2r epilogue reduces into (one launch fewer per iteration)
+    uint32_t* lohi_reset;
+    int lohi_reset_n;
 };
 
 // tridiagonal column pass (k_col_tri.cu)

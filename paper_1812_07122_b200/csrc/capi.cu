@@ -389,10 +389,16 @@ blfls_status enq_solve(blfls_plan_t p, const float* f, const float* tx, const fl
         stage_begin(p, 2, st);
         CK(launch_row_r2c(s, p->rowf.g, planes, p->odd, st));
         stage_end(p, st);
+        // the tridiagonal column pass resets the (lo, hi) slots of the c2r epilogue
+        const bool fused_reset = lohi_out != nullptr && s.tri != nullptr;
+        if (fused_reset) {
+            s.lohi_reset = lohi_out;
+            s.lohi_reset_n = batch;
+        }
         stage_begin(p, 3, st);
         CK(launch_col(s, p->colf.g, planes, st));
         stage_end(p, st);
-        if (lohi_out) {
+        if (lohi_out && !fused_reset) {
             CK(launch_reset_lohi(lohi_out, batch, st));
             p->launches++;
         }

@@ -275,6 +275,11 @@ __global__ void __launch_bounds__(MAXT, tri_minb<RPT, TC, MAXT>())
 {
     constexpr int VF = TC * NCT;
     extern __shared__ float smt[];  // [2][VF][32 K] segment aggregates / entering states
+    if (p.lohi_reset != nullptr && blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = threadIdx.x; i < p.lohi_reset_n; i += blockDim.x) {
+            p.lohi_reset[2 * i] = 0xffffffffu;  // ordered +inf / -inf (k_reset_lohi)
+            p.lohi_reset[2 * i + 1] = 0u;
+        }
     const int H = p.H;
     const int ct = threadIdx.x % NCT, s = threadIdx.x / NCT;
     const int fidx = blockIdx.x * VF + ct * TC;  // float index within the spectrum row
